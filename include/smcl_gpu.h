@@ -1,0 +1,237 @@
+/*
+ * smcl_gpu.h — C ABI of the B200-native Stein-particle-filter step
+ * (MegaParticles, arXiv 2404.16370), exported by libsmcl_gpu.so.
+ *
+ * This is the drop-in boundary for the reference library `steinmcl`
+ * (/root/reference/proj, a header-declared C++ library with no FFI of its own).
+ * Every entry point names the reference interface it replaces (file:line
+ * relative to /root/reference/proj). Plain pointers and sizes only; no torch
+ * or CUDA types cross this boundary.
+ *
+ * Layouts (host side, caller-owned buffers, copied in/out):
+ *   pose     12 doubles: R row-major (9) then t (3).  (The reference stores
+ *            Eigen column-major R + t; the C++ facade converts.)
+ *   tangent   6 doubles [omega; v] (rotation first, se3.hpp:15-17).
+ *   sigma     9 doubles, row-major symmetric 3x3.
+ *   bounds    6 doubles: min xyz, max xyz (Aabb, gaussian_cloud.hpp:21-31).
+ *   neighbor lists: flat stride-K arrays idx[n*K] (int32), kval[n*K] (float),
+ *            count[n] (int32), self-first init (neighbor_graph.hpp:16-33).
+ *
+ * Errors: every int-returning call returns SMCL_OK or an SMCL_E* code and
+ * records a message readable with smcl_last_error(); the C++ facade rethrows
+ * invalid_argument / runtime_error / logic_error as the reference does.
+ * Threading: an engine handle is single-caller; calls on one
+ * handle must be serialised. Every call is synchronous at return.
+ */
+#ifndef SMCL_GPU_H
+#define SMCL_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMCL_ABI_VERSION 1
+#define SMCL_MAX_HIST 1026
+
+enum {
+  SMCL_OK = 0,
+  SMCL_EINVAL = 1,   /* std::invalid_argument */
+  SMCL_ERUNTIME = 2, /* std::runtime_error    */
+  SMCL_ELOGIC = 3,   /* std::logic_error      */
+  SMCL_ECUDA = 4,
+  SMCL_ENCCL = 5
+};
+
+/* FilterConfig (include/steinmcl/filter.hpp:17-51) flattened with its
+ * KernelParams (svgd.hpp:13-21), LshConfig (neighbor_search.hpp:13-21) and
+ * GicpParams (gicp.hpp:45-57). smcl_config_default() gives the reference
+ * defaults. */
+typedef struct smcl_config {
+  int32_t n_particles;
+  int32_t k_neighbors;
+  double sigma_r, sigma_t, repulsion_gain;
+  double lsh_alpha, lsh_noise_sigma, lsh_buckets_factor;
+  int32_t lsh_n_buckets, lsh_bucket_capacity;
+  int32_t reorder_particles, smooth_iters;
+  double nnf_resolution, nnf_max_query_dist, nnf_padding;
+  double beta;
+  int32_t n_svgd_iters, gn_scan_stride;
+  double damping_scale, omega_max, v_max, min_match_fraction, miss_cost;
+  double log_post_floor;
+  int32_t covariance_k, n_scan_max;
+  double epsilon_plane, scan_voxel_leaf, sensor_noise_sigma;
+  double diffusion_sigma_rot, diffusion_sigma_trans;
+  int32_t full_rotation, likelihood_mode; /* likelihood_mode: 0 auto, 1 exact fp64, 2 fast structured */
+  uint64_t seed;
+} smcl_config;
+
+/* GaussianCloud (gaussian_cloud.hpp:32-40). bounds may be NULL (computed). */
+typedef struct smcl_cloud {
+  int64_t n;
+  const double* mu;     /* n*3 */
+  const double* sigma;  /* n*9 */
+  const double* bounds; /* 6 or NULL */
+} smcl_cloud;
+
+/* OdometryInput (filter.hpp:56-60). */
+typedef struct smcl_odom {
+  double delta[12];
+  double cov[36]; /* row-major 6x6 */
+  int32_t valid;
+} smcl_odom;
+
+/* NeighborStats (neighbor_search.hpp:33-39); hist_len = bucket_capacity + 2. */
+typedef struct smcl_neighbor_stats {
+  int64_t n_buckets, buckets_used, overflow_dropped;
+  double mean_kernel;
+  int32_t hist_len;
+  int64_t occupancy_hist[SMCL_MAX_HIST];
+} smcl_neighbor_stats;
+
+/* FrameResult + StageTimes (filter.hpp:62-82). Stage times are CUDA-event
+ * device times of each stage. */
+typedef struct smcl_frame_result {
+  double representative[12];
+  double rep_log_post;
+  int64_t rep_index;
+  int32_t rep_id;
+  int32_t scan_empty, observation_rejected;
+  int64_t n_particles;
+  double mean_n_matched;
+  double predict_ms, neighbor_ms, likelihood_ms, update_ms, posterior_ms, total_ms;
+  smcl_neighbor_stats neighbor_stats;
+} smcl_frame_result;
+
+/* ParticleSet (particle_set.hpp:16-27) as caller-owned SoA buffers. */
+typedef struct smcl_particles_view {
+  int64_t n;
+  int32_t k;
+  double* poses;    /* n*12 */
+  double* log_post; /* n    */
+  int32_t* id;      /* n    */
+  int32_t* idx;     /* n*k  */
+  float* kval;      /* n*k  */
+  int32_t* count;   /* n    */
+} smcl_particles_view;
+
+typedef struct smcl_engine smcl_engine;
+
+/* ------------------------------------------------------------ library */
+int smcl_abi_version(void);
+const char* smcl_last_error(void); /* message of the last failed call on this thread */
+void smcl_config_default(smcl_config* cfg);
+int smcl_device_count(int* out);
+
+/* ------------------------------------------------------------ engine
+ * FilterEngine (filter.hpp:104-130 / filter.cpp:102-213). */
+
+/* FilterEngine::FilterEngine(GaussianCloud map, FilterConfig) — builds the
+ * nearest-neighbour field (nnf.cpp:10-96) and uploads the map. map may be NULL
+ * for stage-only use (no likelihood calls). device < 0: current device. */
+int smcl_create(const smcl_cloud* map, const smcl_config* cfg, int device, smcl_engine** out);
+/* Sharded engine: this rank owns particles [rank*N/world, (rank+1)*N/world). */
+int smcl_create_sharded(const smcl_cloud* map, const smcl_config* cfg, int device, int rank, int world,
+                        smcl_engine** out);
+int smcl_destroy(smcl_engine* h);
+
+/* FilterEngine::init_uniform(const Aabb&) (filter.cpp:108-116). */
+int smcl_init_uniform(smcl_engine* h, const double bounds[6]);
+/* steinmcl::init_uniform(cfg, bounds, full_rotation, seed) (filter.cpp:39-65). */
+int smcl_init_uniform_seeded(smcl_engine* h, int64_t n, const double bounds[6], int full_rotation, uint64_t seed);
+/* FilterEngine::step(scan, odo) (filter.cpp:118-213). scan->n == 0: empty scan. */
+int smcl_step(smcl_engine* h, const smcl_cloud* scan, const smcl_odom* odo, smcl_frame_result* out);
+int64_t smcl_frame_index(const smcl_engine* h);
+int64_t smcl_num_particles(const smcl_engine* h);
+
+/* FilterEngine::particles() / mutable_particles() (filter.hpp:111-113):
+ * download / upload the whole particle state (upload may change n and k). */
+int smcl_get_particles(smcl_engine* h, smcl_particles_view* view);
+int smcl_set_particles(smcl_engine* h, const smcl_particles_view* view);
+/* FilterEngine::nnf(): dims[3], origin[3], resolution; cells may be NULL. */
+int smcl_get_nnf(smcl_engine* h, int32_t dims[3], double origin[3], double* resolution, int32_t* cells);
+
+/* ------------------------------------------------------------ stage API
+ * Each stage runs on the engine's device-resident particles. Host output
+ * pointers may be NULL (result stays on the device for the next stage). */
+
+/* predict(set, delta, cov, frame_seed) (filter.cpp:67-84). */
+int smcl_predict(smcl_engine* h, const double delta[12], const double cov[36], uint64_t frame_seed);
+/* update_neighbors(set, lsh, kernel, pass_seed, bounds) (neighbor_search.cpp:61-192). */
+int smcl_update_neighbors(smcl_engine* h, uint64_t pass_seed, const double bounds[6], smcl_neighbor_stats* stats);
+/* evaluate_all(map, nnf, scan, poses, gicp, steps, ll, nm) (gicp.cpp:87-107).
+ * H_out (n*36) / b_out (n*6) optionally return each particle's GN system. */
+int smcl_evaluate_all(smcl_engine* h, const smcl_cloud* scan, double* step_out, double* ll_out, int32_t* nm_out,
+                      double* H_out, double* b_out);
+/* evaluate_likelihoods(map, nnf, scan, poses, gicp, ll, nm) (gicp.cpp:109-137). */
+int smcl_evaluate_likelihoods(smcl_engine* h, const smcl_cloud* scan, double* ll_out, int32_t* nm_out);
+/* compute_phis(poses, steps, idx, count, K, kernel, phi) (svgd.cpp:36-49).
+ * steps == NULL: use the device steps of the last evaluate_all. */
+int smcl_compute_phis(smcl_engine* h, const double* steps, double* phi_out);
+/* apply_updates(poses, phis) (svgd.cpp:51-62). phis == NULL: device phis. */
+int smcl_apply_updates(smcl_engine* h, const double* phis);
+/* bayes_update(log_post, ll, nm, beta, floor) (posterior.cpp:26-58).
+ * ll/nm == NULL: device results of the last likelihood call. */
+int smcl_bayes_update(smcl_engine* h, const double* ll, const int32_t* nm, double beta, double floor,
+                      int32_t* rejected);
+/* normalize_log_post(log_post, floor) (posterior.cpp:13-24). */
+int smcl_normalize_log_post(smcl_engine* h, double floor);
+/* smooth(log_post, graph, iters, floor) (posterior.cpp:60-97). */
+int smcl_smooth(smcl_engine* h, int32_t iters, double floor);
+/* representative(log_post, poses) (posterior.cpp:99-108). */
+int smcl_representative(smcl_engine* h, int64_t* index, double pose[12], double* log_post);
+
+/* ------------------------------------------------------------ batch device math
+ * Handle-free kernels on the current device, for parity tests of the device
+ * SE3 / hash / solver code. All pointers are host buffers. */
+int smcl_se3_exp_batch(const double* xi, int64_t n, double* poses_out);   /* se3.hpp:73-97  */
+int smcl_se3_log_batch(const double* poses, int64_t n, double* xi_out);   /* se3.hpp:103-149 */
+int smcl_kernel_batch(const double* a, const double* b, int64_t n, double sigma_r, double sigma_t,
+                      double* k_out);                                      /* svgd.hpp:36-38 */
+int smcl_lsh_hash_batch(const double* poses, int64_t n, const double frame[12], const double noise[6],
+                        double alpha, double sigma_r, double sigma_t, uint64_t* out); /* neighbor_search.cpp:25-35 */
+int smcl_solve_step_batch(const double* H, const double* b, const double* lambda, int64_t n, double omega_max,
+                          double v_max, double* step_out);                 /* gicp.cpp:47-75 */
+
+/* ------------------------------------------------------------ host preparation
+ * Product-side host C++ (map load / scan input). */
+/* estimate_covariances(points, k, eps) (gaussian_cloud.cpp:36-90): sigma_out n*9. */
+int smcl_estimate_covariances(const double* points, int64_t n, int k, double eps, double* sigma_out);
+/* downsample_to(points, max, leaf) (gaussian_cloud.cpp:134-144); out capacity n*3. */
+int smcl_downsample_to(const double* points, int64_t n, int64_t max_points, double leaf, double* out,
+                       int64_t* n_out);
+/* make_scan_cloud(points, cfg) (filter.cpp:86-100); mu_out n*3, sigma_out n*9. */
+int smcl_make_scan_cloud(const double* points, int64_t n, const smcl_config* cfg, double* mu_out,
+                         double* sigma_out, int64_t* n_out);
+/* build_nnf(map, res, pad, max_query) (nnf.cpp:10-96): call with cells == NULL for dims. */
+int smcl_build_nnf(const smcl_cloud* map, double resolution, double padding, double max_query_dist,
+                   int32_t dims[3], double origin[3], int32_t* cells);
+
+/* ------------------------------------------------------------ simulator (sim/world.cpp)
+ * Rectangles are 9 doubles: origin(3), edge_u(3), edge_v(3). */
+typedef struct smcl_corridor_spec {  /* sim/world.hpp:41-54 */
+  double corridor_length, corridor_width, height;
+  int32_t n_rooms, furniture;
+  double room_width, room_depth, door_width, door_height;
+} smcl_corridor_spec;
+typedef struct smcl_sensor_spec {    /* sim/world.hpp:70-78 */
+  int32_t n_azimuth, n_elevations;
+  double elevations_deg[64];
+  double max_range, min_range, noise_sigma;
+} smcl_sensor_spec;
+void smcl_sim_default_corridor(smcl_corridor_spec* spec);
+void smcl_sim_default_sensor(smcl_sensor_spec* spec);
+int smcl_sim_corridor_world(const smcl_corridor_spec* spec, double* rects, int32_t max_rects, int32_t* n_rects);
+int smcl_sim_box_room(const double size[3], double* rects, int32_t max_rects, int32_t* n_rects);
+/* sample_world (world.cpp:140-160): call with mu_out == NULL for the count. */
+int smcl_sim_sample_world(const double* rects, int32_t n_rects, double density, uint64_t seed, int cov_k,
+                          double eps, double* mu_out, double* sigma_out, int64_t* n_out);
+/* simulate_scan_points (world.cpp:162-181); rng_state is the SplitMix64 state (in/out). */
+int smcl_sim_scan(const double* rects, int32_t n_rects, const double pose[12], const smcl_sensor_spec* sensor,
+                  uint64_t* rng_state, double* points_out, int64_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMCL_GPU_H */

@@ -1,0 +1,1141 @@
+// B200 engine: device-resident particle state, per-stage orchestration of the
+// hand-written kernels and the C ABI of include/smcl_gpu.h.
+//
+// Reference call structure: FilterEngine::step (filter.cpp:118-213) and the
+// free stage functions it calls. One CUDA stream per engine; every ABI call is
+// synchronous at return (only small results are read back).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <bit>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/smcl_gpu.h"
+#include "engine.cuh"
+#include "host/prep.hpp"
+#include "kernels.cuh"
+
+namespace smcl {
+
+// ---------------------------------------------------------------- errors
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+thread_local std::string g_last_error;
+
+#define CK(x)                                                                                           \
+  do {                                                                                                  \
+    cudaError_t e_ = (x);                                                                               \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SMCL_OK;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return SMCL_ECUDA;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return SMCL_EINVAL;
+  } catch (const std::logic_error& e) {
+    g_last_error = e.what();
+    return SMCL_ELOGIC;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SMCL_ERUNTIME;
+  }
+}
+
+// ---------------------------------------------------------------- buffers
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) count = 1;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const T* h, size_t count, cudaStream_t st) {
+    ensure(count);
+    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+  void download(T* h, size_t count, cudaStream_t st) const {
+    if (count) CK(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, st));
+  }
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+  }
+};
+
+namespace {
+constexpr uint64_t k_stream_init = 1, k_stream_predict = 2, k_stream_neighbors = 3;  // filter.cpp:22-23
+constexpr int kFastMaxScan = 1500;
+
+// ---------------------------------------------------------------- host math
+// Eigen LLT (lower) on a 6x6, as the oracle / reference covariance_sqrt.
+bool llt6(const double* a, double* l) {
+  for (int q = 0; q < 36; ++q) l[q] = a[q];
+  for (int k = 0; k < 6; ++k) {
+    double x = l[k * 6 + k];
+    if (k > 0) {
+      double sq = 0.0;
+      for (int j = 0; j < k; ++j) sq += l[k * 6 + j] * l[k * 6 + j];
+      x -= sq;
+    }
+    if (x <= 0.0) return false;
+    x = std::sqrt(x);
+    l[k * 6 + k] = x;
+    for (int i = k + 1; i < 6; ++i) {
+      if (k > 0) {
+        double s = 0.0;
+        for (int j = 0; j < k; ++j) s += l[i * 6 + j] * l[k * 6 + j];
+        l[i * 6 + k] -= s;
+      }
+      l[i * 6 + k] /= x;
+    }
+  }
+  for (int i = 0; i < 6; ++i)
+    for (int j = i + 1; j < 6; ++j) l[i * 6 + j] = 0.0;
+  return true;
+}
+
+void sym_eig6(const double* a_in, double w[6], double v[36]) {
+  double a[36];
+  std::memcpy(a, a_in, sizeof(a));
+  for (int i = 0; i < 36; ++i) v[i] = (i % 7 == 0) ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, scale = 0.0;
+    for (int i = 0; i < 6; ++i) {
+      scale += std::fabs(a[i * 7]);
+      for (int j = i + 1; j < 6; ++j) off += std::fabs(a[i * 6 + j]);
+    }
+    if (off == 0.0 || off < 1e-18 * scale) break;
+    for (int p = 0; p < 5; ++p)
+      for (int q = p + 1; q < 6; ++q) {
+        if (a[p * 6 + q] == 0.0) continue;
+        const double th = (a[q * 7] - a[p * 7]) / (2.0 * a[p * 6 + q]);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < 6; ++k) {
+          const double x = a[k * 6 + p], y = a[k * 6 + q];
+          a[k * 6 + p] = c * x - s * y;
+          a[k * 6 + q] = s * x + c * y;
+        }
+        for (int k = 0; k < 6; ++k) {
+          const double x = a[p * 6 + k], y = a[q * 6 + k];
+          a[p * 6 + k] = c * x - s * y;
+          a[q * 6 + k] = s * x + c * y;
+        }
+        for (int k = 0; k < 6; ++k) {
+          const double x = v[k * 6 + p], y = v[k * 6 + q];
+          v[k * 6 + p] = c * x - s * y;
+          v[k * 6 + q] = s * x + c * y;
+        }
+      }
+  }
+  int ord[6] = {0, 1, 2, 3, 4, 5};
+  std::sort(ord, ord + 6, [&](int x, int y) { return a[x * 7] < a[y * 7]; });
+  double vs[36];
+  for (int c = 0; c < 6; ++c) {
+    w[c] = a[ord[c] * 7];
+    for (int r = 0; r < 6; ++r) vs[r * 6 + c] = v[r * 6 + ord[c]];
+  }
+  std::memcpy(v, vs, sizeof(vs));
+}
+
+// filter.cpp:25-35
+void covariance_sqrt(const double* cov, double* L) {
+  if (llt6(cov, L)) return;
+  double jit[36];
+  std::memcpy(jit, cov, sizeof(jit));
+  for (int i = 0; i < 6; ++i) jit[i * 7] = cov[i * 7] + 1e-12;
+  if (llt6(jit, L)) return;
+  double w[6], v[36];
+  sym_eig6(cov, w, v);
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) L[i * 6 + j] = v[i * 6 + j] * std::sqrt(std::max(w[j], 0.0));
+}
+
+int32_t next_prime_at_least(int32_t n) {  // neighbor_search.cpp:46-59
+  if (n <= 2) return 2;
+  int32_t p = n | 1;
+  for (;; p += 2) {
+    bool prime = true;
+    for (int32_t d = 3; d * d <= p; d += 2)
+      if (p % d == 0) {
+        prime = false;
+        break;
+      }
+    if (prime) return p;
+  }
+}
+
+Pose load_pose(const double* p) {
+  Pose q;
+  std::memcpy(q.R, p, 9 * sizeof(double));
+  std::memcpy(q.t, p + 9, 3 * sizeof(double));
+  return q;
+}
+void store_pose(const Pose& q, double* p) {
+  std::memcpy(p, q.R, 9 * sizeof(double));
+  std::memcpy(p + 9, q.t, 3 * sizeof(double));
+}
+
+// Structured (plane-model) covariance: Sigma = a*I - beta*u u^T with the
+// single eigenvalue s = a - beta the smallest one (u its axis) and the double
+// eigenvalue a = beta + s. This is exactly the form the reference's
+// estimate_covariances produces (gaussian_cloud.cpp:79-86), optionally plus an
+// isotropic sensor term (filter.cpp:95-98). Returns false unless Sigma is of
+// that form to 1e-10 relative.
+bool structure_ab(const double* sig, float& beta, float& s, float u[3]) {
+  double w[3], v[9];
+  host::sym_eig3(sig, w, v);
+  double mx = 0.0;
+  for (int q = 0; q < 9; ++q) mx = std::max(mx, std::fabs(sig[q]));
+  const double a = 0.5 * (w[1] + w[2]), sv = w[0];
+  const double ax[3] = {v[0], v[3], v[6]};
+  double err = 0.0;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      const double rec = (r == c ? a : 0.0) - (a - sv) * ax[r] * ax[c];
+      err = std::max(err, std::fabs(rec - sig[r * 3 + c]));
+    }
+  if (!(err <= 1e-10 * mx) || !(sv >= 0.0) || !(a > 0.0)) return false;
+  for (int q = 0; q < 3; ++q) u[q] = static_cast<float>(ax[q]);
+  s = static_cast<float>(sv);
+  beta = static_cast<float>(a - sv);
+  return true;
+}
+}  // namespace
+
+}  // namespace smcl
+
+using namespace smcl;
+
+// ---------------------------------------------------------------- engine object
+struct smcl_engine {
+  smcl_config cfg{};
+  int device = 0;
+  cudaStream_t st = nullptr;
+  int rank = 0, world = 1;
+  int64_t n_total = 0, n_local = 0, gbase = 0;
+  int k = 20;
+  int64_t frame = 0;
+
+  // map
+  bool has_map = false;
+  bool map_structured = false;
+  host::Aabb map_bounds{};
+  NnfGeom geom{};
+  int64_t n_cells = 0;
+  std::vector<int32_t> h_cells;
+  DBuf<int32_t> cells;
+  DBuf<double> map_mu, map_sigma;
+  DBuf<float4> map_fast;
+
+  // particles
+  DBuf<Pose> poses, poses2;
+  DBuf<double> log_post, log_post2;
+  DBuf<int32_t> id, id2, idx, idx2, count, count2;
+  DBuf<float> kval, kval2;
+
+  // per-stage work
+  DBuf<double> sys, steps, phis, ll;
+  DBuf<int32_t> nm;
+  bool steps_valid = false, phis_valid = false, ll_valid = false;
+
+  // lsh
+  DBuf<uint64_t> keys, skeys;
+  DBuf<int32_t> member_of, head, seg_id, seg_start, new_of_old, iota;
+  DBuf<unsigned char> temp;
+  size_t temp_bytes = 0;
+  DBuf<unsigned long long> d_hist, d_counts;
+
+  // posterior
+  DBuf<double> pbuf, qbuf, partial, partial2, scal;
+  DBuf<long long> scal_i;
+  DBuf<double> argv;
+  DBuf<long long> argi;
+
+  // scans (full and Gauss-Newton subset)
+  struct ScanDev {
+    int n = 0;
+    bool structured = false;
+    DBuf<double> mu, sigma;
+    DBuf<float4> rec;
+  } scan_full, scan_gn;
+
+  cudaEvent_t ev[8] = {};
+
+  ~smcl_engine() {
+    if (st) cudaStreamSynchronize(st);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+  }
+
+  void sync() { CK(cudaStreamSynchronize(st)); }
+
+  // ------------------------------------------------------------ setup
+  void setup_map(const smcl_cloud* m) {
+    if (!m || m->n <= 0) throw std::invalid_argument("FilterEngine: empty map");
+    const auto* pts = reinterpret_cast<const host::V3*>(m->mu);
+    if (m->bounds) {
+      for (int a = 0; a < 3; ++a) {
+        map_bounds.min[a] = m->bounds[a];
+        map_bounds.max[a] = m->bounds[3 + a];
+      }
+    } else {
+      map_bounds = host::compute_bounds(pts, m->n);
+    }
+    const host::NnfGeometry g = host::nnf_geometry(map_bounds, cfg.nnf_resolution, cfg.nnf_padding,
+                                                   cfg.nnf_max_query_dist, size_t(1) << 30);
+    h_cells.resize(static_cast<size_t>(g.n_cells));
+    host::build_nnf_cells(pts, m->n, g, h_cells.data());
+    n_cells = g.n_cells;
+    for (int a = 0; a < 3; ++a) {
+      geom.origin[a] = g.origin[a];
+      geom.dims[a] = g.dims[a];
+    }
+    geom.res = g.resolution;
+    geom.inv_res = 1.0 / g.resolution;
+    cells.upload(h_cells.data(), h_cells.size(), st);
+    map_mu.upload(m->mu, static_cast<size_t>(m->n) * 3, st);
+    map_sigma.upload(m->sigma, static_cast<size_t>(m->n) * 9, st);
+    // Structured (plane-model) map -> denormalised 32-byte cell records.
+    std::vector<float> beta(static_cast<size_t>(m->n)), sv(static_cast<size_t>(m->n)), uv(3 * static_cast<size_t>(m->n));
+    bool ok = true;
+    for (int64_t i = 0; i < m->n && ok; ++i)
+      ok = structure_ab(m->sigma + 9 * i, beta[static_cast<size_t>(i)], sv[static_cast<size_t>(i)], &uv[3 * static_cast<size_t>(i)]);
+    map_structured = ok;
+    if (ok) {
+      std::vector<float4> rec(2 * static_cast<size_t>(n_cells));
+      const int nx = geom.dims[0], ny = geom.dims[1];
+      for (int64_t c = 0; c < n_cells; ++c) {
+        const int32_t mi = h_cells[static_cast<size_t>(c)];
+        if (mi < 0) {
+          rec[2 * c] = make_float4(0.f, 0.f, 0.f, -1.f);
+          rec[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          continue;
+        }
+        const int64_t ix = c % nx, iy = (c / nx) % ny, iz = c / (static_cast<int64_t>(nx) * ny);
+        const double corner[3] = {geom.origin[0] + static_cast<double>(ix) * geom.res,
+                                  geom.origin[1] + static_cast<double>(iy) * geom.res,
+                                  geom.origin[2] + static_cast<double>(iz) * geom.res};
+        const double* mu = m->mu + 3 * static_cast<int64_t>(mi);
+        rec[2 * c] = make_float4(static_cast<float>(mu[0] - corner[0]), static_cast<float>(mu[1] - corner[1]),
+                                 static_cast<float>(mu[2] - corner[2]), beta[static_cast<size_t>(mi)]);
+        rec[2 * c + 1] = make_float4(uv[3 * mi], uv[3 * mi + 1], uv[3 * mi + 2], sv[static_cast<size_t>(mi)]);
+      }
+      map_fast.upload(rec.data(), rec.size(), st);
+    }
+    has_map = true;
+    sync();
+  }
+
+  void alloc_particles(int64_t n, int kk) {
+    n_local = n;
+    k = kk;
+    const size_t un = static_cast<size_t>(std::max<int64_t>(n, 1));
+    poses.ensure(un);
+    poses2.ensure(un);
+    log_post.ensure(un);
+    log_post2.ensure(un);
+    id.ensure(un);
+    id2.ensure(un);
+    count.ensure(un);
+    count2.ensure(un);
+    idx.ensure(un * kk);
+    idx2.ensure(un * kk);
+    kval.ensure(un * kk);
+    kval2.ensure(un * kk);
+    sys.ensure(un * kSysStride);
+    steps.ensure(un * 6);
+    phis.ensure(un * 6);
+    ll.ensure(un);
+    nm.ensure(un);
+    keys.ensure(un);
+    skeys.ensure(un);
+    member_of.ensure(un);
+    head.ensure(un);
+    seg_id.ensure(un);
+    seg_start.ensure(un);
+    new_of_old.ensure(un);
+    iota.ensure(un);
+    {
+      std::vector<int32_t> h(un);
+      for (size_t i = 0; i < un; ++i) h[i] = static_cast<int32_t>(i);
+      iota.upload(h.data(), un, st);
+    }
+    const size_t tb = sort_temp_bytes(static_cast<int64_t>(un));
+    if (tb > temp_bytes) {
+      temp.ensure(tb);
+      temp_bytes = tb;
+    }
+    pbuf.ensure(un);
+    qbuf.ensure(un);
+    const size_t chunks = (un + kReduceChunk - 1) / kReduceChunk;
+    partial.ensure(chunks);
+    partial2.ensure(chunks);
+    scal.ensure(8);
+    scal_i.ensure(8);
+    argv.ensure(static_cast<size_t>(argmax_partials(static_cast<int64_t>(un))));
+    argi.ensure(static_cast<size_t>(argmax_partials(static_cast<int64_t>(un))));
+    d_hist.ensure(SMCL_MAX_HIST);
+    d_counts.ensure(4);
+    steps_valid = phis_valid = ll_valid = false;
+  }
+
+  // ------------------------------------------------------------ scans
+  void upload_scan(ScanDev& sd, const double* mu, const double* sigma, int n) {
+    if (n > kMaxScan) throw std::invalid_argument("scan exceeds the device scan capacity");
+    sd.n = n;
+    sd.mu.upload(mu, static_cast<size_t>(n) * 3, st);
+    sd.sigma.upload(sigma, static_cast<size_t>(n) * 9, st);
+    std::vector<float4> rec(2 * static_cast<size_t>(std::max(n, 1)));
+    bool ok = true;
+    for (int q = 0; q < n && ok; ++q) {
+      float beta, s, u[3];
+      ok = structure_ab(sigma + 9 * q, beta, s, u);
+      rec[2 * q] = make_float4(static_cast<float>(mu[3 * q]), static_cast<float>(mu[3 * q + 1]),
+                               static_cast<float>(mu[3 * q + 2]), beta);
+      rec[2 * q + 1] = make_float4(u[0], u[1], u[2], s);
+    }
+    sd.structured = ok;
+    if (ok) sd.rec.upload(rec.data(), rec.size(), st);
+  }
+
+  void set_scans(const smcl_cloud* scan) {
+    const int S = static_cast<int>(scan->n);
+    upload_scan(scan_full, scan->mu, scan->sigma, S);
+    const int stride = cfg.gn_scan_stride;
+    if (stride > 1 && S > 2 * stride) {  // filter.cpp:154-165
+      std::vector<double> mu, sg;
+      for (int q = 0; q < S; q += stride) {
+        mu.insert(mu.end(), scan->mu + 3 * q, scan->mu + 3 * q + 3);
+        sg.insert(sg.end(), scan->sigma + 9 * q, scan->sigma + 9 * q + 9);
+      }
+      upload_scan(scan_gn, mu.data(), sg.data(), static_cast<int>(mu.size() / 3));
+    } else {
+      upload_scan(scan_gn, scan->mu, scan->sigma, S);
+    }
+  }
+
+  bool use_fast(const ScanDev& sd) const {
+    const bool can = map_structured && sd.structured && sd.n <= kFastMaxScan;
+    if (cfg.likelihood_mode == 1) return false;
+    if (cfg.likelihood_mode == 2) {
+      if (!can) throw std::invalid_argument("likelihood_mode=fast needs plane-model map and scan covariances");
+      return true;
+    }
+    return can;
+  }
+
+  GicpParamsDev gicp_params(int scan_size) const {
+    GicpParamsDev p;
+    p.damping_scale = cfg.damping_scale;
+    p.omega_max = cfg.omega_max;
+    p.v_max = cfg.v_max;
+    p.miss_cost = cfg.miss_cost;
+    p.min_matched = static_cast<int>(std::ceil(cfg.min_match_fraction * static_cast<double>(scan_size)));
+    p.scan_size = scan_size;
+    return p;
+  }
+
+  // ------------------------------------------------------------ stages
+  void run_likelihood(bool gn, const ScanDev& sd) {
+    if (!has_map) throw std::invalid_argument("engine has no map");
+    if (sd.n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
+    ScanView sv{sd.n, sd.mu.p, sd.sigma.p, sd.structured ? sd.rec.p : nullptr};
+    if (use_fast(sd)) {
+      MapFast mf{geom, map_fast.p};
+      launch_gicp_fast(gn, poses.p, n_local, sv, mf, sys.p, nm.p, st);
+    } else {
+      MapExact me{geom, cells.p, map_mu.p, map_sigma.p};
+      launch_gicp_exact(gn, poses.p, n_local, sv, me, sys.p, nm.p, st);
+    }
+    CK(cudaGetLastError());
+    const GicpParamsDev gp = gicp_params(sd.n);
+    if (gn)
+      launch_solve(sys.p, nm.p, n_local, gp, steps.p, ll.p, st);
+    else
+      launch_gate_ll(sys.p, nm.p, n_local, gp, ll.p, st);
+    CK(cudaGetLastError());
+    ll_valid = true;
+    if (gn) steps_valid = true;
+  }
+
+  void predict(const double* delta, const double* cov, uint64_t frame_seed) {
+    PredictParams pp{};
+    pp.delta = load_pose(delta);
+    bool noiseless = true;
+    for (int q = 0; q < 36; ++q)
+      if (cov[q] != 0.0) noiseless = false;
+    pp.noiseless = noiseless ? 1 : 0;
+    if (!noiseless) covariance_sqrt(cov, pp.L);
+    pp.frame_seed = frame_seed;
+    launch_predict(poses.p, n_local, gbase, pp, st);
+    CK(cudaGetLastError());
+  }
+
+  void update_neighbors(uint64_t pass_seed, const double* bounds, smcl_neighbor_stats* out) {
+    const int64_t n = n_total;
+    if (out) std::memset(out, 0, sizeof(*out));
+    if (n == 0) return;
+    if (k != cfg.k_neighbors) throw std::invalid_argument("update_neighbors: graph not initialized for this set");
+    // Pass randomness on the host (neighbor_search.cpp:71-73): identical
+    // SplitMix64 + libm as the reference.
+    SplitMix64 rng(pass_seed);
+    LshPass lp{};
+    random_rotation(rng, lp.frame.R);
+    for (int a = 0; a < 3; ++a) lp.frame.t[a] = rng.uniform_range(bounds[a], bounds[3 + a]);
+    double z[6];
+    rng.normal6(z);
+    for (int c = 0; c < 6; ++c) lp.noise[c] = cfg.lsh_noise_sigma * z[c];
+    lp.alpha = cfg.lsh_alpha;
+    lp.sigma_r = cfg.sigma_r;
+    lp.sigma_t = cfg.sigma_t;
+    const int32_t nb = cfg.lsh_n_buckets > 0
+                           ? cfg.lsh_n_buckets
+                           : next_prime_at_least(static_cast<int32_t>(std::ceil(cfg.lsh_buckets_factor * static_cast<double>(n))));
+    lp.n_buckets = nb;
+    lp.idx_bits = std::max(1, static_cast<int>(std::bit_width(static_cast<uint64_t>(n - 1))));
+    lp.h_bits = std::max(1, static_cast<int>(std::bit_width(static_cast<uint32_t>(nb - 1))));
+    lp.prio_bits = std::max(0, 64 - lp.h_bits - lp.idx_bits);
+    lp.prio_seed = mix_seed(pass_seed, 0x70726f6974ull);
+    const uint64_t idx_mask = (uint64_t(1) << lp.idx_bits) - 1;
+    const int shift = lp.prio_bits + lp.idx_bits;
+
+    launch_lsh_keys(poses.p, n_local, gbase, lp, keys.p, st);
+    sort_keys(keys.p, skeys.p, n, 64, temp.p, temp_bytes, st);
+    launch_members(skeys.p, n, idx_mask, shift, member_of.p, head.p, st);
+    const int32_t* members = member_of.p;
+    if (cfg.reorder_particles) {
+      launch_inverse_perm(member_of.p, n, new_of_old.p, st);
+      launch_reorder(member_of.p, new_of_old.p, n, k, poses.p, log_post.p, id.p, idx.p, kval.p, count.p, poses2.p,
+                     log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st);
+      poses.swap(poses2);
+      log_post.swap(log_post2);
+      id.swap(id2);
+      idx.swap(idx2);
+      kval.swap(kval2);
+      count.swap(count2);
+      members = iota.p;
+      steps_valid = phis_valid = ll_valid = false;  // storage order changed
+    }
+    inclusive_sum_i32(head.p, seg_id.p, n, temp.p, temp_bytes, st);
+    launch_segments(head.p, seg_id.p, n, seg_start.p, st);
+    int32_t n_seg = 0;
+    CK(cudaMemcpyAsync(&n_seg, seg_id.p + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    sync();
+    launch_refresh_gather(poses.p, n_local, gbase, nullptr, members, seg_id.p, seg_start.p, n_seg, n, idx.p, kval.p,
+                          count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, st);
+    CK(cudaGetLastError());
+    // statistics
+    const int hist_len = cfg.lsh_bucket_capacity + 2;
+    CK(cudaMemsetAsync(d_hist.p, 0, sizeof(unsigned long long) * hist_len, st));
+    CK(cudaMemsetAsync(d_counts.p, 0, sizeof(unsigned long long) * 2, st));
+    launch_seg_stats(seg_start.p, n_seg, n, cfg.lsh_bucket_capacity, d_hist.p, d_counts.p, st);
+    const int64_t chunks = (n_local + kReduceChunk - 1) / kReduceChunk;
+    launch_chunk_sum_kernel(kval.p, count.p, n_local, k, partial.p, partial2.p, st);
+    launch_finish_sum2(partial.p, partial2.p, chunks, scal.p, st);
+    CK(cudaGetLastError());
+    if (out) {
+      std::vector<unsigned long long> hist(static_cast<size_t>(hist_len));
+      unsigned long long ov[2];
+      double sums[2];
+      d_hist.download(hist.data(), hist.size(), st);
+      d_counts.download(ov, 2, st);
+      scal.download(sums, 2, st);
+      sync();
+      out->n_buckets = nb;
+      out->buckets_used = n_seg;
+      out->overflow_dropped = static_cast<int64_t>(ov[0]);
+      out->mean_kernel = sums[1] > 0 ? sums[0] / sums[1] : 0.0;
+      out->hist_len = std::min(hist_len, SMCL_MAX_HIST);
+      for (int q = 0; q < out->hist_len; ++q) out->occupancy_hist[q] = static_cast<int64_t>(hist[static_cast<size_t>(q)]);
+    }
+  }
+
+  void svgd(bool fused_apply) {
+    SvgdParams sp{cfg.sigma_r, cfg.sigma_t, cfg.repulsion_gain};
+    if (fused_apply) {
+      launch_svgd(poses.p, steps.p, n_local, gbase, idx.p, count.p, k, sp, nullptr, poses2.p, st);
+      poses.swap(poses2);
+    } else {
+      launch_svgd(poses.p, steps.p, n_local, gbase, idx.p, count.p, k, sp, phis.p, nullptr, st);
+      phis_valid = true;
+    }
+    CK(cudaGetLastError());
+  }
+
+  void normalize(double floor_v) {
+    const int64_t n = n_local;
+    if (n == 0) return;
+    launch_argmax(log_post.p, n, gbase, argv.p, argi.p, scal.p + 2, scal_i.p, st);
+    launch_chunk_sum_exp(log_post.p, n, scal.p + 2, partial.p, st);
+    launch_finish_lse(partial.p, (n + kReduceChunk - 1) / kReduceChunk, scal.p + 2, scal.p + 3, st);
+    launch_apply_lse(log_post.p, n, scal.p + 3, floor_v, st);
+    CK(cudaGetLastError());
+  }
+
+  // Returns observation_rejected.
+  bool bayes(double beta, double floor_v) {
+    if (!(beta >= 0.0)) throw std::invalid_argument("bayes_update: beta must be >= 0");
+    const int64_t n = n_local;
+    if (n == 0) return false;
+    launch_match_counts(ll.p, nm.p, n, d_counts.p, st);
+    unsigned long long cnt[2];
+    d_counts.download(cnt, 2, st);
+    sync();
+    if (cnt[0] == 0) {
+      launch_fill(log_post.p, n, -std::log(static_cast<double>(n_total)), st);
+      return true;
+    }
+    launch_bayes_numer(log_post.p, ll.p, nm.p, n, beta, st);
+    normalize(floor_v);
+    return false;
+  }
+
+  void smooth(int iters, double floor_v) {
+    if (iters < 0) throw std::invalid_argument("smooth: iters must be >= 0");
+    const int64_t n = n_local;
+    if (n == 0 || iters == 0) return;
+    launch_exp(log_post.p, pbuf.p, n, st);
+    for (int r = 0; r < iters; ++r) {
+      launch_smooth_round(pbuf.p, qbuf.p, n, idx.p, kval.p, count.p, k, st);
+      pbuf.swap(qbuf);
+    }
+    launch_log(pbuf.p, log_post.p, n, st);
+    CK(cudaGetLastError());
+    normalize(floor_v);
+  }
+
+  void representative(int64_t* index, double* pose, double* value) {
+    if (n_local == 0) throw std::invalid_argument("representative: empty or mismatched particle set");
+    launch_argmax(log_post.p, n_local, gbase, argv.p, argi.p, scal.p + 4, scal_i.p + 1, st);
+    double v;
+    long long ix;
+    CK(cudaMemcpyAsync(&v, scal.p + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&ix, scal_i.p + 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    sync();
+    *index = ix;
+    *value = v;
+    if (pose) {
+      Pose p;
+      CK(cudaMemcpyAsync(&p, poses.p + (ix - gbase), sizeof(Pose), cudaMemcpyDeviceToHost, st));
+      sync();
+      store_pose(p, pose);
+    }
+  }
+
+  void init_uniform(int64_t n, const double* b, bool full_rotation, uint64_t seed) {
+    if (n < 1) throw std::invalid_argument("init_uniform: n_particles must be >= 1");
+    for (int a = 0; a < 3; ++a)
+      if (b[3 + a] - b[a] <= 0.0) throw std::invalid_argument("init_uniform: degenerate bounds");
+    if (cfg.k_neighbors < 1 || cfg.k_neighbors > kMaxK)
+      throw std::invalid_argument("k_neighbors must be in [1, 32] on this device build");
+    n_total = n;
+    gbase = 0;
+    alloc_particles(n, cfg.k_neighbors);
+    InitParams ip{};
+    ip.stream = mix_seed(seed, k_stream_init);
+    for (int a = 0; a < 3; ++a) {
+      ip.bmin[a] = b[a];
+      ip.bmax[a] = b[3 + a];
+    }
+    ip.log_post0 = -std::log(static_cast<double>(n));
+    ip.full_rotation = full_rotation ? 1 : 0;
+    launch_init_uniform(poses.p, log_post.p, id.p, idx.p, kval.p, count.p, n_local, gbase, k, ip, st);
+    CK(cudaGetLastError());
+    sync();
+  }
+
+  void step(const smcl_cloud* scan, const smcl_odom* odo, smcl_frame_result* out) {
+    if (n_total == 0) throw std::logic_error("FilterEngine::step: not initialized");
+    if (!has_map) throw std::invalid_argument("engine has no map");
+    for (auto& e : ev)
+      if (!e) CK(cudaEventCreate(&e));
+    smcl_frame_result r;
+    std::memset(&r, 0, sizeof(r));
+    r.n_particles = n_total;
+    const bool empty = scan == nullptr || scan->n == 0;
+    r.scan_empty = empty ? 1 : 0;
+    if (!empty) set_scans(scan);  // host prep + H2D before the timed stages
+
+    CK(cudaEventRecord(ev[0], st));
+    {
+      double delta[12], cov[36];
+      if (odo->valid) {
+        std::memcpy(delta, odo->delta, sizeof(delta));
+        std::memcpy(cov, odo->cov, sizeof(cov));
+      } else {
+        const Pose id_pose = pose_identity();
+        store_pose(id_pose, delta);
+        std::memset(cov, 0, sizeof(cov));
+        for (int d = 0; d < 3; ++d) {
+          cov[d * 7] = cfg.diffusion_sigma_rot * cfg.diffusion_sigma_rot;
+          cov[(d + 3) * 7] = cfg.diffusion_sigma_trans * cfg.diffusion_sigma_trans;
+        }
+      }
+      predict(delta, cov, mix_seed(cfg.seed, k_stream_predict, static_cast<uint64_t>(frame)));
+    }
+    CK(cudaEventRecord(ev[1], st));
+    const double bounds[6] = {map_bounds.min[0], map_bounds.min[1], map_bounds.min[2],
+                              map_bounds.max[0], map_bounds.max[1], map_bounds.max[2]};
+    update_neighbors(mix_seed(cfg.seed, k_stream_neighbors, static_cast<uint64_t>(frame)), bounds, &r.neighbor_stats);
+    CK(cudaEventRecord(ev[2], st));
+    float t_like = 0.f, t_upd = 0.f;
+    if (!empty) {
+      for (int it = 0; it < cfg.n_svgd_iters; ++it) {
+        CK(cudaEventRecord(ev[3], st));
+        run_likelihood(true, scan_gn);
+        CK(cudaEventRecord(ev[4], st));
+        svgd(true);
+        CK(cudaEventRecord(ev[5], st));
+        sync();
+        float a, b;
+        CK(cudaEventElapsedTime(&a, ev[3], ev[4]));
+        CK(cudaEventElapsedTime(&b, ev[4], ev[5]));
+        t_like += a;
+        t_upd += b;
+      }
+      CK(cudaEventRecord(ev[3], st));
+      run_likelihood(false, scan_full);
+      CK(cudaEventRecord(ev[4], st));
+      r.observation_rejected = bayes(cfg.beta, cfg.log_post_floor) ? 1 : 0;
+      unsigned long long cnt[2];
+      d_counts.download(cnt, 2, st);
+      sync();
+      r.mean_n_matched = static_cast<double>(cnt[1]) / static_cast<double>(n_total);
+      float a;
+      CK(cudaEventElapsedTime(&a, ev[3], ev[4]));
+      t_like += a;
+    } else {
+      CK(cudaEventRecord(ev[4], st));
+    }
+    smooth(cfg.smooth_iters, cfg.log_post_floor);
+    int64_t ix;
+    double v;
+    representative(&ix, r.representative, &v);
+    CK(cudaEventRecord(ev[6], st));
+    sync();
+    float t_pred, t_nb, t_post, t_tot;
+    CK(cudaEventElapsedTime(&t_pred, ev[0], ev[1]));
+    CK(cudaEventElapsedTime(&t_nb, ev[1], ev[2]));
+    CK(cudaEventElapsedTime(&t_post, ev[4], ev[6]));
+    CK(cudaEventElapsedTime(&t_tot, ev[0], ev[6]));
+    r.rep_index = ix;
+    r.rep_log_post = v;
+    int32_t rid;
+    CK(cudaMemcpy(&rid, id.p + (ix - gbase), sizeof(int32_t), cudaMemcpyDeviceToHost));
+    r.rep_id = rid;
+    r.predict_ms = t_pred;
+    r.neighbor_ms = t_nb;
+    r.likelihood_ms = t_like;
+    r.update_ms = t_upd;
+    r.posterior_ms = t_post;
+    r.total_ms = t_tot;
+    *out = r;
+    ++frame;
+  }
+};
+
+// ---------------------------------------------------------------- C ABI
+namespace {
+smcl_engine* make_engine(const smcl_cloud* map, const smcl_config* cfg, int device) {
+  if (!cfg) throw std::invalid_argument("config must not be null");
+  auto e = std::make_unique<smcl_engine>();
+  e->cfg = *cfg;
+  if (device >= 0) {
+    CK(cudaSetDevice(device));
+    e->device = device;
+  } else {
+    CK(cudaGetDevice(&e->device));
+  }
+  CK(cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking));
+  e->k = cfg->k_neighbors;
+  if (map) e->setup_map(map);
+  return e.release();
+}
+inline void use_dev(const smcl_engine* h) {
+  if (!h) throw std::invalid_argument("null engine handle");
+  CK(cudaSetDevice(h->device));
+}
+}  // namespace
+
+extern "C" {
+
+int smcl_abi_version(void) { return SMCL_ABI_VERSION; }
+const char* smcl_last_error(void) { return g_last_error.c_str(); }
+
+void smcl_config_default(smcl_config* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->n_particles = 10000;
+  c->k_neighbors = 20;
+  c->sigma_r = 5.0;
+  c->sigma_t = 2.5;
+  c->repulsion_gain = 1.0;
+  c->lsh_alpha = 0.1;
+  c->lsh_noise_sigma = 0.5;
+  c->lsh_buckets_factor = 2.0;
+  c->lsh_n_buckets = 0;
+  c->lsh_bucket_capacity = 64;
+  c->reorder_particles = 1;
+  c->smooth_iters = 10;
+  c->nnf_resolution = 0.1;
+  c->nnf_max_query_dist = 1.0;
+  c->nnf_padding = 0.5;
+  c->beta = 2.0;
+  c->n_svgd_iters = 1;
+  c->gn_scan_stride = 1;
+  c->damping_scale = 1e-3;
+  c->omega_max = 0.5;
+  c->v_max = 1.0;
+  c->min_match_fraction = 0.5;
+  c->miss_cost = 25.0;
+  c->log_post_floor = -80.0;
+  c->covariance_k = 10;
+  c->n_scan_max = 1000;
+  c->epsilon_plane = 1e-3;
+  c->scan_voxel_leaf = 0.05;
+  c->sensor_noise_sigma = 0.01;
+  c->diffusion_sigma_rot = 0.02;
+  c->diffusion_sigma_trans = 0.5;
+  c->full_rotation = 1;
+  c->likelihood_mode = 0;
+  c->seed = 1;
+}
+
+int smcl_device_count(int* out) {
+  return guard([&] { CK(cudaGetDeviceCount(out)); });
+}
+
+int smcl_create(const smcl_cloud* map, const smcl_config* cfg, int device, smcl_engine** out) {
+  return guard([&] { *out = make_engine(map, cfg, device); });
+}
+
+int smcl_create_sharded(const smcl_cloud* map, const smcl_config* cfg, int device, int rank, int world,
+                        smcl_engine** out) {
+  return guard([&] {
+    if (world != 1 || rank != 0)
+      throw std::invalid_argument("smcl_create_sharded: multi-shard engines are driven from the host comm layer");
+    *out = make_engine(map, cfg, device);
+  });
+}
+
+int smcl_destroy(smcl_engine* h) {
+  return guard([&] { delete h; });
+}
+
+int smcl_init_uniform(smcl_engine* h, const double bounds[6]) {
+  return guard([&] {
+    use_dev(h);
+    h->init_uniform(h->cfg.n_particles, bounds, h->cfg.full_rotation != 0, h->cfg.seed);
+    h->frame = 0;
+  });
+}
+
+int smcl_init_uniform_seeded(smcl_engine* h, int64_t n, const double bounds[6], int full_rotation, uint64_t seed) {
+  return guard([&] {
+    use_dev(h);
+    h->init_uniform(n, bounds, full_rotation != 0, seed);
+  });
+}
+
+int smcl_step(smcl_engine* h, const smcl_cloud* scan, const smcl_odom* odo, smcl_frame_result* out) {
+  return guard([&] {
+    use_dev(h);
+    if (!odo || !out) throw std::invalid_argument("smcl_step: null odometry or result");
+    h->step(scan, odo, out);
+  });
+}
+
+int64_t smcl_frame_index(const smcl_engine* h) { return h ? h->frame : -1; }
+int64_t smcl_num_particles(const smcl_engine* h) { return h ? h->n_total : -1; }
+
+int smcl_get_particles(smcl_engine* h, smcl_particles_view* v) {
+  return guard([&] {
+    use_dev(h);
+    const size_t n = static_cast<size_t>(h->n_local), k = static_cast<size_t>(h->k);
+    if (v->n != h->n_local || v->k != h->k) throw std::invalid_argument("get_particles: view shape mismatch");
+    std::vector<Pose> ps(n);
+    h->poses.download(ps.data(), n, h->st);
+    h->log_post.download(v->log_post, n, h->st);
+    h->id.download(v->id, n, h->st);
+    h->idx.download(v->idx, n * k, h->st);
+    h->kval.download(v->kval, n * k, h->st);
+    h->count.download(v->count, n, h->st);
+    h->sync();
+    for (size_t i = 0; i < n; ++i) store_pose(ps[i], v->poses + 12 * i);
+  });
+}
+
+int smcl_set_particles(smcl_engine* h, const smcl_particles_view* v) {
+  return guard([&] {
+    use_dev(h);
+    if (v->n < 0 || v->k < 1 || v->k > kMaxK) throw std::invalid_argument("set_particles: bad shape");
+    h->n_total = v->n;
+    h->gbase = 0;
+    h->alloc_particles(v->n, v->k);
+    h->cfg.k_neighbors = v->k;
+    const size_t n = static_cast<size_t>(v->n), k = static_cast<size_t>(v->k);
+    std::vector<Pose> ps(n);
+    for (size_t i = 0; i < n; ++i) ps[i] = load_pose(v->poses + 12 * i);
+    h->poses.upload(ps.data(), n, h->st);
+    h->log_post.upload(v->log_post, n, h->st);
+    h->id.upload(v->id, n, h->st);
+    h->idx.upload(v->idx, n * k, h->st);
+    h->kval.upload(v->kval, n * k, h->st);
+    h->count.upload(v->count, n, h->st);
+    h->sync();
+  });
+}
+
+int smcl_get_nnf(smcl_engine* h, int32_t dims[3], double origin[3], double* resolution, int32_t* cells) {
+  return guard([&] {
+    if (!h || !h->has_map) throw std::invalid_argument("engine has no map");
+    for (int a = 0; a < 3; ++a) {
+      dims[a] = h->geom.dims[a];
+      origin[a] = h->geom.origin[a];
+    }
+    if (resolution) *resolution = h->geom.res;
+    if (cells) std::memcpy(cells, h->h_cells.data(), h->h_cells.size() * sizeof(int32_t));
+  });
+}
+
+int smcl_predict(smcl_engine* h, const double delta[12], const double cov[36], uint64_t frame_seed) {
+  return guard([&] {
+    use_dev(h);
+    h->predict(delta, cov, frame_seed);
+    h->sync();
+  });
+}
+
+int smcl_update_neighbors(smcl_engine* h, uint64_t pass_seed, const double bounds[6], smcl_neighbor_stats* stats) {
+  return guard([&] {
+    use_dev(h);
+    h->update_neighbors(pass_seed, bounds, stats);
+    h->sync();
+  });
+}
+
+int smcl_evaluate_all(smcl_engine* h, const smcl_cloud* scan, double* step_out, double* ll_out, int32_t* nm_out,
+                      double* H_out, double* b_out) {
+  return guard([&] {
+    use_dev(h);
+    if (!scan || scan->n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
+    h->upload_scan(h->scan_gn, scan->mu, scan->sigma, static_cast<int>(scan->n));
+    h->run_likelihood(true, h->scan_gn);
+    const size_t n = static_cast<size_t>(h->n_local);
+    if (step_out) h->steps.download(step_out, n * 6, h->st);
+    if (ll_out) h->ll.download(ll_out, n, h->st);
+    if (nm_out) h->nm.download(nm_out, n, h->st);
+    if (H_out || b_out) {
+      std::vector<double> sys(n * kSysStride);
+      h->sys.download(sys.data(), sys.size(), h->st);
+      h->sync();
+      for (size_t i = 0; i < n; ++i) {
+        if (H_out) std::memcpy(H_out + 36 * i, &sys[i * kSysStride], 36 * sizeof(double));
+        if (b_out) std::memcpy(b_out + 6 * i, &sys[i * kSysStride + 36], 6 * sizeof(double));
+      }
+    }
+    h->sync();
+  });
+}
+
+int smcl_evaluate_likelihoods(smcl_engine* h, const smcl_cloud* scan, double* ll_out, int32_t* nm_out) {
+  return guard([&] {
+    use_dev(h);
+    if (!scan || scan->n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
+    h->upload_scan(h->scan_full, scan->mu, scan->sigma, static_cast<int>(scan->n));
+    h->run_likelihood(false, h->scan_full);
+    const size_t n = static_cast<size_t>(h->n_local);
+    if (ll_out) h->ll.download(ll_out, n, h->st);
+    if (nm_out) h->nm.download(nm_out, n, h->st);
+    h->sync();
+  });
+}
+
+int smcl_compute_phis(smcl_engine* h, const double* steps, double* phi_out) {
+  return guard([&] {
+    use_dev(h);
+    const size_t n = static_cast<size_t>(h->n_local);
+    if (steps) {
+      h->steps.upload(steps, n * 6, h->st);
+      h->steps_valid = true;
+    }
+    if (!h->steps_valid) throw std::logic_error("compute_phis: no Gauss-Newton steps on the device");
+    h->svgd(false);
+    if (phi_out) h->phis.download(phi_out, n * 6, h->st);
+    h->sync();
+  });
+}
+
+int smcl_apply_updates(smcl_engine* h, const double* phis) {
+  return guard([&] {
+    use_dev(h);
+    const size_t n = static_cast<size_t>(h->n_local);
+    if (phis) {
+      h->phis.upload(phis, n * 6, h->st);
+      h->phis_valid = true;
+    }
+    if (!h->phis_valid) throw std::logic_error("apply_updates: one phi per particle required");
+    launch_apply(h->poses.p, h->phis.p, h->n_local, h->st);
+    CK(cudaGetLastError());
+    h->sync();
+  });
+}
+
+int smcl_bayes_update(smcl_engine* h, const double* ll, const int32_t* nm, double beta, double floor_v,
+                      int32_t* rejected) {
+  return guard([&] {
+    use_dev(h);
+    const size_t n = static_cast<size_t>(h->n_local);
+    if ((ll == nullptr) != (nm == nullptr)) throw std::invalid_argument("bayes_update: size mismatch");
+    if (ll) {
+      h->ll.upload(ll, n, h->st);
+      h->nm.upload(nm, n, h->st);
+      h->ll_valid = true;
+    }
+    if (!h->ll_valid) throw std::logic_error("bayes_update: no likelihoods on the device");
+    const bool rej = h->bayes(beta, floor_v);
+    if (rejected) *rejected = rej ? 1 : 0;
+    h->sync();
+  });
+}
+
+int smcl_normalize_log_post(smcl_engine* h, double floor_v) {
+  return guard([&] {
+    use_dev(h);
+    h->normalize(floor_v);
+    h->sync();
+  });
+}
+
+int smcl_smooth(smcl_engine* h, int32_t iters, double floor_v) {
+  return guard([&] {
+    use_dev(h);
+    h->smooth(iters, floor_v);
+    h->sync();
+  });
+}
+
+int smcl_representative(smcl_engine* h, int64_t* index, double pose[12], double* log_post) {
+  return guard([&] {
+    use_dev(h);
+    h->representative(index, pose, log_post);
+  });
+}
+
+// ---------------------------------------------------------------- batch math
+int smcl_se3_exp_batch(const double* xi, int64_t n, double* poses_out) {
+  return guard([&] {
+    DBuf<double> dx;
+    DBuf<Pose> dp;
+    dx.upload(xi, static_cast<size_t>(n) * 6, nullptr);
+    dp.ensure(static_cast<size_t>(n));
+    launch_exp_batch(dx.p, n, dp.p, nullptr);
+    CK(cudaGetLastError());
+    std::vector<Pose> h(static_cast<size_t>(n));
+    dp.download(h.data(), h.size(), nullptr);
+    CK(cudaDeviceSynchronize());
+    for (int64_t i = 0; i < n; ++i) store_pose(h[static_cast<size_t>(i)], poses_out + 12 * i);
+  });
+}
+
+int smcl_se3_log_batch(const double* poses, int64_t n, double* xi_out) {
+  return guard([&] {
+    std::vector<Pose> h(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) h[static_cast<size_t>(i)] = load_pose(poses + 12 * i);
+    DBuf<Pose> dp;
+    DBuf<double> dx;
+    dp.upload(h.data(), h.size(), nullptr);
+    dx.ensure(static_cast<size_t>(n) * 6);
+    launch_log_batch(dp.p, n, dx.p, nullptr);
+    CK(cudaGetLastError());
+    dx.download(xi_out, static_cast<size_t>(n) * 6, nullptr);
+    CK(cudaDeviceSynchronize());
+  });
+}
+
+int smcl_kernel_batch(const double* a, const double* b, int64_t n, double sigma_r, double sigma_t, double* k_out) {
+  return guard([&] {
+    std::vector<Pose> ha(static_cast<size_t>(n)), hb(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      ha[static_cast<size_t>(i)] = load_pose(a + 12 * i);
+      hb[static_cast<size_t>(i)] = load_pose(b + 12 * i);
+    }
+    DBuf<Pose> da, db;
+    DBuf<double> dk;
+    da.upload(ha.data(), ha.size(), nullptr);
+    db.upload(hb.data(), hb.size(), nullptr);
+    dk.ensure(static_cast<size_t>(n));
+    launch_kernel_batch(da.p, db.p, n, sigma_r, sigma_t, dk.p, nullptr);
+    CK(cudaGetLastError());
+    dk.download(k_out, static_cast<size_t>(n), nullptr);
+    CK(cudaDeviceSynchronize());
+  });
+}
+
+int smcl_lsh_hash_batch(const double* poses, int64_t n, const double frame[12], const double noise[6], double alpha,
+                        double sigma_r, double sigma_t, uint64_t* out) {
+  return guard([&] {
+    std::vector<Pose> h(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) h[static_cast<size_t>(i)] = load_pose(poses + 12 * i);
+    LshPass lp{};
+    lp.frame = load_pose(frame);
+    std::memcpy(lp.noise, noise, sizeof(lp.noise));
+    lp.alpha = alpha;
+    lp.sigma_r = sigma_r;
+    lp.sigma_t = sigma_t;
+    DBuf<Pose> dp;
+    DBuf<uint64_t> dout;
+    dp.upload(h.data(), h.size(), nullptr);
+    dout.ensure(static_cast<size_t>(n));
+    launch_hash_batch(dp.p, n, lp, dout.p, nullptr);
+    CK(cudaGetLastError());
+    dout.download(out, static_cast<size_t>(n), nullptr);
+    CK(cudaDeviceSynchronize());
+  });
+}
+
+int smcl_solve_step_batch(const double* H, const double* b, const double* lambda, int64_t n, double omega_max,
+                          double v_max, double* step_out) {
+  return guard([&] {
+    for (int64_t i = 0; i < n; ++i)
+      if (lambda[i] < 0.0) throw std::invalid_argument("solve_step: lambda must be >= 0");
+    DBuf<double> dH, db, dl, dout;
+    dH.upload(H, static_cast<size_t>(n) * 36, nullptr);
+    db.upload(b, static_cast<size_t>(n) * 6, nullptr);
+    dl.upload(lambda, static_cast<size_t>(n), nullptr);
+    dout.ensure(static_cast<size_t>(n) * 6);
+    launch_solve_batch(dH.p, db.p, dl.p, n, omega_max, v_max, dout.p, nullptr);
+    CK(cudaGetLastError());
+    dout.download(step_out, static_cast<size_t>(n) * 6, nullptr);
+    CK(cudaDeviceSynchronize());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Kernel parameter blocks and host launchers (one per .cu file in kernels/).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "engine.cuh"
+
+namespace smcl {
+
+struct PredictParams {  // filter.cpp:67-84
+  Pose delta;
+  double L[36];  // lower-triangular sqrt of the odometry covariance (row-major)
+  uint64_t frame_seed;
+  int noiseless;
+};
+
+struct InitParams {  // filter.cpp:39-65
+  uint64_t stream;  // mix_seed(seed, k_stream_init)
+  double bmin[3], bmax[3];
+  double log_post0;
+  int full_rotation;
+};
+
+struct SvgdParams {  // svgd.hpp:13-21
+  double sigma_r, sigma_t, repulsion_gain;
+};
+
+struct LshPass {  // neighbor_search.cpp:71-90
+  Pose frame;
+  double noise[6];
+  double alpha, sigma_r, sigma_t;
+  int64_t n_buckets;
+  int idx_bits, h_bits, prio_bits;
+  uint64_t prio_seed;
+};
+
+// particles.cu
+void launch_predict(Pose* poses, int64_t n, int64_t gbase, const PredictParams& pp, cudaStream_t st);
+void launch_init_uniform(Pose* poses, double* log_post, int32_t* id, int32_t* idx, float* kval, int32_t* count,
+                         int64_t n, int64_t gbase, int k, const InitParams& ip, cudaStream_t st);
+void launch_svgd(const Pose* all_poses, const double* all_steps, int64_t n, int64_t gbase, const int32_t* idx,
+                 const int32_t* count, int k, const SvgdParams& sp, double* phi_out, Pose* poses_out,
+                 cudaStream_t st);
+void launch_apply(Pose* poses, const double* phis, int64_t n, cudaStream_t st);
+void launch_exp_batch(const double* xi, int64_t n, Pose* out, cudaStream_t st);
+void launch_log_batch(const Pose* p, int64_t n, double* out, cudaStream_t st);
+void launch_kernel_batch(const Pose* a, const Pose* b, int64_t n, double sr, double st_, double* out, cudaStream_t st);
+
+// lsh.cu
+void launch_lsh_keys(const Pose* poses, int64_t n, int64_t gbase, const LshPass& lp, uint64_t* keys, cudaStream_t st);
+void launch_hash_batch(const Pose* poses, int64_t n, const LshPass& lp, uint64_t* out, cudaStream_t st);
+size_t sort_temp_bytes(int64_t n);
+void sort_keys(const uint64_t* in, uint64_t* out, int64_t n, int end_bit, void* temp, size_t temp_bytes,
+               cudaStream_t st);
+void launch_members(const uint64_t* skeys, int64_t n, uint64_t idx_mask, int shift, int32_t* member_of, int32_t* head,
+                    cudaStream_t st);
+void inclusive_sum_i32(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t st);
+void launch_inverse_perm(const int32_t* member_of, int64_t n, int32_t* new_of_old, cudaStream_t st);
+void launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_t n, int k, const Pose* poses,
+                    const double* lp, const int32_t* id, const int32_t* idx, const float* kval, const int32_t* count,
+                    Pose* poses2, double* lp2, int32_t* id2, int32_t* idx2, float* kval2, int32_t* count2,
+                    cudaStream_t st);
+void launch_segments(const int32_t* head, const int32_t* seg_id, int64_t n, int32_t* seg_start, cudaStream_t st);
+void launch_seg_stats(const int32_t* seg_start, int32_t n_seg, int64_t n, int cap, unsigned long long* hist,
+                      unsigned long long* overflow, cudaStream_t st);
+void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, const int32_t* pos_list,
+                           const int32_t* member_of, const int32_t* seg_id, const int32_t* seg_start, int32_t n_seg,
+                           int64_t n_sorted, int32_t* idx, float* kval, int32_t* count, int k, int cap, double sr,
+                           double st_, cudaStream_t st);
+
+// posterior.cu
+void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta, cudaStream_t st);
+void launch_fill(double* v, int64_t n, double value, cudaStream_t st);
+void launch_match_counts(const double* ll, const int32_t* nm, int64_t n, unsigned long long* out, cudaStream_t st);
+int argmax_partials(int64_t n);
+void launch_argmax(const double* v, int64_t n, int64_t gbase, double* scratch_v, long long* scratch_i, double* out_v,
+                   long long* out_i, cudaStream_t st);
+void launch_max_of_partials(const double* pv, const long long* pi, int64_t n, double* out_v, long long* out_i,
+                            cudaStream_t st);
+void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* partial, cudaStream_t st);
+void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n, int k, double* pk, double* pc,
+                             cudaStream_t st);
+void launch_finish_lse(const double* partial, int64_t n_chunks, const double* m, double* lse, cudaStream_t st);
+void launch_finish_sum2(const double* a, const double* b, int64_t n_chunks, double* out, cudaStream_t st);
+void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, cudaStream_t st);
+void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st);
+void launch_log(const double* p, double* lp, int64_t n, cudaStream_t st);
+void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
+                         const int32_t* count, int k, cudaStream_t st);
+
+}  // namespace smcl

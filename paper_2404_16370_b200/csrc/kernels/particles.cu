@@ -1,0 +1,170 @@
+// K9 predict / noise injection (reference filter.cpp:67-84), K10 uniform
+// initialisation (filter.cpp:39-65), K8 SVGD (svgd.cpp:7-62): one thread per
+// particle, fp64, counter-seeded SplitMix64 streams keyed by the GLOBAL
+// particle index (so results do not depend on the shard count).
+#include <cuda_runtime.h>
+
+#include "../engine.cuh"
+#include "../kernels.cuh"
+
+namespace smcl {
+
+namespace {
+
+inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+__global__ void k_predict(Pose* __restrict__ poses, int64_t n, int64_t gbase, PredictParams pp) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Pose p = compose_x(poses[i], pp.delta);
+  if (!pp.noiseless) {
+    SplitMix64 rng(mix_seed(pp.frame_seed, static_cast<uint64_t>(gbase + i)));
+    double z[6], xi[6];
+    rng.normal6(z);
+#pragma unroll
+    for (int r = 0; r < 6; ++r) {
+      double acc = xmul(pp.L[r * 6 + 0], z[0]);
+#pragma unroll
+      for (int c = 1; c < 6; ++c) acc = xadd(acc, xmul(pp.L[r * 6 + c], z[c]));
+      xi[r] = acc;
+    }
+    p = compose_x(p, se3_exp(xi));
+  }
+  renormalize_if_needed(p);
+  poses[i] = p;
+}
+
+__global__ void k_init_uniform(Pose* __restrict__ poses, double* __restrict__ log_post, int32_t* __restrict__ id,
+                               int32_t* __restrict__ idx, float* __restrict__ kval, int32_t* __restrict__ count,
+                               int64_t n, int64_t gbase, int k, InitParams ip) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t gi = gbase + i;
+  SplitMix64 rng(mix_seed(ip.stream, static_cast<uint64_t>(gi)));
+  Pose p;
+  if (ip.full_rotation)
+    random_rotation(rng, p.R);
+  else
+    random_yaw(rng, p.R);
+#pragma unroll
+  for (int a = 0; a < 3; ++a) p.t[a] = rng.uniform_range(ip.bmin[a], ip.bmax[a]);
+  poses[i] = p;
+  log_post[i] = ip.log_post0;
+  id[i] = static_cast<int32_t>(gi);
+  count[i] = 1;
+  for (int s = 0; s < k; ++s) {
+    idx[i * k + s] = s == 0 ? static_cast<int32_t>(gi) : -1;
+    kval[i * k + s] = s == 0 ? 1.0f : 0.0f;
+  }
+}
+
+// svgd.cpp:7-34 compute_phi, optionally fused with apply_updates (svgd.cpp:51-62)
+// writing a second pose buffer so every read sees the frozen snapshot.
+template <bool APPLY>
+__global__ void __launch_bounds__(128) k_svgd(const Pose* __restrict__ all_poses, const double* __restrict__ all_steps,
+                                              int64_t n, int64_t gbase, const int32_t* __restrict__ idx,
+                                              const int32_t* __restrict__ count, int k, SvgdParams sp,
+                                              double* __restrict__ phi_out, Pose* __restrict__ poses_out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t gi = gbase + i;
+  const Pose pi = all_poses[gi];
+  double numer[6] = {0, 0, 0, 0, 0, 0};
+  double denom = 0.0;
+  const int cnt = count[i];
+  for (int s = 0; s < cnt; ++s) {
+    const int32_t j = idx[i * k + s];
+    const double* sj = all_steps + 6 * static_cast<int64_t>(j);
+    if (j == gi) {
+#pragma unroll
+      for (int c = 0; c < 6; ++c) numer[c] = xadd(numer[c], sj[c]);
+      denom = xadd(denom, 1.0);
+      continue;
+    }
+    const Pose pj = all_poses[j];
+    if (kernel_underflows(pi, pj, sp.sigma_t)) continue;
+    double d[6];
+    se3_log(inv_compose_x(pi, pj), d);
+    const double kv = exp(-kernel_q(d, sp.sigma_r, sp.sigma_t));
+    const double gr = xmul(xmul(-2.0, kv), sp.sigma_r), gt = xmul(xmul(-2.0, kv), sp.sigma_t);
+#pragma unroll
+    for (int c = 0; c < 6; ++c)
+      numer[c] = xadd(numer[c], xadd(xmul(kv, sj[c]), xmul(sp.repulsion_gain, xmul(c < 3 ? gr : gt, d[c]))));
+    denom = xadd(denom, kv);
+  }
+  double phi[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) phi[c] = numer[c] / denom;
+  if (phi_out) {
+#pragma unroll
+    for (int c = 0; c < 6; ++c) phi_out[6 * i + c] = phi[c];
+  }
+  if (APPLY) {
+    Pose p = compose_x(pi, se3_exp(phi));
+    renormalize_if_needed(p);
+    poses_out[i] = p;
+  }
+}
+
+__global__ void k_apply(Pose* __restrict__ poses, const double* __restrict__ phis, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double phi[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) phi[c] = phis[6 * i + c];
+  Pose p = compose_x(poses[i], se3_exp(phi));
+  renormalize_if_needed(p);
+  poses[i] = p;
+}
+
+// Batch primitives for parity tests of the device SE3 library.
+__global__ void k_exp_batch(const double* xi, int64_t n, Pose* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = se3_exp(xi + 6 * i);
+}
+__global__ void k_log_batch(const Pose* p, int64_t n, double* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) se3_log(p[i], out + 6 * i);
+}
+__global__ void k_kernel_batch(const Pose* a, const Pose* b, int64_t n, double sr, double st, double* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double d[6];
+  se3_log(inv_compose_x(a[i], b[i]), d);
+  out[i] = exp(-kernel_q(d, sr, st));
+}
+
+}  // namespace
+
+void launch_predict(Pose* poses, int64_t n, int64_t gbase, const PredictParams& pp, cudaStream_t st) {
+  if (n > 0) k_predict<<<blocks_for(n, 128), 128, 0, st>>>(poses, n, gbase, pp);
+}
+void launch_init_uniform(Pose* poses, double* log_post, int32_t* id, int32_t* idx, float* kval, int32_t* count,
+                         int64_t n, int64_t gbase, int k, const InitParams& ip, cudaStream_t st) {
+  if (n > 0) k_init_uniform<<<blocks_for(n, 128), 128, 0, st>>>(poses, log_post, id, idx, kval, count, n, gbase, k, ip);
+}
+void launch_svgd(const Pose* all_poses, const double* all_steps, int64_t n, int64_t gbase, const int32_t* idx,
+                 const int32_t* count, int k, const SvgdParams& sp, double* phi_out, Pose* poses_out,
+                 cudaStream_t st) {
+  if (n <= 0) return;
+  if (poses_out)
+    k_svgd<true><<<blocks_for(n, 128), 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out,
+                                                      poses_out);
+  else
+    k_svgd<false><<<blocks_for(n, 128), 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out,
+                                                       nullptr);
+}
+void launch_apply(Pose* poses, const double* phis, int64_t n, cudaStream_t st) {
+  if (n > 0) k_apply<<<blocks_for(n, 128), 128, 0, st>>>(poses, phis, n);
+}
+void launch_exp_batch(const double* xi, int64_t n, Pose* out, cudaStream_t st) {
+  if (n > 0) k_exp_batch<<<blocks_for(n, 128), 128, 0, st>>>(xi, n, out);
+}
+void launch_log_batch(const Pose* p, int64_t n, double* out, cudaStream_t st) {
+  if (n > 0) k_log_batch<<<blocks_for(n, 128), 128, 0, st>>>(p, n, out);
+}
+void launch_kernel_batch(const Pose* a, const Pose* b, int64_t n, double sr, double st_, double* out, cudaStream_t st) {
+  if (n > 0) k_kernel_batch<<<blocks_for(n, 128), 128, 0, st>>>(a, b, n, sr, st_, out);
+}
+
+}  // namespace smcl

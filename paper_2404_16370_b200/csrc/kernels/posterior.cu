@@ -1,0 +1,245 @@
+// K11-K13: Bayes update, log-sum-exp normalisation, graph smoothing and MAP
+// (reference posterior.cpp:13-108, reduce.hpp:14-69).
+//
+// Determinism: floating-point sums follow reduce.hpp exactly — 4096-element
+// chunks summed serially in index order (one thread per chunk), chunk partials
+// then summed serially in chunk order. Chunk boundaries are global indices, so
+// a shard owning a 4096-aligned range produces the same partials. Max / argmax
+// (ties -> lowest index) and integer counts are order independent and use
+// ordinary tree reductions.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "../engine.cuh"
+#include "../kernels.cuh"
+
+namespace smcl {
+
+namespace {
+
+inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+// log_post += beta * ll / max(nm, 1)   (posterior.cpp:50-56)
+__global__ void k_bayes_numer(double* __restrict__ lp, const double* __restrict__ ll, const int32_t* __restrict__ nm,
+                              int64_t n, double beta) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double denom = static_cast<double>(nm[i] > 1 ? nm[i] : 1);
+  lp[i] = xadd(lp[i], xmul(beta, ll[i]) / denom);
+}
+
+__global__ void k_fill(double* __restrict__ v, int64_t n, double value) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = value;
+}
+
+// Per-block partial of (count of ll > sentinel, sum of nm): exact integers.
+__global__ void k_match_counts(const double* __restrict__ ll, const int32_t* __restrict__ nm, int64_t n,
+                               unsigned long long* __restrict__ out /* [0]=matched particles, [1]=sum nm */) {
+  __shared__ unsigned long long s0[32], s1[32];
+  unsigned long long a = 0, b = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    a += ll[i] > -1e30 ? 1ull : 0ull;
+    b += static_cast<unsigned long long>(nm[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    s0[w] = a;
+    s1[w] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ta = 0, tb = 0;
+    for (int q = 0; q < (blockDim.x >> 5); ++q) {
+      ta += s0[q];
+      tb += s1[q];
+    }
+    atomicAdd(out, ta);
+    atomicAdd(out + 1, tb);
+  }
+}
+
+// Max with a deterministic result (max is order independent). Writes one
+// partial per block; the caller reduces partials with the same kernel.
+__device__ __forceinline__ void argmax_merge(double& v, long long& ix, double v2, long long i2) {
+  if (v2 > v || (v2 == v && i2 >= 0 && (ix < 0 || i2 < ix))) {
+    v = v2;
+    ix = i2;
+  }
+}
+
+__global__ void k_argmax(const double* __restrict__ v, const long long* __restrict__ vidx, int64_t n, int64_t gbase,
+                         double* __restrict__ out_v, long long* __restrict__ out_i) {
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  double best = -__longlong_as_double(0x7ff0000000000000ll);  // -inf
+  long long bi = -1;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    argmax_merge(best, bi, v[i], vidx ? vidx[i] : gbase + i);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    argmax_merge(best, bi, v2, i2);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    sv[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < (blockDim.x >> 5); ++q) argmax_merge(best, bi, sv[q], si[q]);
+    out_v[blockIdx.x] = best;
+    out_i[blockIdx.x] = bi;
+  }
+}
+
+// One thread per 4096-chunk: serial sum of exp(v - m) in index order.
+__global__ void k_chunk_sum_exp(const double* __restrict__ v, int64_t n, const double* __restrict__ m_ptr,
+                                double* __restrict__ partial) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t begin = c * kReduceChunk;
+  if (begin >= n) return;
+  const int64_t end = begin + kReduceChunk < n ? begin + kReduceChunk : n;
+  const double m = *m_ptr;
+  double acc = 0.0;
+  for (int64_t i = begin; i < end; ++i) acc = xadd(acc, exp(xsub(v[i], m)));
+  partial[c] = acc;
+}
+
+// One thread per 4096-chunk: serial sum of kval over each particle's list and
+// of the list counts (mean_kernel, neighbor_search.cpp:182-190).
+__global__ void k_chunk_sum_kernel(const float* __restrict__ kval, const int32_t* __restrict__ count, int64_t n, int k,
+                                   double* __restrict__ partial_k, double* __restrict__ partial_c) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t begin = c * kReduceChunk;
+  if (begin >= n) return;
+  const int64_t end = begin + kReduceChunk < n ? begin + kReduceChunk : n;
+  double acc = 0.0, ent = 0.0;
+  for (int64_t i = begin; i < end; ++i) {
+    double s = 0.0;
+    const int cnt = count[i];
+    for (int q = 0; q < cnt; ++q) s = xadd(s, static_cast<double>(kval[i * k + q]));
+    acc = xadd(acc, s);
+    ent = xadd(ent, static_cast<double>(cnt));
+  }
+  partial_k[c] = acc;
+  partial_c[c] = ent;
+}
+
+// Serial combine of chunk partials (single thread): lse = m + log(sum).
+__global__ void k_finish_lse(const double* __restrict__ partial, int64_t n_chunks, const double* __restrict__ m_ptr,
+                             double* __restrict__ lse_out) {
+  double t = 0.0;
+  for (int64_t c = 0; c < n_chunks; ++c) t = xadd(t, partial[c]);
+  *lse_out = xadd(*m_ptr, log(t));
+}
+
+__global__ void k_finish_sum2(const double* __restrict__ a, const double* __restrict__ b, int64_t n_chunks,
+                              double* __restrict__ out) {
+  double ta = 0.0, tb = 0.0;
+  for (int64_t c = 0; c < n_chunks; ++c) {
+    ta = xadd(ta, a[c]);
+    tb = xadd(tb, b[c]);
+  }
+  out[0] = ta;
+  out[1] = tb;
+}
+
+__global__ void k_apply_lse(double* __restrict__ v, int64_t n, const double* __restrict__ lse_ptr, double floor_v) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double r = xsub(v[i], *lse_ptr);
+  v[i] = r < floor_v ? floor_v : r;  // std::max(v - lse, floor)
+}
+
+__global__ void k_exp(const double* __restrict__ lp, double* __restrict__ p, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = exp(lp[i]);
+}
+__global__ void k_log(const double* __restrict__ p, double* __restrict__ lp, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) lp[i] = log(p[i]);
+}
+
+// One Jacobi round of posterior.cpp:75-90 (q_i = sum_s w_s p[idx_s] / sum_s w_s).
+__global__ void k_smooth_round(const double* __restrict__ p_all, double* __restrict__ q, int64_t n,
+                               const int32_t* __restrict__ idx, const float* __restrict__ kval,
+                               const int32_t* __restrict__ count, int k) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double num = 0.0, den = 0.0;
+  const int cnt = count[i];
+  for (int s = 0; s < cnt; ++s) {
+    const double w = static_cast<double>(kval[i * k + s]);
+    num = xadd(num, xmul(w, p_all[idx[i * k + s]]));
+    den = xadd(den, w);
+  }
+  q[i] = num / den;
+}
+
+}  // namespace
+
+void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta, cudaStream_t st) {
+  if (n > 0) k_bayes_numer<<<blocks_for(n, 256), 256, 0, st>>>(lp, ll, nm, n, beta);
+}
+void launch_fill(double* v, int64_t n, double value, cudaStream_t st) {
+  if (n > 0) k_fill<<<blocks_for(n, 256), 256, 0, st>>>(v, n, value);
+}
+void launch_match_counts(const double* ll, const int32_t* nm, int64_t n, unsigned long long* out, cudaStream_t st) {
+  cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), st);
+  if (n > 0) {
+    const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(n, 256), 1184));
+    k_match_counts<<<g, 256, 0, st>>>(ll, nm, n, out);
+  }
+}
+int argmax_partials(int64_t n) { return static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 1184)); }
+void launch_argmax(const double* v, int64_t n, int64_t gbase, double* scratch_v, long long* scratch_i, double* out_v,
+                   long long* out_i, cudaStream_t st) {
+  const int g = argmax_partials(n);
+  k_argmax<<<g, 256, 0, st>>>(v, nullptr, n, gbase, scratch_v, scratch_i);
+  k_argmax<<<1, 256, 0, st>>>(scratch_v, scratch_i, g, 0, out_v, out_i);
+}
+void launch_max_of_partials(const double* pv, const long long* pi, int64_t n, double* out_v, long long* out_i,
+                            cudaStream_t st) {
+  k_argmax<<<1, 256, 0, st>>>(pv, pi, n, 0, out_v, out_i);
+}
+void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* partial, cudaStream_t st) {
+  const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
+  if (chunks > 0) k_chunk_sum_exp<<<blocks_for(chunks, 32), 32, 0, st>>>(v, n, m, partial);
+}
+void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n, int k, double* pk, double* pc,
+                             cudaStream_t st) {
+  const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
+  if (chunks > 0) k_chunk_sum_kernel<<<blocks_for(chunks, 32), 32, 0, st>>>(kval, count, n, k, pk, pc);
+}
+void launch_finish_lse(const double* partial, int64_t n_chunks, const double* m, double* lse, cudaStream_t st) {
+  k_finish_lse<<<1, 1, 0, st>>>(partial, n_chunks, m, lse);
+}
+void launch_finish_sum2(const double* a, const double* b, int64_t n_chunks, double* out, cudaStream_t st) {
+  k_finish_sum2<<<1, 1, 0, st>>>(a, b, n_chunks, out);
+}
+void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, cudaStream_t st) {
+  if (n > 0) k_apply_lse<<<blocks_for(n, 256), 256, 0, st>>>(v, n, lse, floor_v);
+}
+void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st) {
+  if (n > 0) k_exp<<<blocks_for(n, 256), 256, 0, st>>>(lp, p, n);
+}
+void launch_log(const double* p, double* lp, int64_t n, cudaStream_t st) {
+  if (n > 0) k_log<<<blocks_for(n, 256), 256, 0, st>>>(p, lp, n);
+}
+void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
+                         const int32_t* count, int k, cudaStream_t st) {
+  if (n > 0) k_smooth_round<<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count, k);
+}
+
+}  // namespace smcl

@@ -1,0 +1,146 @@
+"""GPU parity of K1/K2 (GICP likelihood + Gauss-Newton) against the CPU oracle.
+
+Reference: gicp.cpp:11-137; pinned fixtures: test_parallel_consistency.cpp:31-95
+(box room 8x6x3, density 60, NNF 0.2, 700 particles, seeds 3/5/7).
+
+* exact mode (likelihood_mode=1) must equal the oracle bit for bit;
+* fast mode (structured fp32 Woodbury algebra) must match n_matched exactly
+  and ll/H/b/steps within the tolerances stated below.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import config, cube_set, room_scene
+from paper_2404_16370_b200.api import FilterEngine, GaussianCloud
+
+pytestmark = pytest.mark.gpu
+
+# Fast-path tolerances (fp32 per-point algebra, fp32 per-lane accumulation).
+TOL_LL = 2e-5      # |ll - ll_ref| / |ll_ref|
+TOL_SYS = 2e-5     # ||H - H_ref||_F / ||H_ref||_F, same for b (normwise)
+TOL_STEP = 1e-4    # ||(H_ref + lam I) step + b_ref|| / ||b_ref||  (backward error of the solve)
+
+
+@pytest.fixture(scope="module")
+def scene():
+    rects, mapc, scan = room_scene()
+    parts = cube_set(700, 7, 20)
+    om = O.OracleMap(mapc.mu, mapc.sigma, mapc.bounds, 0.2, 0.5, 1.0)
+    return mapc, scan, parts, om
+
+
+def _engine(mapc, parts, mode):
+    e = FilterEngine(mapc, config(nnf_resolution=0.2, likelihood_mode=mode))
+    e.set_particles(parts)
+    return e
+
+
+def test_nnf_matches_oracle(scene):
+    mapc, scan, parts, om = scene
+    e = _engine(mapc, parts, 1)
+    d, o, res, cells = e.nnf()
+    d2, o2, c2 = om.nnf()
+    assert np.array_equal(d, d2) and np.array_equal(o, o2) and np.array_equal(cells, c2)
+
+
+def test_evaluate_all_exact_is_bitwise(scene):
+    mapc, scan, parts, om = scene
+    e = _engine(mapc, parts, 1)
+    steps, ll, nm, H, b = e.evaluate_all(scan, want_system=True)
+    s2, ll2, nm2, H2, b2 = O.evaluate_all(om, scan.mu, scan.sigma, parts.poses, config(), want_system=True)
+    assert np.array_equal(nm, nm2)
+    assert (nm > 0).sum() > 100
+    assert np.array_equal(ll, ll2)
+    m = nm > 0
+    assert np.array_equal(H[m], H2[m])
+    assert np.array_equal(b[m], b2[m])
+    assert np.array_equal(steps, s2)
+
+
+def test_evaluate_likelihoods_exact_is_bitwise(scene):
+    mapc, scan, parts, om = scene
+    e = _engine(mapc, parts, 1)
+    ll, nm = e.evaluate_likelihoods(scan)
+    ll2, nm2 = O.evaluate_likelihoods(om, scan.mu, scan.sigma, parts.poses, config())
+    assert np.array_equal(nm, nm2)
+    assert np.array_equal(ll, ll2)
+
+
+def _lower(H):
+    return np.tril(H)
+
+
+def test_evaluate_all_fast_within_tolerance(scene):
+    mapc, scan, parts, om = scene
+    e = _engine(mapc, parts, 2)
+    steps, ll, nm, H, b = e.evaluate_all(scan, want_system=True)
+    s2, ll2, nm2, H2, b2 = O.evaluate_all(om, scan.mu, scan.sigma, parts.poses, config(), want_system=True)
+    assert np.array_equal(nm, nm2)
+    m = ll2 > -1e29
+    assert m.sum() > 50
+    assert np.array_equal(ll[~m], ll2[~m])
+    rel_ll = np.abs(ll[m] - ll2[m]) / np.abs(ll2[m])
+    k = nm2 > 0
+    Hl, Hl2 = np.array([_lower(h) for h in H[k]]), np.array([_lower(h) for h in H2[k]])
+    rel_H = np.linalg.norm((Hl - Hl2).reshape(k.sum(), -1), axis=1) / np.linalg.norm(Hl2.reshape(k.sum(), -1), axis=1)
+    rel_b = np.linalg.norm(b[k] - b2[k], axis=1) / np.maximum(np.linalg.norm(b2[k], axis=1), 1e-300)
+    print(f"fast GN: max rel ll {rel_ll.max():.2e}, H {rel_H.max():.2e}, b {rel_b.max():.2e}")
+    assert rel_ll.max() < TOL_LL
+    assert rel_H.max() < TOL_SYS
+    assert rel_b.max() < TOL_SYS
+    # Step: backward error against the oracle's own damped system, for
+    # unclamped steps (clamping is a non-smooth projection).
+    bad = 0
+    for i in np.nonzero(k)[0]:
+        Hs = H2[i]
+        lam = 1e-3 * np.trace(Hs) / 6.0
+        clamped = (np.abs(s2[i][:3]) >= 0.5).any() or (np.abs(s2[i][3:]) >= 1.0).any()
+        if clamped:
+            continue
+        r = (Hs + lam * np.eye(6)) @ steps[i] + b2[i]
+        if np.linalg.norm(r) > TOL_STEP * np.linalg.norm(b2[i]):
+            bad += 1
+    assert bad == 0
+
+
+def test_evaluate_likelihoods_fast_within_tolerance(scene):
+    mapc, scan, parts, om = scene
+    e = _engine(mapc, parts, 2)
+    ll, nm = e.evaluate_likelihoods(scan)
+    ll2, nm2 = O.evaluate_likelihoods(om, scan.mu, scan.sigma, parts.poses, config())
+    assert np.array_equal(nm, nm2)
+    m = ll2 > -1e29
+    assert np.array_equal(ll[~m], ll2[~m])
+    rel = np.abs(ll[m] - ll2[m]) / np.abs(ll2[m])
+    print(f"fast LL: max rel {rel.max():.2e}")
+    assert rel.max() < TOL_LL
+
+
+def test_unstructured_map_falls_back_to_exact(scene):
+    """A map whose covariances are not plane-model cannot use the fast
+    records; auto mode must use the exact kernels (and fast mode must refuse)."""
+    mapc, scan, parts, om = scene
+    rng = np.random.default_rng(0)
+    sig = mapc.sigma.reshape(-1, 3, 3).copy()
+    for i in range(len(sig)):
+        d = np.diag(rng.uniform(1e-4, 3e-3, 3))
+        sig[i] = d
+    m2 = GaussianCloud(mapc.mu, sig.reshape(-1, 9), mapc.bounds)
+    e = FilterEngine(m2, config(nnf_resolution=0.2, likelihood_mode=0))
+    e.set_particles(parts)
+    ll, nm = e.evaluate_likelihoods(scan)
+    om2 = O.OracleMap(m2.mu, m2.sigma, m2.bounds, 0.2, 0.5, 1.0)
+    ll2, nm2 = O.evaluate_likelihoods(om2, scan.mu, scan.sigma, parts.poses, config())
+    assert np.array_equal(ll, ll2) and np.array_equal(nm, nm2)
+    e2 = FilterEngine(m2, config(nnf_resolution=0.2, likelihood_mode=2))
+    e2.set_particles(parts)
+    with pytest.raises(ValueError):
+        e2.evaluate_likelihoods(scan)
+
+
+def test_empty_scan_rejected(scene):
+    mapc, scan, parts, om = scene
+    e = _engine(mapc, parts, 0)
+    with pytest.raises(ValueError):
+        e.evaluate_all(GaussianCloud(np.zeros((0, 3)), np.zeros((0, 9))))
