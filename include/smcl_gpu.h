@@ -142,6 +142,30 @@ int smcl_init_uniform(smcl_engine* h, const double bounds[6]);
 int smcl_init_uniform_seeded(smcl_engine* h, int64_t n, const double bounds[6], int full_rotation, uint64_t seed);
 /* FilterEngine::step(scan, odo) (filter.cpp:118-213). scan->n == 0: empty scan. */
 int smcl_step(smcl_engine* h, const smcl_cloud* scan, const smcl_odom* odo, smcl_frame_result* out);
+/* Device-resident scans: smcl_scan_upload stages a prepared scan into one of
+ * SMCL_MAX_SCAN_SLOTS device slots; smcl_step_slot runs FilterEngine::step on
+ * it (no host->device scan copy inside the step). smcl_step == upload to slot 0
+ * + smcl_step_slot(0). */
+#define SMCL_MAX_SCAN_SLOTS 64
+int smcl_scan_upload(smcl_engine* h, int slot, const smcl_cloud* scan);
+int smcl_step_slot(smcl_engine* h, int slot, const smcl_odom* odo, smcl_frame_result* out);
+
+/* Per-kernel device times (CUDA events on the engine stream) of the last
+ * step, and the algorithmic work they processed. */
+typedef struct smcl_step_profile {
+  double predict_ms, lsh_keys_ms, sort_ms, reorder_ms, segments_ms, refresh_gather_ms, nb_stats_ms;
+  double gn_kernel_ms, solve_ms, svgd_ms, ll_kernel_ms, bayes_ms, smooth_ms, rep_ms, total_ms;
+  int64_t gn_points, ll_points;   /* particle-point evaluations in each pass */
+  int64_t gn_matched, ll_matched; /* matched particle-points in each pass */
+  int32_t fast_path, n_svgd_iters;
+  int64_t kernel_launches;        /* hand-written kernels launched by the step */
+  int64_t h2d_bytes, d2h_bytes;   /* host<->device bytes: last scan upload, step read-backs */
+} smcl_step_profile;
+int smcl_last_step_profile(smcl_engine* h, smcl_step_profile* out);
+/* Device timer on the engine stream (CUDA events): start, then stop returns
+ * the elapsed milliseconds of everything the engine ran in between. */
+int smcl_timer_start(smcl_engine* h);
+int smcl_timer_stop(smcl_engine* h, double* ms);
 int64_t smcl_frame_index(const smcl_engine* h);
 int64_t smcl_num_particles(const smcl_engine* h);
 

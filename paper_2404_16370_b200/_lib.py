@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 from .abi import (SmclCloud, SmclConfig, SmclCorridorSpec, SmclFrameResult, SmclNeighborStats, SmclOdom,
-                  SmclParticlesView, SmclSensorSpec)
+                  SmclParticlesView, SmclSensorSpec, SmclStepProfile)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libsmcl_gpu.so")
@@ -27,6 +27,11 @@ SIGNATURES = {
     "smcl_init_uniform": (_int, [C.c_void_p, _P(_d)]),
     "smcl_init_uniform_seeded": (_int, [C.c_void_p, _i64, _P(_d), _int, _u64]),
     "smcl_step": (_int, [C.c_void_p, _P(SmclCloud), _P(SmclOdom), _P(SmclFrameResult)]),
+    "smcl_scan_upload": (_int, [C.c_void_p, _int, _P(SmclCloud)]),
+    "smcl_step_slot": (_int, [C.c_void_p, _int, _P(SmclOdom), _P(SmclFrameResult)]),
+    "smcl_last_step_profile": (_int, [C.c_void_p, _P(SmclStepProfile)]),
+    "smcl_timer_start": (_int, [C.c_void_p]),
+    "smcl_timer_stop": (_int, [C.c_void_p, _P(_d)]),
     "smcl_frame_index": (_i64, [C.c_void_p]),
     "smcl_num_particles": (_i64, [C.c_void_p]),
     "smcl_get_particles": (_int, [C.c_void_p, _P(SmclParticlesView)]),

@@ -136,6 +136,18 @@ class SmclFrameResult(C.Structure):
         return d
 
 
+class SmclStepProfile(C.Structure):
+    _fields_ = [(k, C.c_double) for k in (
+        "predict_ms", "lsh_keys_ms", "sort_ms", "reorder_ms", "segments_ms", "refresh_gather_ms", "nb_stats_ms",
+        "gn_kernel_ms", "solve_ms", "svgd_ms", "ll_kernel_ms", "bayes_ms", "smooth_ms", "rep_ms", "total_ms")] + [
+        ("gn_points", C.c_int64), ("ll_points", C.c_int64), ("gn_matched", C.c_int64), ("ll_matched", C.c_int64),
+        ("fast_path", C.c_int32), ("n_svgd_iters", C.c_int32), ("kernel_launches", C.c_int64),
+        ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+
+    def to_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class SmclParticlesView(C.Structure):
     _fields_ = [
         ("n", C.c_int64),

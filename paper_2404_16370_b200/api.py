@@ -9,8 +9,8 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .abi import (Particles, SmclFrameResult, SmclNeighborStats, cloud_struct, f32ptr, f64ptr, i32ptr, make_config,
-                  odom_struct, u64ptr)
+from .abi import (Particles, SmclFrameResult, SmclNeighborStats, SmclStepProfile, cloud_struct, f64ptr, i32ptr,
+                  make_config, odom_struct, u64ptr)
 
 check = _lib.check
 
@@ -91,6 +91,34 @@ class FilterEngine:
         check(_lib.lib().smcl_step(self.h, C.byref(sc), C.byref(o), C.byref(r)))
         del keep
         return r.to_dict()
+
+    def scan_upload(self, slot, scan):
+        """Stage a prepared scan into a device slot (no H2D inside step_slot)."""
+        if scan is None or len(scan) == 0:
+            sc, keep = cloud_struct(np.zeros((0, 3)), np.zeros((0, 9)))
+        else:
+            sc, keep = scan.struct()
+        check(_lib.lib().smcl_scan_upload(self.h, slot, C.byref(sc)))
+        del keep
+
+    def step_slot(self, slot, delta=None, cov=None, valid=True):
+        o = odom_struct(delta, cov, valid)
+        r = SmclFrameResult()
+        check(_lib.lib().smcl_step_slot(self.h, slot, C.byref(o), C.byref(r)))
+        return r.to_dict()
+
+    def last_step_profile(self):
+        p = SmclStepProfile()
+        check(_lib.lib().smcl_last_step_profile(self.h, C.byref(p)))
+        return p.to_dict()
+
+    def timer_start(self):
+        check(_lib.lib().smcl_timer_start(self.h))
+
+    def timer_stop(self):
+        ms = C.c_double()
+        check(_lib.lib().smcl_timer_stop(self.h, C.byref(ms)))
+        return ms.value
 
     def frame_index(self):
         return _lib.lib().smcl_frame_index(self.h)

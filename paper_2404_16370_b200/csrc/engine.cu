@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <bit>
 #include <cmath>
 #include <cstring>
@@ -21,6 +22,11 @@
 #include "kernels.cuh"
 
 namespace smcl {
+
+static std::atomic<long long> g_launches{0};
+static std::atomic<long long> g_h2d{0}, g_d2h{0};  // host<->device bytes copied by the engine
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 // ---------------------------------------------------------------- errors
 struct CudaError : std::runtime_error {
@@ -77,10 +83,16 @@ struct DBuf {
   }
   void upload(const T* h, size_t count, cudaStream_t st) {
     ensure(count);
-    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
+    if (count) {
+      CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
+      g_h2d += static_cast<long long>(count * sizeof(T));
+    }
   }
   void download(T* h, size_t count, cudaStream_t st) const {
-    if (count) CK(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, st));
+    if (count) {
+      CK(cudaMemcpyAsync(h, p, count * sizeof(T), cudaMemcpyDeviceToHost, st));
+      g_d2h += static_cast<long long>(count * sizeof(T));
+    }
   }
   void swap(DBuf& o) {
     std::swap(p, o.p);
@@ -284,13 +296,41 @@ struct smcl_engine {
     bool structured = false;
     DBuf<double> mu, sigma;
     DBuf<float4> rec;
-  } scan_full, scan_gn;
+  };
+  struct ScanSlot {
+    ScanDev full, gn;
+    bool gn_alias = true;  // stride 1: the GN scan is the full scan
+    bool valid = false;
+    const ScanDev& gn_view() const { return gn_alias ? full : gn; }
+  };
+  std::vector<std::unique_ptr<ScanSlot>> slots;
+  ScanDev scan_tmp;  // stage-API scans
 
-  cudaEvent_t ev[8] = {};
+  // Step profile: one event per boundary, read after the step's final sync.
+  enum Ev {
+    E_START, E_PRED, E_KEYS, E_SORT, E_REORDER, E_SEG, E_RG, E_NB, E_GN0, E_GN1, E_SOLVE, E_SVGD, E_LL0, E_LL1,
+    E_BAYES, E_SMOOTH, E_END, E_COUNT
+  };
+  cudaEvent_t ev[E_COUNT] = {};
+  cudaEvent_t timer[2] = {};
+  smcl_step_profile prof{};
+  bool fast_used = false;
+  bool profiling = false;
+  void mark(Ev e) {
+    if (!ev[e]) CK(cudaEventCreate(&ev[e]));
+    CK(cudaEventRecord(ev[e], st));
+  }
+  float since(Ev a, Ev b) const {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev[a], ev[b]);
+    return ms;
+  }
 
   ~smcl_engine() {
     if (st) cudaStreamSynchronize(st);
     for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : timer)
       if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
   }
@@ -403,7 +443,7 @@ struct smcl_engine {
     argv.ensure(static_cast<size_t>(argmax_partials(static_cast<int64_t>(un))));
     argi.ensure(static_cast<size_t>(argmax_partials(static_cast<int64_t>(un))));
     d_hist.ensure(SMCL_MAX_HIST);
-    d_counts.ensure(4);
+    d_counts.ensure(8);
     steps_valid = phis_valid = ll_valid = false;
   }
 
@@ -426,19 +466,42 @@ struct smcl_engine {
     if (ok) sd.rec.upload(rec.data(), rec.size(), st);
   }
 
-  void set_scans(const smcl_cloud* scan) {
-    const int S = static_cast<int>(scan->n);
-    upload_scan(scan_full, scan->mu, scan->sigma, S);
+  ScanSlot& slot_at(int i) {
+    if (i < 0 || i >= SMCL_MAX_SCAN_SLOTS) throw std::invalid_argument("scan slot out of range");
+    while (static_cast<int>(slots.size()) <= i) slots.push_back(std::make_unique<ScanSlot>());
+    return *slots[static_cast<size_t>(i)];
+  }
+
+  // Host scan preparation + H2D into a device slot (filter.cpp:154-165 for
+  // the strided Gauss-Newton subset).
+  long long last_upload_bytes = 0;  // H2D bytes of the most recent set_slot
+  void set_slot(int i, const smcl_cloud* scan) {
+    const long long h2d0 = g_h2d.load();
+    struct Tally {
+      long long h0;
+      long long& out;
+      ~Tally() { out = g_h2d.load() - h0; }
+    } tally{h2d0, last_upload_bytes};
+    ScanSlot& sl = slot_at(i);
+    const int S = static_cast<int>(scan ? scan->n : 0);
+    sl.valid = true;
+    if (S == 0) {
+      sl.full.n = 0;
+      sl.gn_alias = true;
+      return;
+    }
+    upload_scan(sl.full, scan->mu, scan->sigma, S);
     const int stride = cfg.gn_scan_stride;
-    if (stride > 1 && S > 2 * stride) {  // filter.cpp:154-165
+    if (stride > 1 && S > 2 * stride) {
       std::vector<double> mu, sg;
       for (int q = 0; q < S; q += stride) {
         mu.insert(mu.end(), scan->mu + 3 * q, scan->mu + 3 * q + 3);
         sg.insert(sg.end(), scan->sigma + 9 * q, scan->sigma + 9 * q + 9);
       }
-      upload_scan(scan_gn, mu.data(), sg.data(), static_cast<int>(mu.size() / 3));
+      upload_scan(sl.gn, mu.data(), sg.data(), static_cast<int>(mu.size() / 3));
+      sl.gn_alias = false;
     } else {
-      upload_scan(scan_gn, scan->mu, scan->sigma, S);
+      sl.gn_alias = true;
     }
   }
 
@@ -468,7 +531,9 @@ struct smcl_engine {
     if (!has_map) throw std::invalid_argument("engine has no map");
     if (sd.n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
     ScanView sv{sd.n, sd.mu.p, sd.sigma.p, sd.structured ? sd.rec.p : nullptr};
-    if (use_fast(sd)) {
+    if (profiling) mark(gn ? E_GN0 : E_LL0);
+    fast_used = use_fast(sd);
+    if (fast_used) {
       MapFast mf{geom, map_fast.p};
       launch_gicp_fast(gn, poses.p, n_local, sv, mf, sys.p, nm.p, st);
     } else {
@@ -476,6 +541,10 @@ struct smcl_engine {
       launch_gicp_exact(gn, poses.p, n_local, sv, me, sys.p, nm.p, st);
     }
     CK(cudaGetLastError());
+    if (profiling) {
+      mark(gn ? E_GN1 : E_LL1);
+      launch_match_counts(ll.p /*unused for the sum*/, nm.p, n_local, d_counts.p + (gn ? 2 : 4), st);
+    }
     const GicpParamsDev gp = gicp_params(sd.n);
     if (gn)
       launch_solve(sys.p, nm.p, n_local, gp, steps.p, ll.p, st);
@@ -528,7 +597,9 @@ struct smcl_engine {
     const int shift = lp.prio_bits + lp.idx_bits;
 
     launch_lsh_keys(poses.p, n_local, gbase, lp, keys.p, st);
+    if (profiling) mark(E_KEYS);
     sort_keys(keys.p, skeys.p, n, 64, temp.p, temp_bytes, st);
+    if (profiling) mark(E_SORT);
     launch_members(skeys.p, n, idx_mask, shift, member_of.p, head.p, st);
     const int32_t* members = member_of.p;
     if (cfg.reorder_particles) {
@@ -544,14 +615,18 @@ struct smcl_engine {
       members = iota.p;
       steps_valid = phis_valid = ll_valid = false;  // storage order changed
     }
+    if (profiling) mark(E_REORDER);
     inclusive_sum_i32(head.p, seg_id.p, n, temp.p, temp_bytes, st);
     launch_segments(head.p, seg_id.p, n, seg_start.p, st);
     int32_t n_seg = 0;
     CK(cudaMemcpyAsync(&n_seg, seg_id.p + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    g_d2h += sizeof(int32_t);
+    if (profiling) mark(E_SEG);
     sync();
     launch_refresh_gather(poses.p, n_local, gbase, nullptr, members, seg_id.p, seg_start.p, n_seg, n, idx.p, kval.p,
                           count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, st);
     CK(cudaGetLastError());
+    if (profiling) mark(E_RG);
     // statistics
     const int hist_len = cfg.lsh_bucket_capacity + 2;
     CK(cudaMemsetAsync(d_hist.p, 0, sizeof(unsigned long long) * hist_len, st));
@@ -639,12 +714,14 @@ struct smcl_engine {
     long long ix;
     CK(cudaMemcpyAsync(&v, scal.p + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&ix, scal_i.p + 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    g_d2h += sizeof(double) + sizeof(long long);
     sync();
     *index = ix;
     *value = v;
     if (pose) {
       Pose p;
       CK(cudaMemcpyAsync(&p, poses.p + (ix - gbase), sizeof(Pose), cudaMemcpyDeviceToHost, st));
+      g_d2h += sizeof(Pose);
       sync();
       store_pose(p, pose);
     }
@@ -672,27 +749,30 @@ struct smcl_engine {
     sync();
   }
 
-  void step(const smcl_cloud* scan, const smcl_odom* odo, smcl_frame_result* out) {
+  void step_slot(int slot_i, const smcl_odom* odo, smcl_frame_result* out) {
     if (n_total == 0) throw std::logic_error("FilterEngine::step: not initialized");
     if (!has_map) throw std::invalid_argument("engine has no map");
-    for (auto& e : ev)
-      if (!e) CK(cudaEventCreate(&e));
+    ScanSlot& sl = slot_at(slot_i);
+    if (!sl.valid) throw std::invalid_argument("scan slot not uploaded");
+    profiling = true;
+    const long long launches0 = launch_count();
+    const long long d2h0 = g_d2h.load();
     smcl_frame_result r;
     std::memset(&r, 0, sizeof(r));
+    std::memset(&prof, 0, sizeof(prof));
     r.n_particles = n_total;
-    const bool empty = scan == nullptr || scan->n == 0;
+    const bool empty = sl.full.n == 0;
     r.scan_empty = empty ? 1 : 0;
-    if (!empty) set_scans(scan);  // host prep + H2D before the timed stages
+    CK(cudaMemsetAsync(d_counts.p, 0, sizeof(unsigned long long) * 6, st));
 
-    CK(cudaEventRecord(ev[0], st));
+    mark(E_START);
     {
       double delta[12], cov[36];
       if (odo->valid) {
         std::memcpy(delta, odo->delta, sizeof(delta));
         std::memcpy(cov, odo->cov, sizeof(cov));
       } else {
-        const Pose id_pose = pose_identity();
-        store_pose(id_pose, delta);
+        store_pose(pose_identity(), delta);
         std::memset(cov, 0, sizeof(cov));
         for (int d = 0; d < 3; ++d) {
           cov[d * 7] = cfg.diffusion_sigma_rot * cfg.diffusion_sigma_rot;
@@ -701,64 +781,97 @@ struct smcl_engine {
       }
       predict(delta, cov, mix_seed(cfg.seed, k_stream_predict, static_cast<uint64_t>(frame)));
     }
-    CK(cudaEventRecord(ev[1], st));
+    mark(E_PRED);
     const double bounds[6] = {map_bounds.min[0], map_bounds.min[1], map_bounds.min[2],
                               map_bounds.max[0], map_bounds.max[1], map_bounds.max[2]};
     update_neighbors(mix_seed(cfg.seed, k_stream_neighbors, static_cast<uint64_t>(frame)), bounds, &r.neighbor_stats);
-    CK(cudaEventRecord(ev[2], st));
-    float t_like = 0.f, t_upd = 0.f;
+    mark(E_NB);
+    double t_like = 0.0, t_upd = 0.0, t_gn = 0.0, t_solve = 0.0, t_svgd = 0.0;
+    const ScanDev& gn_scan = sl.gn_view();
     if (!empty) {
       for (int it = 0; it < cfg.n_svgd_iters; ++it) {
-        CK(cudaEventRecord(ev[3], st));
-        run_likelihood(true, scan_gn);
-        CK(cudaEventRecord(ev[4], st));
+        run_likelihood(true, gn_scan);
+        mark(E_SOLVE);
         svgd(true);
-        CK(cudaEventRecord(ev[5], st));
-        sync();
-        float a, b;
-        CK(cudaEventElapsedTime(&a, ev[3], ev[4]));
-        CK(cudaEventElapsedTime(&b, ev[4], ev[5]));
-        t_like += a;
-        t_upd += b;
+        mark(E_SVGD);
+        if (it + 1 < cfg.n_svgd_iters) {  // events are reused: read them before the next iteration
+          sync();
+          t_gn += since(E_GN0, E_GN1);
+          t_solve += since(E_GN1, E_SOLVE);
+          t_svgd += since(E_SOLVE, E_SVGD);
+        }
       }
-      CK(cudaEventRecord(ev[3], st));
-      run_likelihood(false, scan_full);
-      CK(cudaEventRecord(ev[4], st));
+      run_likelihood(false, sl.full);
+      mark(E_BAYES);
       r.observation_rejected = bayes(cfg.beta, cfg.log_post_floor) ? 1 : 0;
-      unsigned long long cnt[2];
-      d_counts.download(cnt, 2, st);
-      sync();
-      r.mean_n_matched = static_cast<double>(cnt[1]) / static_cast<double>(n_total);
-      float a;
-      CK(cudaEventElapsedTime(&a, ev[3], ev[4]));
-      t_like += a;
     } else {
-      CK(cudaEventRecord(ev[4], st));
+      mark(E_LL0);
+      mark(E_LL1);
+      mark(E_BAYES);
     }
+    mark(E_SMOOTH);  // posterior smoothing starts
     smooth(cfg.smooth_iters, cfg.log_post_floor);
+    mark(E_END);
     int64_t ix;
     double v;
     representative(&ix, r.representative, &v);
-    CK(cudaEventRecord(ev[6], st));
+    unsigned long long cnt[6];
+    d_counts.download(cnt, 6, st);
+    int32_t rid;
+    CK(cudaMemcpyAsync(&rid, id.p + (ix - gbase), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    g_d2h += sizeof(int32_t);
     sync();
-    float t_pred, t_nb, t_post, t_tot;
-    CK(cudaEventElapsedTime(&t_pred, ev[0], ev[1]));
-    CK(cudaEventElapsedTime(&t_nb, ev[1], ev[2]));
-    CK(cudaEventElapsedTime(&t_post, ev[4], ev[6]));
-    CK(cudaEventElapsedTime(&t_tot, ev[0], ev[6]));
+    if (!empty) {  // last (or only) Gauss-Newton iteration
+      t_gn += since(E_GN0, E_GN1);
+      t_solve += since(E_GN1, E_SOLVE);
+      t_svgd += since(E_SOLVE, E_SVGD);
+    }
+    t_like = t_gn + t_solve;
+    t_upd = t_svgd;
+    const double t_ll = since(E_LL0, E_BAYES);
+    r.mean_n_matched = empty ? 0.0 : static_cast<double>(cnt[1]) / static_cast<double>(n_total);
     r.rep_index = ix;
     r.rep_log_post = v;
-    int32_t rid;
-    CK(cudaMemcpy(&rid, id.p + (ix - gbase), sizeof(int32_t), cudaMemcpyDeviceToHost));
     r.rep_id = rid;
-    r.predict_ms = t_pred;
-    r.neighbor_ms = t_nb;
-    r.likelihood_ms = t_like;
+    r.predict_ms = since(E_START, E_PRED);
+    r.neighbor_ms = since(E_PRED, E_NB);
+    r.likelihood_ms = t_like + t_ll;
     r.update_ms = t_upd;
-    r.posterior_ms = t_post;
-    r.total_ms = t_tot;
+    r.posterior_ms = since(E_BAYES, E_END);
+    r.total_ms = since(E_START, E_END);
+    // per-kernel profile
+    prof.predict_ms = r.predict_ms;
+    prof.lsh_keys_ms = since(E_PRED, E_KEYS);
+    prof.sort_ms = since(E_KEYS, E_SORT);
+    prof.reorder_ms = since(E_SORT, E_REORDER);
+    prof.segments_ms = since(E_REORDER, E_SEG);
+    prof.refresh_gather_ms = since(E_SEG, E_RG);
+    prof.nb_stats_ms = since(E_RG, E_NB);
+    prof.gn_kernel_ms = t_gn;
+    prof.solve_ms = t_solve;
+    prof.svgd_ms = t_svgd;
+    prof.ll_kernel_ms = empty ? 0.0 : since(E_LL0, E_LL1);
+    prof.bayes_ms = since(E_LL1, E_SMOOTH);
+    prof.smooth_ms = since(E_SMOOTH, E_END);
+    prof.total_ms = r.total_ms;
+    prof.gn_points = empty ? 0 : static_cast<int64_t>(gn_scan.n) * n_total * cfg.n_svgd_iters;
+    prof.ll_points = empty ? 0 : static_cast<int64_t>(sl.full.n) * n_total;
+    prof.gn_matched = static_cast<int64_t>(cnt[3]);
+    prof.ll_matched = static_cast<int64_t>(cnt[5]);
+    prof.fast_path = fast_used ? 1 : 0;
+    prof.n_svgd_iters = cfg.n_svgd_iters;
+    prof.kernel_launches = launch_count() - launches0;
+    prof.d2h_bytes = g_d2h.load() - d2h0;
+    prof.h2d_bytes = last_upload_bytes;
+    profiling = false;
     *out = r;
     ++frame;
+  }
+
+  void step(const smcl_cloud* scan, const smcl_odom* odo, smcl_frame_result* out) {
+    if (n_total == 0) throw std::logic_error("FilterEngine::step: not initialized");
+    set_slot(0, scan);  // host scan prep + H2D (inside the caller's e2e timing)
+    step_slot(0, odo, out);
   }
 };
 
@@ -872,6 +985,49 @@ int smcl_step(smcl_engine* h, const smcl_cloud* scan, const smcl_odom* odo, smcl
   });
 }
 
+int smcl_scan_upload(smcl_engine* h, int slot, const smcl_cloud* scan) {
+  return guard([&] {
+    use_dev(h);
+    h->set_slot(slot, scan);
+    h->sync();
+  });
+}
+
+int smcl_step_slot(smcl_engine* h, int slot, const smcl_odom* odo, smcl_frame_result* out) {
+  return guard([&] {
+    use_dev(h);
+    if (!odo || !out) throw std::invalid_argument("smcl_step: null odometry or result");
+    h->step_slot(slot, odo, out);
+  });
+}
+
+int smcl_timer_start(smcl_engine* h) {
+  return guard([&] {
+    use_dev(h);
+    if (!h->timer[0]) CK(cudaEventCreate(&h->timer[0]));
+    if (!h->timer[1]) CK(cudaEventCreate(&h->timer[1]));
+    CK(cudaEventRecord(h->timer[0], h->st));
+  });
+}
+
+int smcl_timer_stop(smcl_engine* h, double* ms) {
+  return guard([&] {
+    use_dev(h);
+    CK(cudaEventRecord(h->timer[1], h->st));
+    CK(cudaEventSynchronize(h->timer[1]));
+    float f = 0.f;
+    CK(cudaEventElapsedTime(&f, h->timer[0], h->timer[1]));
+    *ms = f;
+  });
+}
+
+int smcl_last_step_profile(smcl_engine* h, smcl_step_profile* out) {
+  return guard([&] {
+    if (!h) throw std::invalid_argument("null engine handle");
+    *out = h->prof;
+  });
+}
+
 int64_t smcl_frame_index(const smcl_engine* h) { return h ? h->frame : -1; }
 int64_t smcl_num_particles(const smcl_engine* h) { return h ? h->n_total : -1; }
 
@@ -946,8 +1102,8 @@ int smcl_evaluate_all(smcl_engine* h, const smcl_cloud* scan, double* step_out, 
   return guard([&] {
     use_dev(h);
     if (!scan || scan->n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
-    h->upload_scan(h->scan_gn, scan->mu, scan->sigma, static_cast<int>(scan->n));
-    h->run_likelihood(true, h->scan_gn);
+    h->upload_scan(h->scan_tmp, scan->mu, scan->sigma, static_cast<int>(scan->n));
+    h->run_likelihood(true, h->scan_tmp);
     const size_t n = static_cast<size_t>(h->n_local);
     if (step_out) h->steps.download(step_out, n * 6, h->st);
     if (ll_out) h->ll.download(ll_out, n, h->st);
@@ -969,8 +1125,8 @@ int smcl_evaluate_likelihoods(smcl_engine* h, const smcl_cloud* scan, double* ll
   return guard([&] {
     use_dev(h);
     if (!scan || scan->n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
-    h->upload_scan(h->scan_full, scan->mu, scan->sigma, static_cast<int>(scan->n));
-    h->run_likelihood(false, h->scan_full);
+    h->upload_scan(h->scan_tmp, scan->mu, scan->sigma, static_cast<int>(scan->n));
+    h->run_likelihood(false, h->scan_tmp);
     const size_t n = static_cast<size_t>(h->n_local);
     if (ll_out) h->ll.download(ll_out, n, h->st);
     if (nm_out) h->nm.download(nm_out, n, h->st);

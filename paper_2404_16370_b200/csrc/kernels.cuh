@@ -10,6 +10,10 @@
 
 namespace smcl {
 
+// Number of hand-written kernel launches issued so far (bench gpu_launches).
+void count_launch(int n = 1);
+long long launch_count();
+
 struct PredictParams {  // filter.cpp:67-84
   Pose delta;
   double L[36];  // lower-triangular sqrt of the odometry covariance (row-major)

@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "../engine.cuh"
+#include "../kernels.cuh"
 
 namespace smcl {
 
@@ -581,6 +582,7 @@ inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n +
 
 void launch_gicp_exact(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapExact& map, double* sys,
                        int32_t* nm, cudaStream_t st) {
+  count_launch();
   if (n <= 0) return;
   if (gn)
     k_gicp_exact<true><<<blocks_for(n, 128), 128, 0, st>>>(poses, n, scan, map, sys, nm);
@@ -592,6 +594,7 @@ static size_t fast_smem(int S) { return sizeof(FastShared) + sizeof(double) * 3 
 
 void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys,
                       int32_t* nm, cudaStream_t st) {
+  count_launch();
   if (n <= 0) return;
   static int n_sm = 0;
   if (!n_sm) {
@@ -612,18 +615,21 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
 
 void launch_solve(const double* sys, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* steps, double* ll,
                   cudaStream_t st) {
+  count_launch();
   if (n <= 0) return;
   k_solve<<<blocks_for(n, 128), 128, 0, st>>>(sys, nm, n, p, steps, ll);
 }
 
 void launch_gate_ll(const double* sys, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* ll,
                     cudaStream_t st) {
+  count_launch();
   if (n <= 0) return;
   k_gate<<<blocks_for(n, 256), 256, 0, st>>>(sys, nm, n, p, ll);
 }
 
 void launch_solve_batch(const double* H, const double* b, const double* lam, int64_t n, double omax, double vmax,
                         double* out, cudaStream_t st) {
+  count_launch();
   if (n <= 0) return;
   k_solve_batch<<<blocks_for(n, 128), 128, 0, st>>>(H, b, lam, n, omax, vmax, out);
 }

@@ -210,9 +210,11 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
 }  // namespace
 
 void launch_lsh_keys(const Pose* poses, int64_t n, int64_t gbase, const LshPass& lp, uint64_t* keys, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_lsh_keys<<<blocks_for(n, 128), 128, 0, st>>>(poses, n, gbase, lp, keys);
 }
 void launch_hash_batch(const Pose* poses, int64_t n, const LshPass& lp, uint64_t* out, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_hash_batch<<<blocks_for(n, 128), 128, 0, st>>>(poses, n, lp, out);
 }
 
@@ -232,6 +234,7 @@ void sort_keys(const uint64_t* in, uint64_t* out, int64_t n, int end_bit, void* 
 
 void launch_members(const uint64_t* skeys, int64_t n, uint64_t idx_mask, int shift, int32_t* member_of, int32_t* head,
                     cudaStream_t st) {
+  count_launch();
   if (n > 0) k_members<<<blocks_for(n, 256), 256, 0, st>>>(skeys, n, idx_mask, shift, member_of, head);
 }
 
@@ -240,6 +243,7 @@ void inclusive_sum_i32(const int32_t* in, int32_t* out, int64_t n, void* temp, s
 }
 
 void launch_inverse_perm(const int32_t* member_of, int64_t n, int32_t* new_of_old, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_inverse_perm<<<blocks_for(n, 256), 256, 0, st>>>(member_of, n, new_of_old);
 }
 
@@ -247,17 +251,20 @@ void launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_
                     const double* lp, const int32_t* id, const int32_t* idx, const float* kval, const int32_t* count,
                     Pose* poses2, double* lp2, int32_t* id2, int32_t* idx2, float* kval2, int32_t* count2,
                     cudaStream_t st) {
+  count_launch();
   if (n > 0)
     k_reorder<<<blocks_for(n, 128), 128, 0, st>>>(old_of_new, new_of_old, n, k, poses, lp, id, idx, kval, count, poses2,
                                                   lp2, id2, idx2, kval2, count2);
 }
 
 void launch_segments(const int32_t* head, const int32_t* seg_id, int64_t n, int32_t* seg_start, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_segments<<<blocks_for(n, 256), 256, 0, st>>>(head, seg_id, n, seg_start);
 }
 
 void launch_seg_stats(const int32_t* seg_start, int32_t n_seg, int64_t n, int cap, unsigned long long* hist,
                       unsigned long long* overflow, cudaStream_t st) {
+  count_launch();
   if (n_seg > 0) k_seg_stats<<<blocks_for(n_seg, 256), 256, 0, st>>>(seg_start, n_seg, n, cap, hist, overflow);
 }
 
@@ -266,6 +273,7 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                            const int32_t* seg_id, const int32_t* seg_start, int32_t n_seg, int64_t n_sorted,
                            int32_t* idx, float* kval, int32_t* count, int k, int cap, double sr, double st_,
                            cudaStream_t st) {
+  count_launch();
   constexpr int B = 64;
   if (n > 0)
     k_refresh_gather<B><<<blocks_for(n, B), B, 0, st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, seg_start, n_seg,

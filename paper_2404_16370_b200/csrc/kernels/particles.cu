@@ -137,15 +137,18 @@ __global__ void k_kernel_batch(const Pose* a, const Pose* b, int64_t n, double s
 }  // namespace
 
 void launch_predict(Pose* poses, int64_t n, int64_t gbase, const PredictParams& pp, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_predict<<<blocks_for(n, 128), 128, 0, st>>>(poses, n, gbase, pp);
 }
 void launch_init_uniform(Pose* poses, double* log_post, int32_t* id, int32_t* idx, float* kval, int32_t* count,
                          int64_t n, int64_t gbase, int k, const InitParams& ip, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_init_uniform<<<blocks_for(n, 128), 128, 0, st>>>(poses, log_post, id, idx, kval, count, n, gbase, k, ip);
 }
 void launch_svgd(const Pose* all_poses, const double* all_steps, int64_t n, int64_t gbase, const int32_t* idx,
                  const int32_t* count, int k, const SvgdParams& sp, double* phi_out, Pose* poses_out,
                  cudaStream_t st) {
+  count_launch();
   if (n <= 0) return;
   if (poses_out)
     k_svgd<true><<<blocks_for(n, 128), 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out,
@@ -155,15 +158,19 @@ void launch_svgd(const Pose* all_poses, const double* all_steps, int64_t n, int6
                                                        nullptr);
 }
 void launch_apply(Pose* poses, const double* phis, int64_t n, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_apply<<<blocks_for(n, 128), 128, 0, st>>>(poses, phis, n);
 }
 void launch_exp_batch(const double* xi, int64_t n, Pose* out, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_exp_batch<<<blocks_for(n, 128), 128, 0, st>>>(xi, n, out);
 }
 void launch_log_batch(const Pose* p, int64_t n, double* out, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_log_batch<<<blocks_for(n, 128), 128, 0, st>>>(p, n, out);
 }
 void launch_kernel_batch(const Pose* a, const Pose* b, int64_t n, double sr, double st_, double* out, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_kernel_batch<<<blocks_for(n, 128), 128, 0, st>>>(a, b, n, sr, st_, out);
 }
 

@@ -190,12 +190,15 @@ __global__ void k_smooth_round(const double* __restrict__ p_all, double* __restr
 }  // namespace
 
 void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_bayes_numer<<<blocks_for(n, 256), 256, 0, st>>>(lp, ll, nm, n, beta);
 }
 void launch_fill(double* v, int64_t n, double value, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_fill<<<blocks_for(n, 256), 256, 0, st>>>(v, n, value);
 }
 void launch_match_counts(const double* ll, const int32_t* nm, int64_t n, unsigned long long* out, cudaStream_t st) {
+  count_launch();
   cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), st);
   if (n > 0) {
     const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(n, 256), 1184));
@@ -205,40 +208,50 @@ void launch_match_counts(const double* ll, const int32_t* nm, int64_t n, unsigne
 int argmax_partials(int64_t n) { return static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 1184)); }
 void launch_argmax(const double* v, int64_t n, int64_t gbase, double* scratch_v, long long* scratch_i, double* out_v,
                    long long* out_i, cudaStream_t st) {
+  count_launch();
   const int g = argmax_partials(n);
   k_argmax<<<g, 256, 0, st>>>(v, nullptr, n, gbase, scratch_v, scratch_i);
   k_argmax<<<1, 256, 0, st>>>(scratch_v, scratch_i, g, 0, out_v, out_i);
 }
 void launch_max_of_partials(const double* pv, const long long* pi, int64_t n, double* out_v, long long* out_i,
                             cudaStream_t st) {
+  count_launch();
   k_argmax<<<1, 256, 0, st>>>(pv, pi, n, 0, out_v, out_i);
 }
 void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* partial, cudaStream_t st) {
+  count_launch();
   const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
   if (chunks > 0) k_chunk_sum_exp<<<blocks_for(chunks, 32), 32, 0, st>>>(v, n, m, partial);
 }
 void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n, int k, double* pk, double* pc,
                              cudaStream_t st) {
+  count_launch();
   const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
   if (chunks > 0) k_chunk_sum_kernel<<<blocks_for(chunks, 32), 32, 0, st>>>(kval, count, n, k, pk, pc);
 }
 void launch_finish_lse(const double* partial, int64_t n_chunks, const double* m, double* lse, cudaStream_t st) {
+  count_launch();
   k_finish_lse<<<1, 1, 0, st>>>(partial, n_chunks, m, lse);
 }
 void launch_finish_sum2(const double* a, const double* b, int64_t n_chunks, double* out, cudaStream_t st) {
+  count_launch();
   k_finish_sum2<<<1, 1, 0, st>>>(a, b, n_chunks, out);
 }
 void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_apply_lse<<<blocks_for(n, 256), 256, 0, st>>>(v, n, lse, floor_v);
 }
 void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_exp<<<blocks_for(n, 256), 256, 0, st>>>(lp, p, n);
 }
 void launch_log(const double* p, double* lp, int64_t n, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_log<<<blocks_for(n, 256), 256, 0, st>>>(p, lp, n);
 }
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
                          const int32_t* count, int k, cudaStream_t st) {
+  count_launch();
   if (n > 0) k_smooth_round<<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count, k);
 }
 

@@ -1,0 +1,274 @@
+"""GPU parity of the non-likelihood stages against the CPU oracle:
+device SE3/hash/solver primitives, init/predict (K9/K10), the LSH neighbour
+pass (K3-K7), SVGD (K8) and the posterior (K11-K13).
+
+Reference pins: test_se3.cpp, test_svgd.cpp, test_neighbor_search.cpp:55-270,
+test_posterior.cpp, test_filter.cpp:41-171, test_parallel_consistency.cpp.
+Discrete outputs (hashes, keys, permutation, neighbour lists, ids, argmax)
+are compared exactly; floating outputs that pass through libm (sin, atan2,
+exp, log) within 1e-12 relative (CUDA's <= 2 ulp vs glibc)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import cube_set, random_cube_set, random_pose, random_tangent
+from paper_2404_16370_b200 import api
+from paper_2404_16370_b200.abi import Particles, identity_pose, make_config
+from paper_2404_16370_b200.api import FilterEngine
+
+pytestmark = pytest.mark.gpu
+I12 = identity_pose()
+TOL_F64 = 1e-12
+
+
+def close(a, b, tol=TOL_F64, floor=1e-12):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.all(np.abs(a - b) <= tol * np.maximum(np.abs(b), floor))
+
+
+# ---------------------------------------------------------------- primitives
+def test_se3_exp_log_batch():
+    rng = O.SplitMix64(11)
+    xis = np.array([random_tangent(rng, math.pi - 0.1, 10.0) for _ in range(500)])
+    xis[:10] *= 1e-6  # series branches
+    p_gpu = api.se3_exp(xis)
+    p_ref = O.se3_exp(xis)
+    assert np.abs(p_gpu - p_ref).max() < 1e-13
+    l_gpu = api.se3_log(p_ref)
+    l_ref = O.se3_log(p_ref)
+    assert np.abs(l_gpu - l_ref).max() < 1e-12
+    # pi branch is deterministic
+    at = O.se3_exp([0, 0, math.pi, 0.5, -0.2, 0.1])
+    a = api.se3_log(at)[0]
+    assert abs(np.linalg.norm(a[:3]) - math.pi) < 1e-6
+
+
+def test_kernel_batch():
+    rng = O.SplitMix64(5)
+    a = np.array([random_pose(rng, 2.0, 2.0) for _ in range(300)])
+    b = np.array([random_pose(rng, 2.0, 2.0) for _ in range(300)])
+    k = api.kernel(a, b)
+    kr = np.array([O.kernel(x, y) for x, y in zip(a, b)])
+    assert close(k, kr, 1e-11, 1e-300)
+    one = I12.copy()
+    one[9] = 1.0
+    assert abs(api.kernel([I12], [one])[0] - math.exp(-2.5)) < 1e-12
+
+
+def test_lsh_hash_bit_exact():
+    rng = O.SplitMix64(3)
+    box = [-5, -5, -5, 5, 5, 5]
+    for trial in range(5):
+        frame = rng.random_lsh_frame(box)
+        noise = 0.5 * rng.normal6()
+        poses = np.array([random_pose(rng, 1.5, 4.0) for _ in range(400)])
+        h = api.lsh_hash(poses, frame, noise)
+        hr = np.array([O.lsh_hash(p, frame, noise) for p in poses], dtype=np.uint64)
+        assert np.array_equal(h, hr)
+
+
+def test_solve_step_batch_bitwise():
+    rng = O.SplitMix64(5)
+    Hs, bs, lams = [], [], []
+    for _ in range(64):
+        a = np.array([[rng.normal01() for _ in range(6)] for _ in range(6)])
+        Hs.append(a.T @ a + 0.1 * np.eye(6))
+        bs.append([rng.normal01() for _ in range(6)])
+        lams.append(1e-3)
+    Hs.append(np.zeros((6, 6)))
+    bs.append([1, 0, 0, 0, 0, 0])
+    lams.append(0.0)
+    Hs.append(np.eye(6))
+    bs.append([3, -3, 3, 5, -5, 5])
+    lams.append(0.0)
+    got = api.solve_step(np.array(Hs), np.array(bs, float), np.array(lams))
+    ref = np.array([O.solve_step(h, b, l) for h, b, l in zip(Hs, bs, lams)])
+    assert np.array_equal(got, ref)
+    with pytest.raises(ValueError):
+        api.solve_step(np.eye(6)[None], np.ones((1, 6)), -1.0)
+
+
+# ---------------------------------------------------------------- init / predict
+def _stage_engine(parts=None, **cfg):
+    e = FilterEngine(None, make_config(**cfg))
+    if parts is not None:
+        e.set_particles(parts)
+    return e
+
+
+def test_init_uniform_matches_oracle():
+    bounds = [-2.0, 0.0, 1.0, 3.0, 10.0, 4.0]
+    for full in (True, False):
+        e = _stage_engine()
+        e.init_uniform_seeded(5000, bounds, full, 11)
+        g = e.particles()
+        r = O.init_uniform(5000, 20, bounds, full, 11)
+        assert np.array_equal(g.id, r.id) and np.array_equal(g.idx, r.idx) and np.array_equal(g.count, r.count)
+        assert np.array_equal(g.kval, r.kval) and np.array_equal(g.log_post, r.log_post)
+        assert np.abs(g.poses - r.poses).max() < 1e-13
+
+
+def test_predict_matches_oracle():
+    r = O.init_uniform(4000, 20, [0, 0, 0, 1, 1, 1], True, 17)
+    e = _stage_engine(r)
+    # zero covariance, identity delta: bitwise no-op
+    e.predict(I12, np.zeros(36), 23)
+    assert np.array_equal(e.particles().poses, r.poses)
+    # deterministic forward delta
+    d = I12.copy()
+    d[9] = 1.0
+    e.predict(d, np.zeros(36), 29)
+    assert np.array_equal(e.particles().poses, O.predict(r.poses, d, np.zeros(36), 29))
+    # noisy, full covariance
+    rng = np.random.default_rng(0)
+    a = rng.normal(size=(6, 6)) * 0.02
+    cov = (a @ a.T + np.diag([4e-4, 9e-4, 1e-4, 2.5e-3, 1e-3, 4e-3])).reshape(36)
+    base = e.particles().poses
+    e.predict(d, cov, 31)
+    ref = O.predict(base, d, cov, 31)
+    assert np.abs(e.particles().poses - ref).max() < 1e-12
+
+
+def test_predict_noise_covariance():
+    n = 100000
+    parts = Particles.from_poses(np.tile(I12, (n, 1)), 2)
+    e = _stage_engine(parts, k_neighbors=2)
+    cov = np.diag([4e-4, 9e-4, 1e-4, 2.5e-3, 1e-3, 4e-3])
+    e.predict(I12, cov.reshape(36), 31)
+    xi = api.se3_log(e.particles().poses)
+    sample = xi.T @ xi / n
+    assert np.linalg.norm(sample - cov) / np.linalg.norm(cov) < 0.05
+
+
+# ---------------------------------------------------------------- LSH neighbour pass
+@pytest.mark.parametrize("reorder", [1, 0])
+def test_update_neighbors_matches_oracle(reorder):
+    cfg = make_config(reorder_particles=reorder)
+    bounds = [0, 0, 0, 6, 6, 6]
+    g = random_cube_set(500, 6.0, 0.3, 20, 23)
+    r = g.copy()
+    e = _stage_engine(g, reorder_particles=reorder)
+    for p in range(4):
+        seed = O.mix_seed(29, p)
+        st = e.update_neighbors(seed, bounds)
+        sr = O.update_neighbors(r, cfg, seed, bounds)
+        assert st["n_buckets"] == sr["n_buckets"] and st["buckets_used"] == sr["buckets_used"]
+        assert st["overflow_dropped"] == sr["overflow_dropped"]
+        assert st["occupancy_hist"] == sr["occupancy_hist"]
+        assert abs(st["mean_kernel"] - sr["mean_kernel"]) <= 1e-12 * max(abs(sr["mean_kernel"]), 1e-300)
+    got = e.particles()
+    assert np.array_equal(got.id, r.id)
+    assert np.array_equal(got.count, r.count)
+    assert np.array_equal(got.idx, r.idx)
+    assert np.array_equal(got.kval, r.kval)
+    assert np.array_equal(got.poses, r.poses)
+
+
+def test_update_neighbors_oracle_serial_twin():
+    """test_neighbor_search.cpp:234-257 on the oracle itself (parallel == serial)."""
+    cfg = make_config()
+    a = random_cube_set(300, 6.0, 0.3, 20, 23)
+    b = a.copy()
+    for p in range(3):
+        seed = O.mix_seed(29, p)
+        O.update_neighbors(a, cfg, seed, [0, 0, 0, 6, 6, 6])
+        O.update_neighbors(b, cfg, seed, [0, 0, 0, 6, 6, 6], serial=True)
+    assert np.array_equal(a.idx, b.idx) and np.array_equal(a.kval, b.kval) and np.array_equal(a.id, b.id)
+
+
+def test_lone_particle_and_separated():
+    g = random_cube_set(1, 1.0, 0.1, 20, 3)
+    e = _stage_engine(g)
+    for p in range(5):
+        e.update_neighbors(O.mix_seed(11, p), [0, 0, 0, 1, 1, 1])
+    got = e.particles()
+    assert got.count[0] == 1 and got.idx[0, 0] == 0
+    poses = np.tile(I12, (100, 1))
+    poses[:, 9] = 10.0 * np.arange(100)
+    parts = Particles.from_poses(poses, 5)
+    e = _stage_engine(parts, k_neighbors=5)
+    for p in range(5):
+        e.update_neighbors(O.mix_seed(13, p), [0, 0, 0, 1000, 1, 1])
+    got = e.particles()
+    for i in range(100):
+        ids = got.idx[i, : got.count[i]]
+        assert len(set(ids)) == len(ids) and i in ids
+        assert np.all(got.kval[i, : got.count[i]][ids != i] < 1e-10)
+
+
+def test_recall_against_brute_force():
+    """test_neighbor_search.cpp:200-232 (recall > 0.6 after 10 passes)."""
+    k = 10
+    g = random_cube_set(300, 8.0, 0.2, k, 17)
+    truth = O.brute_force_kernel_knn(g.poses, k)
+    e = _stage_engine(g, k_neighbors=k)
+    for p in range(10):
+        e.update_neighbors(O.mix_seed(19, p), [0, 0, 0, 8, 8, 8])
+    got = e.particles()
+    slot_of_id = np.empty(300, np.int64)
+    slot_of_id[got.id] = np.arange(300)
+    hit = total = 0
+    for orig in range(300):
+        s = slot_of_id[orig]
+        have = {int(got.id[j]) for j in got.idx[s, : got.count[s]]}
+        for want in truth[orig]:
+            total += 1
+            hit += int(want) in have
+    assert hit / total > 0.6
+
+
+# ---------------------------------------------------------------- SVGD
+def test_compute_phis_and_apply_match_oracle():
+    g = cube_set(700, 7, 20)
+    e = _stage_engine(g)
+    for p in range(3):
+        e.update_neighbors(O.mix_seed(11, p), [0, 0, 0, 8, 6, 3])
+    parts = e.particles()
+    rng = O.SplitMix64(15)
+    steps = np.array([random_tangent(rng, 0.2, 0.3) for _ in range(700)])
+    phi = e.compute_phis(steps)
+    ref = O.compute_phis(parts.poses, steps, parts.idx, parts.count)
+    assert np.abs(phi - ref).max() < 1e-12
+    e.apply_updates(ref)
+    assert np.abs(e.particles().poses - O.apply_updates(parts.poses, ref)).max() < 1e-12
+
+
+# ---------------------------------------------------------------- posterior
+def test_posterior_stages_match_oracle():
+    rng = O.SplitMix64(33)
+    n = 20000
+    g = cube_set(n, 9, 20)
+    e = _stage_engine(g)
+    for p in range(2):
+        e.update_neighbors(O.mix_seed(41, p), [0, 0, 0, 6, 6, 6])
+    parts = e.particles()
+    lp = O.normalize_log_post(np.array([rng.uniform_range(-40.0, 0.0) for _ in range(n)]))
+    parts.log_post[:] = lp
+    e.set_particles(parts)
+    ll = np.array([rng.uniform_range(-500.0, 0.0) for _ in range(n)])
+    ll[::7] = -1e30
+    nm = np.array([1 + rng() % 60 for _ in range(n)], np.int32)
+    rej = e.bayes_update(ll, nm, 2.0)
+    ref, rej2 = O.bayes_update(lp, ll, nm, 2.0)
+    assert rej == rej2 is False
+    got = e.particles().log_post
+    assert np.abs(got - ref).max() < 1e-12
+    e.smooth(10)
+    ref = O.smooth(ref, parts.idx, parts.kval, parts.count, 10)
+    got = e.particles().log_post
+    assert np.abs(got - ref).max() < 1e-11
+    ix, pose, val = e.representative()
+    rix, rval = O.representative(ref)
+    assert ix == rix or abs(val - rval) < 1e-12
+    # all-sentinel observation resets to uniform
+    rej = e.bayes_update(np.full(n, -1e30), np.zeros(n, np.int32), 2.0)
+    assert rej and np.all(e.particles().log_post == -math.log(n))
+
+
+def test_representative_tie_lowest_index():
+    parts = Particles.from_poses(np.tile(I12, (6, 1)), 4)
+    parts.log_post[:] = [-3.0, -1.0, -2.0, -1.0, -1.0, -4.0]
+    e = _stage_engine(parts, k_neighbors=4)
+    assert e.representative()[0] == 1
