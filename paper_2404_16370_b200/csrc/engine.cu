@@ -633,7 +633,7 @@ struct smcl_engine {
     CK(cudaMemsetAsync(d_counts.p, 0, sizeof(unsigned long long) * 2, st));
     launch_seg_stats(seg_start.p, n_seg, n, cfg.lsh_bucket_capacity, d_hist.p, d_counts.p, st);
     const int64_t chunks = (n_local + kReduceChunk - 1) / kReduceChunk;
-    launch_chunk_sum_kernel(kval.p, count.p, n_local, k, partial.p, partial2.p, st);
+    launch_chunk_sum_kernel(kval.p, count.p, n_local, k, pbuf.p, qbuf.p, partial.p, partial2.p, st);
     launch_finish_sum2(partial.p, partial2.p, chunks, scal.p, st);
     CK(cudaGetLastError());
     if (out) {
@@ -669,7 +669,7 @@ struct smcl_engine {
     const int64_t n = n_local;
     if (n == 0) return;
     launch_argmax(log_post.p, n, gbase, argv.p, argi.p, scal.p + 2, scal_i.p, st);
-    launch_chunk_sum_exp(log_post.p, n, scal.p + 2, partial.p, st);
+    launch_chunk_sum_exp(log_post.p, n, scal.p + 2, pbuf.p, partial.p, st);
     launch_finish_lse(partial.p, (n + kReduceChunk - 1) / kReduceChunk, scal.p + 2, scal.p + 3, st);
     launch_apply_lse(log_post.p, n, scal.p + 3, floor_v, st);
     CK(cudaGetLastError());

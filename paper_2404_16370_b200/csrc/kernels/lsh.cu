@@ -10,6 +10,8 @@
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "../engine.cuh"
 #include "../kernels.cuh"
 
@@ -90,8 +92,8 @@ __global__ void k_reorder(const int32_t* __restrict__ old_of_new, const int32_t*
     if (s < c) {
       idx2[p * k + s] = new_of_old[idx[src * k + s]];
       kval2[p * k + s] = kval[src * k + s];
-    } else {
-      idx2[p * k + s] = -1;
+    } else {  // particle_set.cpp:17-19 value-initialises the new arrays
+      idx2[p * k + s] = 0;
       kval2[p * k + s] = 0.0f;
     }
   }
@@ -107,13 +109,22 @@ __global__ void k_segments(const int32_t* __restrict__ head, const int32_t* __re
 // order independent, so the histogram is exact.
 __global__ void k_seg_stats(const int32_t* __restrict__ seg_start, int32_t n_seg, int64_t n, int cap,
                             unsigned long long* __restrict__ hist, unsigned long long* __restrict__ overflow) {
-  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s >= n_seg) return;
-  const int64_t end = s + 1 < n_seg ? seg_start[s + 1] : n;
-  const int64_t size = end - seg_start[s];
-  const int64_t bin = size < cap + 1 ? size : cap + 1;
-  atomicAdd(hist + bin, 1ull);
-  if (size > cap) atomicAdd(overflow, static_cast<unsigned long long>(size - cap));
+  // Block-private histogram in shared memory, one global atomic per bin per block.
+  extern __shared__ unsigned long long s_hist[];  // cap + 3 (last = overflow)
+  for (int b = threadIdx.x; b < cap + 3; b += blockDim.x) s_hist[b] = 0ull;
+  __syncthreads();
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < n_seg;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t end = s + 1 < n_seg ? seg_start[s + 1] : n;
+    const int64_t size = end - seg_start[s];
+    const int64_t bin = size < cap + 1 ? size : cap + 1;
+    atomicAdd(s_hist + bin, 1ull);
+    if (size > cap) atomicAdd(s_hist + cap + 2, static_cast<unsigned long long>(size - cap));
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < cap + 2; b += blockDim.x)
+    if (s_hist[b]) atomicAdd(hist + b, s_hist[b]);
+  if (threadIdx.x == 0 && s_hist[cap + 2]) atomicAdd(overflow, s_hist[cap + 2]);
 }
 
 // Fused NeighborGraph::refresh (neighbor_graph.hpp:76-90) and the gather/offer
@@ -265,7 +276,10 @@ void launch_segments(const int32_t* head, const int32_t* seg_id, int64_t n, int3
 void launch_seg_stats(const int32_t* seg_start, int32_t n_seg, int64_t n, int cap, unsigned long long* hist,
                       unsigned long long* overflow, cudaStream_t st) {
   count_launch();
-  if (n_seg > 0) k_seg_stats<<<blocks_for(n_seg, 256), 256, 0, st>>>(seg_start, n_seg, n, cap, hist, overflow);
+  if (n_seg > 0) {
+    const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(n_seg, 256), 296));
+    k_seg_stats<<<g, 256, sizeof(unsigned long long) * (cap + 3), st>>>(seg_start, n_seg, n, cap, hist, overflow);
+  }
 }
 
 void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, const int32_t* pos_list,

@@ -103,37 +103,46 @@ __global__ void k_argmax(const double* __restrict__ v, const long long* __restri
   }
 }
 
-// One thread per 4096-chunk: serial sum of exp(v - m) in index order.
-__global__ void k_chunk_sum_exp(const double* __restrict__ v, int64_t n, const double* __restrict__ m_ptr,
-                                double* __restrict__ partial) {
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t begin = c * kReduceChunk;
-  if (begin >= n) return;
-  const int64_t end = begin + kReduceChunk < n ? begin + kReduceChunk : n;
-  const double m = *m_ptr;
-  double acc = 0.0;
-  for (int64_t i = begin; i < end; ++i) acc = xadd(acc, exp(xsub(v[i], m)));
-  partial[c] = acc;
+// exp(v - m), elementwise (the value_at of posterior.cpp:17).
+__global__ void k_exp_shift(const double* __restrict__ v, int64_t n, const double* __restrict__ m_ptr,
+                            double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = exp(xsub(v[i], *m_ptr));
 }
 
-// One thread per 4096-chunk: serial sum of kval over each particle's list and
-// of the list counts (mean_kernel, neighbor_search.cpp:182-190).
-__global__ void k_chunk_sum_kernel(const float* __restrict__ kval, const int32_t* __restrict__ count, int64_t n, int k,
-                                   double* __restrict__ partial_k, double* __restrict__ partial_c) {
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+// Per-particle list sums for mean_kernel (neighbor_search.cpp:182-190): the
+// kval sum in slot order and the entry count.
+__global__ void k_list_sums(const float* __restrict__ kval, const int32_t* __restrict__ count, int64_t n, int k,
+                            double* __restrict__ ksum, double* __restrict__ csum) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  const int cnt = count[i];
+  for (int q = 0; q < cnt; ++q) s = xadd(s, static_cast<double>(kval[i * k + q]));
+  ksum[i] = s;
+  csum[i] = static_cast<double>(cnt);
+}
+
+// reduce.hpp:22-27: one warp per 4096-element chunk; the warp stages 1024
+// values at a time in shared memory (coalesced) and lane 0 adds them serially
+// in index order, so every chunk partial is bit-identical to the reference's.
+constexpr int kStage = 1024;
+__global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ v, int64_t n,
+                                                     double* __restrict__ partial) {
+  __shared__ double s[kStage];
+  const int64_t c = blockIdx.x;
   const int64_t begin = c * kReduceChunk;
-  if (begin >= n) return;
   const int64_t end = begin + kReduceChunk < n ? begin + kReduceChunk : n;
-  double acc = 0.0, ent = 0.0;
-  for (int64_t i = begin; i < end; ++i) {
-    double s = 0.0;
-    const int cnt = count[i];
-    for (int q = 0; q < cnt; ++q) s = xadd(s, static_cast<double>(kval[i * k + q]));
-    acc = xadd(acc, s);
-    ent = xadd(ent, static_cast<double>(cnt));
+  double acc = 0.0;
+  for (int64_t b = begin; b < end; b += kStage) {
+    const int64_t m = end - b < kStage ? end - b : kStage;
+    for (int q = threadIdx.x; q < m; q += 32) s[q] = v[b + q];
+    __syncwarp();
+    if (threadIdx.x == 0)
+      for (int q = 0; q < m; ++q) acc = xadd(acc, s[q]);
+    __syncwarp();
   }
-  partial_k[c] = acc;
-  partial_c[c] = ent;
+  if (threadIdx.x == 0) partial[c] = acc;
 }
 
 // Serial combine of chunk partials (single thread): lse = m + log(sum).
@@ -218,16 +227,25 @@ void launch_max_of_partials(const double* pv, const long long* pi, int64_t n, do
   count_launch();
   k_argmax<<<1, 256, 0, st>>>(pv, pi, n, 0, out_v, out_i);
 }
-void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* partial, cudaStream_t st) {
+static void chunk_serial(const double* v, int64_t n, double* partial, cudaStream_t st) {
   count_launch();
   const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
-  if (chunks > 0) k_chunk_sum_exp<<<blocks_for(chunks, 32), 32, 0, st>>>(v, n, m, partial);
+  if (chunks > 0) k_chunk_serial<<<static_cast<unsigned>(chunks), 32, 0, st>>>(v, n, partial);
 }
-void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n, int k, double* pk, double* pc,
-                             cudaStream_t st) {
+void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* scratch, double* partial,
+                          cudaStream_t st) {
   count_launch();
-  const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
-  if (chunks > 0) k_chunk_sum_kernel<<<blocks_for(chunks, 32), 32, 0, st>>>(kval, count, n, k, pk, pc);
+  if (n <= 0) return;
+  k_exp_shift<<<blocks_for(n, 256), 256, 0, st>>>(v, n, m, scratch);
+  chunk_serial(scratch, n, partial, st);
+}
+void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n, int k, double* s1, double* s2,
+                             double* pk, double* pc, cudaStream_t st) {
+  count_launch();
+  if (n <= 0) return;
+  k_list_sums<<<blocks_for(n, 256), 256, 0, st>>>(kval, count, n, k, s1, s2);
+  chunk_serial(s1, n, pk, st);
+  chunk_serial(s2, n, pc, st);
 }
 void launch_finish_lse(const double* partial, int64_t n_chunks, const double* m, double* lse, cudaStream_t st) {
   count_launch();

@@ -1,0 +1,124 @@
+"""CPU checks of the drop-in boundary: libsmcl_gpu.so loads, exports every
+symbol include/smcl_gpu.h declares, its host-side preparation (map load / scan
+input, reference gaussian_cloud.cpp / nnf.cpp / filter.cpp:86-100) equals the
+oracle bit for bit, and the product never routes through the oracle."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import room_scene
+from paper_2404_16370_b200 import _lib, api, sim
+from paper_2404_16370_b200.abi import make_config
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "smcl_gpu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(smcl_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    names = header_functions()
+    assert len(names) >= 40
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(_lib.SIGNATURES), set(names) ^ set(_lib.SIGNATURES)
+    assert L.smcl_abi_version() == 1
+
+
+def test_default_config_matches_reference_defaults():
+    c = make_config()
+    from paper_2404_16370_b200.abi import SmclConfig
+    d = SmclConfig()
+    import ctypes
+    _lib.lib().smcl_config_default(ctypes.byref(d))
+    for k, _ in SmclConfig._fields_:
+        assert getattr(c, k) == getattr(d, k), k
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2404_16370_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "libsmcl_oracle" not in txt and "oracle/src" not in txt, f
+
+
+def test_host_prep_matches_oracle_bitwise():
+    rects, mapc, scan = room_scene()
+    assert np.array_equal(O.estimate_covariances(mapc.mu, 10), mapc.sigma)
+    d1, o1, c1 = api.build_nnf(mapc, 0.2, 0.5, 1.0)
+    om = O.OracleMap(mapc.mu, mapc.sigma, None, 0.2, 0.5, 1.0)
+    d2, o2, c2 = om.nnf()
+    assert np.array_equal(d1, d2) and np.array_equal(o1, o2) and np.array_equal(c1, c2)
+    pose = np.zeros(12)
+    pose[[0, 4, 8]] = 1.0
+    pose[9:] = [4.0, 3.0, 1.5]
+    pts, _ = sim.simulate_scan_points(rects, pose, sim.sensor_spec(n_azimuth=256), 9)
+    for leaf in (0.05, 0.2):
+        assert np.array_equal(api.downsample_to(pts, 300, leaf), O.downsample_to(pts, 300, leaf))
+    cfg = make_config(n_scan_max=200)
+    a = api.make_scan_cloud(pts, cfg)
+    mu, sg = O.make_scan_cloud(pts, cfg)
+    assert np.array_equal(a.mu, mu) and np.array_equal(a.sigma, sg)
+    assert len(api.make_scan_cloud(np.zeros((3, 3)), cfg)) == 0
+
+
+def test_nnf_exhaustive_brute_force():
+    """test_map_model.cpp: every cell holds the exact nearest map point within
+    max_query_dist (ties to the lower index), else -1."""
+    rng = np.random.default_rng(3)
+    mu = rng.uniform(0.0, 2.0, size=(150, 3))
+    sig = np.tile((1e-4 * np.eye(3)).reshape(9), (150, 1))
+    cloud = api.GaussianCloud(mu, sig)
+    dims, origin, cells = api.build_nnf(cloud, 0.2, 0.3, 0.5)
+    nx, ny, nz = dims
+    for c in range(0, len(cells), 7):
+        x, y, z = c % nx, (c // nx) % ny, c // (nx * ny)
+        ctr = origin + 0.2 * (np.array([x, y, z]) + 0.5)
+        d2 = np.sum((mu - ctr) ** 2, 1)
+        ok = d2 < 0.25
+        want = -1 if not ok.any() else int(np.flatnonzero(d2 == d2[ok].min())[0])
+        assert cells[c] == want
+
+
+def test_nnf_budget_and_errors():
+    mu = np.array([[0.0, 0.0, 0.0], [100.0, 100.0, 100.0]])
+    cloud = api.GaussianCloud(mu, np.tile(np.eye(3).reshape(9), (2, 1)))
+    with pytest.raises(_lib.SmclError):
+        api.build_nnf(cloud, 0.01, 0.5)  # > 2^30 cells: runtime_error
+    with pytest.raises(ValueError):
+        api.build_nnf(cloud, -1.0, 0.5)
+
+
+def test_sim_world_matches_reference_geometry():
+    rects = sim.corridor_world()
+    b = sim.world_bounds(rects)
+    assert np.allclose(b, [0, 0, 0, 40.0, 8.0, 3.0])
+    pts = sim.sample_world_points(rects, 100.0, 5)
+    assert len(pts) == 94590  # sum of round(area * 100) over the rectangles
+    box = sim.box_room([10.0, 10.0, 3.0])
+    pose = np.zeros(12)
+    pose[[0, 4, 8]] = 1.0
+    pose[9:] = [5.0, 5.0, 1.5]
+    p, st = sim.simulate_scan_points(box, pose, sim.sensor_spec(noise_sigma=0.0), 1)
+    w = p + pose[9:]
+    on_wall = np.isclose(w[:, 0], 0) | np.isclose(w[:, 0], 10) | np.isclose(w[:, 1], 0) | np.isclose(
+        w[:, 1], 10) | np.isclose(w[:, 2], 0) | np.isclose(w[:, 2], 3)
+    assert len(p) == 80 and on_wall.all()
+
+
+def test_no_gpu_means_loud_failure():
+    if api.device_count() > 0:
+        pytest.skip("GPU present")
+    rects, mapc, scan = room_scene()
+    with pytest.raises(Exception):
+        api.FilterEngine(mapc, make_config(nnf_resolution=0.2))
