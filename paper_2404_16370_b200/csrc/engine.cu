@@ -294,6 +294,7 @@ struct smcl_engine {
   struct ScanDev {
     int n = 0;
     bool structured = false;
+    double l1max = 0.0;  // max_k |mu_k|_1 (fast-path error bound)
     DBuf<double> mu, sigma;
     DBuf<float4> rec;
   };
@@ -463,6 +464,9 @@ struct smcl_engine {
       rec[2 * q + 1] = make_float4(u[0], u[1], u[2], s);
     }
     sd.structured = ok;
+    sd.l1max = 0.0;
+    for (int q = 0; q < n; ++q)
+      sd.l1max = std::max(sd.l1max, std::fabs(mu[3 * q]) + std::fabs(mu[3 * q + 1]) + std::fabs(mu[3 * q + 2]));
     if (ok) sd.rec.upload(rec.data(), rec.size(), st);
   }
 
@@ -506,7 +510,9 @@ struct smcl_engine {
   }
 
   bool use_fast(const ScanDev& sd) const {
-    const bool can = map_structured && sd.structured && sd.n <= kFastMaxScan;
+    // Fast-path queue entries pack (k, ix, iy, iz) in 16-bit fields.
+    const bool small_dims = geom.dims[0] < 65535 && geom.dims[1] < 65535 && geom.dims[2] < 65535;
+    const bool can = map_structured && sd.structured && sd.n <= kFastMaxScan && small_dims;
     if (cfg.likelihood_mode == 1) return false;
     if (cfg.likelihood_mode == 2) {
       if (!can) throw std::invalid_argument("likelihood_mode=fast needs plane-model map and scan covariances");
@@ -530,7 +536,7 @@ struct smcl_engine {
   void run_likelihood(bool gn, const ScanDev& sd) {
     if (!has_map) throw std::invalid_argument("engine has no map");
     if (sd.n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
-    ScanView sv{sd.n, sd.mu.p, sd.sigma.p, sd.structured ? sd.rec.p : nullptr};
+    ScanView sv{sd.n, sd.mu.p, sd.sigma.p, sd.structured ? sd.rec.p : nullptr, sd.l1max};
     if (profiling) mark(gn ? E_GN0 : E_LL0);
     fast_used = use_fast(sd);
     if (fast_used) {

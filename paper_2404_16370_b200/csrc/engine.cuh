@@ -46,6 +46,7 @@ struct ScanView {
   const double* mu;     // n*3 fp64 (exact transform input)
   const double* sigma;  // n*9 fp64 (exact mode)
   const float4* rec;    // n*2 (fast mode, may be null)
+  double mu_l1_max;     // max_k |mu_k|_1, for the fp32 prefilter error bound
 };
 
 // Particle-point GN system accumulators as written by the likelihood kernels:

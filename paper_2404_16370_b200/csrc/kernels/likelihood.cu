@@ -181,261 +181,6 @@ __global__ void __launch_bounds__(128) k_gicp_exact(const Pose* __restrict__ pos
   nm_out[i] = nmatch;
 }
 
-// ---------------------------------------------------------------- fast kernel
-constexpr int kFastWarps = 8;             // warps per CTA
-constexpr int kFastUnroll = 4;            // points per lane in flight in phase A
-constexpr int kQueue = 32 * kFastUnroll + 32;
-
-struct FastShared {
-  // per-warp compaction queues (SoA): frac xyz, scan index, cell index
-  float qfx[kFastWarps][kQueue];
-  float qfy[kFastWarps][kQueue];
-  float qfz[kFastWarps][kQueue];
-  int qk[kFastWarps][kQueue];
-  int qc[kFastWarps][kQueue];
-};
-
-template <bool GN>
-struct Acc {
-  float hbr[6];   // Omega' lower: 00,10,11,20,21,22
-  float htr[9];   // [mu]x Omega'
-  float htl[6];   // lower of -W [mu]x
-  float b[6];
-  float cost;     // sum e^T Omega e
-};
-
-template <bool GN>
-__device__ __forceinline__ void fast_item(Acc<GN>& acc, const float Rf[9], const float fr[3], float res,
-                                          const float4 m0, const float4 m1, const float4 s0, const float4 s1) {
-  // World residual e = mu_M - p = (mu_M - corner) - frac*res.
-  const float ewx = fmaf(-fr[0], res, m0.x), ewy = fmaf(-fr[1], res, m0.y), ewz = fmaf(-fr[2], res, m0.z);
-  // Body frame: e' = R^T e_w, m' = R^T u_M, n' = u_s, mu = scan mean.
-  const float ex = Rf[0] * ewx + Rf[3] * ewy + Rf[6] * ewz;
-  const float ey = Rf[1] * ewx + Rf[4] * ewy + Rf[7] * ewz;
-  const float ez = Rf[2] * ewx + Rf[5] * ewy + Rf[8] * ewz;
-  const float mx = Rf[0] * m1.x + Rf[3] * m1.y + Rf[6] * m1.z;
-  const float my = Rf[1] * m1.x + Rf[4] * m1.y + Rf[7] * m1.z;
-  const float mz = Rf[2] * m1.x + Rf[5] * m1.y + Rf[8] * m1.z;
-  const float nx = s1.x, ny = s1.y, nz = s1.z;
-  const float beta = m0.w, sM = m1.w, gam = s0.w, sS = s1.w;
-  // Sigma_M' + Sigma_s = A I - beta m m^T - gam n n^T; Woodbury with
-  // Delta = A (sM + sS) + beta gam |m x n|^2 (all terms >= 0: no cancellation).
-  const float A = (beta + sM) + (gam + sS);
-  const float Ssum = sM + sS;
-  const float AmB = sM + gam + sS;   // A - beta
-  const float AmG = beta + sM + sS;  // A - gam
-  const float c = mx * nx + my * ny + mz * nz;
-  const float cx = my * nz - mz * ny, cy = mz * nx - mx * nz, cz = mx * ny - my * nx;
-  const float w = cx * cx + cy * cy + cz * cz;
-  const float bg = beta * gam;
-  const float invD = 1.0f / fmaf(A, Ssum, bg * w);
-  const float invA = 1.0f / A;
-  const float P = beta * AmG * invD, Q = gam * AmB * invD, T = c * bg * invD;
-  const float x = mx * ex + my * ey + mz * ez;
-  const float y = nx * ex + ny * ey + nz * ez;
-  const float am = fmaf(P, x, T * y), an = fmaf(Q, y, T * x);
-  acc.cost += (ex * ex + ey * ey + ez * ez + am * x + an * y) * invA;
-  if (GN) {
-    const float gx = (ex + am * mx + an * nx) * invA;
-    const float gy = (ey + am * my + an * ny) * invA;
-    const float gz = (ez + am * mz + an * nz) * invA;
-    const float ux = s0.x, uy = s0.y, uz = s0.z;  // scan mean (body frame)
-    // b_top += g x mu ; b_bot -= g
-    acc.b[0] += gy * uz - gz * uy;
-    acc.b[1] += gz * ux - gx * uz;
-    acc.b[2] += gx * uy - gy * ux;
-    acc.b[3] -= gx;
-    acc.b[4] -= gy;
-    acc.b[5] -= gz;
-    // Omega' = invA (I + P m m^T + Q n n^T + T (m n^T + n m^T))
-    const float pm[3] = {P * mx, P * my, P * mz};
-    const float qn[3] = {Q * nx, Q * ny, Q * nz};
-    const float tm[3] = {T * mx, T * my, T * mz};
-    const float tn[3] = {T * nx, T * ny, T * nz};
-    const float mv[3] = {mx, my, mz}, nv[3] = {nx, ny, nz};
-    float O[3][3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int q = 0; q <= r; ++q) {
-        float v = pm[r] * mv[q] + qn[r] * nv[q] + tm[r] * nv[q] + tn[r] * mv[q];
-        if (r == q) v += 1.0f;
-        O[r][q] = O[q][r] = v * invA;
-      }
-    acc.hbr[0] += O[0][0];
-    acc.hbr[1] += O[1][0];
-    acc.hbr[2] += O[1][1];
-    acc.hbr[3] += O[2][0];
-    acc.hbr[4] += O[2][1];
-    acc.hbr[5] += O[2][2];
-    // W = [mu]x Omega'
-    float W[3][3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      W[0][j] = uy * O[2][j] - uz * O[1][j];
-      W[1][j] = uz * O[0][j] - ux * O[2][j];
-      W[2][j] = ux * O[1][j] - uy * O[0][j];
-    }
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int q = 0; q < 3; ++q) acc.htr[r * 3 + q] += W[r][q];
-    // H_tl -= W [mu]x  (lower triangle)
-    float V[3][3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      V[r][0] = W[r][1] * uz - W[r][2] * uy;
-      V[r][1] = W[r][2] * ux - W[r][0] * uz;
-      V[r][2] = W[r][0] * uy - W[r][1] * ux;
-    }
-    acc.htl[0] -= V[0][0];
-    acc.htl[1] -= V[1][0];
-    acc.htl[2] -= V[1][1];
-    acc.htl[3] -= V[2][0];
-    acc.htl[4] -= V[2][1];
-    acc.htl[5] -= V[2][2];
-  }
-}
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-template <bool GN>
-__global__ void __launch_bounds__(kFastWarps * 32, 2)
-    k_gicp_fast(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, double* __restrict__ sys,
-                int32_t* __restrict__ nm_out) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  FastShared& sh = *reinterpret_cast<FastShared*>(smem_raw);
-  double* s_mu = reinterpret_cast<double*>(smem_raw + sizeof(FastShared));       // S*3
-  float4* s_rec = reinterpret_cast<float4*>(s_mu + 3 * ((scan.n + 1) & ~1));     // S*2
-  const int S = scan.n;
-  for (int q = threadIdx.x; q < 3 * S; q += blockDim.x) s_mu[q] = scan.mu[q];
-  for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) s_rec[q] = scan.rec[q];
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kFastWarps + wid;
-  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kFastWarps;
-  const NnfGeom g = map.g;
-  const float res = static_cast<float>(g.res);
-  float* qfx = sh.qfx[wid];
-  float* qfy = sh.qfy[wid];
-  float* qfz = sh.qfz[wid];
-  int* qk = sh.qk[wid];
-  int* qc = sh.qc[wid];
-
-  for (int64_t i = gwarp; i < n; i += nwarps) {
-    const Pose P = poses[i];
-    float Rf[9];
-#pragma unroll
-    for (int q = 0; q < 9; ++q) Rf[q] = static_cast<float>(P.R[q]);
-    Acc<GN> acc;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) acc.hbr[q] = acc.htl[q] = acc.b[q] = 0.f;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) acc.htr[q] = 0.f;
-    acc.cost = 0.f;
-    int head = 0, tail = 0;  // ring: [head, tail)
-    int nmatch = 0;
-
-    auto drain = [&](int avail_min) {
-      while (tail - head >= avail_min && tail - head > 0) {
-        const int take = min(32, tail - head);
-        if (lane < take) {
-          const int slot = (head + lane) % kQueue;
-          const int k = qk[slot];
-          const int64_t c = qc[slot];
-          const float fr[3] = {qfx[slot], qfy[slot], qfz[slot]};
-          const float4 m0 = __ldg(map.rec + 2 * c), m1 = __ldg(map.rec + 2 * c + 1);
-          fast_item<GN>(acc, Rf, fr, res, m0, m1, s_rec[2 * k], s_rec[2 * k + 1]);
-        }
-        head += take;
-      }
-    };
-
-    for (int base = 0; base < S; base += 32 * kFastUnroll) {
-      int64_t cell[kFastUnroll];
-      float fr[kFastUnroll][3];
-      float4 r0[kFastUnroll];
-#pragma unroll
-      for (int u = 0; u < kFastUnroll; ++u) {
-        const int k = base + u * 32 + lane;
-        cell[u] = -1;
-        if (k < S) {
-          const double mu[3] = {s_mu[3 * k], s_mu[3 * k + 1], s_mu[3 * k + 2]};
-          double p[3], f64[3];
-          transform_x(P, mu, p);
-          cell[u] = nnf_cell(g, p, f64);
-          fr[u][0] = static_cast<float>(f64[0]);
-          fr[u][1] = static_cast<float>(f64[1]);
-          fr[u][2] = static_cast<float>(f64[2]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kFastUnroll; ++u)
-        r0[u] = cell[u] >= 0 ? __ldg(map.rec + 2 * cell[u]) : make_float4(0.f, 0.f, 0.f, -1.f);
-#pragma unroll
-      for (int u = 0; u < kFastUnroll; ++u) {
-        const bool hit = r0[u].w >= 0.f;
-        const unsigned mask = __ballot_sync(0xffffffffu, hit);
-        if (hit) {
-          const int slot = (tail + __popc(mask & ((1u << lane) - 1u))) % kQueue;
-          qk[slot] = base + u * 32 + lane;
-          qc[slot] = static_cast<int>(cell[u]);
-          qfx[slot] = fr[u][0];
-          qfy[slot] = fr[u][1];
-          qfz[slot] = fr[u][2];
-        }
-        tail += __popc(mask);
-        nmatch += __popc(mask);
-      }
-      __syncwarp();
-      drain(32);
-      __syncwarp();
-    }
-    drain(1);
-    __syncwarp();
-
-    // Warp reduction of the 28 accumulators; lane 0 writes the system record.
-    double* out = sys + i * kSysStride;
-    const float cost = warp_sum(acc.cost);
-    if (GN) {
-      float hbr[6], htl[6], htr[9], b[6];
-#pragma unroll
-      for (int q = 0; q < 6; ++q) {
-        hbr[q] = warp_sum(acc.hbr[q]);
-        htl[q] = warp_sum(acc.htl[q]);
-        b[q] = warp_sum(acc.b[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < 9; ++q) htr[q] = warp_sum(acc.htr[q]);
-      if (lane == 0) {
-        const int li[6][2] = {{0, 0}, {1, 0}, {1, 1}, {2, 0}, {2, 1}, {2, 2}};
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const int r = li[q][0], c = li[q][1];
-          out[r * 6 + c] = out[c * 6 + r] = htl[q];
-          out[(r + 3) * 6 + c + 3] = out[(c + 3) * 6 + r + 3] = hbr[q];
-        }
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) out[r * 6 + c + 3] = out[(c + 3) * 6 + r] = htr[r * 3 + c];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) out[36 + q] = b[q];
-      }
-    }
-    if (lane == 0) {
-      out[42] = nmatch == 0 ? -1e30 : -static_cast<double>(cost);
-      nm_out[i] = nmatch;
-    }
-    __syncwarp();
-  }
-}
-
 // ---------------------------------------------------------------- solve
 // Eigen LLT (lower, unblocked) + two triangular solves, oracle order.
 __device__ bool llt6_solve(const double* A, const double* b, double* x) {
@@ -588,29 +333,6 @@ void launch_gicp_exact(bool gn, const Pose* poses, int64_t n, const ScanView& sc
     k_gicp_exact<true><<<blocks_for(n, 128), 128, 0, st>>>(poses, n, scan, map, sys, nm);
   else
     k_gicp_exact<false><<<blocks_for(n, 128), 128, 0, st>>>(poses, n, scan, map, sys, nm);
-}
-
-static size_t fast_smem(int S) { return sizeof(FastShared) + sizeof(double) * 3 * ((S + 1) & ~1) + sizeof(float4) * 2 * S; }
-
-void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys,
-                      int32_t* nm, cudaStream_t st) {
-  count_launch();
-  if (n <= 0) return;
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_gicp_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
-    cudaFuncSetAttribute(k_gicp_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
-  }
-  const size_t smem = fast_smem(scan.n);
-  const int64_t want = (n + kFastWarps - 1) / kFastWarps;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(n_sm) * 2 * 8));
-  if (gn)
-    k_gicp_fast<true><<<grid, kFastWarps * 32, smem, st>>>(poses, n, scan, map, sys, nm);
-  else
-    k_gicp_fast<false><<<grid, kFastWarps * 32, smem, st>>>(poses, n, scan, map, sys, nm);
 }
 
 void launch_solve(const double* sys, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* steps, double* ll,

@@ -1,0 +1,385 @@
+// K1 / K2 fast path: per-particle GICP likelihood (+ Gauss-Newton system) for
+// plane-model maps and scans (reference gicp.cpp:11-45, 109-137).
+//
+// One warp per particle; lanes stride over the scan points.
+//
+// Phase A (every point, fp32 + int only): the point is transformed with an
+// fp32 copy of the pose pre-scaled to voxel units; the fp32 voxel coordinate
+// carries a rigorous error bound E, so the floor is exact unless the
+// fractional part lies within E of a cell face ("ambiguous"). Certain
+// out-of-bounds points and certain empty cells (one 4-byte flag read of the
+// 32-byte cell record) are dropped here; the rest — matched or ambiguous —
+// are ballot-compacted into a per-warp shared-memory ring.
+//
+// Phase B (compacted candidates, full warps): the exact fp64 transform in the
+// reference's evaluation order (the oracle's bits), the residual from the
+// fp64 fractional voxel coordinate, then the body-frame structured-covariance
+// algebra in fp32:
+//   Sigma_M' + Sigma_s = A I - beta m m^T - gamma n n^T,
+//   Omega' = (1/A)(I + P m m^T + Q n n^T + T (m n^T + n m^T)),
+//   Delta  = A (s_M + s_S) + beta gamma |m x n|^2   (no cancellation),
+// accumulating ll, H (21) and b (6) per lane; a shuffle reduction gives the
+// per-particle system. Ambiguous candidates resolve their cell exactly in fp64.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "../engine.cuh"
+#include "../kernels.cuh"
+
+namespace smcl {
+
+namespace {
+
+constexpr int kFastWarps = 8;      // warps per CTA
+constexpr int kFastUnroll = 4;     // points per lane per phase-A step (loads in flight)
+constexpr int kQueue = 256;        // per-warp ring (>= 32*U + 31), power of two
+constexpr unsigned kResolve = 0xFFFFu;
+
+struct FastShared {
+  uint32_t qa[kFastWarps][kQueue];  // scan index k | iz << 16 (iz == 0xFFFF: resolve exactly)
+  uint32_t qb[kFastWarps][kQueue];  // ix | iy << 16
+};
+
+struct Acc {
+  float hbr[6];  // Omega' lower: 00,10,11,20,21,22
+  float htr[9];  // [mu]x Omega'
+  float htl[6];  // lower of -W [mu]x
+  float b[6];
+  float cost;    // sum e^T Omega e
+};
+
+template <bool GN>
+__device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const float fr[3], float res, const float4 m0,
+                                          const float4 m1, const float4 s0, const float4 s1) {
+  // World residual e = mu_M - p = (mu_M - corner) - frac*res.
+  const float ewx = fmaf(-fr[0], res, m0.x), ewy = fmaf(-fr[1], res, m0.y), ewz = fmaf(-fr[2], res, m0.z);
+  // Body frame: e' = R^T e_w, m' = R^T u_M, n' = u_s, mu = scan mean.
+  const float ex = Rf[0] * ewx + Rf[3] * ewy + Rf[6] * ewz;
+  const float ey = Rf[1] * ewx + Rf[4] * ewy + Rf[7] * ewz;
+  const float ez = Rf[2] * ewx + Rf[5] * ewy + Rf[8] * ewz;
+  const float mx = Rf[0] * m1.x + Rf[3] * m1.y + Rf[6] * m1.z;
+  const float my = Rf[1] * m1.x + Rf[4] * m1.y + Rf[7] * m1.z;
+  const float mz = Rf[2] * m1.x + Rf[5] * m1.y + Rf[8] * m1.z;
+  const float nx = s1.x, ny = s1.y, nz = s1.z;
+  const float beta = m0.w, sM = m1.w, gam = s0.w, sS = s1.w;
+  const float A = (beta + sM) + (gam + sS);
+  const float Ssum = sM + sS;
+  const float AmB = sM + gam + sS;   // A - beta
+  const float AmG = beta + sM + sS;  // A - gamma
+  const float c = mx * nx + my * ny + mz * nz;
+  const float cx = my * nz - mz * ny, cy = mz * nx - mx * nz, cz = mx * ny - my * nx;
+  const float w = cx * cx + cy * cy + cz * cz;
+  const float bg = beta * gam;
+  const float invD = 1.0f / fmaf(A, Ssum, bg * w);
+  const float invA = 1.0f / A;
+  const float P = beta * AmG * invD, Q = gam * AmB * invD, T = c * bg * invD;
+  const float x = mx * ex + my * ey + mz * ez;
+  const float y = nx * ex + ny * ey + nz * ez;
+  const float am = fmaf(P, x, T * y), an = fmaf(Q, y, T * x);
+  acc.cost += (ex * ex + ey * ey + ez * ez + am * x + an * y) * invA;
+  if (GN) {
+    const float gx = (ex + am * mx + an * nx) * invA;
+    const float gy = (ey + am * my + an * ny) * invA;
+    const float gz = (ez + am * mz + an * nz) * invA;
+    const float ux = s0.x, uy = s0.y, uz = s0.z;  // scan mean (body frame)
+    acc.b[0] += gy * uz - gz * uy;  // b_top += g x mu
+    acc.b[1] += gz * ux - gx * uz;
+    acc.b[2] += gx * uy - gy * ux;
+    acc.b[3] -= gx;  // b_bot -= g
+    acc.b[4] -= gy;
+    acc.b[5] -= gz;
+    const float pm[3] = {P * mx, P * my, P * mz};
+    const float qn[3] = {Q * nx, Q * ny, Q * nz};
+    const float tm[3] = {T * mx, T * my, T * mz};
+    const float tn[3] = {T * nx, T * ny, T * nz};
+    const float mv[3] = {mx, my, mz}, nv[3] = {nx, ny, nz};
+    float O[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int q = 0; q <= r; ++q) {
+        float v = pm[r] * mv[q] + qn[r] * nv[q] + tm[r] * nv[q] + tn[r] * mv[q];
+        if (r == q) v += 1.0f;
+        O[r][q] = O[q][r] = v * invA;
+      }
+    acc.hbr[0] += O[0][0];
+    acc.hbr[1] += O[1][0];
+    acc.hbr[2] += O[1][1];
+    acc.hbr[3] += O[2][0];
+    acc.hbr[4] += O[2][1];
+    acc.hbr[5] += O[2][2];
+    float W[3][3];  // W = [mu]x Omega'
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      W[0][j] = uy * O[2][j] - uz * O[1][j];
+      W[1][j] = uz * O[0][j] - ux * O[2][j];
+      W[2][j] = ux * O[1][j] - uy * O[0][j];
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) acc.htr[r * 3 + q] += W[r][q];
+    // H_tl -= W [mu]x (lower triangle)
+    acc.htl[0] -= W[0][1] * uz - W[0][2] * uy;
+    acc.htl[1] -= W[1][1] * uz - W[1][2] * uy;
+    acc.htl[2] -= W[1][2] * ux - W[1][0] * uz;
+    acc.htl[3] -= W[2][1] * uz - W[2][2] * uy;
+    acc.htl[4] -= W[2][2] * ux - W[2][0] * uz;
+    acc.htl[5] -= W[2][0] * uy - W[2][1] * ux;
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fp64 value in [0, 1) -> fp32 by truncating the mantissa (|err| < 2^-23),
+// integer ops only (no F2F on the conversion pipe).
+__device__ __forceinline__ float unit_to_f32(double f) {
+  const double one = __dadd_rn(1.0, f);  // [1, 2]
+  const unsigned hi = static_cast<unsigned>(__double2hiint(one));
+  const unsigned lo = static_cast<unsigned>(__double2loint(one));
+  const unsigned m = ((hi & 0xFFFFFu) << 3) | (lo >> 29);
+  return __uint_as_float(0x3F800000u | m) - 1.0f;
+}
+
+// int in [0, 2^31) -> double without the conversion pipe (1.5*2^52 trick).
+__device__ __forceinline__ double i2d(int v) { return __hiloint2double(0x43380000, v) - 6755399441055744.0; }
+
+__device__ __forceinline__ void transform_x(const double* R, const double* t, const double mu[3], double p[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    p[i] = xadd(xadd(xadd(xmul(R[i * 3 + 0], mu[0]), xmul(R[i * 3 + 1], mu[1])), xmul(R[i * 3 + 2], mu[2])), t[i]);
+}
+
+template <bool GN>
+__global__ void __launch_bounds__(kFastWarps * 32, 2)
+    k_gicp_fast(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, double* __restrict__ sys,
+                int32_t* __restrict__ nm_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  FastShared& sh = *reinterpret_cast<FastShared*>(smem_raw);
+  double* s_mu = reinterpret_cast<double*>(smem_raw + sizeof(FastShared));    // S*3 fp64
+  float4* s_rec = reinterpret_cast<float4*>(s_mu + 3 * ((scan.n + 1) & ~1));  // S*2
+  const int S = scan.n;
+  for (int q = threadIdx.x; q < 3 * S; q += blockDim.x) s_mu[q] = scan.mu[q];
+  for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) s_rec[q] = scan.rec[q];
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kFastWarps + wid;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kFastWarps;
+  const NnfGeom g = map.g;
+  const float res = static_cast<float>(g.res);
+  const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2];
+  uint32_t* qa = sh.qa[wid];
+  uint32_t* qb = sh.qb[wid];
+
+  for (int64_t i = gwarp; i < n; i += nwarps) {
+    const Pose P = poses[i];
+    // fp32 pose in voxel units: x = Rs mu + ts, Rs = R/res, ts = (t - o)/res.
+    float Rs[9], ts[3], Rf[9];
+    float tmax = 0.f;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      Rs[q] = static_cast<float>(P.R[q] * g.inv_res);
+      Rf[q] = static_cast<float>(P.R[q]);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      ts[a] = static_cast<float>((P.t[a] - g.origin[a]) * g.inv_res);
+      tmax = fmaxf(tmax, fabsf(ts[a]));
+    }
+    // Rigorous bound on |x32 - x64| (2x slack): see DESIGN.md §3 (K1).
+    const float E = 2.0f * 5.9604645e-8f *
+                        (7.0f * static_cast<float>(scan.mu_l1_max * g.inv_res) + 4.0f * tmax) + 1e-6f;
+    const bool finite_pose = tmax < 1.0e6f;  // NaN or far away: resolve exactly
+    Acc acc;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) acc.hbr[q] = acc.htl[q] = acc.b[q] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc.htr[q] = 0.f;
+    acc.cost = 0.f;
+    int head = 0, tail = 0;
+    int nmatch = 0;
+
+    auto drain = [&](int avail_min) {
+      while (tail - head >= avail_min && tail - head > 0) {
+        const int take = min(32, tail - head);
+        bool valid = false;
+        if (lane < take) {
+          const int slot = (head + lane) & (kQueue - 1);
+          const uint32_t a = qa[slot], b = qb[slot];
+          const int k = static_cast<int>(a & 0xFFFFu);
+          int iz = static_cast<int>(a >> 16), ix = static_cast<int>(b & 0xFFFFu), iy = static_cast<int>(b >> 16);
+          const double mu[3] = {s_mu[3 * k], s_mu[3 * k + 1], s_mu[3 * k + 2]};
+          double p[3], x[3];
+          transform_x(P.R, P.t, mu, p);
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) x[ax] = xmul(xsub(p[ax], g.origin[ax]), g.inv_res);
+          valid = true;
+          double f[3];
+          bool resolve = iz == static_cast<int>(kResolve);
+          if (!resolve) {
+            f[0] = xsub(x[0], i2d(ix));
+            f[1] = xsub(x[1], i2d(iy));
+            f[2] = xsub(x[2], i2d(iz));
+            // Safety net: the fp32 floor must agree with the exact one.
+            resolve = !(f[0] >= 0.0 && f[0] < 1.0 && f[1] >= 0.0 && f[1] < 1.0 && f[2] >= 0.0 && f[2] < 1.0);
+          }
+          if (resolve) {  // exact floor + bounds (nnf.hpp:24-35)
+            int c3[3];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+              const double fl = floor(x[ax]);
+              valid = valid && (fl >= 0.0 && fl < static_cast<double>(g.dims[ax]));
+              c3[ax] = valid ? static_cast<int>(fl) : 0;
+              f[ax] = xsub(x[ax], fl);
+            }
+            ix = c3[0];
+            iy = c3[1];
+            iz = c3[2];
+          }
+          const int64_t c = (static_cast<int64_t>(iz) * ny + iy) * nx + ix;
+          float4 m0 = make_float4(0.f, 0.f, 0.f, -1.f), m1 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (valid) {
+            m0 = __ldg(map.rec + 2 * c);
+            m1 = __ldg(map.rec + 2 * c + 1);
+          }
+          valid = valid && m0.w >= 0.f;
+          if (valid) {
+            const float fr[3] = {unit_to_f32(f[0]), unit_to_f32(f[1]), unit_to_f32(f[2])};
+            fast_item<GN>(acc, Rf, fr, res, m0, m1, s_rec[2 * k], s_rec[2 * k + 1]);
+          }
+        }
+        nmatch += __popc(__ballot_sync(0xffffffffu, valid));
+        head += take;
+      }
+    };
+
+    for (int base = 0; base < S; base += 32 * kFastUnroll) {
+      int cell[kFastUnroll];
+      uint32_t pa[kFastUnroll], pb[kFastUnroll];
+      bool cand[kFastUnroll];
+#pragma unroll
+      for (int u = 0; u < kFastUnroll; ++u) {
+        const int k = base + u * 32 + lane;
+        cell[u] = -1;
+        cand[u] = false;
+        if (k < S) {
+          const float4 s0 = s_rec[2 * k];
+          int ic[3];
+          bool amb = !finite_pose, inb = true;
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) {
+            const float xv =
+                fmaf(Rs[ax * 3 + 2], s0.z, fmaf(Rs[ax * 3 + 1], s0.y, Rs[ax * 3 + 0] * s0.x)) + ts[ax];
+            const float y = __fadd_rd(xv, 12582912.0f);  // floor via 1.5*2^23 (|x| < 2^21 here)
+            const float fl = y - 12582912.0f;
+            const float fr = xv - fl;
+            ic[ax] = __float_as_int(y) - 0x4B400000;
+            amb = amb || !(fabsf(xv) < 2097152.0f) || fr < E || fr > 1.0f - E;
+            inb = inb && static_cast<unsigned>(ic[ax]) < static_cast<unsigned>(g.dims[ax]);
+          }
+          pa[u] = static_cast<uint32_t>(k);
+          if (amb) {
+            cand[u] = true;
+            pa[u] |= kResolve << 16;
+            pb[u] = 0u;
+          } else if (inb) {
+            cell[u] = (ic[2] * ny + ic[1]) * nx + ic[0];
+            pa[u] |= static_cast<uint32_t>(ic[2]) << 16;
+            pb[u] = static_cast<uint32_t>(ic[0]) | (static_cast<uint32_t>(ic[1]) << 16);
+          }
+        }
+      }
+      float flag[kFastUnroll];
+#pragma unroll
+      for (int u = 0; u < kFastUnroll; ++u)
+        flag[u] = cell[u] >= 0 ? __ldg(reinterpret_cast<const float*>(map.rec + 2 * static_cast<int64_t>(cell[u])) + 3)
+                               : -1.f;
+#pragma unroll
+      for (int u = 0; u < kFastUnroll; ++u) {
+        const bool hit = cand[u] || flag[u] >= 0.f;
+        const unsigned mask = __ballot_sync(0xffffffffu, hit);
+        if (hit) {
+          const int slot = (tail + __popc(mask & ((1u << lane) - 1u))) & (kQueue - 1);
+          qa[slot] = pa[u];
+          qb[slot] = pb[u];
+        }
+        tail += __popc(mask);
+      }
+      __syncwarp();
+      drain(32);
+      __syncwarp();
+    }
+    drain(1);
+    __syncwarp();
+
+    double* out = sys + i * kSysStride;
+    const float cost = warp_sum(acc.cost);
+    if (GN) {
+      float hbr[6], htl[6], htr[9], b[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        hbr[q] = warp_sum(acc.hbr[q]);
+        htl[q] = warp_sum(acc.htl[q]);
+        b[q] = warp_sum(acc.b[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 9; ++q) htr[q] = warp_sum(acc.htr[q]);
+      if (lane == 0) {
+        const int li[6][2] = {{0, 0}, {1, 0}, {1, 1}, {2, 0}, {2, 1}, {2, 2}};
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+          const int r = li[q][0], c = li[q][1];
+          out[r * 6 + c] = out[c * 6 + r] = htl[q];
+          out[(r + 3) * 6 + c + 3] = out[(c + 3) * 6 + r + 3] = hbr[q];
+        }
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) out[r * 6 + c + 3] = out[(c + 3) * 6 + r] = htr[r * 3 + c];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) out[36 + q] = b[q];
+      }
+    }
+    if (lane == 0) {
+      out[42] = nmatch == 0 ? -1e30 : -static_cast<double>(cost);
+      nm_out[i] = nmatch;
+    }
+    __syncwarp();
+  }
+}
+
+size_t fast_smem(int S) { return sizeof(FastShared) + sizeof(double) * 3 * ((S + 1) & ~1) + sizeof(float4) * 2 * S; }
+
+}  // namespace
+
+void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys,
+                      int32_t* nm, cudaStream_t st) {
+  count_launch();
+  if (n <= 0) return;
+  static int grid_full[2] = {0, 0};
+  const size_t smem = fast_smem(scan.n);
+  const int gi = gn ? 1 : 0;
+  if (!grid_full[gi]) {
+    int dev, n_sm, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    auto fn = gn ? k_gicp_fast<true> : k_gicp_fast<false>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFastWarps * 32, fast_smem(1024));
+    grid_full[gi] = n_sm * std::max(per_sm, 1);
+  }
+  const int64_t want = (n + kFastWarps - 1) / kFastWarps;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, grid_full[gi]));
+  if (gn)
+    k_gicp_fast<true><<<grid, kFastWarps * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+  else
+    k_gicp_fast<false><<<grid, kFastWarps * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+}
+
+}  // namespace smcl
