@@ -1,15 +1,19 @@
 // K1 / K2 fast path: per-particle GICP likelihood (+ Gauss-Newton system) for
 // plane-model maps and scans (reference gicp.cpp:11-45, 109-137).
 //
-// One warp per particle; lanes stride over the scan points.
+// One warp per particle; lanes stride over the scan points, 256 points per
+// step (8 per lane).
 //
 // Phase A (every point, fp32 + int only): the point is transformed with an
 // fp32 copy of the pose pre-scaled to voxel units; the fp32 voxel coordinate
-// carries a rigorous error bound E, so the floor is exact unless the
-// fractional part lies within E of a cell face ("ambiguous"). Certain
-// out-of-bounds points and certain empty cells (one 4-byte flag read of the
-// 32-byte cell record) are dropped here; the rest — matched or ambiguous —
-// are ballot-compacted into a per-warp shared-memory ring.
+// carries a rigorous error bound E, so its floor equals the reference's fp64
+// floor unless the fractional part lies within E of a cell face
+// ("ambiguous"). Certain out-of-bounds points are dropped; every other
+// unambiguous point starts a cp.async of its 32-byte cell record into a
+// per-warp shared-memory stage, so 16 x 16-byte gathers per lane are in flight
+// at once (the global-init workload's record gathers are random: the kernel is
+// L2-latency bound, not bandwidth bound). After the wait, empty cells are
+// dropped and the survivors (plus ambiguous points) are ballot-compacted.
 //
 // Phase B (compacted candidates, full warps): the exact fp64 transform in the
 // reference's evaluation order (the oracle's bits), the residual from the
@@ -31,14 +35,16 @@ namespace smcl {
 
 namespace {
 
-constexpr int kFastWarps = 8;      // warps per CTA
-constexpr int kFastUnroll = 4;     // points per lane per phase-A step (loads in flight)
-constexpr int kQueue = 256;        // per-warp ring (>= 32*U + 31), power of two
+constexpr int kFastWarps = 16;         // warps per CTA (one CTA per SM: 16 warps x 128 registers)
 constexpr unsigned kResolve = 0xFFFFu;
 
-struct FastShared {
-  uint32_t qa[kFastWarps][kQueue];  // scan index k | iz << 16 (iz == 0xFFFF: resolve exactly)
-  uint32_t qb[kFastWarps][kQueue];  // ix | iy << 16
+template <int kStep>
+struct WarpStage {
+  float4 m0[kStep];     // staged cell records (SoA halves: conflict-free LDS.128)
+  float4 m1[kStep];
+  uint32_t qa[kStep];   // compacted candidates: k | iz << 16 (iz == 0xFFFF: resolve exactly)
+  uint32_t qb[kStep];   // ix | iy << 16
+  uint16_t qs[kStep];   // stage slot of the candidate's record
 };
 
 struct Acc {
@@ -48,6 +54,15 @@ struct Acc {
   float b[6];
   float cost;    // sum e^T Omega e
 };
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
 
 template <bool GN>
 __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const float fr[3], float res, const float4 m0,
@@ -155,14 +170,16 @@ __device__ __forceinline__ void transform_x(const double* R, const double* t, co
     p[i] = xadd(xadd(xadd(xmul(R[i * 3 + 0], mu[0]), xmul(R[i * 3 + 1], mu[1])), xmul(R[i * 3 + 2], mu[2])), t[i]);
 }
 
-template <bool GN>
-__global__ void __launch_bounds__(kFastWarps * 32, 2)
+template <bool GN, int kFastUnroll>
+__global__ void __launch_bounds__(kFastWarps * 32, 1)
     k_gicp_fast(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, double* __restrict__ sys,
                 int32_t* __restrict__ nm_out) {
+  constexpr int kStep = 32 * kFastUnroll;
+  using Stage = WarpStage<kStep>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  FastShared& sh = *reinterpret_cast<FastShared*>(smem_raw);
-  double* s_mu = reinterpret_cast<double*>(smem_raw + sizeof(FastShared));    // S*3 fp64
-  float4* s_rec = reinterpret_cast<float4*>(s_mu + 3 * ((scan.n + 1) & ~1));  // S*2
+  Stage* stages = reinterpret_cast<Stage*>(smem_raw);
+  double* s_mu = reinterpret_cast<double*>(smem_raw + sizeof(Stage) * kFastWarps);  // S*3 fp64
+  float4* s_rec = reinterpret_cast<float4*>(s_mu + 3 * ((scan.n + 1) & ~1));            // S*2
   const int S = scan.n;
   for (int q = threadIdx.x; q < 3 * S; q += blockDim.x) s_mu[q] = scan.mu[q];
   for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) s_rec[q] = scan.rec[q];
@@ -173,9 +190,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2)
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kFastWarps;
   const NnfGeom g = map.g;
   const float res = static_cast<float>(g.res);
-  const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2];
-  uint32_t* qa = sh.qa[wid];
-  uint32_t* qb = sh.qb[wid];
+  const int nx = g.dims[0], ny = g.dims[1];
+  Stage& ws = stages[wid];
 
   for (int64_t i = gwarp; i < n; i += nwarps) {
     const Pose P = poses[i];
@@ -192,7 +208,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2)
       ts[a] = static_cast<float>((P.t[a] - g.origin[a]) * g.inv_res);
       tmax = fmaxf(tmax, fabsf(ts[a]));
     }
-    // Rigorous bound on |x32 - x64| (2x slack): see DESIGN.md §3 (K1).
+    // Rigorous bound on |x32 - x64| with 2x slack (K1).
     const float E = 2.0f * 5.9604645e-8f *
                         (7.0f * static_cast<float>(scan.mu_l1_max * g.inv_res) + 4.0f * tmax) + 1e-6f;
     const bool finite_pose = tmax < 1.0e6f;  // NaN or far away: resolve exactly
@@ -202,72 +218,18 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2)
 #pragma unroll
     for (int q = 0; q < 9; ++q) acc.htr[q] = 0.f;
     acc.cost = 0.f;
-    int head = 0, tail = 0;
     int nmatch = 0;
 
-    auto drain = [&](int avail_min) {
-      while (tail - head >= avail_min && tail - head > 0) {
-        const int take = min(32, tail - head);
-        bool valid = false;
-        if (lane < take) {
-          const int slot = (head + lane) & (kQueue - 1);
-          const uint32_t a = qa[slot], b = qb[slot];
-          const int k = static_cast<int>(a & 0xFFFFu);
-          int iz = static_cast<int>(a >> 16), ix = static_cast<int>(b & 0xFFFFu), iy = static_cast<int>(b >> 16);
-          const double mu[3] = {s_mu[3 * k], s_mu[3 * k + 1], s_mu[3 * k + 2]};
-          double p[3], x[3];
-          transform_x(P.R, P.t, mu, p);
-#pragma unroll
-          for (int ax = 0; ax < 3; ++ax) x[ax] = xmul(xsub(p[ax], g.origin[ax]), g.inv_res);
-          valid = true;
-          double f[3];
-          bool resolve = iz == static_cast<int>(kResolve);
-          if (!resolve) {
-            f[0] = xsub(x[0], i2d(ix));
-            f[1] = xsub(x[1], i2d(iy));
-            f[2] = xsub(x[2], i2d(iz));
-            // Safety net: the fp32 floor must agree with the exact one.
-            resolve = !(f[0] >= 0.0 && f[0] < 1.0 && f[1] >= 0.0 && f[1] < 1.0 && f[2] >= 0.0 && f[2] < 1.0);
-          }
-          if (resolve) {  // exact floor + bounds (nnf.hpp:24-35)
-            int c3[3];
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-              const double fl = floor(x[ax]);
-              valid = valid && (fl >= 0.0 && fl < static_cast<double>(g.dims[ax]));
-              c3[ax] = valid ? static_cast<int>(fl) : 0;
-              f[ax] = xsub(x[ax], fl);
-            }
-            ix = c3[0];
-            iy = c3[1];
-            iz = c3[2];
-          }
-          const int64_t c = (static_cast<int64_t>(iz) * ny + iy) * nx + ix;
-          float4 m0 = make_float4(0.f, 0.f, 0.f, -1.f), m1 = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (valid) {
-            m0 = __ldg(map.rec + 2 * c);
-            m1 = __ldg(map.rec + 2 * c + 1);
-          }
-          valid = valid && m0.w >= 0.f;
-          if (valid) {
-            const float fr[3] = {unit_to_f32(f[0]), unit_to_f32(f[1]), unit_to_f32(f[2])};
-            fast_item<GN>(acc, Rf, fr, res, m0, m1, s_rec[2 * k], s_rec[2 * k + 1]);
-          }
-        }
-        nmatch += __popc(__ballot_sync(0xffffffffu, valid));
-        head += take;
-      }
-    };
-
-    for (int base = 0; base < S; base += 32 * kFastUnroll) {
-      int cell[kFastUnroll];
+    for (int base = 0; base < S; base += kStep) {
+      // ---- phase A: fp32 cell guess, async record gather
       uint32_t pa[kFastUnroll], pb[kFastUnroll];
-      bool cand[kFastUnroll];
+      uint8_t status[kFastUnroll];  // 0 skip, 1 record staged, 2 resolve exactly
 #pragma unroll
       for (int u = 0; u < kFastUnroll; ++u) {
         const int k = base + u * 32 + lane;
-        cell[u] = -1;
-        cand[u] = false;
+        status[u] = 0;
+        pa[u] = static_cast<uint32_t>(k);
+        pb[u] = 0u;
         if (k < S) {
           const float4 s0 = s_rec[2 * k];
           int ic[3];
@@ -277,46 +239,90 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2)
             const float xv =
                 fmaf(Rs[ax * 3 + 2], s0.z, fmaf(Rs[ax * 3 + 1], s0.y, Rs[ax * 3 + 0] * s0.x)) + ts[ax];
             const float y = __fadd_rd(xv, 12582912.0f);  // floor via 1.5*2^23 (|x| < 2^21 here)
-            const float fl = y - 12582912.0f;
-            const float fr = xv - fl;
+            const float fr = xv - (y - 12582912.0f);
             ic[ax] = __float_as_int(y) - 0x4B400000;
             amb = amb || !(fabsf(xv) < 2097152.0f) || fr < E || fr > 1.0f - E;
             inb = inb && static_cast<unsigned>(ic[ax]) < static_cast<unsigned>(g.dims[ax]);
           }
-          pa[u] = static_cast<uint32_t>(k);
           if (amb) {
-            cand[u] = true;
+            status[u] = 2;
             pa[u] |= kResolve << 16;
-            pb[u] = 0u;
           } else if (inb) {
-            cell[u] = (ic[2] * ny + ic[1]) * nx + ic[0];
+            status[u] = 1;
             pa[u] |= static_cast<uint32_t>(ic[2]) << 16;
             pb[u] = static_cast<uint32_t>(ic[0]) | (static_cast<uint32_t>(ic[1]) << 16);
+            const float4* src = map.rec + 2 * ((static_cast<int64_t>(ic[2]) * ny + ic[1]) * nx + ic[0]);
+            cp_async16(&ws.m0[u * 32 + lane], src);
+            cp_async16(&ws.m1[u * 32 + lane], src + 1);
           }
         }
       }
-      float flag[kFastUnroll];
-#pragma unroll
-      for (int u = 0; u < kFastUnroll; ++u)
-        flag[u] = cell[u] >= 0 ? __ldg(reinterpret_cast<const float*>(map.rec + 2 * static_cast<int64_t>(cell[u])) + 3)
-                               : -1.f;
+      cp_async_wait_all();
+      __syncwarp();
+      int n_cand = 0;
 #pragma unroll
       for (int u = 0; u < kFastUnroll; ++u) {
-        const bool hit = cand[u] || flag[u] >= 0.f;
-        const unsigned mask = __ballot_sync(0xffffffffu, hit);
-        if (hit) {
-          const int slot = (tail + __popc(mask & ((1u << lane) - 1u))) & (kQueue - 1);
-          qa[slot] = pa[u];
-          qb[slot] = pb[u];
+        const bool keep = status[u] == 2 || (status[u] == 1 && ws.m0[u * 32 + lane].w >= 0.f);
+        const unsigned mask = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          const int pos = n_cand + __popc(mask & ((1u << lane) - 1u));
+          ws.qa[pos] = pa[u];
+          ws.qb[pos] = pb[u];
+          ws.qs[pos] = static_cast<uint16_t>(u * 32 + lane);
         }
-        tail += __popc(mask);
+        n_cand += __popc(mask);
       }
       __syncwarp();
-      drain(32);
+      // ---- phase B: exact residual + structured algebra on full warps
+      for (int b0 = 0; b0 < n_cand; b0 += 32) {
+        const int e = b0 + lane;
+        bool valid = false;
+        if (e < n_cand) {
+          const uint32_t a = ws.qa[e], bq = ws.qb[e];
+          const int k = static_cast<int>(a & 0xFFFFu);
+          int iz = static_cast<int>(a >> 16), ix = static_cast<int>(bq & 0xFFFFu), iy = static_cast<int>(bq >> 16);
+          const double mu[3] = {s_mu[3 * k], s_mu[3 * k + 1], s_mu[3 * k + 2]};
+          double p[3], x[3], f[3];
+          transform_x(P.R, P.t, mu, p);
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) x[ax] = xmul(xsub(p[ax], g.origin[ax]), g.inv_res);
+          valid = true;
+          bool resolve = iz == static_cast<int>(kResolve);
+          if (!resolve) {
+            f[0] = xsub(x[0], i2d(ix));
+            f[1] = xsub(x[1], i2d(iy));
+            f[2] = xsub(x[2], i2d(iz));
+            // Safety net: the fp32 floor must agree with the exact one.
+            resolve = !(f[0] >= 0.0 && f[0] < 1.0 && f[1] >= 0.0 && f[1] < 1.0 && f[2] >= 0.0 && f[2] < 1.0);
+          }
+          float4 m0, m1;
+          if (resolve) {  // exact floor + bounds (nnf.hpp:24-35), direct gather
+            int c3[3];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+              const double fl = floor(x[ax]);
+              valid = valid && (fl >= 0.0 && fl < static_cast<double>(g.dims[ax]));
+              c3[ax] = valid ? static_cast<int>(fl) : 0;
+              f[ax] = xsub(x[ax], fl);
+            }
+            const int64_t c = (static_cast<int64_t>(c3[2]) * ny + c3[1]) * nx + c3[0];
+            m0 = valid ? __ldg(map.rec + 2 * c) : make_float4(0.f, 0.f, 0.f, -1.f);
+            m1 = valid ? __ldg(map.rec + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            const int slot = ws.qs[e];
+            m0 = ws.m0[slot];
+            m1 = ws.m1[slot];
+          }
+          valid = valid && m0.w >= 0.f;
+          if (valid) {
+            const float fr[3] = {unit_to_f32(f[0]), unit_to_f32(f[1]), unit_to_f32(f[2])};
+            fast_item<GN>(acc, Rf, fr, res, m0, m1, s_rec[2 * k], s_rec[2 * k + 1]);
+          }
+        }
+        nmatch += __popc(__ballot_sync(0xffffffffu, valid));
+      }
       __syncwarp();
     }
-    drain(1);
-    __syncwarp();
 
     double* out = sys + i * kSysStride;
     const float cost = warp_sum(acc.cost);
@@ -354,32 +360,40 @@ __global__ void __launch_bounds__(kFastWarps * 32, 2)
   }
 }
 
-size_t fast_smem(int S) { return sizeof(FastShared) + sizeof(double) * 3 * ((S + 1) & ~1) + sizeof(float4) * 2 * S; }
+template <int U>
+size_t fast_smem(int S) {
+  return sizeof(WarpStage<32 * U>) * kFastWarps + sizeof(double) * 3 * ((S + 1) & ~1) + sizeof(float4) * 2 * S;
+}
+
+template <bool GN, int U>
+void launch_fast_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys, int32_t* nm,
+                   cudaStream_t st) {
+  const size_t smem = fast_smem<U>(scan.n);
+  int dev, n_sm, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(k_gicp_fast<GN, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gicp_fast<GN, U>, kFastWarps * 32, smem);
+  const int64_t want = (n + kFastWarps - 1) / kFastWarps;
+  const unsigned grid =
+      static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(n_sm) * std::max(per_sm, 1)));
+  k_gicp_fast<GN, U><<<grid, kFastWarps * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+}
 
 }  // namespace
 
+// U = 8 points per lane in flight when the per-SM shared memory allows it
+// (S <= ~640 with 16 warps), else 4.
 void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys,
                       int32_t* nm, cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
-  static int grid_full[2] = {0, 0};
-  const size_t smem = fast_smem(scan.n);
-  const int gi = gn ? 1 : 0;
-  if (!grid_full[gi]) {
-    int dev, n_sm, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    auto fn = gn ? k_gicp_fast<true> : k_gicp_fast<false>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFastWarps * 32, fast_smem(1024));
-    grid_full[gi] = n_sm * std::max(per_sm, 1);
-  }
-  const int64_t want = (n + kFastWarps - 1) / kFastWarps;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(want, grid_full[gi]));
+  const bool big = fast_smem<8>(scan.n) <= 200 * 1024;
   if (gn)
-    k_gicp_fast<true><<<grid, kFastWarps * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+    big ? launch_fast_t<true, 8>(poses, n, scan, map, sys, nm, st) : launch_fast_t<true, 4>(poses, n, scan, map, sys, nm, st);
   else
-    k_gicp_fast<false><<<grid, kFastWarps * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+    big ? launch_fast_t<false, 8>(poses, n, scan, map, sys, nm, st)
+        : launch_fast_t<false, 4>(poses, n, scan, map, sys, nm, st);
 }
 
 }  // namespace smcl

@@ -127,10 +127,39 @@ __global__ void k_seg_stats(const int32_t* __restrict__ seg_start, int32_t n_seg
   if (threadIdx.x == 0 && s_hist[cap + 2]) atomicAdd(overflow, s_hist[cap + 2]);
 }
 
+// Exact float kernel value of the pair (a, b) (neighbor_graph.hpp:84-86,
+// neighbor_search.cpp:161-166): 0 if the translation bound underflows, else
+// (float)exp(-q) with q from the full SE3 log in the reference's order.
+__device__ __forceinline__ float kval_exact(const Pose& a, const Pose& b, double sr, double st) {
+  if (kernel_underflows(a, b, st)) return 0.0f;
+  double d[6];
+  se3_log(inv_compose_x(a, b), d);
+  return __double2float_rn(exp(-kernel_q(d, sr, st)));
+}
+
+// Lower bound of the kernel exponent q = sr |w|^2 + st |v|^2 of the pair:
+// |w| = rotation angle of Ra^T Rb, and |v| >= |tb - ta| because V^-1 of the
+// SE3 log expands (svgd.hpp:40-44). fp32 acos with a 2e-3 rad margin covers
+// its rounding and the <= 1e-7 non-orthonormality renormalize_if_needed allows.
+__device__ __forceinline__ double q_lower_bound(const Pose& a, const Pose& b, double sr, double st) {
+  double tr = 0.0;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) tr = fma(a.R[q], b.R[q], tr);
+  const float c = fminf(1.0f, fmaxf(-1.0f, static_cast<float>(0.5 * (tr - 1.0))));
+  const float th = fmaxf(0.0f, acosf(c) - 2e-3f);
+  const double d0 = b.t[0] - a.t[0], d1 = b.t[1] - a.t[1], d2 = b.t[2] - a.t[2];
+  return (sr * static_cast<double>(th) * static_cast<double>(th) + st * (d0 * d0 + d1 * d1 + d2 * d2)) *
+         (1.0 - 1e-9);
+}
+
 // Fused NeighborGraph::refresh (neighbor_graph.hpp:76-90) and the gather/offer
 // loop (neighbor_search.cpp:151-169) for the particle at sorted position p.
 // Refresh and gather of one particle touch only its own list, so fusing them
-// per particle preserves the reference's two-phase result exactly.
+// per particle preserves the reference's two-phase result exactly. Two exact
+// shortcuts avoid SE3 logs whose outcome is already decided:
+//  * offer() ignores duplicates before looking at k_ij;
+//  * with a full list, a candidate whose kernel upper bound exp(-q_lb) does
+//    not exceed the weakest non-self entry can never be inserted.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict__ all_poses, int64_t n,
                                                           int64_t gbase, const int32_t* __restrict__ pos_list,
@@ -140,8 +169,9 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
                                                           int64_t n_sorted, int32_t* __restrict__ idx,
                                                           float* __restrict__ kval, int32_t* __restrict__ count, int k,
                                                           int cap, double sr, double st) {
-  __shared__ int32_t s_idx[kMaxK][BLOCK];
-  __shared__ float s_kv[kMaxK][BLOCK];
+  extern __shared__ unsigned char rg_smem[];
+  int32_t* s_idx = reinterpret_cast<int32_t*>(rg_smem);         // [k][BLOCK]
+  float* s_kv = reinterpret_cast<float*>(s_idx + k * BLOCK);    // [k][BLOCK]
   const int t = threadIdx.x;
   const int64_t r = static_cast<int64_t>(blockIdx.x) * BLOCK + t;
   if (r >= n) return;
@@ -156,65 +186,59 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
   const int64_t vis_end = re < rb + cap ? re : rb + cap;
 
   int cnt = count[li];
-  for (int s = 0; s < cnt; ++s) {
-    s_idx[s][t] = idx[li * k + s];
-  }
+  for (int s = 0; s < cnt; ++s) s_idx[s * BLOCK + t] = idx[li * k + s];
   const Pose pi = all_poses[gi];
-  // refresh
-  for (int s = 0; s < cnt; ++s) {
-    const int32_t j = s_idx[s][t];
-    float kv = 0.0f;
-    if (j == gi) {
-      kv = 1.0f;
-    } else {
-      const Pose pj = all_poses[j];
-      if (!kernel_underflows(pi, pj, st)) {
-        double d[6];
-        se3_log(inv_compose_x(pi, pj), d);
-        kv = __double2float_rn(exp(-kernel_q(d, sr, st)));
-      }
-    }
-    s_kv[s][t] = kv;
+  for (int s = 0; s < cnt; ++s) {  // refresh
+    const int32_t j = s_idx[s * BLOCK + t];
+    s_kv[s * BLOCK + t] = (j == gi) ? 1.0f : kval_exact(pi, all_poses[j], sr, st);
   }
-  // gather / offer
-  for (int64_t q = rb; q < vis_end; ++q) {
-    const int32_t j = member_of[q];
-    if (j == gi) continue;
-    bool dup = false;
-    for (int s = 0; s < cnt; ++s) dup |= (s_idx[s][t] == j);
-    if (dup) continue;  // offer() ignores duplicates before looking at k_ij
-    const Pose pj = all_poses[j];
-    float kij = 0.0f;
-    if (!kernel_underflows(pi, pj, st)) {
-      double d[6];
-      se3_log(inv_compose_x(pi, pj), d);
-      kij = __double2float_rn(exp(-kernel_q(d, sr, st)));
-    }
-    if (cnt < k) {
-      s_idx[cnt][t] = j;
-      s_kv[cnt][t] = kij;
-      ++cnt;
-      continue;
-    }
-    int weakest = -1;
-    float wk = __int_as_float(0x7f800000);  // +inf
+  // Weakest non-self entry (first strict minimum, neighbor_graph.hpp:60-72)
+  // and its threshold in exponent space.
+  int weakest = -1;
+  float wk = __int_as_float(0x7f800000);
+  double q_skip = 0.0;
+  auto find_weakest = [&]() {
+    weakest = -1;
+    wk = __int_as_float(0x7f800000);
     for (int s = 0; s < cnt; ++s) {
-      if (s_idx[s][t] == gi) continue;
-      const float v = s_kv[s][t];
+      if (s_idx[s * BLOCK + t] == gi) continue;
+      const float v = s_kv[s * BLOCK + t];
       if (v < wk) {
         wk = v;
         weakest = s;
       }
     }
-    if (weakest >= 0 && kij > wk) {
-      s_idx[weakest][t] = j;
-      s_kv[weakest][t] = kij;
+    // k_ij <= exp(-q_lb) <= wk  <=>  q_lb >= -log(wk); 0.0f entries: only
+    // k_ij that round to 0.0f (q > 150 ln 2) are excluded.
+    q_skip = weakest < 0 ? 1e300 : (wk > 0.0f ? -log(static_cast<double>(wk)) * (1.0 + 1e-12) + 1e-12 : 104.0);
+  };
+  if (cnt == k) find_weakest();
+  for (int64_t q = rb; q < vis_end; ++q) {  // gather / offer
+    const int32_t j = member_of[q];
+    if (j == gi) continue;
+    bool dup = false;
+    for (int s = 0; s < cnt; ++s) dup |= (s_idx[s * BLOCK + t] == j);
+    if (dup) continue;
+    const Pose pj = all_poses[j];
+    if (cnt == k && (weakest < 0 || q_lower_bound(pi, pj, sr, st) >= q_skip)) continue;
+    const float kij = kval_exact(pi, pj, sr, st);
+    if (cnt < k) {
+      s_idx[cnt * BLOCK + t] = j;
+      s_kv[cnt * BLOCK + t] = kij;
+      ++cnt;
+      if (cnt == k) find_weakest();
+      continue;
+    }
+    if (kij > wk) {
+      s_idx[weakest * BLOCK + t] = j;
+      s_kv[weakest * BLOCK + t] = kij;
+      find_weakest();
     }
   }
   count[li] = cnt;
   for (int s = 0; s < cnt; ++s) {
-    idx[li * k + s] = s_idx[s][t];
-    kval[li * k + s] = s_kv[s][t];
+    idx[li * k + s] = s_idx[s * BLOCK + t];
+    kval[li * k + s] = s_kv[s * BLOCK + t];
   }
 }
 
@@ -290,7 +314,7 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
   count_launch();
   constexpr int B = 64;
   if (n > 0)
-    k_refresh_gather<B><<<blocks_for(n, B), B, 0, st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, seg_start, n_seg,
+    k_refresh_gather<B><<<blocks_for(n, B), B, static_cast<size_t>(k) * B * 8, st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, seg_start, n_seg,
                                                          n_sorted, idx, kval, count, k, cap, sr, st_);
 }
 
