@@ -86,8 +86,10 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
   const float cx = my * nz - mz * ny, cy = mz * nx - mx * nz, cz = mx * ny - my * nx;
   const float w = cx * cx + cy * cy + cz * cz;
   const float bg = beta * gam;
-  const float invD = 1.0f / fmaf(A, Ssum, bg * w);
-  const float invA = 1.0f / A;
+  // MUFU reciprocals (2 ulp): A in [1e-8, 1e3], Delta in [1e-16, 1e6] for any
+  // physical covariance, well inside __fdividef's range.
+  const float invD = __fdividef(1.0f, fmaf(A, Ssum, bg * w));
+  const float invA = __fdividef(1.0f, A);
   const float P = beta * AmG * invD, Q = gam * AmB * invD, T = c * bg * invD;
   const float x = mx * ex + my * ey + mz * ez;
   const float y = nx * ex + ny * ey + nz * ez;
@@ -151,18 +153,20 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// fp64 value in [0, 1) -> fp32 by truncating the mantissa (|err| < 2^-23),
-// integer ops only (no F2F on the conversion pipe).
-__device__ __forceinline__ float unit_to_f32(double f) {
-  const double one = __dadd_rn(1.0, f);  // [1, 2]
-  const unsigned hi = static_cast<unsigned>(__double2hiint(one));
-  const unsigned lo = static_cast<unsigned>(__double2loint(one));
+// y = 1 + f with f in [0, 1) (fp64) -> f as fp32 by truncating the mantissa
+// (|err| < 2^-23): integer ops only, no F2F on the conversion pipe.
+__device__ __forceinline__ float one_plus_to_frac(double y) {
+  const unsigned hi = static_cast<unsigned>(__double2hiint(y));
+  const unsigned lo = static_cast<unsigned>(__double2loint(y));
   const unsigned m = ((hi & 0xFFFFFu) << 3) | (lo >> 29);
   return __uint_as_float(0x3F800000u | m) - 1.0f;
 }
 
-// int in [0, 2^31) -> double without the conversion pipe (1.5*2^52 trick).
-__device__ __forceinline__ double i2d(int v) { return __hiloint2double(0x43380000, v) - 6755399441055744.0; }
+// Exact int32 -> double without the conversion pipe (1.5*2^52 + 2^31 trick).
+__device__ __forceinline__ double int_to_double(int v) {
+  return __hiloint2double(0x43380000, static_cast<int>(static_cast<unsigned>(v) ^ 0x80000000u)) -
+         6755401588539392.0;
+}
 
 __device__ __forceinline__ void transform_x(const double* R, const double* t, const double mu[3], double p[3]) {
 #pragma unroll
@@ -194,24 +198,34 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
   Stage& ws = stages[wid];
 
   for (int64_t i = gwarp; i < n; i += nwarps) {
-    const Pose P = poses[i];
-    // fp32 pose in voxel units: x = Rs mu + ts, Rs = R/res, ts = (t - o)/res.
+    // Pose in voxel units, x = Rv mu + tv (Rv = R/res, tv = (t - o)/res): fp64
+    // for the residual of proven cells, fp32 (Rs, ts) for the cell guess.
+    double Rv[9], tv[3];
     float Rs[9], ts[3], Rf[9];
     float tmax = 0.f;
+    {
+      const Pose P = poses[i];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) {
-      Rs[q] = static_cast<float>(P.R[q] * g.inv_res);
-      Rf[q] = static_cast<float>(P.R[q]);
-    }
+      for (int q = 0; q < 9; ++q) {
+        Rv[q] = P.R[q] * g.inv_res;
+        Rs[q] = static_cast<float>(Rv[q]);
+        Rf[q] = static_cast<float>(P.R[q]);
+      }
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      ts[a] = static_cast<float>((P.t[a] - g.origin[a]) * g.inv_res);
-      tmax = fmaxf(tmax, fabsf(ts[a]));
+      for (int a = 0; a < 3; ++a) {
+        tv[a] = (P.t[a] - g.origin[a]) * g.inv_res;
+        ts[a] = static_cast<float>(tv[a]);
+        tmax = fmaxf(tmax, fabsf(ts[a]));
+      }
     }
-    // Rigorous bound on |x32 - x64| with 2x slack (K1).
-    const float E = 2.0f * 5.9604645e-8f *
-                        (7.0f * static_cast<float>(scan.mu_l1_max * g.inv_res) + 4.0f * tmax) + 1e-6f;
-    const bool finite_pose = tmax < 1.0e6f;  // NaN or far away: resolve exactly
+    // Rigorous bound on |x32 - x64| with 2x slack (K1). Beyond
+    // 1e6 voxels (or NaN) every point resolves exactly in fp64.
+    const float l1v = static_cast<float>(scan.mu_l1_max * g.inv_res);
+    const float E = 2.0f * 5.9604645e-8f * (7.0f * l1v + 4.0f * tmax) + 1e-6f;
+    float rsum = 0.f;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) rsum += fabsf(Rs[q]);
+    const bool finite_pose = (tmax + rsum + l1v) < 1.0e6f;  // false for NaN too
     Acc acc;
 #pragma unroll
     for (int q = 0; q < 6; ++q) acc.hbr[q] = acc.htl[q] = acc.b[q] = 0.f;
@@ -236,12 +250,12 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
           bool amb = !finite_pose, inb = true;
 #pragma unroll
           for (int ax = 0; ax < 3; ++ax) {
-            const float xv =
-                fmaf(Rs[ax * 3 + 2], s0.z, fmaf(Rs[ax * 3 + 1], s0.y, Rs[ax * 3 + 0] * s0.x)) + ts[ax];
-            const float y = __fadd_rd(xv, 12582912.0f);  // floor via 1.5*2^23 (|x| < 2^21 here)
+            // |xv| < 2^21 whenever finite_pose: floor via the 1.5*2^23 trick.
+            const float xv = fmaf(Rs[ax * 3 + 2], s0.z, fmaf(Rs[ax * 3 + 1], s0.y, fmaf(Rs[ax * 3 + 0], s0.x, ts[ax])));
+            const float y = __fadd_rd(xv, 12582912.0f);
             const float fr = xv - (y - 12582912.0f);
             ic[ax] = __float_as_int(y) - 0x4B400000;
-            amb = amb || !(fabsf(xv) < 2097152.0f) || fr < E || fr > 1.0f - E;
+            amb = amb || fabsf(fr - 0.5f) > 0.5f - E;
             inb = inb && static_cast<unsigned>(ic[ax]) < static_cast<unsigned>(g.dims[ax]);
           }
           if (amb) {
@@ -282,28 +296,36 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
           const int k = static_cast<int>(a & 0xFFFFu);
           int iz = static_cast<int>(a >> 16), ix = static_cast<int>(bq & 0xFFFFu), iy = static_cast<int>(bq >> 16);
           const double mu[3] = {s_mu[3 * k], s_mu[3 * k + 1], s_mu[3 * k + 2]};
-          double p[3], x[3], f[3];
-          transform_x(P.R, P.t, mu, p);
-#pragma unroll
-          for (int ax = 0; ax < 3; ++ax) x[ax] = xmul(xsub(p[ax], g.origin[ax]), g.inv_res);
+          // yv = 1 + fractional voxel coordinate, expected in [1, 2).
+          double yv[3];
           valid = true;
           bool resolve = iz == static_cast<int>(kResolve);
           if (!resolve) {
-            f[0] = xsub(x[0], i2d(ix));
-            f[1] = xsub(x[1], i2d(iy));
-            f[2] = xsub(x[2], i2d(iz));
-            // Safety net: the fp32 floor must agree with the exact one.
-            resolve = !(f[0] >= 0.0 && f[0] < 1.0 && f[1] >= 0.0 && f[1] < 1.0 && f[2] >= 0.0 && f[2] < 1.0);
+            // Cell proven by the fp32 bound; residual from an FMA transform
+            // (|error| ~1e-13 voxel, far below the fp32 record precision).
+            const int ic3[3] = {ix, iy, iz};
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+              const double xr =
+                  fma(Rv[ax * 3 + 2], mu[2], fma(Rv[ax * 3 + 1], mu[1], fma(Rv[ax * 3 + 0], mu[0], tv[ax])));
+              yv[ax] = xr + int_to_double(1 - ic3[ax]);
+              // Safety net: exponent of yv must be that of [1, 2).
+              resolve = resolve || (__double2hiint(yv[ax]) >> 20) != 0x3FF;
+            }
           }
           float4 m0, m1;
-          if (resolve) {  // exact floor + bounds (nnf.hpp:24-35), direct gather
+          if (resolve) {  // exact transform, floor and bounds (nnf.hpp:24-35), direct gather
+            const Pose P = poses[i];
+            double p[3];
+            transform_x(P.R, P.t, mu, p);
             int c3[3];
 #pragma unroll
             for (int ax = 0; ax < 3; ++ax) {
-              const double fl = floor(x[ax]);
+              const double x = xmul(xsub(p[ax], g.origin[ax]), g.inv_res);
+              const double fl = floor(x);
               valid = valid && (fl >= 0.0 && fl < static_cast<double>(g.dims[ax]));
               c3[ax] = valid ? static_cast<int>(fl) : 0;
-              f[ax] = xsub(x[ax], fl);
+              yv[ax] = 1.0 + xsub(x, fl);
             }
             const int64_t c = (static_cast<int64_t>(c3[2]) * ny + c3[1]) * nx + c3[0];
             m0 = valid ? __ldg(map.rec + 2 * c) : make_float4(0.f, 0.f, 0.f, -1.f);
@@ -315,7 +337,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
           }
           valid = valid && m0.w >= 0.f;
           if (valid) {
-            const float fr[3] = {unit_to_f32(f[0]), unit_to_f32(f[1]), unit_to_f32(f[2])};
+            const float fr[3] = {one_plus_to_frac(yv[0]), one_plus_to_frac(yv[1]), one_plus_to_frac(yv[2])};
             fast_item<GN>(acc, Rf, fr, res, m0, m1, s_rec[2 * k], s_rec[2 * k + 1]);
           }
         }

@@ -127,39 +127,94 @@ __global__ void k_seg_stats(const int32_t* __restrict__ seg_start, int32_t n_seg
   if (threadIdx.x == 0 && s_hist[cap + 2]) atomicAdd(overflow, s_hist[cap + 2]);
 }
 
-// Exact float kernel value of the pair (a, b) (neighbor_graph.hpp:84-86,
-// neighbor_search.cpp:161-166): 0 if the translation bound underflows, else
-// (float)exp(-q) with q from the full SE3 log in the reference's order.
-__device__ __forceinline__ float kval_exact(const Pose& a, const Pose& b, double sr, double st) {
+// Float kernel value of a pair as the reference caches it
+// (neighbor_graph.hpp:84-86, neighbor_search.cpp:161-166): 0 if the
+// translation bound underflows, else (float)exp(-q) with q from the SE3 log.
+//
+// Fast evaluation. With Rrel = Ra^T Rb,
+// vee = (Rrel - Rrel^T)^vee, s = |vee|/2, c = (tr Rrel - 1)/2, r = hypot(s, c),
+// theta = atan2(s, c), the reference's log (se3.hpp:103-149) gives
+// |w| = theta*r, and V^-1 acts as the identity along w and as a scaled
+// rotation with |V^-1 x|^2 = |x|^2 (th/2)^2 / sin^2(th/2) across it, so
+//   q = sr th^2 + st ( (u.w^)^2 + (|u|^2 - (u.w^)^2) th^2 / (4 sin^2(th/2)) ),
+// u = Ra^T (tb - ta), th = theta*r. No sin/cos calls: sin/cos of th follow
+// from s/r, c/r and the tiny th - theta. q agrees with the reference's to
+// ~1e-14 relative; the float is returned only if exp(-q)*(1 -+ 4e-12) round
+// to the same float, otherwise *ok = false and kval_of takes the reference-order log.
+__device__ __forceinline__ float kval_fast(const Pose& a, const Pose& b, double sr, double st, bool* ok) {
+  double m[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      m[i * 3 + j] = fma(a.R[0 * 3 + i], b.R[0 * 3 + j], fma(a.R[1 * 3 + i], b.R[1 * 3 + j], a.R[2 * 3 + i] * b.R[2 * 3 + j]));
+  const double d0 = b.t[0] - a.t[0], d1 = b.t[1] - a.t[1], d2 = b.t[2] - a.t[2];
+  double u[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) u[i] = fma(a.R[0 * 3 + i], d0, fma(a.R[1 * 3 + i], d1, a.R[2 * 3 + i] * d2));
+  const double v0 = m[7] - m[5], v1 = m[2] - m[6], v2 = m[3] - m[1];
+  const double vv = fma(v0, v0, fma(v1, v1, v2 * v2));  // |vee|^2 = 4 s^2
+  const double s = 0.5 * sqrt(vv);
+  const double c = fmin(1.0, fmax(-1.0, 0.5 * ((m[0] + m[4]) + m[8] - 1.0)));
+  const double theta = atan2(s, c);
+  const double uu = fma(u[0], u[0], fma(u[1], u[1], u[2] * u[2]));
+  double q;
+  if (theta > 3.14159265358979323846 - 1e-2) {  // near the pi branch: reference path
+    *ok = false;
+    return 0.0f;
+  }
+  if (vv == 0.0) {  // identical rotations: w = 0, v = u
+    q = st * uu;
+  } else {
+    const double r2 = fma(s, s, c * c);
+    const double inv_r = rsqrt(r2);
+    const double r = r2 * inv_r;
+    const double th = theta * r;  // |w|
+    const double th2 = th * th;
+    const double uw = fma(u[0], v0, fma(u[1], v1, u[2] * v2));
+    const double par = uw * uw / vv;  // (u . w^)^2
+    const double perp = fmax(uu - par, 0.0);
+    double F;  // th^2 / (4 sin^2(th/2))
+    if (th2 < 1e-6) {
+      F = fma(th2, fma(th2, 1.0 / 240.0, 1.0 / 12.0), 1.0);
+    } else {
+      const double S = s * inv_r, Cc = c * inv_r, dl = theta * (r - 1.0);  // th = theta + dl
+      const double sin_th = fma(dl, Cc, S) - 0.5 * dl * dl * S;
+      const double cos_th = fma(-dl, S, Cc) - 0.5 * dl * dl * Cc;
+      // 4 sin^2(th/2) = 2(1 - cos th) = 2 sin^2 th / (1 + cos th)
+      const double four_s2 = cos_th < 0.0 ? 2.0 * (1.0 - cos_th) : 2.0 * sin_th * sin_th / (1.0 + cos_th);
+      F = th2 / four_s2;
+    }
+    q = fma(sr, th2, st * fma(perp, F, par));
+  }
+  if (!(q == q)) {
+    *ok = false;
+    return 0.0f;
+  }
+  const double k = exp(-q);
+  const float lo = __double2float_rn(k * (1.0 - 4e-12)), hi = __double2float_rn(k * (1.0 + 4e-12));
+  *ok = lo == hi;
+  return hi;
+}
+
+// Kernel value of the pair as the reference computes it, via kval_fast when
+// its float is provably the same.
+__device__ __forceinline__ float kval_of(const Pose& a, const Pose& b, double sr, double st) {
   if (kernel_underflows(a, b, st)) return 0.0f;
+  bool ok;
+  const float f = kval_fast(a, b, sr, st, &ok);
+  if (ok) return f;
   double d[6];
   se3_log(inv_compose_x(a, b), d);
   return __double2float_rn(exp(-kernel_q(d, sr, st)));
 }
 
-// Lower bound of the kernel exponent q = sr |w|^2 + st |v|^2 of the pair:
-// |w| = rotation angle of Ra^T Rb, and |v| >= |tb - ta| because V^-1 of the
-// SE3 log expands (svgd.hpp:40-44). fp32 acos with a 2e-3 rad margin covers
-// its rounding and the <= 1e-7 non-orthonormality renormalize_if_needed allows.
-__device__ __forceinline__ double q_lower_bound(const Pose& a, const Pose& b, double sr, double st) {
-  double tr = 0.0;
-#pragma unroll
-  for (int q = 0; q < 9; ++q) tr = fma(a.R[q], b.R[q], tr);
-  const float c = fminf(1.0f, fmaxf(-1.0f, static_cast<float>(0.5 * (tr - 1.0))));
-  const float th = fmaxf(0.0f, acosf(c) - 2e-3f);
-  const double d0 = b.t[0] - a.t[0], d1 = b.t[1] - a.t[1], d2 = b.t[2] - a.t[2];
-  return (sr * static_cast<double>(th) * static_cast<double>(th) + st * (d0 * d0 + d1 * d1 + d2 * d2)) *
-         (1.0 - 1e-9);
-}
-
 // Fused NeighborGraph::refresh (neighbor_graph.hpp:76-90) and the gather/offer
 // loop (neighbor_search.cpp:151-169) for the particle at sorted position p.
 // Refresh and gather of one particle touch only its own list, so fusing them
-// per particle preserves the reference's two-phase result exactly. Two exact
-// shortcuts avoid SE3 logs whose outcome is already decided:
-//  * offer() ignores duplicates before looking at k_ij;
-//  * with a full list, a candidate whose kernel upper bound exp(-q_lb) does
-//    not exceed the weakest non-self entry can never be inserted.
+// per particle preserves the reference's two-phase result exactly. offer()
+// ignores duplicates before looking at k_ij, so duplicates skip the kernel
+// evaluation; every evaluation goes through kval_of (bit-exact float).
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict__ all_poses, int64_t n,
                                                           int64_t gbase, const int32_t* __restrict__ pos_list,
@@ -190,13 +245,11 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
   const Pose pi = all_poses[gi];
   for (int s = 0; s < cnt; ++s) {  // refresh
     const int32_t j = s_idx[s * BLOCK + t];
-    s_kv[s * BLOCK + t] = (j == gi) ? 1.0f : kval_exact(pi, all_poses[j], sr, st);
+    s_kv[s * BLOCK + t] = (j == gi) ? 1.0f : kval_of(pi, all_poses[j], sr, st);
   }
-  // Weakest non-self entry (first strict minimum, neighbor_graph.hpp:60-72)
-  // and its threshold in exponent space.
+  // Weakest non-self entry (first strict minimum, neighbor_graph.hpp:60-72).
   int weakest = -1;
   float wk = __int_as_float(0x7f800000);
-  double q_skip = 0.0;
   auto find_weakest = [&]() {
     weakest = -1;
     wk = __int_as_float(0x7f800000);
@@ -208,9 +261,6 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
         weakest = s;
       }
     }
-    // k_ij <= exp(-q_lb) <= wk  <=>  q_lb >= -log(wk); 0.0f entries: only
-    // k_ij that round to 0.0f (q > 150 ln 2) are excluded.
-    q_skip = weakest < 0 ? 1e300 : (wk > 0.0f ? -log(static_cast<double>(wk)) * (1.0 + 1e-12) + 1e-12 : 104.0);
   };
   if (cnt == k) find_weakest();
   for (int64_t q = rb; q < vis_end; ++q) {  // gather / offer
@@ -219,9 +269,8 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
     bool dup = false;
     for (int s = 0; s < cnt; ++s) dup |= (s_idx[s * BLOCK + t] == j);
     if (dup) continue;
-    const Pose pj = all_poses[j];
-    if (cnt == k && (weakest < 0 || q_lower_bound(pi, pj, sr, st) >= q_skip)) continue;
-    const float kij = kval_exact(pi, pj, sr, st);
+    if (cnt == k && weakest < 0) continue;  // self-only full list (k == 1): nothing evictable
+    const float kij = kval_of(pi, all_poses[j], sr, st);
     if (cnt < k) {
       s_idx[cnt * BLOCK + t] = j;
       s_kv[cnt * BLOCK + t] = kij;
