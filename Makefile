@@ -20,7 +20,7 @@ HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/host/*.hpp) include/smcl_gp
 CU_OBJ := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRC))
 CPP_OBJ := $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(CPP_SRC))
 
-all: $(LIB) oracle
+all: $(LIB) oracle examples/facade_demo
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(dir $@)
@@ -41,3 +41,7 @@ clean:
 	rm -rf build $(PKG)/lib oracle/build
 
 .PHONY: all oracle clean
+
+# C++ facade example (reference-shaped API over the C ABI).
+examples/facade_demo: examples/facade_demo.cpp include/steinmcl_b200.hpp include/smcl_gpu.h $(LIB)
+	$(HOSTCXX) -std=c++20 -O2 -Iinclude -o $@ examples/facade_demo.cpp -L$(PKG)/lib -lsmcl_gpu -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'

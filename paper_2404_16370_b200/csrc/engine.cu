@@ -1119,7 +1119,12 @@ int smcl_evaluate_all(smcl_engine* h, const smcl_cloud* scan, double* step_out, 
       h->sys.download(sys.data(), sys.size(), h->st);
       h->sync();
       for (size_t i = 0; i < n; ++i) {
-        if (H_out) std::memcpy(H_out + 36 * i, &sys[i * kSysStride], 36 * sizeof(double));
+        if (H_out) {
+          std::memcpy(H_out + 36 * i, &sys[i * kSysStride], 36 * sizeof(double));
+          if (h->fast_used)  // the fast kernel writes the (authoritative) lower triangle only
+            for (int r = 0; r < 6; ++r)
+              for (int c = r + 1; c < 6; ++c) H_out[36 * i + r * 6 + c] = H_out[36 * i + c * 6 + r];
+        }
         if (b_out) std::memcpy(b_out + 6 * i, &sys[i * kSysStride + 36], 6 * sizeof(double));
       }
     }

@@ -45,6 +45,7 @@ struct WarpStage {
   uint32_t qa[kStep];   // compacted candidates: k | iz << 16 (iz == 0xFFFF: resolve exactly)
   uint32_t qb[kStep];   // ix | iy << 16
   uint16_t qs[kStep];   // stage slot of the candidate's record
+  double pose_v[12];    // fp64 pose in voxel units (Rv row-major, tv)
 };
 
 struct Acc {
@@ -59,9 +60,23 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+// 16-byte async copy; when !pred nothing is read and the destination is zero-filled.
+__device__ __forceinline__ void cp_async16_pred(void* smem, const void* gmem, bool pred) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int src_bytes = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// MUFU reciprocal (~1 ulp): A in [1e-8, 1e3], Delta in [1e-16, 1e6] for any
+// physical covariance, far from the flush-to-zero range.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
 }
 
 template <bool GN>
@@ -88,8 +103,8 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
   const float bg = beta * gam;
   // MUFU reciprocals (2 ulp): A in [1e-8, 1e3], Delta in [1e-16, 1e6] for any
   // physical covariance, well inside __fdividef's range.
-  const float invD = __fdividef(1.0f, fmaf(A, Ssum, bg * w));
-  const float invA = __fdividef(1.0f, A);
+  const float invD = rcp_approx(fmaf(A, Ssum, bg * w));
+  const float invA = rcp_approx(A);
   const float P = beta * AmG * invD, Q = gam * AmB * invD, T = c * bg * invD;
   const float x = mx * ex + my * ey + mz * ez;
   const float y = nx * ex + ny * ey + nz * ez;
@@ -174,6 +189,14 @@ __device__ __forceinline__ void transform_x(const double* R, const double* t, co
     p[i] = xadd(xadd(xadd(xmul(R[i * 3 + 0], mu[0]), xmul(R[i * 3 + 1], mu[1])), xmul(R[i * 3 + 2], mu[2])), t[i]);
 }
 
+// Lower-triangle / b / ll offsets of the 28 per-lane accumulators in the
+// per-particle system record (kSysStride layout: H row-major, b, ll).
+__constant__ int c_sys_off[28] = {0,  6,  7,  12, 13, 14,                 // htl -> H(r, c), c <= r < 3
+                                  18, 24, 30, 19, 25, 31, 20, 26, 32,     // htr(r, c) -> H(c+3, r)
+                                  21, 27, 28, 33, 34, 35,                 // hbr -> H(r+3, c+3)
+                                  36, 37, 38, 39, 40, 41,                 // b
+                                  42};                                    // ll
+
 template <bool GN, int kFastUnroll>
 __global__ void __launch_bounds__(kFastWarps * 32, 1)
     k_gicp_fast(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, double* __restrict__ sys,
@@ -183,7 +206,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage* stages = reinterpret_cast<Stage*>(smem_raw);
   double* s_mu = reinterpret_cast<double*>(smem_raw + sizeof(Stage) * kFastWarps);  // S*3 fp64
-  float4* s_rec = reinterpret_cast<float4*>(s_mu + 3 * ((scan.n + 1) & ~1));            // S*2
+  float4* s_rec = reinterpret_cast<float4*>(s_mu + 3 * ((scan.n + 1) & ~1));        // S*2
   const int S = scan.n;
   for (int q = threadIdx.x; q < 3 * S; q += blockDim.x) s_mu[q] = scan.mu[q];
   for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) s_rec[q] = scan.rec[q];
@@ -195,26 +218,31 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
   const NnfGeom g = map.g;
   const float res = static_cast<float>(g.res);
   const int nx = g.dims[0], ny = g.dims[1];
+  const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
+                 dz = static_cast<unsigned>(g.dims[2]);
   Stage& ws = stages[wid];
 
   for (int64_t i = gwarp; i < n; i += nwarps) {
-    // Pose in voxel units, x = Rv mu + tv (Rv = R/res, tv = (t - o)/res): fp64
-    // for the residual of proven cells, fp32 (Rs, ts) for the cell guess.
-    double Rv[9], tv[3];
+    // Pose in voxel units x = Rv mu + tv (Rv = R/res, tv = (t - o)/res): fp64
+    // in shared memory for the residual of proven cells, fp32 (Rs, ts) for the
+    // cell guess, Rf = R (fp32) for the body-frame algebra.
     float Rs[9], ts[3], Rf[9];
-    float tmax = 0.f;
+    float tmax = 0.f, rsum = 0.f;
     {
       const Pose P = poses[i];
 #pragma unroll
       for (int q = 0; q < 9; ++q) {
-        Rv[q] = P.R[q] * g.inv_res;
-        Rs[q] = static_cast<float>(Rv[q]);
+        const double rv = P.R[q] * g.inv_res;
+        if (lane == 0) ws.pose_v[q] = rv;
+        Rs[q] = static_cast<float>(rv);
         Rf[q] = static_cast<float>(P.R[q]);
+        rsum += fabsf(Rs[q]);
       }
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        tv[a] = (P.t[a] - g.origin[a]) * g.inv_res;
-        ts[a] = static_cast<float>(tv[a]);
+        const double tvv = (P.t[a] - g.origin[a]) * g.inv_res;
+        if (lane == 0) ws.pose_v[9 + a] = tvv;
+        ts[a] = static_cast<float>(tvv);
         tmax = fmaxf(tmax, fabsf(ts[a]));
       }
     }
@@ -222,9 +250,6 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
     // 1e6 voxels (or NaN) every point resolves exactly in fp64.
     const float l1v = static_cast<float>(scan.mu_l1_max * g.inv_res);
     const float E = 2.0f * 5.9604645e-8f * (7.0f * l1v + 4.0f * tmax) + 1e-6f;
-    float rsum = 0.f;
-#pragma unroll
-    for (int q = 0; q < 9; ++q) rsum += fabsf(Rs[q]);
     const bool finite_pose = (tmax + rsum + l1v) < 1.0e6f;  // false for NaN too
     Acc acc;
 #pragma unroll
@@ -233,50 +258,46 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
     for (int q = 0; q < 9; ++q) acc.htr[q] = 0.f;
     acc.cost = 0.f;
     int nmatch = 0;
+    __syncwarp();
 
     for (int base = 0; base < S; base += kStep) {
-      // ---- phase A: fp32 cell guess, async record gather
+      // ---- phase A (branch free): fp32 cell guess, predicated async gather
       uint32_t pa[kFastUnroll], pb[kFastUnroll];
-      uint8_t status[kFastUnroll];  // 0 skip, 1 record staged, 2 resolve exactly
+      uint32_t status = 0;  // 2 bits per point: 1 record staged, 2 resolve exactly
 #pragma unroll
       for (int u = 0; u < kFastUnroll; ++u) {
         const int k = base + u * 32 + lane;
-        status[u] = 0;
-        pa[u] = static_cast<uint32_t>(k);
-        pb[u] = 0u;
-        if (k < S) {
-          const float4 s0 = s_rec[2 * k];
-          int ic[3];
-          bool amb = !finite_pose, inb = true;
+        const bool live = k < S;
+        const float4 s0 = s_rec[2 * (live ? k : 0)];
+        int ic[3];
+        bool amb = !finite_pose, inb = live;
 #pragma unroll
-          for (int ax = 0; ax < 3; ++ax) {
-            // |xv| < 2^21 whenever finite_pose: floor via the 1.5*2^23 trick.
-            const float xv = fmaf(Rs[ax * 3 + 2], s0.z, fmaf(Rs[ax * 3 + 1], s0.y, fmaf(Rs[ax * 3 + 0], s0.x, ts[ax])));
-            const float y = __fadd_rd(xv, 12582912.0f);
-            const float fr = xv - (y - 12582912.0f);
-            ic[ax] = __float_as_int(y) - 0x4B400000;
-            amb = amb || fabsf(fr - 0.5f) > 0.5f - E;
-            inb = inb && static_cast<unsigned>(ic[ax]) < static_cast<unsigned>(g.dims[ax]);
-          }
-          if (amb) {
-            status[u] = 2;
-            pa[u] |= kResolve << 16;
-          } else if (inb) {
-            status[u] = 1;
-            pa[u] |= static_cast<uint32_t>(ic[2]) << 16;
-            pb[u] = static_cast<uint32_t>(ic[0]) | (static_cast<uint32_t>(ic[1]) << 16);
-            const float4* src = map.rec + 2 * ((static_cast<int64_t>(ic[2]) * ny + ic[1]) * nx + ic[0]);
-            cp_async16(&ws.m0[u * 32 + lane], src);
-            cp_async16(&ws.m1[u * 32 + lane], src + 1);
-          }
+        for (int ax = 0; ax < 3; ++ax) {
+          const float xv = fmaf(Rs[ax * 3 + 2], s0.z, fmaf(Rs[ax * 3 + 1], s0.y, fmaf(Rs[ax * 3 + 0], s0.x, ts[ax])));
+          const float y = __fadd_rd(xv, 12582912.0f);  // floor via 1.5*2^23 (|x| < 2^21 when finite_pose)
+          const float fr = xv - (y - 12582912.0f);
+          ic[ax] = __float_as_int(y) - 0x4B400000;
+          amb = amb || fabsf(fr - 0.5f) > 0.5f - E;
         }
+        inb = inb && static_cast<unsigned>(ic[0]) < dx && static_cast<unsigned>(ic[1]) < dy &&
+              static_cast<unsigned>(ic[2]) < dz;
+        amb = amb && live;
+        const bool stage = inb && !amb;
+        status |= (amb ? 2u : (stage ? 1u : 0u)) << (2 * u);
+        pa[u] = static_cast<uint32_t>(k) | ((amb ? kResolve : static_cast<uint32_t>(ic[2])) << 16);
+        pb[u] = static_cast<uint32_t>(ic[0] & 0xFFFF) | (static_cast<uint32_t>(ic[1]) << 16);
+        const int64_t cell = stage ? (static_cast<int64_t>(ic[2]) * ny + ic[1]) * nx + ic[0] : 0;
+        const float4* src = map.rec + 2 * cell;
+        cp_async16_pred(&ws.m0[u * 32 + lane], src, stage);
+        cp_async16_pred(&ws.m1[u * 32 + lane], src + 1, stage);
       }
       cp_async_wait_all();
       __syncwarp();
       int n_cand = 0;
 #pragma unroll
       for (int u = 0; u < kFastUnroll; ++u) {
-        const bool keep = status[u] == 2 || (status[u] == 1 && ws.m0[u * 32 + lane].w >= 0.f);
+        const uint32_t st = (status >> (2 * u)) & 3u;
+        const bool keep = st == 2u || (st == 1u && ws.m0[u * 32 + lane].w >= 0.f);
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
         if (keep) {
           const int pos = n_cand + __popc(mask & ((1u << lane) - 1u));
@@ -294,7 +315,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
         if (e < n_cand) {
           const uint32_t a = ws.qa[e], bq = ws.qb[e];
           const int k = static_cast<int>(a & 0xFFFFu);
-          int iz = static_cast<int>(a >> 16), ix = static_cast<int>(bq & 0xFFFFu), iy = static_cast<int>(bq >> 16);
+          const int iz = static_cast<int>(a >> 16), ix = static_cast<int>(bq & 0xFFFFu),
+                    iy = static_cast<int>(bq >> 16);
           const double mu[3] = {s_mu[3 * k], s_mu[3 * k + 1], s_mu[3 * k + 2]};
           // yv = 1 + fractional voxel coordinate, expected in [1, 2).
           double yv[3];
@@ -306,11 +328,11 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
             const int ic3[3] = {ix, iy, iz};
 #pragma unroll
             for (int ax = 0; ax < 3; ++ax) {
+              const double* pv = ws.pose_v;
               const double xr =
-                  fma(Rv[ax * 3 + 2], mu[2], fma(Rv[ax * 3 + 1], mu[1], fma(Rv[ax * 3 + 0], mu[0], tv[ax])));
+                  fma(pv[ax * 3 + 2], mu[2], fma(pv[ax * 3 + 1], mu[1], fma(pv[ax * 3 + 0], mu[0], pv[9 + ax])));
               yv[ax] = xr + int_to_double(1 - ic3[ax]);
-              // Safety net: exponent of yv must be that of [1, 2).
-              resolve = resolve || (__double2hiint(yv[ax]) >> 20) != 0x3FF;
+              resolve = resolve || (__double2hiint(yv[ax]) >> 20) != 0x3FF;  // safety net
             }
           }
           float4 m0, m1;
@@ -346,38 +368,39 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
       __syncwarp();
     }
 
+    // ---- epilogue: lane q ends up with the warp total of accumulator q
     double* out = sys + i * kSysStride;
-    const float cost = warp_sum(acc.cost);
     if (GN) {
-      float hbr[6], htl[6], htr[9], b[6];
+      float v[32];
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
-        hbr[q] = warp_sum(acc.hbr[q]);
-        htl[q] = warp_sum(acc.htl[q]);
-        b[q] = warp_sum(acc.b[q]);
+        v[q] = acc.htl[q];
+        v[15 + q] = acc.hbr[q];
+        v[21 + q] = acc.b[q];
       }
 #pragma unroll
-      for (int q = 0; q < 9; ++q) htr[q] = warp_sum(acc.htr[q]);
-      if (lane == 0) {
-        const int li[6][2] = {{0, 0}, {1, 0}, {1, 1}, {2, 0}, {2, 1}, {2, 2}};
+      for (int q = 0; q < 9; ++q) v[6 + q] = acc.htr[q];
+      v[27] = acc.cost;
+      v[28] = v[29] = v[30] = v[31] = 0.f;
+      // Butterfly reduce-scatter: after the step with offset s each lane keeps
+      // the half selected by (lane & s); 31 shuffles instead of 140.
 #pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const int r = li[q][0], c = li[q][1];
-          out[r * 6 + c] = out[c * 6 + r] = htl[q];
-          out[(r + 3) * 6 + c + 3] = out[(c + 3) * 6 + r + 3] = hbr[q];
+      for (int s = 16; s >= 1; s >>= 1) {
+        const bool up = (lane & s) != 0;
+#pragma unroll
+        for (int j = 0; j < s; ++j) {
+          const float send = up ? v[j] : v[j + s];
+          const float keep = up ? v[j + s] : v[j];
+          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
         }
-#pragma unroll
-        for (int r = 0; r < 3; ++r)
-#pragma unroll
-          for (int c = 0; c < 3; ++c) out[r * 6 + c + 3] = out[(c + 3) * 6 + r] = htr[r * 3 + c];
-#pragma unroll
-        for (int q = 0; q < 6; ++q) out[36 + q] = b[q];
       }
+      if (lane < 27) out[c_sys_off[lane]] = static_cast<double>(v[0]);
+      if (lane == 27) out[42] = nmatch == 0 ? -1e30 : -static_cast<double>(v[0]);
+    } else {
+      const float cost = warp_sum(acc.cost);
+      if (lane == 0) out[42] = nmatch == 0 ? -1e30 : -static_cast<double>(cost);
     }
-    if (lane == 0) {
-      out[42] = nmatch == 0 ? -1e30 : -static_cast<double>(cost);
-      nm_out[i] = nmatch;
-    }
+    if (lane == 0) nm_out[i] = nmatch;
     __syncwarp();
   }
 }
