@@ -36,7 +36,8 @@ namespace smcl {
 namespace {
 
 constexpr int kFastWarps = 16;         // warps per CTA (one CTA per SM: 16 warps x 128 registers)
-constexpr unsigned kResolve = 0xFFFFu;
+constexpr unsigned kResolve = 0xFFFFu;  // queue iz field: resolve the cell exactly in fp64
+constexpr unsigned kDrop = 0xFFFEu;     // queue iz field: certainly out of bounds
 
 template <int kStep>
 struct WarpStage {
@@ -44,7 +45,6 @@ struct WarpStage {
   float4 m1[kStep];
   uint32_t qa[kStep];   // compacted candidates: k | iz << 16 (iz == 0xFFFF: resolve exactly)
   uint32_t qb[kStep];   // ix | iy << 16
-  uint16_t qs[kStep];   // stage slot of the candidate's record
   double pose_v[12];    // fp64 pose in voxel units (Rv row-major, tv)
 };
 
@@ -205,11 +205,19 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
   using Stage = WarpStage<kStep>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage* stages = reinterpret_cast<Stage*>(smem_raw);
-  double* s_mu = reinterpret_cast<double*>(smem_raw + sizeof(Stage) * kFastWarps);  // S*3 fp64
-  float4* s_rec = reinterpret_cast<float4*>(s_mu + 3 * ((scan.n + 1) & ~1));        // S*2
+  // Scan in shared memory, padded with NaN points to a multiple of kStep:
+  // fp64 means (exact transform), fp32 records split in two conflict-free halves.
   const int S = scan.n;
-  for (int q = threadIdx.x; q < 3 * S; q += blockDim.x) s_mu[q] = scan.mu[q];
-  for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) s_rec[q] = scan.rec[q];
+  const int Sp = (S + kStep - 1) / kStep * kStep;
+  float4* s_r0 = reinterpret_cast<float4*>(smem_raw + sizeof(Stage) * kFastWarps);  // Sp: mu.xyz, gamma
+  float4* s_r1 = s_r0 + Sp;                                                        // Sp: u.xyz, s
+  double* s_mu = reinterpret_cast<double*>(s_r1 + Sp);                             // Sp*3
+  const float fnan = __int_as_float(0x7fc00000);
+  for (int q = threadIdx.x; q < Sp; q += blockDim.x) {
+    s_r0[q] = q < S ? scan.rec[2 * q] : make_float4(fnan, fnan, fnan, 0.f);
+    s_r1[q] = q < S ? scan.rec[2 * q + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int q = threadIdx.x; q < 3 * Sp; q += blockDim.x) s_mu[q] = q < 3 * S ? scan.mu[q] : __longlong_as_double(0x7ff8000000000000ll);
   __syncthreads();
 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -261,16 +269,16 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
     __syncwarp();
 
     for (int base = 0; base < S; base += kStep) {
-      // ---- phase A (branch free): fp32 cell guess, predicated async gather
+      // ---- phase A (branch free): fp32 cell guess, predicated async gather.
+      // Queue word qa = k | iz << 16 with iz = 0xFFFF "resolve exactly",
+      // 0xFFFE "drop"; padded points (k >= S) carry NaN coordinates and drop.
       uint32_t pa[kFastUnroll], pb[kFastUnroll];
-      uint32_t status = 0;  // 2 bits per point: 1 record staged, 2 resolve exactly
 #pragma unroll
       for (int u = 0; u < kFastUnroll; ++u) {
         const int k = base + u * 32 + lane;
-        const bool live = k < S;
-        const float4 s0 = s_rec[2 * (live ? k : 0)];
+        const float4 s0 = s_r0[k];
         int ic[3];
-        bool amb = !finite_pose, inb = live;
+        bool amb = !finite_pose;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
           const float xv = fmaf(Rs[ax * 3 + 2], s0.z, fmaf(Rs[ax * 3 + 1], s0.y, fmaf(Rs[ax * 3 + 0], s0.x, ts[ax])));
@@ -279,31 +287,35 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
           ic[ax] = __float_as_int(y) - 0x4B400000;
           amb = amb || fabsf(fr - 0.5f) > 0.5f - E;
         }
-        inb = inb && static_cast<unsigned>(ic[0]) < dx && static_cast<unsigned>(ic[1]) < dy &&
-              static_cast<unsigned>(ic[2]) < dz;
-        amb = amb && live;
-        const bool stage = inb && !amb;
-        status |= (amb ? 2u : (stage ? 1u : 0u)) << (2 * u);
-        pa[u] = static_cast<uint32_t>(k) | ((amb ? kResolve : static_cast<uint32_t>(ic[2])) << 16);
+        amb = amb && k < S;
+        const bool stage = !amb && static_cast<unsigned>(ic[0]) < dx && static_cast<unsigned>(ic[1]) < dy &&
+                           static_cast<unsigned>(ic[2]) < dz;
+        const uint32_t izf = amb ? kResolve : (stage ? static_cast<uint32_t>(ic[2]) : kDrop);
+        pa[u] = static_cast<uint32_t>(k) | (izf << 16);
         pb[u] = static_cast<uint32_t>(ic[0] & 0xFFFF) | (static_cast<uint32_t>(ic[1]) << 16);
-        const int64_t cell = stage ? (static_cast<int64_t>(ic[2]) * ny + ic[1]) * nx + ic[0] : 0;
-        const float4* src = map.rec + 2 * cell;
+        const uint32_t cell = stage ? (static_cast<uint32_t>(ic[2]) * ny + ic[1]) * nx + ic[0] : 0u;
+        const float4* src = map.rec + 2 * static_cast<uint64_t>(cell);
         cp_async16_pred(&ws.m0[u * 32 + lane], src, stage);
         cp_async16_pred(&ws.m1[u * 32 + lane], src + 1, stage);
       }
       cp_async_wait_all();
       __syncwarp();
+      // In-place compaction of the candidates and their records (a kept
+      // item moves to a position <= its own slot, rows are read before any
+      // write of the same row): phase B then reads consecutive entries.
       int n_cand = 0;
 #pragma unroll
       for (int u = 0; u < kFastUnroll; ++u) {
-        const uint32_t st = (status >> (2 * u)) & 3u;
-        const bool keep = st == 2u || (st == 1u && ws.m0[u * 32 + lane].w >= 0.f);
+        const float4 r0 = ws.m0[u * 32 + lane], r1 = ws.m1[u * 32 + lane];
+        const uint32_t izf = pa[u] >> 16;
+        const bool keep = izf == kResolve || (izf != kDrop && r0.w >= 0.f);
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
         if (keep) {
           const int pos = n_cand + __popc(mask & ((1u << lane) - 1u));
           ws.qa[pos] = pa[u];
           ws.qb[pos] = pb[u];
-          ws.qs[pos] = static_cast<uint16_t>(u * 32 + lane);
+          ws.m0[pos] = r0;
+          ws.m1[pos] = r1;
         }
         n_cand += __popc(mask);
       }
@@ -353,14 +365,13 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
             m0 = valid ? __ldg(map.rec + 2 * c) : make_float4(0.f, 0.f, 0.f, -1.f);
             m1 = valid ? __ldg(map.rec + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
           } else {
-            const int slot = ws.qs[e];
-            m0 = ws.m0[slot];
-            m1 = ws.m1[slot];
+            m0 = ws.m0[e];
+            m1 = ws.m1[e];
           }
           valid = valid && m0.w >= 0.f;
           if (valid) {
             const float fr[3] = {one_plus_to_frac(yv[0]), one_plus_to_frac(yv[1]), one_plus_to_frac(yv[2])};
-            fast_item<GN>(acc, Rf, fr, res, m0, m1, s_rec[2 * k], s_rec[2 * k + 1]);
+            fast_item<GN>(acc, Rf, fr, res, m0, m1, s_r0[k], s_r1[k]);
           }
         }
         nmatch += __popc(__ballot_sync(0xffffffffu, valid));
@@ -407,7 +418,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
 
 template <int U>
 size_t fast_smem(int S) {
-  return sizeof(WarpStage<32 * U>) * kFastWarps + sizeof(double) * 3 * ((S + 1) & ~1) + sizeof(float4) * 2 * S;
+  const size_t Sp = static_cast<size_t>((S + 32 * U - 1) / (32 * U) * (32 * U));
+  return sizeof(WarpStage<32 * U>) * kFastWarps + sizeof(float4) * 2 * Sp + sizeof(double) * 3 * Sp;
 }
 
 template <bool GN, int U>
