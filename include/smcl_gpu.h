@@ -131,9 +131,28 @@ int smcl_device_count(int* out);
  * nearest-neighbour field (nnf.cpp:10-96) and uploads the map. map may be NULL
  * for stage-only use (no likelihood calls). device < 0: current device. */
 int smcl_create(const smcl_cloud* map, const smcl_config* cfg, int device, smcl_engine** out);
-/* Sharded engine: this rank owns particles [rank*N/world, (rank+1)*N/world). */
-int smcl_create_sharded(const smcl_cloud* map, const smcl_config* cfg, int device, int rank, int world,
+/* Collective backend of a sharded engine (one engine per rank / GPU).
+ * allgather: every rank contributes `bytes` at `send` (device memory of the
+ * engine's device); `recv` (device, world*bytes) receives the contributions in
+ * rank order. `stream` is the engine's cudaStream_t: the callee must order its
+ * work after everything already enqueued on it and before anything enqueued
+ * after the call returns (e.g. NCCL on that stream). Returns 0 on success. */
+typedef struct smcl_comm {
+  void* ctx;
+  int32_t rank, world;
+  int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes, void* stream);
+} smcl_comm;
+
+/* Sharded engine: this rank owns the particles with global indices
+ * [rank*N/world, (rank+1)*N/world) (N/world must be a multiple of 4096 so
+ * reduction chunks never straddle shards); the map is replicated. Results are
+ * bit-identical to a single engine with reorder_particles = 0 (required). */
+int smcl_create_sharded(const smcl_cloud* map, const smcl_config* cfg, int device, const smcl_comm* comm,
                         smcl_engine** out);
+/* In-process loopback collectives for `world` engines driven by `world` host
+ * threads (shard-count invariance tests on one device): fills comms[world]. */
+int smcl_comm_loopback_create(int32_t world, smcl_comm* comms);
+void smcl_comm_loopback_destroy(smcl_comm* comms);
 int smcl_destroy(smcl_engine* h);
 
 /* FilterEngine::init_uniform(const Aabb&) (filter.cpp:108-116). */

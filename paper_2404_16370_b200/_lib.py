@@ -7,7 +7,7 @@ product path can silently run on the CPU.
 import ctypes as C
 import os
 
-from .abi import (SmclCloud, SmclConfig, SmclCorridorSpec, SmclFrameResult, SmclNeighborStats, SmclOdom,
+from .abi import (SmclCloud, SmclComm, SmclConfig, SmclCorridorSpec, SmclFrameResult, SmclNeighborStats, SmclOdom,
                   SmclParticlesView, SmclSensorSpec, SmclStepProfile)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -22,7 +22,9 @@ SIGNATURES = {
     "smcl_config_default": (None, [_P(SmclConfig)]),
     "smcl_device_count": (_int, [_P(_int)]),
     "smcl_create": (_int, [_P(SmclCloud), _P(SmclConfig), _int, _P(C.c_void_p)]),
-    "smcl_create_sharded": (_int, [_P(SmclCloud), _P(SmclConfig), _int, _int, _int, _P(C.c_void_p)]),
+    "smcl_create_sharded": (_int, [_P(SmclCloud), _P(SmclConfig), _int, _P(SmclComm), _P(C.c_void_p)]),
+    "smcl_comm_loopback_create": (_int, [_i32, _P(SmclComm)]),
+    "smcl_comm_loopback_destroy": (None, [_P(SmclComm)]),
     "smcl_destroy": (_int, [C.c_void_p]),
     "smcl_init_uniform": (_int, [C.c_void_p, _P(_d)]),
     "smcl_init_uniform_seeded": (_int, [C.c_void_p, _i64, _P(_d), _int, _u64]),

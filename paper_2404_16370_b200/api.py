@@ -48,9 +48,13 @@ class FilterEngine:
 
     ``map_cloud`` may be None for stage-only use (neighbour search, SVGD,
     posterior) on particles uploaded with ``set_particles``.
+
+    ``comm`` (an ``SmclComm`` or an object with a ``.struct`` one, see
+    ``comm.py``) makes this engine one shard of a particle set split across
+    ranks; ``particles()`` / ``set_particles`` then move this rank's shard.
     """
 
-    def __init__(self, map_cloud, cfg=None, device=0):
+    def __init__(self, map_cloud, cfg=None, device=0, comm=None):
         self.cfg = cfg if cfg is not None else make_config()
         self.h = C.c_void_p()
         if map_cloud is not None:
@@ -58,7 +62,14 @@ class FilterEngine:
             mp = C.byref(self._map_c)
         else:
             mp = None
-        check(_lib.lib().smcl_create(mp, C.byref(self.cfg), device, C.byref(self.h)))
+        self.comm = comm
+        if comm is None:
+            self.rank, self.world = 0, 1
+            check(_lib.lib().smcl_create(mp, C.byref(self.cfg), device, C.byref(self.h)))
+        else:
+            cs = getattr(comm, "struct", comm)
+            self.rank, self.world = cs.rank, cs.world
+            check(_lib.lib().smcl_create_sharded(mp, C.byref(self.cfg), device, C.byref(cs), C.byref(self.h)))
         self.map = map_cloud
 
     def close(self):
@@ -127,7 +138,7 @@ class FilterEngine:
         return _lib.lib().smcl_num_particles(self.h)
 
     def particles(self):
-        n = self.num_particles()
+        n = self.num_particles() // self.world
         p = Particles(n, self.cfg.k_neighbors)
         v = p.view()
         check(_lib.lib().smcl_get_particles(self.h, C.byref(v)))

@@ -1,0 +1,108 @@
+"""Collective backends for sharded engines.
+
+A sharded engine (``smcl_create_sharded``) owns the particles with global
+indices ``[rank*N/world, (rank+1)*N/world)`` and calls ONE collective, an
+all-gather on its own CUDA stream, at the exchange points of
+``FilterEngine::step`` (filter.cpp:118-213): LSH keys before the global sort,
+poses/steps before each SVGD iteration, per-chunk partial sums and argmax
+partials of the posterior reductions, the per-round probabilities of the
+smoothing passes and the representative pose. Everything else is shard-local.
+
+Backends:
+
+* ``LoopbackComms`` — in-process, ``world`` engines driven by ``world`` host
+  threads (one device or several); implemented in C (engine.cu).
+* ``TorchComm`` — ``torch.distributed`` over NCCL (device buffers, one process
+  per GPU) or gloo (host buffers; used by the CPU tests of this layer).
+
+torch is plumbing here: it is imported lazily and only by ``TorchComm``.
+"""
+import ctypes as C
+
+from . import _lib
+from .abi import ALLGATHER_FN, SmclComm
+
+SHARD_ALIGN = 4096  # reduce.hpp chunk: no posterior reduction chunk straddles two shards
+
+
+def shard_range(n_total, rank, world):
+    """(gbase, n_local) of ``rank`` for ``n_total`` particles over ``world`` shards."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank/world {rank}/{world}")
+    if n_total % world or (n_total // world) % SHARD_ALIGN:
+        raise ValueError(f"N={n_total} over {world} shards: N/world must be a multiple of {SHARD_ALIGN}")
+    n_local = n_total // world
+    return rank * n_local, n_local
+
+
+class LoopbackComms:
+    """``world`` in-process communicators (smcl_comm_loopback_create)."""
+
+    def __init__(self, world):
+        self.world = world
+        self.structs = (SmclComm * world)()
+        _lib.check(_lib.lib().smcl_comm_loopback_create(world, self.structs))
+
+    def __getitem__(self, rank):
+        return self.structs[rank]
+
+    def close(self):
+        if self.structs is not None:
+            _lib.lib().smcl_comm_loopback_destroy(self.structs)
+            self.structs = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _DeviceBytes:
+    """Zero-copy uint8 view of raw device memory for torch.as_tensor."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class TorchComm:
+    """smcl_comm over a torch.distributed process group.
+
+    ``device=True`` (NCCL): send/recv are device pointers of the engine's GPU
+    and the all-gather is enqueued on the engine's stream (ExternalStream), so
+    it is ordered after the engine's producers and before its consumers.
+    ``device=False`` (gloo): send/recv are host pointers.
+    """
+
+    def __init__(self, group=None, device=True):
+        import torch.distributed as dist
+        self.group = group
+        self.device = device
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.error = None
+        self._fn = ALLGATHER_FN(self._allgather)  # keep the trampoline alive
+        self.struct = SmclComm(None, self.rank, self.world, self._fn)
+
+    def _allgather(self, ctx, send, recv, nbytes, stream):
+        try:
+            import torch
+            import torch.distributed as dist
+            nbytes = int(nbytes)
+            if nbytes == 0:
+                return 0
+            if self.device:
+                dev = torch.device("cuda", torch.cuda.current_device())
+                s = torch.as_tensor(_DeviceBytes(send, nbytes), device=dev)
+                r = torch.as_tensor(_DeviceBytes(recv, nbytes * self.world), device=dev)
+                with torch.cuda.stream(torch.cuda.ExternalStream(int(stream or 0), device=dev)):
+                    dist.all_gather_into_tensor(r, s, group=self.group)
+            else:
+                s = torch.frombuffer((C.c_uint8 * nbytes).from_address(send), dtype=torch.uint8)
+                r = torch.frombuffer((C.c_uint8 * (nbytes * self.world)).from_address(recv), dtype=torch.uint8)
+                dist.all_gather(list(r.split(nbytes)), s.clone(), group=self.group)
+            return 0
+        except Exception as e:  # surfaced by the engine as an SMCL error
+            self.error = e
+            return 1

@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <atomic>
 #include <bit>
+#include <condition_variable>
+#include <mutex>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -255,6 +257,41 @@ struct smcl_engine {
   int k = 20;
   int64_t frame = 0;
 
+  // Sharding: particles [gbase, gbase + n_local) live here; the
+  // global arrays below are assembled by all-gathers at the reference's
+  // exchange points. Unsharded engines alias them to the local arrays.
+  smcl_comm comm{};
+  bool sharded = false;
+  DBuf<Pose> g_poses;
+  DBuf<double> g_steps, g_p, g_part, g_part2;
+  DBuf<uint64_t> g_keys;
+  DBuf<int32_t> g_flag, pos_list;
+  DBuf<unsigned long long> g_counts;
+  DBuf<double> g_argv;
+  DBuf<long long> g_argi;
+  DBuf<Pose> g_rep;
+  DBuf<int32_t> g_repid;
+
+  // All-gather `bytes` per rank from send (device) into recv (device).
+  void allgather(const void* send, void* recv, size_t bytes) {
+    if (!sharded) {
+      if (send != recv) CK(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, st));
+      return;
+    }
+    if (comm.allgather(comm.ctx, send, recv, static_cast<uint64_t>(bytes), st) != 0)
+      throw std::runtime_error("smcl_comm allgather failed");
+  }
+  const Pose* all_poses() {  // current poses of every particle
+    if (!sharded) return poses.p;
+    allgather(poses.p, g_poses.p, sizeof(Pose) * static_cast<size_t>(n_local));
+    return g_poses.p;
+  }
+  const double* all_steps() {
+    if (!sharded) return steps.p;
+    allgather(steps.p, g_steps.p, sizeof(double) * 6 * static_cast<size_t>(n_local));
+    return g_steps.p;
+  }
+
   // map
   bool has_map = false;
   bool map_structured = false;
@@ -317,6 +354,8 @@ struct smcl_engine {
   smcl_step_profile prof{};
   bool fast_used = false;
   bool profiling = false;
+  int32_t rep_id = -1;                // id of the last representative
+  unsigned long long last_nm_sum = 0;  // sum of n_matched over all shards (last Bayes update)
   void mark(Ev e) {
     if (!ev[e]) CK(cudaEventCreate(&ev[e]));
     CK(cudaEventRecord(ev[e], st));
@@ -395,10 +434,40 @@ struct smcl_engine {
     sync();
   }
 
+  // Shard geometry for n_total particles: contiguous global
+  // index ranges; 4096-aligned so reduction chunks never straddle shards.
+  void set_shape(int64_t n) {
+    if (sharded) {
+      if (n % world != 0 || (n / world) % kReduceChunk != 0)
+        throw std::invalid_argument("sharded engine: N/world must be a multiple of 4096");
+      if (cfg.reorder_particles) throw std::invalid_argument("sharded engine requires reorder_particles = 0");
+    }
+    n_total = n;
+    n_local = n / world;
+    gbase = static_cast<int64_t>(rank) * n_local;
+  }
+
   void alloc_particles(int64_t n, int kk) {
     n_local = n;
     k = kk;
     const size_t un = static_cast<size_t>(std::max<int64_t>(n, 1));
+    const size_t ug = static_cast<size_t>(std::max<int64_t>(n_total, 1));
+    if (sharded) {
+      const size_t w = static_cast<size_t>(world);
+      g_poses.ensure(ug);
+      g_steps.ensure(ug * 6);
+      g_p.ensure(ug);
+      g_keys.ensure(ug);
+      g_flag.ensure(ug);
+      pos_list.ensure(un);
+      g_part.ensure(w * ((un + kReduceChunk - 1) / kReduceChunk));
+      g_part2.ensure(w * ((un + kReduceChunk - 1) / kReduceChunk));
+      g_counts.ensure(w * 2);
+      g_argv.ensure(w);
+      g_argi.ensure(w);
+      g_rep.ensure(w);
+      g_repid.ensure(w);
+    }
     poses.ensure(un);
     poses2.ensure(un);
     log_post.ensure(un);
@@ -417,19 +486,19 @@ struct smcl_engine {
     ll.ensure(un);
     nm.ensure(un);
     keys.ensure(un);
-    skeys.ensure(un);
-    member_of.ensure(un);
-    head.ensure(un);
-    seg_id.ensure(un);
-    seg_start.ensure(un);
-    new_of_old.ensure(un);
-    iota.ensure(un);
+    skeys.ensure(ug);  // the sort and the bucket runs are over all N keys
+    member_of.ensure(ug);
+    head.ensure(ug);
+    seg_id.ensure(ug);
+    seg_start.ensure(ug);
+    new_of_old.ensure(ug);
+    iota.ensure(ug);
     {
-      std::vector<int32_t> h(un);
-      for (size_t i = 0; i < un; ++i) h[i] = static_cast<int32_t>(i);
-      iota.upload(h.data(), un, st);
+      std::vector<int32_t> h(ug);
+      for (size_t i = 0; i < ug; ++i) h[i] = static_cast<int32_t>(i);
+      iota.upload(h.data(), ug, st);
     }
-    const size_t tb = sort_temp_bytes(static_cast<int64_t>(un));
+    const size_t tb = sort_temp_bytes(static_cast<int64_t>(ug));
     if (tb > temp_bytes) {
       temp.ensure(tb);
       temp_bytes = tb;
@@ -603,8 +672,16 @@ struct smcl_engine {
     const int shift = lp.prio_bits + lp.idx_bits;
 
     launch_lsh_keys(poses.p, n_local, gbase, lp, keys.p, st);
+    // Exchange 1: every rank needs all N keys (global sort, bucket
+    // runs) and all N poses (candidates of its own particles).
+    const uint64_t* keys_all = keys.p;
+    if (sharded) {
+      allgather(keys.p, g_keys.p, sizeof(uint64_t) * static_cast<size_t>(n_local));
+      keys_all = g_keys.p;
+    }
+    const Pose* poses_all = all_poses();
     if (profiling) mark(E_KEYS);
-    sort_keys(keys.p, skeys.p, n, 64, temp.p, temp_bytes, st);
+    sort_keys(keys_all, skeys.p, n, 64, temp.p, temp_bytes, st);
     if (profiling) mark(E_SORT);
     launch_members(skeys.p, n, idx_mask, shift, member_of.p, head.p, st);
     const int32_t* members = member_of.p;
@@ -627,9 +704,17 @@ struct smcl_engine {
     int32_t n_seg = 0;
     CK(cudaMemcpyAsync(&n_seg, seg_id.p + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     g_d2h += sizeof(int32_t);
+    // Sorted positions of this shard's particles, in sorted order.
+    const int32_t* owned = nullptr;
+    if (sharded) {
+      launch_owned_flags(members, n, gbase, n_local, g_flag.p, st);
+      inclusive_sum_i32(g_flag.p, new_of_old.p, n, temp.p, temp_bytes, st);
+      launch_owned_scatter(g_flag.p, new_of_old.p, n, pos_list.p, st);
+      owned = pos_list.p;
+    }
     if (profiling) mark(E_SEG);
     sync();
-    launch_refresh_gather(poses.p, n_local, gbase, nullptr, members, seg_id.p, seg_start.p, n_seg, n, idx.p, kval.p,
+    launch_refresh_gather(poses_all, n_local, gbase, owned, members, seg_id.p, seg_start.p, n_seg, n, idx.p, kval.p,
                           count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, st);
     CK(cudaGetLastError());
     if (profiling) mark(E_RG);
@@ -640,7 +725,13 @@ struct smcl_engine {
     launch_seg_stats(seg_start.p, n_seg, n, cfg.lsh_bucket_capacity, d_hist.p, d_counts.p, st);
     const int64_t chunks = (n_local + kReduceChunk - 1) / kReduceChunk;
     launch_chunk_sum_kernel(kval.p, count.p, n_local, k, pbuf.p, qbuf.p, partial.p, partial2.p, st);
-    launch_finish_sum2(partial.p, partial2.p, chunks, scal.p, st);
+    if (sharded) {  // chunk partials of every shard, combined in global chunk order
+      allgather(partial.p, g_part.p, sizeof(double) * static_cast<size_t>(chunks));
+      allgather(partial2.p, g_part2.p, sizeof(double) * static_cast<size_t>(chunks));
+      launch_finish_sum2(g_part.p, g_part2.p, chunks * world, scal.p, st);
+    } else {
+      launch_finish_sum2(partial.p, partial2.p, chunks, scal.p, st);
+    }
     CK(cudaGetLastError());
     if (out) {
       std::vector<unsigned long long> hist(static_cast<size_t>(hist_len));
@@ -661,24 +752,63 @@ struct smcl_engine {
 
   void svgd(bool fused_apply) {
     SvgdParams sp{cfg.sigma_r, cfg.sigma_t, cfg.repulsion_gain};
+    // Exchange 2: neighbours' poses and Gauss-Newton steps.
+    const Pose* pa = all_poses();
+    const double* sa = all_steps();
     if (fused_apply) {
-      launch_svgd(poses.p, steps.p, n_local, gbase, idx.p, count.p, k, sp, nullptr, poses2.p, st);
+      launch_svgd(pa, sa, n_local, gbase, idx.p, count.p, k, sp, nullptr, poses2.p, st);
       poses.swap(poses2);
     } else {
-      launch_svgd(poses.p, steps.p, n_local, gbase, idx.p, count.p, k, sp, phis.p, nullptr, st);
+      launch_svgd(pa, sa, n_local, gbase, idx.p, count.p, k, sp, phis.p, nullptr, st);
       phis_valid = true;
     }
     CK(cudaGetLastError());
   }
 
+  // Global argmax (value, index; ties -> lowest index) of log_post into
+  // scal[slot], scal_i[slot_i]: per-shard partial, all-gathered, merged.
+  void global_argmax(int slot, int slot_i) {
+    launch_argmax(log_post.p, n_local, gbase, argv.p, argi.p, scal.p + slot, scal_i.p + slot_i, st);
+    if (sharded) {
+      allgather(scal.p + slot, g_argv.p, sizeof(double));
+      allgather(scal_i.p + slot_i, g_argi.p, sizeof(long long));
+      launch_max_of_partials(g_argv.p, g_argi.p, world, scal.p + slot, scal_i.p + slot_i, st);
+    }
+  }
+
   void normalize(double floor_v) {
     const int64_t n = n_local;
     if (n == 0) return;
-    launch_argmax(log_post.p, n, gbase, argv.p, argi.p, scal.p + 2, scal_i.p, st);
+    global_argmax(2, 0);
     launch_chunk_sum_exp(log_post.p, n, scal.p + 2, pbuf.p, partial.p, st);
-    launch_finish_lse(partial.p, (n + kReduceChunk - 1) / kReduceChunk, scal.p + 2, scal.p + 3, st);
+    const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
+    if (sharded) {  // reduce.hpp order: every chunk partial, in global chunk order
+      allgather(partial.p, g_part.p, sizeof(double) * static_cast<size_t>(chunks));
+      launch_finish_lse(g_part.p, chunks * world, scal.p + 2, scal.p + 3, st);
+    } else {
+      launch_finish_lse(partial.p, chunks, scal.p + 2, scal.p + 3, st);
+    }
     launch_apply_lse(log_post.p, n, scal.p + 3, floor_v, st);
     CK(cudaGetLastError());
+  }
+
+  // (matched particles, sum of n_matched) over all shards: exact integers.
+  void global_match_counts(unsigned long long* cnt) {
+    launch_match_counts(ll.p, nm.p, n_local, d_counts.p, st);
+    if (sharded) {
+      allgather(d_counts.p, g_counts.p, 2 * sizeof(unsigned long long));
+      std::vector<unsigned long long> all(2 * static_cast<size_t>(world));
+      g_counts.download(all.data(), all.size(), st);
+      sync();
+      cnt[0] = cnt[1] = 0;
+      for (int r = 0; r < world; ++r) {
+        cnt[0] += all[2 * static_cast<size_t>(r)];
+        cnt[1] += all[2 * static_cast<size_t>(r) + 1];
+      }
+      return;
+    }
+    d_counts.download(cnt, 2, st);
+    sync();
   }
 
   // Returns observation_rejected.
@@ -686,10 +816,9 @@ struct smcl_engine {
     if (!(beta >= 0.0)) throw std::invalid_argument("bayes_update: beta must be >= 0");
     const int64_t n = n_local;
     if (n == 0) return false;
-    launch_match_counts(ll.p, nm.p, n, d_counts.p, st);
     unsigned long long cnt[2];
-    d_counts.download(cnt, 2, st);
-    sync();
+    global_match_counts(cnt);
+    last_nm_sum = cnt[1];
     if (cnt[0] == 0) {
       launch_fill(log_post.p, n, -std::log(static_cast<double>(n_total)), st);
       return true;
@@ -705,7 +834,13 @@ struct smcl_engine {
     if (n == 0 || iters == 0) return;
     launch_exp(log_post.p, pbuf.p, n, st);
     for (int r = 0; r < iters; ++r) {
-      launch_smooth_round(pbuf.p, qbuf.p, n, idx.p, kval.p, count.p, k, st);
+      // Exchange 3: neighbours' probabilities every round.
+      const double* p_all = pbuf.p;
+      if (sharded) {
+        allgather(pbuf.p, g_p.p, sizeof(double) * static_cast<size_t>(n));
+        p_all = g_p.p;
+      }
+      launch_smooth_round(p_all, qbuf.p, n, idx.p, kval.p, count.p, k, st);
       pbuf.swap(qbuf);
     }
     launch_log(pbuf.p, log_post.p, n, st);
@@ -715,7 +850,7 @@ struct smcl_engine {
 
   void representative(int64_t* index, double* pose, double* value) {
     if (n_local == 0) throw std::invalid_argument("representative: empty or mismatched particle set");
-    launch_argmax(log_post.p, n_local, gbase, argv.p, argi.p, scal.p + 4, scal_i.p + 1, st);
+    global_argmax(4, 1);
     double v;
     long long ix;
     CK(cudaMemcpyAsync(&v, scal.p + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -724,13 +859,24 @@ struct smcl_engine {
     sync();
     *index = ix;
     *value = v;
-    if (pose) {
-      Pose p;
-      CK(cudaMemcpyAsync(&p, poses.p + (ix - gbase), sizeof(Pose), cudaMemcpyDeviceToHost, st));
-      g_d2h += sizeof(Pose);
-      sync();
-      store_pose(p, pose);
+    // The owner rank publishes the winner's pose and id (one slot per rank).
+    const int64_t owner = sharded ? ix / n_local : 0;
+    const int64_t li = ix - owner * n_local;
+    if (sharded) {
+      const int64_t mine = owner == rank ? li : 0;
+      CK(cudaMemcpyAsync(g_rep.p + rank, poses.p + mine, sizeof(Pose), cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(g_repid.p + rank, id.p + mine, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      allgather(g_rep.p + rank, g_rep.p, sizeof(Pose));
+      allgather(g_repid.p + rank, g_repid.p, sizeof(int32_t));
     }
+    const Pose* src_pose = sharded ? g_rep.p + owner : poses.p + li;
+    const int32_t* src_id = sharded ? g_repid.p + owner : id.p + li;
+    Pose p;
+    CK(cudaMemcpyAsync(&p, src_pose, sizeof(Pose), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&rep_id, src_id, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    g_d2h += sizeof(Pose) + sizeof(int32_t);
+    sync();
+    if (pose) store_pose(p, pose);
   }
 
   void init_uniform(int64_t n, const double* b, bool full_rotation, uint64_t seed) {
@@ -739,9 +885,8 @@ struct smcl_engine {
       if (b[3 + a] - b[a] <= 0.0) throw std::invalid_argument("init_uniform: degenerate bounds");
     if (cfg.k_neighbors < 1 || cfg.k_neighbors > kMaxK)
       throw std::invalid_argument("k_neighbors must be in [1, 32] on this device build");
-    n_total = n;
-    gbase = 0;
-    alloc_particles(n, cfg.k_neighbors);
+    set_shape(n);
+    alloc_particles(n_local, cfg.k_neighbors);
     InitParams ip{};
     ip.stream = mix_seed(seed, k_stream_init);
     for (int a = 0; a < 3; ++a) {
@@ -823,9 +968,8 @@ struct smcl_engine {
     representative(&ix, r.representative, &v);
     unsigned long long cnt[6];
     d_counts.download(cnt, 6, st);
-    int32_t rid;
-    CK(cudaMemcpyAsync(&rid, id.p + (ix - gbase), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    g_d2h += sizeof(int32_t);
+    const int32_t rid = rep_id;
+    cnt[1] = last_nm_sum;  // global sum of n_matched (bayes)
     sync();
     if (!empty) {  // last (or only) Gauss-Newton iteration
       t_gn += since(E_GN0, E_GN1);
@@ -955,13 +1099,91 @@ int smcl_create(const smcl_cloud* map, const smcl_config* cfg, int device, smcl_
   return guard([&] { *out = make_engine(map, cfg, device); });
 }
 
-int smcl_create_sharded(const smcl_cloud* map, const smcl_config* cfg, int device, int rank, int world,
+int smcl_create_sharded(const smcl_cloud* map, const smcl_config* cfg, int device, const smcl_comm* comm,
                         smcl_engine** out) {
   return guard([&] {
-    if (world != 1 || rank != 0)
-      throw std::invalid_argument("smcl_create_sharded: multi-shard engines are driven from the host comm layer");
-    *out = make_engine(map, cfg, device);
+    if (!comm || comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world || !comm->allgather)
+      throw std::invalid_argument("smcl_create_sharded: invalid communicator");
+    std::unique_ptr<smcl_engine> e(make_engine(map, cfg, device));
+    e->comm = *comm;
+    e->rank = comm->rank;
+    e->world = comm->world;
+    e->sharded = comm->world > 1;
+    if (e->sharded && cfg->reorder_particles)
+      throw std::invalid_argument("sharded engine requires reorder_particles = 0");
+    *out = e.release();
   });
+}
+
+// ---------------------------------------------------------------- loopback collectives
+namespace {
+struct LoopShared {
+  int world;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long generation = 0;
+  std::vector<const void*> send;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long long gen = generation;
+    if (++arrived == world) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+struct LoopRank {
+  std::shared_ptr<LoopShared> shared;
+  int rank;
+};
+// Every rank posts its send pointer, then copies all ranks' buffers into its
+// own recv on its own stream; host barriers order the phases (no device-side
+// waiting between kernels of different ranks).
+int loopback_allgather(void* ctx, const void* send, void* recv, uint64_t bytes, void* stream) {
+  auto* lr = static_cast<LoopRank*>(ctx);
+  LoopShared& sh = *lr->shared;
+  auto st = static_cast<cudaStream_t>(stream);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return 1;
+  sh.send[static_cast<size_t>(lr->rank)] = send;
+  sh.barrier();
+  for (int r = 0; r < sh.world; ++r) {
+    char* dst = static_cast<char*>(recv) + static_cast<size_t>(r) * bytes;
+    const void* src = sh.send[static_cast<size_t>(r)];
+    if (src == dst) continue;  // in place
+    if (cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return 1;
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) return 1;
+  sh.barrier();  // no rank reuses its send buffer before every rank has read it
+  return 0;
+}
+}  // namespace
+
+int smcl_comm_loopback_create(int32_t world, smcl_comm* comms) {
+  return guard([&] {
+    if (world < 1) throw std::invalid_argument("loopback: world must be >= 1");
+    auto sh = std::make_shared<LoopShared>();
+    sh->world = world;
+    sh->send.assign(static_cast<size_t>(world), nullptr);
+    for (int r = 0; r < world; ++r) {
+      comms[r].ctx = new LoopRank{sh, r};
+      comms[r].rank = r;
+      comms[r].world = world;
+      comms[r].allgather = loopback_allgather;
+    }
+  });
+}
+
+void smcl_comm_loopback_destroy(smcl_comm* comms) {
+  if (!comms) return;
+  const int world = comms[0].world;
+  for (int r = 0; r < world; ++r) {
+    delete static_cast<LoopRank*>(comms[r].ctx);
+    comms[r].ctx = nullptr;
+  }
 }
 
 int smcl_destroy(smcl_engine* h) {
@@ -1058,8 +1280,7 @@ int smcl_set_particles(smcl_engine* h, const smcl_particles_view* v) {
   return guard([&] {
     use_dev(h);
     if (v->n < 0 || v->k < 1 || v->k > kMaxK) throw std::invalid_argument("set_particles: bad shape");
-    h->n_total = v->n;
-    h->gbase = 0;
+    h->set_shape(v->n * h->world);  // a sharded engine receives its own shard
     h->alloc_particles(v->n, v->k);
     h->cfg.k_neighbors = v->k;
     const size_t n = static_cast<size_t>(v->n), k = static_cast<size_t>(v->k);

@@ -291,7 +291,32 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
   }
 }
 
+// Sharded pass: flag sorted positions whose particle this shard owns, then
+// scatter them (inclusive-sum ranks) into a dense list in sorted order.
+__global__ void k_owned_flags(const int32_t* __restrict__ member_of, int64_t n, int64_t gbase, int64_t n_local,
+                              int32_t* __restrict__ flag) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t gi = member_of[p];
+  flag[p] = (gi >= gbase && gi < gbase + n_local) ? 1 : 0;
+}
+__global__ void k_owned_scatter(const int32_t* __restrict__ flag, const int32_t* __restrict__ incl, int64_t n,
+                                int32_t* __restrict__ pos_list) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p < n && flag[p]) pos_list[incl[p] - 1] = static_cast<int32_t>(p);
+}
+
 }  // namespace
+
+void launch_owned_flags(const int32_t* member_of, int64_t n, int64_t gbase, int64_t n_local, int32_t* flag,
+                        cudaStream_t st) {
+  count_launch();
+  if (n > 0) k_owned_flags<<<blocks_for(n, 256), 256, 0, st>>>(member_of, n, gbase, n_local, flag);
+}
+void launch_owned_scatter(const int32_t* flag, const int32_t* incl, int64_t n, int32_t* pos_list, cudaStream_t st) {
+  count_launch();
+  if (n > 0) k_owned_scatter<<<blocks_for(n, 256), 256, 0, st>>>(flag, incl, n, pos_list);
+}
 
 void launch_lsh_keys(const Pose* poses, int64_t n, int64_t gbase, const LshPass& lp, uint64_t* keys, cudaStream_t st) {
   count_launch();
