@@ -679,7 +679,6 @@ struct smcl_engine {
       allgather(keys.p, g_keys.p, sizeof(uint64_t) * static_cast<size_t>(n_local));
       keys_all = g_keys.p;
     }
-    const Pose* poses_all = all_poses();
     if (profiling) mark(E_KEYS);
     sort_keys(keys_all, skeys.p, n, 64, temp.p, temp_bytes, st);
     if (profiling) mark(E_SORT);
@@ -698,6 +697,7 @@ struct smcl_engine {
       members = iota.p;
       steps_valid = phis_valid = ll_valid = false;  // storage order changed
     }
+    const Pose* poses_all = all_poses();  // after the reorder: candidates read the current storage
     if (profiling) mark(E_REORDER);
     inclusive_sum_i32(head.p, seg_id.p, n, temp.p, temp_bytes, st);
     launch_segments(head.p, seg_id.p, n, seg_start.p, st);
