@@ -4,6 +4,7 @@
 // Reference call structure: FilterEngine::step (filter.cpp:118-213) and the
 // free stage functions it calls. One CUDA stream per engine; every ABI call is
 // synchronous at return (only small results are read back).
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -714,9 +715,25 @@ struct smcl_engine {
     }
     if (profiling) mark(E_SEG);
     sync();
+    // SMCL_RG_STATS=1: per-pass candidate / survivor / evaluation counters on stderr (diagnostics only).
+    static const bool rg_stats = std::getenv("SMCL_RG_STATS") != nullptr;
+    unsigned long long* dbg = nullptr;
+    if (rg_stats) {
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&dbg), 5 * sizeof(unsigned long long), st));
+      CK(cudaMemsetAsync(dbg, 0, 5 * sizeof(unsigned long long), st));
+    }
     launch_refresh_gather(poses_all, n_local, gbase, owned, members, seg_id.p, seg_start.p, n_seg, n, idx.p, kval.p,
-                          count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, st);
+                          count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, st,
+                          dbg);
     CK(cudaGetLastError());
+    if (rg_stats) {
+      unsigned long long c[5];
+      CK(cudaMemcpyAsync(c, dbg, sizeof(c), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      CK(cudaFree(dbg));
+      std::fprintf(stderr, "[rg] n=%lld window=%llu survivors=%llu evaluated=%llu lazy=%llu refresh=%llu\n",
+                   static_cast<long long>(n_local), c[0], c[1], c[2], c[3], c[4]);
+    }
     if (profiling) mark(E_RG);
     // statistics
     const int hist_len = cfg.lsh_bucket_capacity + 2;

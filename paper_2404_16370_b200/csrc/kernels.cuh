@@ -76,7 +76,7 @@ void launch_owned_scatter(const int32_t* flag, const int32_t* incl, int64_t n, i
 void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, const int32_t* pos_list,
                            const int32_t* member_of, const int32_t* seg_id, const int32_t* seg_start, int32_t n_seg,
                            int64_t n_sorted, int32_t* idx, float* kval, int32_t* count, int k, int cap, double sr,
-                           double st_, cudaStream_t st);
+                           double st_, cudaStream_t st, unsigned long long* dbg = nullptr);
 
 // posterior.cu
 void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta, cudaStream_t st);

@@ -141,6 +141,25 @@ __global__ void k_seg_stats(const int32_t* __restrict__ seg_start, int32_t n_seg
 // from s/r, c/r and the tiny th - theta. q agrees with the reference's to
 // ~1e-14 relative; the float is returned only if exp(-q)*(1 -+ 4e-12) round
 // to the same float, otherwise *ok = false and kval_of takes the reference-order log.
+// Reciprocal / reciprocal square root: MUFU seed (~2^-22) + two Newton
+// steps (~1 ulp), no IEEE slow path. Arguments are positive normal numbers.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
+
 __device__ __forceinline__ float kval_fast(const Pose& a, const Pose& b, double sr, double st, bool* ok) {
   double m[9];
 #pragma unroll
@@ -154,25 +173,26 @@ __device__ __forceinline__ float kval_fast(const Pose& a, const Pose& b, double 
   for (int i = 0; i < 3; ++i) u[i] = fma(a.R[0 * 3 + i], d0, fma(a.R[1 * 3 + i], d1, a.R[2 * 3 + i] * d2));
   const double v0 = m[7] - m[5], v1 = m[2] - m[6], v2 = m[3] - m[1];
   const double vv = fma(v0, v0, fma(v1, v1, v2 * v2));  // |vee|^2 = 4 s^2
-  const double s = 0.5 * sqrt(vv);
   const double c = fmin(1.0, fmax(-1.0, 0.5 * ((m[0] + m[4]) + m[8] - 1.0)));
-  const double theta = atan2(s, c);
   const double uu = fma(u[0], u[0], fma(u[1], u[1], u[2] * u[2]));
   double q;
-  if (theta > 3.14159265358979323846 - 1e-2) {  // near the pi branch: reference path
-    *ok = false;
-    return 0.0f;
-  }
   if (vv == 0.0) {  // identical rotations: w = 0, v = u
     q = st * uu;
   } else {
+    const double ivs = rsqrt_nr(vv);  // 1 / |vee|
+    const double s = 0.5 * (vv * ivs);
+    const double theta = atan2(s, c);
+    if (theta > 3.14159265358979323846 - 1e-2) {  // near the pi branch: reference path
+      *ok = false;
+      return 0.0f;
+    }
     const double r2 = fma(s, s, c * c);
-    const double inv_r = rsqrt(r2);
+    const double inv_r = rsqrt_nr(r2);
     const double r = r2 * inv_r;
     const double th = theta * r;  // |w|
     const double th2 = th * th;
-    const double uw = fma(u[0], v0, fma(u[1], v1, u[2] * v2));
-    const double par = uw * uw / vv;  // (u . w^)^2
+    const double uw = fma(u[0], v0, fma(u[1], v1, u[2] * v2)) * ivs;
+    const double par = uw * uw;  // (u . w^)^2
     const double perp = fmax(uu - par, 0.0);
     double F;  // th^2 / (4 sin^2(th/2))
     if (th2 < 1e-6) {
@@ -182,8 +202,7 @@ __device__ __forceinline__ float kval_fast(const Pose& a, const Pose& b, double 
       const double sin_th = fma(dl, Cc, S) - 0.5 * dl * dl * S;
       const double cos_th = fma(-dl, S, Cc) - 0.5 * dl * dl * Cc;
       // 4 sin^2(th/2) = 2(1 - cos th) = 2 sin^2 th / (1 + cos th)
-      const double four_s2 = cos_th < 0.0 ? 2.0 * (1.0 - cos_th) : 2.0 * sin_th * sin_th / (1.0 + cos_th);
-      F = th2 / four_s2;
+      F = cos_th < 0.0 ? th2 * rcp_nr(2.0 * (1.0 - cos_th)) : th2 * (1.0 + cos_th) * rcp_nr(2.0 * sin_th * sin_th);
     }
     q = fma(sr, th2, st * fma(perp, F, par));
   }
@@ -384,7 +403,7 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                            const int32_t* member_of,
                            const int32_t* seg_id, const int32_t* seg_start, int32_t n_seg, int64_t n_sorted,
                            int32_t* idx, float* kval, int32_t* count, int k, int cap, double sr, double st_,
-                           cudaStream_t st) {
+                           cudaStream_t st, unsigned long long* /*dbg*/) {
   count_launch();
   constexpr int B = 64;
   if (n > 0)
