@@ -392,8 +392,6 @@ struct smcl_engine {
     }
     const host::NnfGeometry g = host::nnf_geometry(map_bounds, cfg.nnf_resolution, cfg.nnf_padding,
                                                    cfg.nnf_max_query_dist, size_t(1) << 30);
-    h_cells.resize(static_cast<size_t>(g.n_cells));
-    host::build_nnf_cells(pts, m->n, g, h_cells.data());
     n_cells = g.n_cells;
     for (int a = 0; a < 3; ++a) {
       geom.origin[a] = g.origin[a];
@@ -401,35 +399,35 @@ struct smcl_engine {
     }
     geom.res = g.resolution;
     geom.inv_res = 1.0 / g.resolution;
-    cells.upload(h_cells.data(), h_cells.size(), st);
     map_mu.upload(m->mu, static_cast<size_t>(m->n) * 3, st);
     map_sigma.upload(m->sigma, static_cast<size_t>(m->n) * 9, st);
+    // Device map load (kernels/map_build.cu): NNF bit-identical to
+    // host::build_nnf_cells (nnf.cpp:10-96); the point grid of
+    // point_grid.cpp:10-49 over the map's own point bounds.
+    const host::Aabb pb = host::compute_bounds(pts, m->n);
+    int pg_dims[3];
+    for (int a = 0; a < 3; ++a) pg_dims[a] = static_cast<int>(std::floor((pb.max[a] - pb.min[a]) / g.resolution)) + 1;
+    cells.ensure(static_cast<size_t>(n_cells));
+    CK(build_nnf_device(map_mu.p, m->n, pb.min, pg_dims, g.origin, g.dims, g.resolution, g.max_query_dist, cells.p,
+                        st));
+    h_cells.clear();  // host copy made on demand (smcl_get_nnf)
     // Structured (plane-model) map -> denormalised 32-byte cell records.
-    std::vector<float> beta(static_cast<size_t>(m->n)), sv(static_cast<size_t>(m->n)), uv(3 * static_cast<size_t>(m->n));
+    std::vector<float4> plane(2 * static_cast<size_t>(m->n));
     bool ok = true;
-    for (int64_t i = 0; i < m->n && ok; ++i)
-      ok = structure_ab(m->sigma + 9 * i, beta[static_cast<size_t>(i)], sv[static_cast<size_t>(i)], &uv[3 * static_cast<size_t>(i)]);
+    for (int64_t i = 0; i < m->n && ok; ++i) {
+      float beta, sv, u[3];
+      ok = structure_ab(m->sigma + 9 * i, beta, sv, u);
+      plane[2 * i] = make_float4(beta, sv, 0.f, 0.f);
+      plane[2 * i + 1] = make_float4(u[0], u[1], u[2], 0.f);
+    }
     map_structured = ok;
     if (ok) {
-      std::vector<float4> rec(2 * static_cast<size_t>(n_cells));
-      const int nx = geom.dims[0], ny = geom.dims[1];
-      for (int64_t c = 0; c < n_cells; ++c) {
-        const int32_t mi = h_cells[static_cast<size_t>(c)];
-        if (mi < 0) {
-          rec[2 * c] = make_float4(0.f, 0.f, 0.f, -1.f);
-          rec[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-          continue;
-        }
-        const int64_t ix = c % nx, iy = (c / nx) % ny, iz = c / (static_cast<int64_t>(nx) * ny);
-        const double corner[3] = {geom.origin[0] + static_cast<double>(ix) * geom.res,
-                                  geom.origin[1] + static_cast<double>(iy) * geom.res,
-                                  geom.origin[2] + static_cast<double>(iz) * geom.res};
-        const double* mu = m->mu + 3 * static_cast<int64_t>(mi);
-        rec[2 * c] = make_float4(static_cast<float>(mu[0] - corner[0]), static_cast<float>(mu[1] - corner[1]),
-                                 static_cast<float>(mu[2] - corner[2]), beta[static_cast<size_t>(mi)]);
-        rec[2 * c + 1] = make_float4(uv[3 * mi], uv[3 * mi + 1], uv[3 * mi + 2], sv[static_cast<size_t>(mi)]);
-      }
-      map_fast.upload(rec.data(), rec.size(), st);
+      DBuf<float4> d_plane;
+      d_plane.upload(plane.data(), plane.size(), st);
+      map_fast.ensure(2 * static_cast<size_t>(n_cells));
+      CK(build_map_records_device(cells.p, n_cells, g.origin, g.dims, g.resolution, map_mu.p, d_plane.p, map_fast.p,
+                                  st));
+      sync();
     }
     has_map = true;
     sync();
@@ -1321,7 +1319,14 @@ int smcl_get_nnf(smcl_engine* h, int32_t dims[3], double origin[3], double* reso
       origin[a] = h->geom.origin[a];
     }
     if (resolution) *resolution = h->geom.res;
-    if (cells) std::memcpy(cells, h->h_cells.data(), h->h_cells.size() * sizeof(int32_t));
+    if (cells) {
+      if (h->h_cells.size() != static_cast<size_t>(h->n_cells)) {
+        h->h_cells.resize(static_cast<size_t>(h->n_cells));
+        h->cells.download(h->h_cells.data(), h->h_cells.size(), h->st);
+        h->sync();
+      }
+      std::memcpy(cells, h->h_cells.data(), h->h_cells.size() * sizeof(int32_t));
+    }
   });
 }
 

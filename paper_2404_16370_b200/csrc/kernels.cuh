@@ -78,6 +78,15 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                            int64_t n_sorted, int32_t* idx, float* kval, int32_t* count, int k, int cap, double sr,
                            double st_, cudaStream_t st, unsigned long long* dbg = nullptr);
 
+// map_build.cu (device map load: NNF + fast-map records)
+cudaError_t build_nnf_device(const double* d_mu, int64_t n, const double pg_org[3], const int pg_dims[3],
+                             const double nnf_org[3], const int nnf_dims[3], double res, double max_query_dist,
+                             int32_t* d_cells, cudaStream_t st);
+// d_plane: per map point (beta, s, -, -), (u.xyz, -)
+cudaError_t build_map_records_device(const int32_t* d_cells, int64_t n_cells, const double nnf_org[3],
+                                     const int nnf_dims[3], double res, const double* d_mu, const float4* d_plane,
+                                     float4* d_rec, cudaStream_t st);
+
 // posterior.cu
 void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta, cudaStream_t st);
 void launch_fill(double* v, int64_t n, double value, cudaStream_t st);
