@@ -30,6 +30,9 @@ $(BUILD)/%.o: $(CSRC)/%.cpp $(HDRS)
 	@mkdir -p $(dir $@)
 	$(HOSTCXX) $(CXXFLAGS) -c $< -o $@
 
+# Device scan preparation must round like the -ffp-contract=off host build.
+$(BUILD)/kernels/scan_prep.o: NVFLAGS += -fmad=false
+
 $(LIB): $(CU_OBJ) $(CPP_OBJ)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -ccbin $(HOSTCXX) -o $@ $^ -Xcompiler -fopenmp -lgomp

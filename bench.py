@@ -11,8 +11,12 @@ n_svgd_iters + S).
 
   value  device-resident throughput: scans pre-staged in HBM slots, K steps
          timed with CUDA events on the engine stream (smcl_timer_*).
-  e2e    the same metric through the public step call with host scan buffers
-         (host scan prep + H2D + FrameResult D2H inside the timed region).
+  e2e    the same metric through the public step call (smcl_step) with host
+         scan buffers: H2D of the prepared scan + FrameResult D2H inside the
+         timed region.
+  e2e_raw_points  step_points on the raw sensor points of each frame: H2D of
+         the points, device make_scan_cloud (downsample + kNN covariances),
+         the step and the FrameResult D2H (the scenario runner's frame).
 
 Under torchrun (N>1) the SAME 1,048,576 particles are split into N
 particle-index shards (smcl_create_sharded, NCCL all-gathers at the
@@ -206,6 +210,7 @@ def main():
     wl = workload.build(args.workload, n_particles=args.particles, scan_points=args.scan_points, n_frames=n_frames)
     cfg = wl.cfg
     cfg.likelihood_mode = {"auto": 0, "exact": 1, "fast": 2}[args.mode]
+    cfg.n_scan_max = args.scan_points  # make_scan_cloud target of the raw-points e2e leg
     t_setup = time.perf_counter()
     comm = None
     if pg:  # particle-index shards of the same N (strong scaling), NCCL all-gathers at the exchange points
@@ -269,6 +274,38 @@ def main():
         e2e_ms = float(t.item())
     e2e = pp / (e2e_ms * 1e-3)
 
+    # ---- end to end on raw sensor points: device make_scan_cloud + step
+    # (the scenario runner's frame, scenario.cpp:315-338), n_scan_max = S.
+    barrier()
+    pp_raw = 0
+    h2d_raw = 0
+    t0 = time.perf_counter()
+    for f in range(args.warmup + args.steps, args.warmup + 2 * args.steps):
+        d, c, v = wl.odometry[f]
+        res_raw = eng.step_points(wl.raw[f], d, c, v)
+        p = eng.last_step_profile()
+        pp_raw += p["gn_points"] + p["ll_points"]
+        h2d_raw += wl.raw[f].nbytes + 12 * 8 + 36 * 8 + 4
+        assert math.isfinite(res_raw["rep_log_post"])
+    raw_ms = 1e3 * (time.perf_counter() - t0) / args.steps
+    if pg:
+        import torch
+        t = torch.tensor([raw_ms], device=f"cuda:{local}", dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        raw_ms = float(t.item())
+    pp_raw_step = pp_raw / args.steps * (world if pg else 1)
+    # scan preparation alone: device pipeline vs the host product path
+    from paper_2404_16370_b200.api import make_scan_cloud
+    f0 = args.warmup
+    t0 = time.perf_counter()
+    for _ in range(5):
+        eng.scan_prepare(1, wl.raw[f0])
+    dev_prep_ms = 1e3 * (time.perf_counter() - t0) / 5
+    t0 = time.perf_counter()
+    for _ in range(5):
+        make_scan_cloud(wl.raw[f0], cfg)
+    host_prep_ms = 1e3 * (time.perf_counter() - t0) / 5
+
     keys = [k for k in profs[0] if k.endswith("_ms")]
     avg = {k: float(np.mean([p[k] for p in profs])) for k in profs[0]}
     hbm, kind = peaks()
@@ -289,6 +326,11 @@ def main():
                    "engine_setup_s": setup_s},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
                 "d2h_bytes_per_step": int(d2h / args.steps), "ms_per_step": e2e_ms},
+        "e2e_raw_points": {"value": pp_raw_step / (raw_ms * 1e-3), "unit": UNIT, "ms_per_step": raw_ms,
+                           "pp_per_step": pp_raw_step, "h2d_bytes_per_step": int(h2d_raw / args.steps),
+                           "what": f"step_points: {len(wl.raw[f0])} raw sensor points/frame -> device "
+                                   f"make_scan_cloud (n_scan_max={S}) -> step"},
+        "scan_prep_ms": {"device": dev_prep_ms, "host": host_prep_ms, "raw_points": len(wl.raw[f0])},
         "gpu_launches": int(sum(p["kernel_launches"] for p in profs)),
         "roofline": roof,
         "clocks": clk,

@@ -168,6 +168,16 @@ int smcl_step(smcl_engine* h, const smcl_cloud* scan, const smcl_odom* odo, smcl
 #define SMCL_MAX_SCAN_SLOTS 64
 int smcl_scan_upload(smcl_engine* h, int slot, const smcl_cloud* scan);
 int smcl_step_slot(smcl_engine* h, int slot, const smcl_odom* odo, smcl_frame_result* out);
+/* make_scan_cloud(points, cfg) (filter.cpp:86-100) on the device: raw sensor
+ * points (n*3) -> voxel downsample with leaf doubling, kNN plane-model
+ * covariances + sensor noise, staged into a device slot. Bit-identical to
+ * smcl_make_scan_cloud. */
+int smcl_scan_prepare(smcl_engine* h, int slot, const double* points, int64_t n);
+/* Prepared scan of a slot (mu_out n*3, sigma_out n*9; NULL pointers: count only). */
+int smcl_scan_get(smcl_engine* h, int slot, double* mu_out, double* sigma_out, int64_t* n_out);
+/* Scenario-runner frame (scenario.cpp:315-338): make_scan_cloud + step on raw
+ * points == smcl_scan_prepare(slot 0) + smcl_step_slot(0). */
+int smcl_step_points(smcl_engine* h, const double* points, int64_t n, const smcl_odom* odo, smcl_frame_result* out);
 
 /* Per-kernel device times (CUDA events on the engine stream) of the last
  * step, and the algorithmic work they processed. */

@@ -118,6 +118,27 @@ class FilterEngine:
         check(_lib.lib().smcl_step_slot(self.h, slot, C.byref(o), C.byref(r)))
         return r.to_dict()
 
+    def scan_prepare(self, slot, points):
+        """make_scan_cloud (filter.cpp:86-100) on the device, staged into a slot."""
+        pts = _a(points, (-1, 3))
+        check(_lib.lib().smcl_scan_prepare(self.h, slot, f64ptr(pts), pts.shape[0]))
+
+    def scan_get(self, slot):
+        """Prepared scan of a slot as a GaussianCloud."""
+        n = C.c_int64()
+        check(_lib.lib().smcl_scan_get(self.h, slot, None, None, C.byref(n)))
+        mu, sg = np.empty((n.value, 3)), np.empty((n.value, 9))
+        check(_lib.lib().smcl_scan_get(self.h, slot, f64ptr(mu), f64ptr(sg), C.byref(n)))
+        return GaussianCloud(mu, sg)
+
+    def step_points(self, points, delta=None, cov=None, valid=True):
+        """Scenario-runner frame: make_scan_cloud + FilterEngine::step on raw points (device scan prep)."""
+        pts = _a(points, (-1, 3))
+        o = odom_struct(delta, cov, valid)
+        r = SmclFrameResult()
+        check(_lib.lib().smcl_step_points(self.h, f64ptr(pts), pts.shape[0], C.byref(o), C.byref(r)))
+        return r.to_dict()
+
     def last_step_profile(self):
         p = SmclStepProfile()
         check(_lib.lib().smcl_last_step_profile(self.h, C.byref(p)))

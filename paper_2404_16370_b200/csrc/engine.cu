@@ -343,6 +343,13 @@ struct smcl_engine {
     const ScanDev& gn_view() const { return gn_alias ? full : gn; }
   };
   std::vector<std::unique_ptr<ScanSlot>> slots;
+  // Device scan preparation (kernels/scan_prep.cu): raw points, downsampled
+  // points, per-point L1 norms and the CUB/sort scratch.
+  DBuf<double> raw_pts, down_pts, scan_l1;
+  struct PrepDeleter {
+    void operator()(ScanPrepWork* w) const { scan_prep_destroy(w); }
+  };
+  std::unique_ptr<ScanPrepWork, PrepDeleter> prep_work;
   ScanDev scan_tmp;  // stage-API scans
 
   // Step profile: one event per boundary, read after the step's final sync.
@@ -575,6 +582,103 @@ struct smcl_engine {
     } else {
       sl.gn_alias = true;
     }
+  }
+
+  // make_scan_cloud (filter.cpp:86-100) on the device into slot i: raw
+  // points in, prepared Gaussian scan + fast records out, no host math on the
+  // data path. Falls back to the host preparation only for inputs outside the
+  // device path's envelope (voxel keys beyond 21 bits, k + 1 > 16).
+  void prepare_slot(int i, const double* points, int64_t n) {
+    if (n < 0 || (n > 0 && !points)) throw std::invalid_argument("scan_prepare: null points");
+    ScanSlot& sl = slot_at(i);
+    const long long h2d0 = g_h2d.load();
+    auto empty = [&]() {
+      sl.valid = true;
+      sl.full.n = 0;
+      sl.gn_alias = true;
+    };
+    if (n < static_cast<int64_t>(cfg.covariance_k) + 1 || n < 5) return empty();
+    if (n > (int64_t(1) << 30)) throw std::invalid_argument("scan_prepare: too many points");
+    auto host_fallback = [&]() {
+      std::vector<double> mu(static_cast<size_t>(n) * 3), sg(static_cast<size_t>(n) * 9);
+      int64_t m = 0;
+      if (smcl_make_scan_cloud(points, n, &cfg, mu.data(), sg.data(), &m) != SMCL_OK)
+        throw std::runtime_error(smcl_last_error());
+      smcl_cloud c{};
+      c.n = m;
+      c.mu = mu.data();
+      c.sigma = sg.data();
+      set_slot(i, &c);
+    };
+    if (cfg.covariance_k + 1 > 16) return host_fallback();
+    raw_pts.upload(points, static_cast<size_t>(n) * 3, st);
+    if (!prep_work) prep_work.reset(scan_prep_create());
+    const int ni = static_cast<int>(n);
+    const double* d_down = raw_pts.p;
+    int m = ni;
+    if (n > cfg.n_scan_max) {  // downsample_to (gaussian_cloud.cpp:134-144)
+      down_pts.ensure(static_cast<size_t>(n) * 3);
+      double leaf = cfg.scan_voxel_leaf;
+      bool overflow = false;
+      CK(scan_voxel_downsample(prep_work.get(), raw_pts.p, ni, leaf, down_pts.p, &m, &overflow, st));
+      while (!overflow && m > cfg.n_scan_max) {
+        leaf *= 2.0;
+        CK(scan_voxel_downsample(prep_work.get(), raw_pts.p, ni, leaf, down_pts.p, &m, &overflow, st));
+      }
+      if (overflow) return host_fallback();
+      d_down = down_pts.p;
+    }
+    const int k = std::min<int>(cfg.covariance_k, m - 1);
+    if (k < 4) return empty();
+    if (m > kMaxScan) throw std::invalid_argument("scan exceeds the device scan capacity");
+    // kNN grid (point_grid.cpp:10-49 over the downsampled points,
+    // gaussian_cloud.cpp:24-32 cell size) — scalars on the host.
+    double b[6];
+    CK(scan_bounds(prep_work.get(), d_down, m, b, st));
+    double ext[3];
+    for (int a = 0; a < 3; ++a) ext[a] = std::max(b[3 + a] - b[a], 1e-6);
+    const double volume = (ext[0] * ext[1]) * ext[2];
+    const double per_cell = std::max(1.0, static_cast<double>(k) / 2.0);
+    const double cell = std::max(1e-6, std::cbrt(volume * per_cell / static_cast<double>(m)));
+    int dims[3];
+    for (int a = 0; a < 3; ++a) {
+      const double d = std::floor((b[3 + a] - b[a]) / cell) + 1.0;
+      if (!(d < 65535.0)) return host_fallback();
+      dims[a] = static_cast<int>(d);
+    }
+    ScanDev& sd = sl.full;
+    sd.n = m;
+    sd.mu.ensure(static_cast<size_t>(m) * 3);
+    sd.sigma.ensure(static_cast<size_t>(m) * 9);
+    sd.rec.ensure(2 * static_cast<size_t>(m));
+    scan_l1.ensure(static_cast<size_t>(m));
+    CK(cudaMemcpyAsync(sd.mu.p, d_down, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, st));
+    const double nv = cfg.sensor_noise_sigma * cfg.sensor_noise_sigma;
+    CK(scan_covariances(sd.mu.p, m, k, cfg.epsilon_plane, nv > 0.0 ? nv : 0.0, b, cell, dims, sd.sigma.p, st));
+    CK(scan_records(prep_work.get(), sd.mu.p, sd.sigma.p, m, sd.rec.p, scan_l1.p, &sd.structured, &sd.l1max, st));
+    const int stride = cfg.gn_scan_stride;
+    if (stride > 1 && m > 2 * stride) {  // filter.cpp:154-165 strided GN subset
+      const int ng = (m + stride - 1) / stride;
+      ScanDev& g = sl.gn;
+      g.n = ng;
+      g.mu.ensure(static_cast<size_t>(ng) * 3);
+      g.sigma.ensure(static_cast<size_t>(ng) * 9);
+      g.rec.ensure(2 * static_cast<size_t>(ng));
+      scan_l1.ensure(static_cast<size_t>(std::max(m, ng)));
+      CK(scan_gather_stride(sd.mu.p, sd.sigma.p, ng, stride, g.mu.p, g.sigma.p, st));
+      CK(scan_records(prep_work.get(), g.mu.p, g.sigma.p, ng, g.rec.p, scan_l1.p, &g.structured, &g.l1max, st));
+      sl.gn_alias = false;
+    } else {
+      sl.gn_alias = true;
+    }
+    sl.valid = true;
+    last_upload_bytes = g_h2d.load() - h2d0;
+  }
+
+  void step_points(const double* points, int64_t n, const smcl_odom* odo, smcl_frame_result* out) {
+    if (n_total == 0) throw std::logic_error("FilterEngine::step: not initialized");
+    prepare_slot(0, points, n);
+    step_slot(0, odo, out);
   }
 
   bool use_fast(const ScanDev& sd) const {
@@ -1241,6 +1345,35 @@ int smcl_step_slot(smcl_engine* h, int slot, const smcl_odom* odo, smcl_frame_re
     use_dev(h);
     if (!odo || !out) throw std::invalid_argument("smcl_step: null odometry or result");
     h->step_slot(slot, odo, out);
+  });
+}
+
+int smcl_scan_prepare(smcl_engine* h, int slot, const double* points, int64_t n) {
+  return guard([&] {
+    use_dev(h);
+    h->prepare_slot(slot, points, n);
+    h->sync();
+  });
+}
+
+int smcl_scan_get(smcl_engine* h, int slot, double* mu_out, double* sigma_out, int64_t* n_out) {
+  return guard([&] {
+    use_dev(h);
+    if (!n_out) throw std::invalid_argument("smcl_scan_get: null count");
+    auto& sl = h->slot_at(slot);
+    if (!sl.valid) throw std::invalid_argument("smcl_scan_get: empty slot");
+    *n_out = sl.full.n;
+    if (sl.full.n > 0 && mu_out) sl.full.mu.download(mu_out, static_cast<size_t>(sl.full.n) * 3, h->st);
+    if (sl.full.n > 0 && sigma_out) sl.full.sigma.download(sigma_out, static_cast<size_t>(sl.full.n) * 9, h->st);
+    h->sync();
+  });
+}
+
+int smcl_step_points(smcl_engine* h, const double* points, int64_t n, const smcl_odom* odo, smcl_frame_result* out) {
+  return guard([&] {
+    use_dev(h);
+    if (!odo || !out) throw std::invalid_argument("smcl_step: null odometry or result");
+    h->step_points(points, n, odo, out);
   });
 }
 

@@ -87,6 +87,21 @@ cudaError_t build_map_records_device(const int32_t* d_cells, int64_t n_cells, co
                                      const int nnf_dims[3], double res, const double* d_mu, const float4* d_plane,
                                      float4* d_rec, cudaStream_t st);
 
+// scan_prep.cu (device make_scan_cloud, compiled with -fmad=false)
+struct ScanPrepWork;
+ScanPrepWork* scan_prep_create();
+void scan_prep_destroy(ScanPrepWork* w);
+cudaError_t scan_voxel_downsample(ScanPrepWork* w, const double* d_pts, int n, double leaf, double* d_out, int* n_out,
+                                  bool* overflow, cudaStream_t st);
+cudaError_t scan_bounds(ScanPrepWork* w, const double* d_pts, int n, double b[6], cudaStream_t st);
+cudaError_t scan_covariances(const double* d_pts, int n, int k, double eps, double noise_var,
+                             const double grid_org[3], double grid_cell, const int grid_dims[3], double* d_sigma,
+                             cudaStream_t st);
+cudaError_t scan_records(ScanPrepWork* w, const double* d_mu, const double* d_sigma, int n, float4* d_rec,
+                         double* d_l1, bool* structured, double* l1max, cudaStream_t st);
+cudaError_t scan_gather_stride(const double* d_mu, const double* d_sigma, int n_out, int stride, double* mu_out,
+                               double* sigma_out, cudaStream_t st);
+
 // posterior.cu
 void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta, cudaStream_t st);
 void launch_fill(double* v, int64_t n, double value, cudaStream_t st);

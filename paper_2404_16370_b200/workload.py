@@ -35,9 +35,10 @@ def scan_of_points(pts, n_points, cfg):
 
 
 class Workload:
-    def __init__(self, name, cfg, mapc, rects, scans, odometry, truth):
+    def __init__(self, name, cfg, mapc, rects, scans, odometry, truth, raw=None):
         self.name, self.cfg, self.map, self.rects = name, cfg, mapc, rects
         self.scans, self.odometry, self.truth = scans, odometry, truth
+        self.raw = raw or []  # raw sensor points per frame (make_scan_cloud input)
 
     @property
     def bounds(self):
@@ -58,8 +59,9 @@ def build(kind="global_init", n_particles=1 << 20, scan_points=512, n_frames=13,
     sc.n_frames = max(sc.n_frames, n_frames)
     truth = sim.build_trajectory(sc)[:n_frames]
     odo = sim.build_odometry(sc, truth)
-    scans = []
+    scans, raw = [], []
     for f in range(n_frames):
         pts = sim.scan_points_for_frame(sc, rects, truth, f)
+        raw.append(pts)
         scans.append(scan_of_points(pts, scan_points, cfg))
-    return Workload(kind, cfg, mapc, rects, scans, odo, truth)
+    return Workload(kind, cfg, mapc, rects, scans, odo, truth, raw)
