@@ -4,6 +4,7 @@
 // Reference call structure: FilterEngine::step (filter.cpp:118-213) and the
 // free stage functions it calls. One CUDA stream per engine; every ABI call is
 // synchronous at return (only small results are read back).
+#include <chrono>
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -611,30 +612,52 @@ struct smcl_engine {
       set_slot(i, &c);
     };
     if (cfg.covariance_k + 1 > 16) return host_fallback();
+    // SMCL_PREP_STATS=1: per-phase host-timed breakdown on stderr (diagnostics only).
+    static const bool prep_stats = std::getenv("SMCL_PREP_STATS") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!prep_stats) return;
+      sync();
+      const auto t = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[prep] %s %.1f us\n", what, std::chrono::duration<double, std::micro>(t - t_prev).count());
+      t_prev = t;
+    };
     raw_pts.upload(points, static_cast<size_t>(n) * 3, st);
     if (!prep_work) prep_work.reset(scan_prep_create());
+    lap("upload");
     const int ni = static_cast<int>(n);
     const double* d_down = raw_pts.p;
     int m = ni;
+    double b[6];
+    bool have_bounds = false;
     if (n > cfg.n_scan_max) {  // downsample_to (gaussian_cloud.cpp:134-144)
       down_pts.ensure(static_cast<size_t>(n) * 3);
-      double leaf = cfg.scan_voxel_leaf;
       bool overflow = false;
-      CK(scan_voxel_downsample(prep_work.get(), raw_pts.p, ni, leaf, down_pts.p, &m, &overflow, st));
-      while (!overflow && m > cfg.n_scan_max) {
-        leaf *= 2.0;
+      if (n <= 4096) {  // one block, leaf doubling on the device
+        CK(scan_downsample_block(prep_work.get(), raw_pts.p, ni, cfg.scan_voxel_leaf, cfg.n_scan_max, down_pts.p, &m,
+                                 &overflow, b, st));
+        have_bounds = true;
+      } else {
+        double leaf = cfg.scan_voxel_leaf;
         CK(scan_voxel_downsample(prep_work.get(), raw_pts.p, ni, leaf, down_pts.p, &m, &overflow, st));
+        while (!overflow && m > cfg.n_scan_max) {
+          leaf *= 2.0;
+          CK(scan_voxel_downsample(prep_work.get(), raw_pts.p, ni, leaf, down_pts.p, &m, &overflow, st));
+        }
       }
       if (overflow) return host_fallback();
       d_down = down_pts.p;
+      lap("downsample");
     }
     const int k = std::min<int>(cfg.covariance_k, m - 1);
     if (k < 4) return empty();
     if (m > kMaxScan) throw std::invalid_argument("scan exceeds the device scan capacity");
     // kNN grid (point_grid.cpp:10-49 over the downsampled points,
     // gaussian_cloud.cpp:24-32 cell size) — scalars on the host.
-    double b[6];
-    CK(scan_bounds(prep_work.get(), d_down, m, b, st));
+    if (!have_bounds) {
+      CK(scan_bounds(prep_work.get(), d_down, m, b, st));
+      lap("bounds");
+    }
     double ext[3];
     for (int a = 0; a < 3; ++a) ext[a] = std::max(b[3 + a] - b[a], 1e-6);
     const double volume = (ext[0] * ext[1]) * ext[2];
@@ -654,8 +677,9 @@ struct smcl_engine {
     scan_l1.ensure(static_cast<size_t>(m));
     CK(cudaMemcpyAsync(sd.mu.p, d_down, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, st));
     const double nv = cfg.sensor_noise_sigma * cfg.sensor_noise_sigma;
-    CK(scan_covariances(sd.mu.p, m, k, cfg.epsilon_plane, nv > 0.0 ? nv : 0.0, b, cell, dims, sd.sigma.p, st));
-    CK(scan_records(prep_work.get(), sd.mu.p, sd.sigma.p, m, sd.rec.p, scan_l1.p, &sd.structured, &sd.l1max, st));
+    CK(scan_knn_cov_records(prep_work.get(), sd.mu.p, m, k, cfg.epsilon_plane, nv > 0.0 ? nv : 0.0, b, cell, dims,
+                            sd.sigma.p, sd.rec.p, &sd.structured, &sd.l1max, st));
+    lap("knn+cov+records");
     const int stride = cfg.gn_scan_stride;
     if (stride > 1 && m > 2 * stride) {  // filter.cpp:154-165 strided GN subset
       const int ng = (m + stride - 1) / stride;

@@ -94,11 +94,15 @@ void scan_prep_destroy(ScanPrepWork* w);
 cudaError_t scan_voxel_downsample(ScanPrepWork* w, const double* d_pts, int n, double leaf, double* d_out, int* n_out,
                                   bool* overflow, cudaStream_t st);
 cudaError_t scan_bounds(ScanPrepWork* w, const double* d_pts, int n, double b[6], cudaStream_t st);
-cudaError_t scan_covariances(const double* d_pts, int n, int k, double eps, double noise_var,
-                             const double grid_org[3], double grid_cell, const int grid_dims[3], double* d_sigma,
-                             cudaStream_t st);
 cudaError_t scan_records(ScanPrepWork* w, const double* d_mu, const double* d_sigma, int n, float4* d_rec,
                          double* d_l1, bool* structured, double* l1max, cudaStream_t st);
+// n <= 4096: the whole leaf-doubling downsample in one block; bounds of the result.
+cudaError_t scan_downsample_block(ScanPrepWork* w, const double* d_pts, int n, double leaf0, int max_points,
+                                  double* d_out, int* n_out, bool* overflow, double bounds[6], cudaStream_t st);
+// kNN covariances + noise + fast records + L1 bound, one sync.
+cudaError_t scan_knn_cov_records(ScanPrepWork* w, const double* d_pts, int n, int k, double eps, double noise_var,
+                                 const double grid_org[3], double grid_cell, const int grid_dims[3],
+                                 double* d_sigma, float4* d_rec, bool* structured, double* l1max, cudaStream_t st);
 cudaError_t scan_gather_stride(const double* d_mu, const double* d_sigma, int n_out, int stride, double* mu_out,
                                double* sigma_out, cudaStream_t st);
 

@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
+#include <vector>
 
 #include "../engine.cuh"
 #include "../kernels.cuh"
@@ -88,6 +90,157 @@ __global__ void k_voxel_centroids(const double* __restrict__ p, const uint64_t* 
   out[3 * o] = sx / d;
   out[3 * o + 1] = sy / d;
   out[3 * o + 2] = sz / d;
+}
+
+// Whole downsample_to (gaussian_cloud.cpp:134-144) in one block for n <=
+// kBlockItems points: keys, stable block radix sort, voxel heads, leaf
+// doubling until <= max_points voxels, first-appearance positions, centroids
+// in input order, and the bounds of the result (kNN grid). One launch, no host
+// round trip between leaf levels.
+constexpr int kBlockThreads = 512, kBlockIpt = 8, kBlockItems = kBlockThreads * kBlockIpt;
+using BlockSort = cub::BlockRadixSort<uint64_t, kBlockThreads, kBlockIpt, int32_t>;
+using BlockScanI = cub::BlockScan<int32_t, kBlockThreads>;
+struct BlockSmem {
+  union {
+    typename BlockSort::TempStorage sort;
+    typename BlockScanI::TempStorage scan;
+  } tmp;
+  uint64_t key[kBlockItems];
+  int32_t idx[kBlockItems];
+  int32_t flag[kBlockItems];  // first-appearance flag by input index, then its exclusive scan
+  int count, overflow;
+  double lo[3][kBlockThreads / 32], hi[3][kBlockThreads / 32];
+};
+
+__global__ void __launch_bounds__(kBlockThreads) k_downsample_block(const double* __restrict__ p, int n, double leaf0,
+                                                                   int max_points, double* __restrict__ out,
+                                                                   int* __restrict__ info, double* __restrict__ bounds) {
+  extern __shared__ __align__(16) unsigned char ds_raw[];
+  BlockSmem& sm = *reinterpret_cast<BlockSmem*>(ds_raw);
+  const int t = threadIdx.x;
+  double leaf = leaf0;
+  if (t == 0) {
+    sm.count = 0;
+    sm.overflow = 0;
+  }
+  __syncthreads();
+  for (int level = 0; level < 64; ++level) {
+    uint64_t keys[kBlockIpt];
+    int32_t vals[kBlockIpt];
+#pragma unroll
+    for (int u = 0; u < kBlockIpt; ++u) {
+      const int i = t * kBlockIpt + u;
+      vals[u] = i;
+      keys[u] = ~0ull;
+      if (i < n) {
+        uint64_t k = 0;
+        for (int a = 0; a < 3; ++a) {
+          const double f = floor(p[3 * i + a] / leaf);
+          int64_t c = (f >= -9.2e18 && f <= 9.2e18) ? static_cast<int64_t>(f) : INT64_MIN;
+          c += kKeyBias;
+          if (c < 0 || c >= 2 * kKeyBias) {
+            sm.overflow = 1;
+            c = 0;
+          }
+          k = (k << 21) | static_cast<uint64_t>(c);
+        }
+        keys[u] = k;
+      }
+    }
+    __syncthreads();
+    BlockSort(sm.tmp.sort).Sort(keys, vals, 0, 64);  // stable; padding keys (all ones) sort last
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kBlockIpt; ++u) {
+      sm.key[t * kBlockIpt + u] = keys[u];
+      sm.idx[t * kBlockIpt + u] = vals[u];
+    }
+    __syncthreads();
+    int heads = 0;
+#pragma unroll
+    for (int u = 0; u < kBlockIpt; ++u) {
+      const int q = t * kBlockIpt + u;
+      if (q < n) {
+        const bool h = q == 0 || sm.key[q] != sm.key[q - 1];
+        sm.flag[sm.idx[q]] = h ? 1 : 0;
+        heads += h;
+      }
+    }
+    atomicAdd(&sm.count, heads);
+    __syncthreads();
+    if (sm.overflow || sm.count <= max_points) break;
+    leaf *= 2.0;
+    __syncthreads();  // everyone has read count/overflow
+    if (t == 0) sm.count = 0;
+    __syncthreads();
+  }
+  const int m = sm.count;
+  if (sm.overflow) {
+    if (t == 0) {
+      info[0] = m;
+      info[1] = 1;
+    }
+    return;
+  }
+  // exclusive scan of the first-appearance flags in input order -> output position
+  int32_t f[kBlockIpt];
+#pragma unroll
+  for (int u = 0; u < kBlockIpt; ++u) {
+    const int i = t * kBlockIpt + u;
+    f[u] = i < n ? sm.flag[i] : 0;
+  }
+  BlockScanI(sm.tmp.scan).ExclusiveSum(f, f);
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kBlockIpt; ++u) sm.flag[t * kBlockIpt + u] = f[u];
+  __syncthreads();
+  double lo[3] = {1e308, 1e308, 1e308}, hi[3] = {-1e308, -1e308, -1e308};
+#pragma unroll
+  for (int u = 0; u < kBlockIpt; ++u) {
+    const int s = t * kBlockIpt + u;
+    if (s >= n || !(s == 0 || sm.key[s] != sm.key[s - 1])) continue;
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    int c = 0;
+    for (int q = s; q < n && (q == s || sm.key[q] == sm.key[s]); ++q) {
+      const int32_t i = sm.idx[q];
+      sx = sx + p[3 * i];
+      sy = sy + p[3 * i + 1];
+      sz = sz + p[3 * i + 2];
+      ++c;
+    }
+    const double d = static_cast<double>(c);
+    const double v[3] = {sx / d, sy / d, sz / d};
+    const int o = sm.flag[sm.idx[s]];
+    for (int a = 0; a < 3; ++a) {
+      out[3 * o + a] = v[a];
+      lo[a] = fmin(lo[a], v[a]);
+      hi[a] = fmax(hi[a], v[a]);
+    }
+  }
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+  if ((t & 31) == 0)
+    for (int a = 0; a < 3; ++a) {
+      sm.lo[a][t >> 5] = lo[a];
+      sm.hi[a][t >> 5] = hi[a];
+    }
+  __syncthreads();
+  if (t == 0) {
+    for (int a = 0; a < 3; ++a) {
+      double l = sm.lo[a][0], h = sm.hi[a][0];
+      for (int w = 1; w < kBlockThreads / 32; ++w) {
+        l = fmin(l, sm.lo[a][w]);
+        h = fmax(h, sm.hi[a][w]);
+      }
+      bounds[a] = l;
+      bounds[3 + a] = h;
+    }
+    info[0] = m;
+    info[1] = 0;
+  }
 }
 
 __global__ void k_bounds(const double* __restrict__ p, int n, double* __restrict__ b) {
@@ -182,58 +335,34 @@ __device__ __forceinline__ void grid_cell(const KnnGrid& g, const double* p, int
   }
 }
 
-constexpr int kKnnMax = 32;  // k + 1 <= kKnnMax
+constexpr int kKnnMax = 16;  // k + 1 <= kKnnMax (std::sort of <= 16 items is a stable insertion sort)
 
-// gaussian_cloud.cpp:36-90 + filter.cpp:95-98 for point i.
-__global__ void k_scan_covariances(const double* __restrict__ p, int n, int k, double eps, double noise_var,
-                                   KnnGrid g, double* __restrict__ sigma) {
+// (d2, rank, index) lexicographic order of the reference's stable top-K.
+struct KnnKey {
+  double d2;
+  uint64_t rank;
+  int32_t j;
+};
+__device__ __forceinline__ bool knn_less(const KnnKey& a, const KnnKey& b) {
+  return a.d2 < b.d2 || (a.d2 == b.d2 && (a.rank < b.rank || (a.rank == b.rank && a.j < b.j)));
+}
+
+// Grid cell of every scan point (point_grid.cpp:45-49).
+__global__ void k_scan_cells(const double* __restrict__ p, int n, KnnGrid g, int4* __restrict__ cell) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const int K = k + 1;
-  double bd[kKnnMax];
-  uint64_t brank[kKnnMax];
-  int32_t bidx[kKnnMax];
-  int cnt = 0;
-  const double q[3] = {p[3 * i], p[3 * i + 1], p[3 * i + 2]};
-  int c0[3];
-  grid_cell(g, q, c0);
-  for (int j = 0; j < n; ++j) {
-    const double dx = p[3 * j] - q[0], dy = p[3 * j + 1] - q[1], dz = p[3 * j + 2] - q[2];
-    const double d2 = (dx * dx + dy * dy) + dz * dz;
-    int cj[3];
-    grid_cell(g, p + 3 * j, cj);
-    const int ring = max(abs(cj[0] - c0[0]), max(abs(cj[1] - c0[1]), abs(cj[2] - c0[2])));
-    const uint64_t rank = (static_cast<uint64_t>(ring) << 48) | (static_cast<uint64_t>(cj[2]) << 32) |
-                          (static_cast<uint64_t>(cj[1]) << 16) | static_cast<uint64_t>(cj[0]);
-    // insert (d2, rank, j) into the ascending top-K list (lexicographic order)
-    auto less = [&](int s) {
-      return d2 < bd[s] || (d2 == bd[s] && (rank < brank[s] || (rank == brank[s] && j < bidx[s])));
-    };
-    int pos;
-    if (cnt < K) {
-      pos = cnt++;
-    } else {
-      if (!less(K - 1)) continue;
-      pos = K - 1;
-    }
-    while (pos > 0 && less(pos - 1)) {
-      bd[pos] = bd[pos - 1];
-      brank[pos] = brank[pos - 1];
-      bidx[pos] = bidx[pos - 1];
-      --pos;
-    }
-    bd[pos] = d2;
-    brank[pos] = rank;
-    bidx[pos] = j;
-  }
-  // neighbours: the list without the point itself, at most k
+  int c[3];
+  grid_cell(g, p + 3 * i, c);
+  cell[i] = make_int4(c[0], c[1], c[2], 0);
+}
+
+// Covariance + structure record of point i from its k neighbours (one lane).
+__device__ void cov_and_record(const double* __restrict__ p, int i, const int32_t* nbi, int m, double eps,
+                               double noise_var, double* __restrict__ sigma, float4* __restrict__ rec,
+                               int* __restrict__ not_structured, unsigned long long* __restrict__ l1max_bits) {
   double nb[kKnnMax][3];
-  int m = 0;
-  for (int s = 0; s < cnt && m < k; ++s) {
-    if (bidx[s] == i) continue;
-    for (int a = 0; a < 3; ++a) nb[m][a] = p[3 * bidx[s] + a];
-    ++m;
-  }
+  for (int s = 0; s < m; ++s)
+    for (int a = 0; a < 3; ++a) nb[s][a] = p[3 * nbi[s] + a];
   // canonical order (x, y, z) — insertion sort
   for (int s = 1; s < m; ++s) {
     const double x0 = nb[s][0], x1 = nb[s][1], x2 = nb[s][2];
@@ -265,13 +394,97 @@ __global__ void k_scan_covariances(const double* __restrict__ p, int n, int k, d
   sym_eig3_dev(cov, w, v);
   const double lmax = fmax(w[2], 1e-12);
   const double reg[3] = {eps * lmax, lmax, lmax};
-  double* s = sigma + 9 * i;
+  double sg[9];
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c)
-      s[r * 3 + c] = ((v[r * 3 + 0] * reg[0]) * v[c * 3 + 0] + (v[r * 3 + 1] * reg[1]) * v[c * 3 + 1]) +
-                     (v[r * 3 + 2] * reg[2]) * v[c * 3 + 2];
+      sg[r * 3 + c] = ((v[r * 3 + 0] * reg[0]) * v[c * 3 + 0] + (v[r * 3 + 1] * reg[1]) * v[c * 3 + 1]) +
+                      (v[r * 3 + 2] * reg[2]) * v[c * 3 + 2];
   if (noise_var > 0.0)
-    for (int d = 0; d < 3; ++d) s[4 * d] = s[4 * d] + noise_var;
+    for (int d = 0; d < 3; ++d) sg[4 * d] = sg[4 * d] + noise_var;
+  for (int e = 0; e < 9; ++e) sigma[9 * i + e] = sg[e];
+  // engine.cu structure_ab on the final covariance -> fast-path record
+  sym_eig3_dev(sg, w, v);
+  double mx = 0.0;
+  for (int e = 0; e < 9; ++e) mx = fmax(mx, fabs(sg[e]));
+  const double a = 0.5 * (w[1] + w[2]), sv = w[0];
+  const double ax[3] = {v[0], v[3], v[6]};
+  double err = 0.0;
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      const double recv = (r == c ? a : 0.0) - (a - sv) * ax[r] * ax[c];
+      err = fmax(err, fabs(recv - sg[r * 3 + c]));
+    }
+  if (!(err <= 1e-10 * mx) || !(sv >= 0.0) || !(a > 0.0)) atomicExch(not_structured, 1);
+  const double* mu = p + 3 * i;
+  rec[2 * i] = make_float4(static_cast<float>(mu[0]), static_cast<float>(mu[1]), static_cast<float>(mu[2]),
+                           static_cast<float>(a - sv));
+  rec[2 * i + 1] = make_float4(static_cast<float>(ax[0]), static_cast<float>(ax[1]), static_cast<float>(ax[2]),
+                               static_cast<float>(sv));
+  const double l1 = (fabs(mu[0]) + fabs(mu[1])) + fabs(mu[2]);
+  atomicMax(l1max_bits, static_cast<unsigned long long>(__double_as_longlong(l1)));  // l1 >= 0: bit order = value order
+}
+
+// gaussian_cloud.cpp:36-90 + filter.cpp:95-98: warp per query point. Lanes
+// stride over the candidates keeping a private stable top-K; the warp merges
+// the 32 sorted lists by K rounds of a lexicographic warp minimum.
+__global__ void __launch_bounds__(128) k_scan_knn_cov(const double* __restrict__ p, const int4* __restrict__ cell,
+                                                     int n, int k, double eps, double noise_var,
+                                                     double* __restrict__ sigma, float4* __restrict__ rec,
+                                                     int* __restrict__ not_structured,
+                                                     unsigned long long* __restrict__ l1max_bits) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;  // warp-uniform
+  const int K = k + 1;
+  const double q[3] = {p[3 * i], p[3 * i + 1], p[3 * i + 2]};
+  const int4 c0 = cell[i];
+  KnnKey best[kKnnMax];
+  int cnt = 0;
+  for (int j = lane; j < n; j += 32) {
+    const double dx = p[3 * j] - q[0], dy = p[3 * j + 1] - q[1], dz = p[3 * j + 2] - q[2];
+    KnnKey e;
+    e.d2 = (dx * dx + dy * dy) + dz * dz;
+    const int4 cj = cell[j];
+    const int ring = max(abs(cj.x - c0.x), max(abs(cj.y - c0.y), abs(cj.z - c0.z)));
+    e.rank = (static_cast<uint64_t>(ring) << 48) | (static_cast<uint64_t>(cj.z) << 32) |
+             (static_cast<uint64_t>(cj.y) << 16) | static_cast<uint64_t>(cj.x);
+    e.j = j;
+    int pos;
+    if (cnt < K) {
+      pos = cnt++;
+    } else {
+      if (!knn_less(e, best[K - 1])) continue;
+      pos = K - 1;
+    }
+    while (pos > 0 && knn_less(e, best[pos - 1])) {
+      best[pos] = best[pos - 1];
+      --pos;
+    }
+    best[pos] = e;
+  }
+  // merge: K rounds of the warp-wide minimum of the list heads
+  int head = 0;
+  int32_t nbi[kKnnMax];
+  int m = 0;
+  for (int r = 0; r < K; ++r) {
+    KnnKey h;
+    h.d2 = __longlong_as_double(0x7ff0000000000000ll);
+    h.rank = ~0ull;
+    h.j = 0x7fffffff;
+    if (head < cnt) h = best[head];
+    KnnKey mn = h;
+    for (int o = 16; o > 0; o >>= 1) {
+      KnnKey other;
+      other.d2 = __shfl_xor_sync(FULL, mn.d2, o);
+      other.rank = __shfl_xor_sync(FULL, mn.rank, o);
+      other.j = __shfl_xor_sync(FULL, mn.j, o);
+      if (knn_less(other, mn)) mn = other;
+    }
+    if (head < cnt && h.j == mn.j) ++head;  // the owning lane pops its head (indices are unique)
+    if (mn.j != i && m < k) nbi[m++] = mn.j;  // the point itself is skipped (gaussian_cloud.cpp:55-59)
+  }
+  if (lane == 0) cov_and_record(p, i, nbi, m, eps, noise_var, sigma, rec, not_structured, l1max_bits);
 }
 
 // engine.cu structure_ab on the device: plane-model parameters of a scan
@@ -330,7 +543,10 @@ cudaError_t grow(T*& p, size_t& cap, size_t n, cudaStream_t st) {
 struct ScanPrepWork {
   uint64_t *key = nullptr, *skey = nullptr;
   int32_t *iota = nullptr, *sidx = nullptr, *head = nullptr, *first = nullptr, *pos = nullptr;
-  int* flag = nullptr;  // [0] overflow, [1] not structured
+  int* flag = nullptr;  // [0] overflow / count, [1] not structured, [2] not structured (kNN path)
+  int4* cells = nullptr;
+  unsigned long long* l1bits = nullptr;
+  size_t c_cells = 0, c_l1bits = 0;
   double* bounds = nullptr;
   void* temp = nullptr;
   size_t cap = 0, temp_cap = 0, c_key = 0, c_skey = 0, c_iota = 0, c_sidx = 0, c_head = 0, c_first = 0, c_pos = 0;
@@ -342,7 +558,8 @@ void scan_prep_destroy(ScanPrepWork* w) {
   if (!w) return;
   for (void* p : {static_cast<void*>(w->key), static_cast<void*>(w->skey), static_cast<void*>(w->iota),
                   static_cast<void*>(w->sidx), static_cast<void*>(w->head), static_cast<void*>(w->first),
-                  static_cast<void*>(w->pos), static_cast<void*>(w->flag), static_cast<void*>(w->bounds), w->temp})
+                  static_cast<void*>(w->pos), static_cast<void*>(w->flag), static_cast<void*>(w->bounds),
+                  static_cast<void*>(w->cells), static_cast<void*>(w->l1bits), w->temp})
     if (p) cudaFree(p);
   delete w;
 }
@@ -399,21 +616,6 @@ cudaError_t scan_bounds(ScanPrepWork* w, const double* d_pts, int n, double b[6]
   return cudaStreamSynchronize(st);
 }
 
-cudaError_t scan_covariances(const double* d_pts, int n, int k, double eps, double noise_var,
-                             const double grid_org[3], double grid_cell, const int grid_dims[3], double* d_sigma,
-                             cudaStream_t st) {
-  if (k + 1 > kKnnMax) return cudaErrorInvalidValue;
-  KnnGrid g;
-  for (int a = 0; a < 3; ++a) {
-    g.org[a] = grid_org[a];
-    g.dims[a] = grid_dims[a];
-  }
-  g.cell = grid_cell;
-  count_launch();
-  k_scan_covariances<<<blocks_for(n, 64), 64, 0, st>>>(d_pts, n, k, eps, noise_var, g, d_sigma);
-  return cudaGetLastError();
-}
-
 cudaError_t scan_records(ScanPrepWork* w, const double* d_mu, const double* d_sigma, int n, float4* d_rec,
                          double* d_l1, bool* structured, double* l1max, cudaStream_t st) {
   SP_CK(grow(w->flag, w->c_flag, 2, st));
@@ -429,6 +631,55 @@ cudaError_t scan_records(ScanPrepWork* w, const double* d_mu, const double* d_si
   double m = 0.0;
   for (double v : l1) m = std::max(m, v);
   *l1max = m;
+  return cudaSuccess;
+}
+
+cudaError_t scan_downsample_block(ScanPrepWork* w, const double* d_pts, int n, double leaf0, int max_points,
+                                  double* d_out, int* n_out, bool* overflow, double bounds[6], cudaStream_t st) {
+  if (n > kBlockItems) return cudaErrorInvalidValue;
+  SP_CK(grow(w->flag, w->c_flag, 4, st));
+  SP_CK(grow(w->bounds, w->c_bounds, 6, st));
+  const size_t smem = sizeof(BlockSmem);
+  SP_CK(cudaFuncSetAttribute(k_downsample_block, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  count_launch();
+  k_downsample_block<<<1, kBlockThreads, smem, st>>>(d_pts, n, leaf0, max_points, d_out, w->flag, w->bounds);
+  SP_CK(cudaGetLastError());
+  int info[2];
+  SP_CK(cudaMemcpyAsync(info, w->flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  SP_CK(cudaMemcpyAsync(bounds, w->bounds, 6 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  SP_CK(cudaStreamSynchronize(st));
+  *n_out = info[0];
+  *overflow = info[1] != 0;
+  return cudaSuccess;
+}
+
+cudaError_t scan_knn_cov_records(ScanPrepWork* w, const double* d_pts, int n, int k, double eps, double noise_var,
+                                 const double grid_org[3], double grid_cell, const int grid_dims[3],
+                                 double* d_sigma, float4* d_rec, bool* structured, double* l1max, cudaStream_t st) {
+  if (k + 1 > kKnnMax) return cudaErrorInvalidValue;
+  KnnGrid g;
+  for (int a = 0; a < 3; ++a) {
+    g.org[a] = grid_org[a];
+    g.dims[a] = grid_dims[a];
+  }
+  g.cell = grid_cell;
+  SP_CK(grow(w->cells, w->c_cells, static_cast<size_t>(n), st));
+  SP_CK(grow(w->flag, w->c_flag, 4, st));
+  SP_CK(cudaMemsetAsync(w->flag + 2, 0, 2 * sizeof(int), st));  // [2] not structured, [3] unused
+  SP_CK(grow(w->l1bits, w->c_l1bits, 1, st));
+  SP_CK(cudaMemsetAsync(w->l1bits, 0, sizeof(unsigned long long), st));
+  count_launch(2);
+  k_scan_cells<<<blocks_for(n, 128), 128, 0, st>>>(d_pts, n, g, w->cells);
+  k_scan_knn_cov<<<blocks_for(static_cast<int64_t>(n) * 32, 128), 128, 0, st>>>(
+      d_pts, w->cells, n, k, eps, noise_var, d_sigma, d_rec, w->flag + 2, w->l1bits);
+  SP_CK(cudaGetLastError());
+  int ns = 0;
+  unsigned long long bits = 0;
+  SP_CK(cudaMemcpyAsync(&ns, w->flag + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SP_CK(cudaMemcpyAsync(&bits, w->l1bits, sizeof(bits), cudaMemcpyDeviceToHost, st));
+  SP_CK(cudaStreamSynchronize(st));
+  *structured = ns == 0;
+  std::memcpy(l1max, &bits, sizeof(double));
   return cudaSuccess;
 }
 
