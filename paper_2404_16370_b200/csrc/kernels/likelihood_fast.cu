@@ -1,32 +1,34 @@
 // K1 / K2 fast path: per-particle GICP likelihood (+ Gauss-Newton system) for
 // plane-model maps and scans (reference gicp.cpp:11-45, 109-137).
 //
-// One warp per particle; lanes stride over the scan points, 256 points per
-// step (8 per lane).
+// One warp per particle; lanes stride over the scan points, 32*U points per
+// step (U per lane).
 //
-// Phase A (every point, fp32 + int only): the point is transformed with an
-// fp32 copy of the pose pre-scaled to voxel units; the fp32 voxel coordinate
-// carries a rigorous error bound E, so its floor equals the reference's fp64
-// floor unless the fractional part lies within E of a cell face
-// ("ambiguous"). Certain out-of-bounds points are dropped; every other
-// unambiguous point starts a cp.async of its 32-byte cell record into a
-// per-warp shared-memory stage, so 16 x 16-byte gathers per lane are in flight
-// at once (the global-init workload's record gathers are random: the kernel is
-// L2-latency bound, not bandwidth bound). After the wait, empty cells are
-// dropped and the survivors (plus ambiguous points) are ballot-compacted.
-//
-// Phase B (compacted candidates, full warps): the exact fp64 transform in the
-// reference's evaluation order (the oracle's bits), the residual from the
-// fp64 fractional voxel coordinate, then the body-frame structured-covariance
-// algebra in fp32:
+// Phase A (every point): the point is transformed in fp64 with the pose
+// pre-scaled to voxel units (x = Rv mu + tv, 9 DFMA); floor by a round-down
+// add of 1.5*2^52, the exact fractional coordinate f = x - floor(x) goes to
+// shared memory as fp32 (its 1e-8 m resolution is below the fp32 map record
+// precision). x differs from the reference's ((R mu + t) - o) * inv_res
+// (nnf.hpp:24-35) by < 1e-12 voxel, so the cell is the reference's unless f is
+// within 1e-9 of a face: such points "resolve" in phase B through the
+// reference-order fp64 transform. In-bounds points start a cp.async of their
+// 32-byte cell record into the warp's stage, so U x 2 16-byte gathers per lane
+// are in flight (the global-init gathers are random L2 hits).
+// Compaction: after the wait, empty cells are dropped and the slots of the
+// survivors (plus resolving points) are ballot-compacted; records and
+// fractions stay where phase A put them.
+// Phase B (compacted candidates, full warps): the body-frame
+// structured-covariance algebra in fp32:
 //   Sigma_M' + Sigma_s = A I - beta m m^T - gamma n n^T,
 //   Omega' = (1/A)(I + P m m^T + Q n n^T + T (m n^T + n m^T)),
 //   Delta  = A (s_M + s_S) + beta gamma |m x n|^2   (no cancellation),
 // accumulating ll, H (21) and b (6) per lane; a shuffle reduction gives the
-// per-particle system. Ambiguous candidates resolve their cell exactly in fp64.
+// per-particle system.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../engine.cuh"
 #include "../kernels.cuh"
@@ -35,17 +37,16 @@ namespace smcl {
 
 namespace {
 
-constexpr int kFastWarps = 16;         // warps per CTA (one CTA per SM: 16 warps x 128 registers)
-constexpr unsigned kResolve = 0xFFFFu;  // queue iz field: resolve the cell exactly in fp64
-constexpr unsigned kDrop = 0xFFFEu;     // queue iz field: certainly out of bounds
+constexpr uint32_t kMetaStage = 1u << 16;    // fq.w: record staged (in bounds, cell proven)
+constexpr uint32_t kMetaResolve = 1u << 17;  // fq.w: fraction within 1e-9 of a cell face: reference-order path
 
 template <int kStep>
 struct WarpStage {
-  float4 m0[kStep];     // staged cell records (SoA halves: conflict-free LDS.128)
+  float4 m0[kStep];  // staged cell records by point slot (SoA halves: conflict-free LDS.128)
   float4 m1[kStep];
-  uint32_t qa[kStep];   // compacted candidates: k | iz << 16 (iz == 0xFFFF: resolve exactly)
-  uint32_t qb[kStep];   // ix | iy << 16
-  double pose_v[12];    // fp64 pose in voxel units (Rv row-major, tv)
+  float4 fq[kStep];  // (fraction.xyz fp32, meta bits: k | kMetaStage | kMetaResolve) by point slot
+  uint16_t q[kStep];  // compacted candidate slots
+  double pose_v[12];  // Rv (row-major), tv: reloaded by phase A each step (no registers held in phase B)
 };
 
 struct Acc {
@@ -168,21 +169,6 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// y = 1 + f with f in [0, 1) (fp64) -> f as fp32 by truncating the mantissa
-// (|err| < 2^-23): integer ops only, no F2F on the conversion pipe.
-__device__ __forceinline__ float one_plus_to_frac(double y) {
-  const unsigned hi = static_cast<unsigned>(__double2hiint(y));
-  const unsigned lo = static_cast<unsigned>(__double2loint(y));
-  const unsigned m = ((hi & 0xFFFFFu) << 3) | (lo >> 29);
-  return __uint_as_float(0x3F800000u | m) - 1.0f;
-}
-
-// Exact int32 -> double without the conversion pipe (1.5*2^52 + 2^31 trick).
-__device__ __forceinline__ double int_to_double(int v) {
-  return __hiloint2double(0x43380000, static_cast<int>(static_cast<unsigned>(v) ^ 0x80000000u)) -
-         6755401588539392.0;
-}
-
 __device__ __forceinline__ void transform_x(const double* R, const double* t, const double mu[3], double p[3]) {
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -197,8 +183,8 @@ __constant__ int c_sys_off[28] = {0,  6,  7,  12, 13, 14,                 // htl
                                   36, 37, 38, 39, 40, 41,                 // b
                                   42};                                    // ll
 
-template <bool GN, int kFastUnroll>
-__global__ void __launch_bounds__(kFastWarps * 32, 1)
+template <bool GN, int kFastUnroll, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32, 1)
     k_gicp_fast(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, double* __restrict__ sys,
                 int32_t* __restrict__ nm_out) {
   constexpr int kStep = 32 * kFastUnroll;
@@ -206,59 +192,47 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Stage* stages = reinterpret_cast<Stage*>(smem_raw);
   // Scan in shared memory, padded with NaN points to a multiple of kStep:
-  // fp64 means (exact transform), fp32 records split in two conflict-free halves.
+  // fp64 means (phase A transform), fp32 records split in two conflict-free halves.
   const int S = scan.n;
   const int Sp = (S + kStep - 1) / kStep * kStep;
-  float4* s_r0 = reinterpret_cast<float4*>(smem_raw + sizeof(Stage) * kFastWarps);  // Sp: mu.xyz, gamma
-  float4* s_r1 = s_r0 + Sp;                                                        // Sp: u.xyz, s
-  double* s_mu = reinterpret_cast<double*>(s_r1 + Sp);                             // Sp*3
-  const float fnan = __int_as_float(0x7fc00000);
+  float4* s_r0 = reinterpret_cast<float4*>(smem_raw + sizeof(Stage) * kWarps);  // Sp: mu.xyz, gamma
+  float4* s_r1 = s_r0 + Sp;                                                    // Sp: u.xyz, s
+  double* s_mu = reinterpret_cast<double*>(s_r1 + Sp);                         // Sp*3
   for (int q = threadIdx.x; q < Sp; q += blockDim.x) {
-    s_r0[q] = q < S ? scan.rec[2 * q] : make_float4(fnan, fnan, fnan, 0.f);
+    s_r0[q] = q < S ? scan.rec[2 * q] : make_float4(0.f, 0.f, 0.f, 0.f);
     s_r1[q] = q < S ? scan.rec[2 * q + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  for (int q = threadIdx.x; q < 3 * Sp; q += blockDim.x) s_mu[q] = q < 3 * S ? scan.mu[q] : __longlong_as_double(0x7ff8000000000000ll);
+  for (int q = threadIdx.x; q < 3 * Sp; q += blockDim.x)
+    s_mu[q] = q < 3 * S ? scan.mu[q] : __longlong_as_double(0x7ff8000000000000ll);
   __syncthreads();
 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kFastWarps + wid;
-  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kFastWarps;
+  const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
   const NnfGeom g = map.g;
   const float res = static_cast<float>(g.res);
   const int nx = g.dims[0], ny = g.dims[1];
   const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
                  dz = static_cast<unsigned>(g.dims[2]);
   Stage& ws = stages[wid];
+  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-down add leaves floor(x) in the low word
 
   for (int64_t i = gwarp; i < n; i += nwarps) {
-    // Pose in voxel units x = Rv mu + tv (Rv = R/res, tv = (t - o)/res): fp64
-    // in shared memory for the residual of proven cells, fp32 (Rs, ts) for the
-    // cell guess, Rf = R (fp32) for the body-frame algebra.
-    float Rs[9], ts[3], Rf[9];
-    float tmax = 0.f, rsum = 0.f;
+    // Pose in voxel units x = Rv mu + tv (Rv = R/res, tv = (t - o)/res) in
+    // fp64 registers; Rf = R (fp32) for the body-frame algebra.
+    float Rf[9];
     {
       const Pose P = poses[i];
 #pragma unroll
       for (int q = 0; q < 9; ++q) {
-        const double rv = P.R[q] * g.inv_res;
-        if (lane == 0) ws.pose_v[q] = rv;
-        Rs[q] = static_cast<float>(rv);
+        if (lane == q) ws.pose_v[q] = P.R[q] * g.inv_res;
         Rf[q] = static_cast<float>(P.R[q]);
-        rsum += fabsf(Rs[q]);
       }
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double tvv = (P.t[a] - g.origin[a]) * g.inv_res;
-        if (lane == 0) ws.pose_v[9 + a] = tvv;
-        ts[a] = static_cast<float>(tvv);
-        tmax = fmaxf(tmax, fabsf(ts[a]));
-      }
+      for (int a = 0; a < 3; ++a)
+        if (lane == 9 + a) ws.pose_v[9 + a] = (P.t[a] - g.origin[a]) * g.inv_res;
     }
-    // Rigorous bound on |x32 - x64| with 2x slack (K1). Beyond
-    // 1e6 voxels (or NaN) every point resolves exactly in fp64.
-    const float l1v = static_cast<float>(scan.mu_l1_max * g.inv_res);
-    const float E = 2.0f * 5.9604645e-8f * (7.0f * l1v + 4.0f * tmax) + 1e-6f;
-    const bool finite_pose = (tmax + rsum + l1v) < 1.0e6f;  // false for NaN too
+    __syncwarp();
     Acc acc;
 #pragma unroll
     for (int q = 0; q < 6; ++q) acc.hbr[q] = acc.htl[q] = acc.b[q] = 0.f;
@@ -266,90 +240,71 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
     for (int q = 0; q < 9; ++q) acc.htr[q] = 0.f;
     acc.cost = 0.f;
     int nmatch = 0;
-    __syncwarp();
 
     for (int base = 0; base < S; base += kStep) {
-      // ---- phase A (branch free): fp32 cell guess, predicated async gather.
-      // Queue word qa = k | iz << 16 with iz = 0xFFFF "resolve exactly",
-      // 0xFFFE "drop"; padded points (k >= S) carry NaN coordinates and drop.
-      uint32_t pa[kFastUnroll], pb[kFastUnroll];
+      // ---- phase A: fp64 cell + exact fraction, predicated async gather
+      double Rv[9], tv[3];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) Rv[q] = ws.pose_v[q];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) tv[a] = ws.pose_v[9 + a];
 #pragma unroll
       for (int u = 0; u < kFastUnroll; ++u) {
-        const int k = base + u * 32 + lane;
-        const float4 s0 = s_r0[k];
+        const int slot = u * 32 + lane, k = base + slot;
+        const double m0 = s_mu[3 * k], m1 = s_mu[3 * k + 1], m2 = s_mu[3 * k + 2];
+        float fr[3];
         int ic[3];
-        bool amb = !finite_pose;
+        bool amb = false, inb = true;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
-          const float xv = fmaf(Rs[ax * 3 + 2], s0.z, fmaf(Rs[ax * 3 + 1], s0.y, fmaf(Rs[ax * 3 + 0], s0.x, ts[ax])));
-          const float y = __fadd_rd(xv, 12582912.0f);  // floor via 1.5*2^23 (|x| < 2^21 when finite_pose)
-          const float fr = xv - (y - 12582912.0f);
-          ic[ax] = __float_as_int(y) - 0x4B400000;
-          amb = amb || fabsf(fr - 0.5f) > 0.5f - E;
+          const double x = fma(Rv[ax * 3 + 2], m2, fma(Rv[ax * 3 + 1], m1, fma(Rv[ax * 3 + 0], m0, tv[ax])));
+          const double y = __dadd_rd(x, kMagic);
+          const double f = x - (y - kMagic);
+          ic[ax] = __double2loint(y);
+          // |x| < 2^40 and f at least 1e-9 from a face (NaN fails both)
+          amb = amb || !(fabs(x) < 1.0995e12) || !(fabs(f - 0.5) < 0.5 - 1e-9);
+          inb = inb && static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz));
+          fr[ax] = __double2float_rn(f);
         }
-        amb = amb && k < S;
-        const bool stage = !amb && static_cast<unsigned>(ic[0]) < dx && static_cast<unsigned>(ic[1]) < dy &&
-                           static_cast<unsigned>(ic[2]) < dz;
-        const uint32_t izf = amb ? kResolve : (stage ? static_cast<uint32_t>(ic[2]) : kDrop);
-        pa[u] = static_cast<uint32_t>(k) | (izf << 16);
-        pb[u] = static_cast<uint32_t>(ic[0] & 0xFFFF) | (static_cast<uint32_t>(ic[1]) << 16);
+        const bool real = k < S;
+        const bool resolve = amb && real;
+        const bool stage = !amb && inb;  // padded points are NaN: never staged
         const uint32_t cell = stage ? (static_cast<uint32_t>(ic[2]) * ny + ic[1]) * nx + ic[0] : 0u;
         const float4* src = map.rec + 2 * static_cast<uint64_t>(cell);
-        cp_async16_pred(&ws.m0[u * 32 + lane], src, stage);
-        cp_async16_pred(&ws.m1[u * 32 + lane], src + 1, stage);
+        cp_async16_pred(&ws.m0[slot], src, stage);
+        cp_async16_pred(&ws.m1[slot], src + 1, stage);
+        const uint32_t meta = static_cast<uint32_t>(k) | (stage ? kMetaStage : 0u) | (resolve ? kMetaResolve : 0u);
+        ws.fq[slot] = make_float4(fr[0], fr[1], fr[2], __uint_as_float(meta));
       }
       cp_async_wait_all();
       __syncwarp();
-      // In-place compaction of the candidates and their records (a kept
-      // item moves to a position <= its own slot, rows are read before any
-      // write of the same row): phase B then reads consecutive entries.
+      // ---- compaction of the candidate slots (records stay in place)
       int n_cand = 0;
 #pragma unroll
       for (int u = 0; u < kFastUnroll; ++u) {
-        const float4 r0 = ws.m0[u * 32 + lane], r1 = ws.m1[u * 32 + lane];
-        const uint32_t izf = pa[u] >> 16;
-        const bool keep = izf == kResolve || (izf != kDrop && r0.w >= 0.f);
+        const int slot = u * 32 + lane;
+        const uint32_t meta = __float_as_uint(ws.fq[slot].w);
+        const bool keep = (meta & kMetaResolve) || ((meta & kMetaStage) && ws.m0[slot].w >= 0.f);
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
-        if (keep) {
-          const int pos = n_cand + __popc(mask & ((1u << lane) - 1u));
-          ws.qa[pos] = pa[u];
-          ws.qb[pos] = pb[u];
-          ws.m0[pos] = r0;
-          ws.m1[pos] = r1;
-        }
+        if (keep) ws.q[n_cand + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(slot);
         n_cand += __popc(mask);
       }
       __syncwarp();
-      // ---- phase B: exact residual + structured algebra on full warps
+      // ---- phase B: structured algebra on full warps
       for (int b0 = 0; b0 < n_cand; b0 += 32) {
         const int e = b0 + lane;
         bool valid = false;
         if (e < n_cand) {
-          const uint32_t a = ws.qa[e], bq = ws.qb[e];
-          const int k = static_cast<int>(a & 0xFFFFu);
-          const int iz = static_cast<int>(a >> 16), ix = static_cast<int>(bq & 0xFFFFu),
-                    iy = static_cast<int>(bq >> 16);
-          const double mu[3] = {s_mu[3 * k], s_mu[3 * k + 1], s_mu[3 * k + 2]};
-          // yv = 1 + fractional voxel coordinate, expected in [1, 2).
-          double yv[3];
-          valid = true;
-          bool resolve = iz == static_cast<int>(kResolve);
-          if (!resolve) {
-            // Cell proven by the fp32 bound; residual from an FMA transform
-            // (|error| ~1e-13 voxel, far below the fp32 record precision).
-            const int ic3[3] = {ix, iy, iz};
-#pragma unroll
-            for (int ax = 0; ax < 3; ++ax) {
-              const double* pv = ws.pose_v;
-              const double xr =
-                  fma(pv[ax * 3 + 2], mu[2], fma(pv[ax * 3 + 1], mu[1], fma(pv[ax * 3 + 0], mu[0], pv[9 + ax])));
-              yv[ax] = xr + int_to_double(1 - ic3[ax]);
-              resolve = resolve || (__double2hiint(yv[ax]) >> 20) != 0x3FF;  // safety net
-            }
-          }
+          const int slot = ws.q[e];
+          const float4 fq = ws.fq[slot];
+          const uint32_t meta = __float_as_uint(fq.w);
+          const int k = static_cast<int>(meta & 0xFFFFu);
+          float fr[3] = {fq.x, fq.y, fq.z};
           float4 m0, m1;
-          if (resolve) {  // exact transform, floor and bounds (nnf.hpp:24-35), direct gather
+          valid = true;
+          if (meta & kMetaResolve) {  // exact transform, floor and bounds (nnf.hpp:24-35), direct gather
             const Pose P = poses[i];
+            const double mu[3] = {scan.mu[3 * k], scan.mu[3 * k + 1], scan.mu[3 * k + 2]};
             double p[3];
             transform_x(P.R, P.t, mu, p);
             int c3[3];
@@ -359,20 +314,17 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
               const double fl = floor(x);
               valid = valid && (fl >= 0.0 && fl < static_cast<double>(g.dims[ax]));
               c3[ax] = valid ? static_cast<int>(fl) : 0;
-              yv[ax] = 1.0 + xsub(x, fl);
+              fr[ax] = __double2float_rn(xsub(x, fl));
             }
             const int64_t c = (static_cast<int64_t>(c3[2]) * ny + c3[1]) * nx + c3[0];
             m0 = valid ? __ldg(map.rec + 2 * c) : make_float4(0.f, 0.f, 0.f, -1.f);
             m1 = valid ? __ldg(map.rec + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
           } else {
-            m0 = ws.m0[e];
-            m1 = ws.m1[e];
+            m0 = ws.m0[slot];
+            m1 = ws.m1[slot];
           }
           valid = valid && m0.w >= 0.f;
-          if (valid) {
-            const float fr[3] = {one_plus_to_frac(yv[0]), one_plus_to_frac(yv[1]), one_plus_to_frac(yv[2])};
-            fast_item<GN>(acc, Rf, fr, res, m0, m1, s_r0[k], s_r1[k]);
-          }
+          if (valid) fast_item<GN>(acc, Rf, fr, res, m0, m1, s_r0[k], s_r1[k]);
         }
         nmatch += __popc(__ballot_sync(0xffffffffu, valid));
       }
@@ -416,41 +368,67 @@ __global__ void __launch_bounds__(kFastWarps * 32, 1)
   }
 }
 
-template <int U>
+template <int U, int W>
 size_t fast_smem(int S) {
   const size_t Sp = static_cast<size_t>((S + 32 * U - 1) / (32 * U) * (32 * U));
-  return sizeof(WarpStage<32 * U>) * kFastWarps + sizeof(float4) * 2 * Sp + sizeof(double) * 3 * Sp;
+  return sizeof(WarpStage<32 * U>) * W + sizeof(float4) * 2 * Sp + sizeof(double) * 3 * Sp;
 }
 
-template <bool GN, int U>
+template <bool GN, int U, int W>
 void launch_fast_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys, int32_t* nm,
                    cudaStream_t st) {
-  const size_t smem = fast_smem<U>(scan.n);
+  const size_t smem = fast_smem<U, W>(scan.n);
   int dev, n_sm, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(k_gicp_fast<GN, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gicp_fast<GN, U>, kFastWarps * 32, smem);
-  const int64_t want = (n + kFastWarps - 1) / kFastWarps;
+  cudaFuncSetAttribute(k_gicp_fast<GN, U, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gicp_fast<GN, U, W>, W * 32, smem);
+  const int64_t want = (n + W - 1) / W;
   const unsigned grid =
       static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(n_sm) * std::max(per_sm, 1)));
-  k_gicp_fast<GN, U><<<grid, kFastWarps * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+  k_gicp_fast<GN, U, W><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sys, nm);
 }
 
 }  // namespace
 
-// U = 8 points per lane in flight when the per-SM shared memory allows it
-// (S <= ~640 with 16 warps), else 4.
+// U points per lane in flight x W warps per SM (one CTA per SM).
+// SMCL_FAST_CFG=UxW overrides the default (tuning sweeps only).
 void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys,
                       int32_t* nm, cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
-  const bool big = fast_smem<8>(scan.n) <= 200 * 1024;
-  if (gn)
-    big ? launch_fast_t<true, 8>(poses, n, scan, map, sys, nm, st) : launch_fast_t<true, 4>(poses, n, scan, map, sys, nm, st);
-  else
-    big ? launch_fast_t<false, 8>(poses, n, scan, map, sys, nm, st)
-        : launch_fast_t<false, 4>(poses, n, scan, map, sys, nm, st);
+  static const int cfg = [] {
+    const char* e = std::getenv("SMCL_FAST_CFG");
+    if (!e) return 0;
+    int u = 0, w = 0;
+    return std::sscanf(e, "%dx%d", &u, &w) == 2 ? u * 100 + w : 0;
+  }();
+  // Measured on B200 at 1M x 512 (profiles/README.md): the GN pass is
+  // register bound (128 regs, 16 warps); the likelihood-only pass needs 80
+  // registers and gains from 24 warps of latency hiding.
+  int c = cfg;
+  if (c == 0) c = gn ? 416 : 424;
+#define FAST_CASE(U, W)                                                                    \
+  case U * 100 + W:                                                                        \
+    if (fast_smem<U, W>(scan.n) <= 227 * 1024) {                                           \
+      gn ? launch_fast_t<true, U, W>(poses, n, scan, map, sys, nm, st)                     \
+         : launch_fast_t<false, U, W>(poses, n, scan, map, sys, nm, st);                   \
+      return;                                                                              \
+    }                                                                                      \
+    break;
+  switch (c) {
+    FAST_CASE(8, 14)
+    FAST_CASE(4, 16)
+    FAST_CASE(4, 20)
+    FAST_CASE(4, 24)
+    FAST_CASE(4, 32)
+    FAST_CASE(2, 32)
+    default:
+      break;
+  }
+#undef FAST_CASE
+  gn ? launch_fast_t<true, 4, 16>(poses, n, scan, map, sys, nm, st)
+     : launch_fast_t<false, 4, 16>(poses, n, scan, map, sys, nm, st);
 }
 
 }  // namespace smcl
