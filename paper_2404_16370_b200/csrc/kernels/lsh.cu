@@ -141,25 +141,6 @@ __global__ void k_seg_stats(const int32_t* __restrict__ seg_start, int32_t n_seg
 // from s/r, c/r and the tiny th - theta. q agrees with the reference's to
 // ~1e-14 relative; the float is returned only if exp(-q)*(1 -+ 4e-12) round
 // to the same float, otherwise *ok = false and kval_of takes the reference-order log.
-// Reciprocal / reciprocal square root: MUFU seed (~2^-22) + two Newton
-// steps (~1 ulp), no IEEE slow path. Arguments are positive normal numbers.
-__device__ __forceinline__ double rcp_nr(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
-  return y * fma(-hx * y, y, 1.5);
-}
-
 __device__ __forceinline__ float kval_fast(const Pose& a, const Pose& b, double sr, double st, bool* ok) {
   double m[9];
 #pragma unroll

@@ -58,6 +58,76 @@ __global__ void k_init_uniform(Pose* __restrict__ poses, double* __restrict__ lo
   }
 }
 
+// d = log(a^-1 b) (se3.hpp:103-149) for the SVGD sums, without libm sin
+// calls and with FMA contraction (svgd results are compared within 1e-12
+// relative, not bitwise). With Rrel = Ra^T Rb, vee = (Rrel - Rrel^T)^vee,
+// s = |vee|/2, c = (tr Rrel - 1)/2, r = hypot(s, c), theta = atan2(s, c):
+//   sin theta = s / r exactly, so the reference's w = theta / (2 sin theta) vee
+//   is theta r / (2 s) vee; |w| = th = theta r, and sin/cos of th follow from
+//   those of theta and the tiny th - theta (second order). V^-1 u =
+//   u - w x u / 2 + coef w x (w x u) with coef = (1 - (th/2) cot(th/2)) / th^2
+//   (the reference's (1 - (a/2)/b) / th^2). Near pi the reference branch is used.
+__device__ __forceinline__ void se3_log_rel_fast(const Pose& a, const Pose& b, double d[6]) {
+  double m[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      m[i * 3 + j] = fma(a.R[0 * 3 + i], b.R[0 * 3 + j], fma(a.R[1 * 3 + i], b.R[1 * 3 + j], a.R[2 * 3 + i] * b.R[2 * 3 + j]));
+  const double v0 = m[7] - m[5], v1 = m[2] - m[6], v2 = m[3] - m[1];
+  const double vv = fma(v0, v0, fma(v1, v1, v2 * v2));
+  const double c = fmin(1.0, fmax(-1.0, 0.5 * ((m[0] + m[4]) + m[8] - 1.0)));
+  double s = 0.0, ivs = 0.0;
+  if (vv > 0.0) {
+    ivs = rsqrt_nr(vv);
+    s = 0.5 * (vv * ivs);
+  }
+  const double theta = atan2(s, c);
+  if (theta > kPi - 1e-6) {  // reference pi branch
+    se3_log(inv_compose_x(a, b), d);
+    return;
+  }
+  double w0, w1, w2, th;
+  if (theta < 1e-8) {
+    w0 = 0.5 * v0;
+    w1 = 0.5 * v1;
+    w2 = 0.5 * v2;
+    th = sqrt(fma(w0, w0, fma(w1, w1, w2 * w2)));
+  } else {
+    const double r2 = fma(s, s, c * c);
+    const double inv_r = rsqrt_nr(r2);
+    const double r = r2 * inv_r;
+    const double f = theta * r * ivs;  // theta r / (2 s) = theta r / |vee|
+    w0 = f * v0;
+    w1 = f * v1;
+    w2 = f * v2;
+    th = theta * r;
+  }
+  const double th2 = th * th;
+  double coef;
+  if (th2 < 1e-8) {
+    coef = 1.0 / 12.0 + th2 / 720.0;
+  } else {
+    const double S = s / sqrt(fma(s, s, c * c)), C = c / sqrt(fma(s, s, c * c)), dl = th - theta;
+    const double sin_th = fma(dl, C, S) - 0.5 * dl * dl * S;
+    const double cos_th = fma(-dl, S, C) - 0.5 * dl * dl * C;
+    // (th/2) cot(th/2) = (th/2) (1 + cos th) / sin th
+    coef = (1.0 - 0.5 * th * (1.0 + cos_th) * rcp_nr(sin_th)) * rcp_nr(th2);
+  }
+  const double e0 = b.t[0] - a.t[0], e1 = b.t[1] - a.t[1], e2 = b.t[2] - a.t[2];
+  double u[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) u[i] = fma(a.R[0 * 3 + i], e0, fma(a.R[1 * 3 + i], e1, a.R[2 * 3 + i] * e2));
+  const double x0 = w1 * u[2] - w2 * u[1], x1 = w2 * u[0] - w0 * u[2], x2 = w0 * u[1] - w1 * u[0];  // w x u
+  const double y0 = w1 * x2 - w2 * x1, y1 = w2 * x0 - w0 * x2, y2 = w0 * x1 - w1 * x0;              // w x (w x u)
+  d[0] = w0;
+  d[1] = w1;
+  d[2] = w2;
+  d[3] = fma(coef, y0, fma(-0.5, x0, u[0]));
+  d[4] = fma(coef, y1, fma(-0.5, x1, u[1]));
+  d[5] = fma(coef, y2, fma(-0.5, x2, u[2]));
+}
+
 // svgd.cpp:7-34 compute_phi, optionally fused with apply_updates (svgd.cpp:51-62)
 // writing a second pose buffer so every read sees the frozen snapshot.
 template <bool APPLY>
@@ -77,24 +147,26 @@ __global__ void __launch_bounds__(128) k_svgd(const Pose* __restrict__ all_poses
     const double* sj = all_steps + 6 * static_cast<int64_t>(j);
     if (j == gi) {
 #pragma unroll
-      for (int c = 0; c < 6; ++c) numer[c] = xadd(numer[c], sj[c]);
-      denom = xadd(denom, 1.0);
+      for (int c = 0; c < 6; ++c) numer[c] = numer[c] + sj[c];
+      denom = denom + 1.0;
       continue;
     }
     const Pose pj = all_poses[j];
     if (kernel_underflows(pi, pj, sp.sigma_t)) continue;
     double d[6];
-    se3_log(inv_compose_x(pi, pj), d);
-    const double kv = exp(-kernel_q(d, sp.sigma_r, sp.sigma_t));
-    const double gr = xmul(xmul(-2.0, kv), sp.sigma_r), gt = xmul(xmul(-2.0, kv), sp.sigma_t);
+    se3_log_rel_fast(pi, pj, d);
+    const double q = fma(sp.sigma_r, fma(d[0], d[0], fma(d[1], d[1], d[2] * d[2])),
+                         sp.sigma_t * fma(d[3], d[3], fma(d[4], d[4], d[5] * d[5])));
+    const double kv = exp(-q);
+    const double gr = -2.0 * kv * sp.sigma_r * sp.repulsion_gain, gt = -2.0 * kv * sp.sigma_t * sp.repulsion_gain;
 #pragma unroll
-    for (int c = 0; c < 6; ++c)
-      numer[c] = xadd(numer[c], xadd(xmul(kv, sj[c]), xmul(sp.repulsion_gain, xmul(c < 3 ? gr : gt, d[c]))));
-    denom = xadd(denom, kv);
+    for (int c = 0; c < 6; ++c) numer[c] = fma(kv, sj[c], fma(c < 3 ? gr : gt, d[c], numer[c]));
+    denom = denom + kv;
   }
   double phi[6];
+  const double inv = 1.0 / denom;
 #pragma unroll
-  for (int c = 0; c < 6; ++c) phi[c] = numer[c] / denom;
+  for (int c = 0; c < 6; ++c) phi[c] = numer[c] * inv;
   if (phi_out) {
 #pragma unroll
     for (int c = 0; c < 6; ++c) phi_out[6 * i + c] = phi[c];

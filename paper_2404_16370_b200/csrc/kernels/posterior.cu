@@ -196,6 +196,44 @@ __global__ void k_smooth_round(const double* __restrict__ p_all, double* __restr
   q[i] = num / den;
 }
 
+// K = 20 (the default list size): the particle's idx / kval rows (80 B
+// each, 16-byte aligned) are read with five 128-bit loads each and all 20 p
+// gathers are issued before the (reference-order) sums.
+template <int K>
+__global__ void __launch_bounds__(128) k_smooth_round_k(const double* __restrict__ p_all, double* __restrict__ q,
+                                                        int64_t n, const int32_t* __restrict__ idx,
+                                                        const float* __restrict__ kval,
+                                                        const int32_t* __restrict__ count) {
+  static_assert(K % 4 == 0, "rows must be whole 16-byte vectors");
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cnt = count[i];
+  int32_t j[K];
+  float w[K];
+  const int4* ir = reinterpret_cast<const int4*>(idx + i * K);
+  const float4* kr = reinterpret_cast<const float4*>(kval + i * K);
+#pragma unroll
+  for (int v = 0; v < K / 4; ++v) {
+    const int4 a = ir[v];
+    const float4 b = kr[v];
+    j[4 * v] = a.x, j[4 * v + 1] = a.y, j[4 * v + 2] = a.z, j[4 * v + 3] = a.w;
+    w[4 * v] = b.x, w[4 * v + 1] = b.y, w[4 * v + 2] = b.z, w[4 * v + 3] = b.w;
+  }
+  double pv[K];
+#pragma unroll
+  for (int s = 0; s < K; ++s) pv[s] = s < cnt ? p_all[j[s]] : 0.0;
+  double num = 0.0, den = 0.0;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    if (s < cnt) {
+      const double ws = static_cast<double>(w[s]);
+      num = xadd(num, xmul(ws, pv[s]));
+      den = xadd(den, ws);
+    }
+  }
+  q[i] = num / den;
+}
+
 }  // namespace
 
 void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta, cudaStream_t st) {
@@ -270,7 +308,11 @@ void launch_log(const double* p, double* lp, int64_t n, cudaStream_t st) {
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
                          const int32_t* count, int k, cudaStream_t st) {
   count_launch();
-  if (n > 0) k_smooth_round<<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count, k);
+  if (n <= 0) return;
+  if (k == 20)
+    k_smooth_round_k<20><<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count);
+  else
+    k_smooth_round<<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count, k);
 }
 
 }  // namespace smcl

@@ -37,6 +37,27 @@ SMCL_HD double xsub(double a, double b) { return a - b; }
 
 constexpr double kPi = 3.14159265358979323846;
 
+#ifdef __CUDACC__
+// Reciprocal / reciprocal square root: MUFU seed (~2^-22) + Newton steps
+// (~1 ulp), no IEEE slow path. Arguments are positive normal numbers.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y * fma(-hx * y, y, 1.5);
+}
+#endif
+
 // Pose: R row-major, t. 96 bytes, 16-byte aligned (6 x 128-bit loads).
 struct SMCL_ALIGN16 Pose {
   double R[9];
