@@ -368,6 +368,137 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   }
 }
 
+// K2 with one lane per particle (likelihood only). The likelihood algebra is
+// short (~45 instructions), so running it on every lane for every point that
+// matches on ANY lane costs less than compaction and queue traffic; the scan
+// point is warp-uniform (broadcast shared-memory reads), each lane gathers its
+// own particle's cell record (U points per lane in flight through cp.async).
+// Costs are accumulated in fp64 per lane (~S terms, no warp reduction).
+template <int U, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __restrict__ poses, int64_t n,
+                                                             ScanView scan, MapFast map, double* __restrict__ sys,
+                                                             int32_t* __restrict__ nm_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4* stage = reinterpret_cast<float4*>(smem_raw);  // [kWarps][U][2][32]
+  const int S = scan.n;
+  float4* s_r0 = stage + kWarps * U * 2 * 32;  // S: mu.xyz, gamma
+  float4* s_r1 = s_r0 + S;                     // S: u.xyz, s
+  double* s_mu = reinterpret_cast<double*>(s_r1 + S);
+  for (int q = threadIdx.x; q < S; q += blockDim.x) {
+    s_r0[q] = scan.rec[2 * q];
+    s_r1[q] = scan.rec[2 * q + 1];
+  }
+  for (int q = threadIdx.x; q < 3 * S; q += blockDim.x) s_mu[q] = scan.mu[q];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * (kWarps * 32) + threadIdx.x;
+  const bool active = i < n;
+  float4* ws = stage + wid * U * 2 * 32;
+  const NnfGeom g = map.g;
+  const float res = static_cast<float>(g.res);
+  const int nx = g.dims[0], ny = g.dims[1];
+  const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
+                 dz = static_cast<unsigned>(g.dims[2]);
+  constexpr double kMagic = 6755399441055744.0;
+  double Rv[9], tv[3];
+  float Rf[9];
+  {
+    const Pose P = poses[active ? i : 0];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      Rv[q] = P.R[q] * g.inv_res;
+      Rf[q] = static_cast<float>(P.R[q]);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) tv[a] = (P.t[a] - g.origin[a]) * g.inv_res;
+  }
+  double cost = 0.0;
+  int nmatch = 0;
+  for (int base = 0; base < S; base += U) {
+    float fr[U][3];
+    uint32_t st[U];  // bit 0 staged, bit 1 resolve
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = base + u;
+      const bool real = k < S && active;
+      const double m0 = s_mu[3 * (k < S ? k : 0)], m1 = s_mu[3 * (k < S ? k : 0) + 1],
+                   m2 = s_mu[3 * (k < S ? k : 0) + 2];
+      int ic[3];
+      bool amb = false, inb = true;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        const double x = fma(Rv[ax * 3 + 2], m2, fma(Rv[ax * 3 + 1], m1, fma(Rv[ax * 3 + 0], m0, tv[ax])));
+        const double y = __dadd_rd(x, kMagic);
+        const double f = x - (y - kMagic);
+        ic[ax] = __double2loint(y);
+        amb = amb || !(fabs(x) < 1.0995e12) || !(fabs(f - 0.5) < 0.5 - 1e-9);
+        inb = inb && static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz));
+        fr[u][ax] = __double2float_rn(f);
+      }
+      const bool stg = real && !amb && inb;
+      st[u] = (stg ? 1u : 0u) | (real && amb ? 2u : 0u);
+      const uint32_t cell = stg ? (static_cast<uint32_t>(ic[2]) * ny + ic[1]) * nx + ic[0] : 0u;
+      const float4* src = map.rec + 2 * static_cast<uint64_t>(cell);
+      cp_async16_pred(&ws[(u * 2) * 32 + lane], src, stg);
+      cp_async16_pred(&ws[(u * 2 + 1) * 32 + lane], src + 1, stg);
+    }
+    cp_async_wait_all();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = base + u;
+      float4 m0 = ws[(u * 2) * 32 + lane], m1 = ws[(u * 2 + 1) * 32 + lane];
+      bool valid = (st[u] & 1u) != 0;
+      if (st[u] & 2u) {  // reference-order transform, floor and bounds (nnf.hpp:24-35)
+        const Pose P = poses[i];
+        const double mu[3] = {s_mu[3 * k], s_mu[3 * k + 1], s_mu[3 * k + 2]};
+        double p[3];
+        transform_x(P.R, P.t, mu, p);
+        int c3[3];
+        valid = true;
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          const double x = xmul(xsub(p[ax], g.origin[ax]), g.inv_res);
+          const double fl = floor(x);
+          valid = valid && (fl >= 0.0 && fl < static_cast<double>(g.dims[ax]));
+          c3[ax] = valid ? static_cast<int>(fl) : 0;
+          fr[u][ax] = __double2float_rn(xsub(x, fl));
+        }
+        const int64_t c = (static_cast<int64_t>(c3[2]) * ny + c3[1]) * nx + c3[0];
+        m0 = valid ? __ldg(map.rec + 2 * c) : make_float4(0.f, 0.f, 0.f, -1.f);
+        m1 = valid ? __ldg(map.rec + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      valid = valid && m0.w >= 0.f;
+      if (valid) {
+        Acc a;
+        a.cost = 0.f;
+        fast_item<false>(a, Rf, fr[u], res, m0, m1, s_r0[k], s_r1[k]);
+        cost += static_cast<double>(a.cost);
+        ++nmatch;
+      }
+    }
+    __syncwarp();
+  }
+  if (active) {
+    sys[i * kSysStride + 42] = nmatch == 0 ? -1e30 : -cost;
+    nm_out[i] = nmatch;
+  }
+}
+
+template <int U, int W>
+size_t ll_lanes_smem(int S) {
+  return sizeof(float4) * (static_cast<size_t>(W) * U * 2 * 32 + 2 * static_cast<size_t>(S)) +
+         sizeof(double) * 3 * static_cast<size_t>(S);
+}
+
+template <int U, int W>
+void launch_ll_lanes_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys, int32_t* nm,
+                       cudaStream_t st) {
+  const size_t smem = ll_lanes_smem<U, W>(scan.n);
+  cudaFuncSetAttribute(k_gicp_ll_lanes<U, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  const unsigned grid = static_cast<unsigned>((n + W * 32 - 1) / (W * 32));
+  k_gicp_ll_lanes<U, W><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+}
+
 template <int U, int W>
 size_t fast_smem(int S) {
   const size_t Sp = static_cast<size_t>((S + 32 * U - 1) / (32 * U) * (32 * U));
@@ -401,13 +532,31 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
     const char* e = std::getenv("SMCL_FAST_CFG");
     if (!e) return 0;
     int u = 0, w = 0;
+    if (std::sscanf(e, "L%dx%d", &u, &w) == 2) return 9000 + u * 100 + w;  // lane-per-particle likelihood
     return std::sscanf(e, "%dx%d", &u, &w) == 2 ? u * 100 + w : 0;
   }();
   // Measured on B200 at 1M x 512 (profiles/README.md): the GN pass is
   // register bound (128 regs, 16 warps); the likelihood-only pass needs 80
   // registers and gains from 24 warps of latency hiding.
   int c = cfg;
-  if (c == 0) c = gn ? 416 : 424;
+  if (!gn && c == 0) c = 9000;  // lane-per-particle likelihood pass
+  if (c == 0) c = 416;
+  if (c >= 9000) {  // SMCL_FAST_CFG=9UWW: lane-per-particle variants (9000 = default 8 points x 8 warps)
+    const int u = c == 9000 ? 8 : (c / 100) % 10, w = c == 9000 ? 8 : c % 100;
+    if (!gn && u == 8 && w == 8 && ll_lanes_smem<8, 8>(scan.n) <= 227 * 1024) {
+      launch_ll_lanes_t<8, 8>(poses, n, scan, map, sys, nm, st);
+      return;
+    }
+    if (!gn && u == 4 && w == 8 && ll_lanes_smem<4, 8>(scan.n) <= 227 * 1024) {
+      launch_ll_lanes_t<4, 8>(poses, n, scan, map, sys, nm, st);
+      return;
+    }
+    if (!gn && u == 8 && w == 4 && ll_lanes_smem<8, 4>(scan.n) <= 227 * 1024) {
+      launch_ll_lanes_t<8, 4>(poses, n, scan, map, sys, nm, st);
+      return;
+    }
+    c = gn ? 416 : 424;
+  }
 #define FAST_CASE(U, W)                                                                    \
   case U * 100 + W:                                                                        \
     if (fast_smem<U, W>(scan.n) <= 227 * 1024) {                                           \
