@@ -55,6 +55,40 @@ def box_room(size):
     return out
 
 
+def _box_rects(x0, y0, z0, sx, sy, sz, floor=False):
+    """Axis-aligned box as rectangles (4 walls + roof [+ floor])."""
+    o = np.array([x0, y0, z0])
+    ex, ey, ez = np.array([sx, 0, 0.0]), np.array([0, sy, 0.0]), np.array([0, 0, sz])
+    faces = [(o, ex, ez), (o + ey, ex, ez), (o, ey, ez), (o + ex, ey, ez), (o + ez, ex, ey)]
+    if floor:
+        faces.append((o, ex, ey))
+    return [np.concatenate(f) for f in faces]
+
+
+def outdoor_world(size=(280.0, 200.0, 30.0), block=40.0, street=12.0, seed=7):
+    """Builder-defined outdoor world for the kidnap configs (the
+    reference has no outdoor preset): a ground plane of size[0] x size[1] m
+    and a city grid of blocks (pitch `block`, streets `street` wide) holding
+    one or two box buildings each, heights up to size[2]. Seeded; rects in the
+    reference's (origin, edge_u, edge_v) form so sample_world / ray casting
+    (world.cpp) consume them unchanged."""
+    sx, sy, sz = size
+    rng = np.random.default_rng(seed)
+    rects = [np.concatenate([[0.0, 0.0, 0.0], [sx, 0.0, 0.0], [0.0, sy, 0.0]])]  # ground
+    for bx in np.arange(street, sx - block / 2, block):
+        for by in np.arange(street, sy - block / 2, block):
+            w = block - street
+            n_b = 1 + int(rng.integers(0, 2))
+            for b in range(n_b):
+                fx = rng.uniform(0.4, 0.9) * w / n_b
+                fy = rng.uniform(0.5, 0.95) * w
+                x0 = bx + b * w / n_b + rng.uniform(0.0, w / n_b - fx)
+                y0 = by + rng.uniform(0.0, w - fy)
+                h = rng.uniform(0.25, 1.0) * sz
+                rects += _box_rects(x0, y0, 0.0, fx, fy, h)
+    return np.array(rects)
+
+
 def world_bounds(rects):
     r = np.asarray(rects).reshape(-1, 9)
     o, u, v = r[:, 0:3], r[:, 3:6], r[:, 6:9]
@@ -172,7 +206,7 @@ def yaw_rotation(yaw):
 class Scenario:
     def __init__(self, name, world_kind="corridor", n_frames=150, waypoints=(), occlusions=(), teleports=(),
                  box_size=(10.0, 10.0, 3.0), density=100.0, sensor=None, sensor_height=1.5, rate_hz=10.0, speed=1.0,
-                 odom_sigma_rot=0.002, odom_sigma_trans=0.005, seed=1, corridor=None):
+                 odom_sigma_rot=0.002, odom_sigma_trans=0.005, seed=1, corridor=None, outdoor=None):
         self.name, self.world_kind, self.n_frames = name, world_kind, n_frames
         self.waypoints = [np.array(w, float) for w in waypoints]
         self.occlusions, self.teleports = list(occlusions), list(teleports)
@@ -181,12 +215,15 @@ class Scenario:
         self.sensor_height, self.rate_hz, self.speed = sensor_height, rate_hz, speed
         self.odom_sigma_rot, self.odom_sigma_trans, self.seed = odom_sigma_rot, odom_sigma_trans, seed
         self.corridor = corridor or {}
+        self.outdoor = outdoor or {}
 
     def build_world(self):
         if self.world_kind == "corridor":
             return corridor_world(**self.corridor)
         if self.world_kind == "box":
             return box_room(self.box_size)
+        if self.world_kind == "outdoor":
+            return outdoor_world(**self.outdoor)
         raise RuntimeError(f"unknown world kind: {self.world_kind}")
 
     def odom_cov(self):
@@ -208,6 +245,13 @@ def scenario_preset(name, **kw):
                                    (38.5, 1.5, 0.0)],
                         occlusions=[(80, 180), (260, 360)],
                         teleports=[(130, (15.0, 5.5, 0.0)), (310, (35.0, 5.5, 0.0))], **kw)
+    if name == "outdoor_kidnap":
+        # configs[3]: drive along a street, scan blackout, teleport to another
+        # street, recover (the corridor_kidnap pattern of scenario.cpp:47-58 on
+        # the builder-defined outdoor world; 10 pts/m^2, 5 m/s).
+        return Scenario(name, world_kind="outdoor", n_frames=90, density=10.0, speed=5.0, sensor_height=2.0,
+                        waypoints=[(6.0, 6.0, 0.0), (120.0, 6.0, 0.0), (126.0, 126.0, 0.0), (250.0, 126.0, 0.0)],
+                        occlusions=[(30, 50)], teleports=[(40, (126.0, 126.0, 0.0))], **kw)
     if name == "box_easy":
         return Scenario(name, world_kind="box", n_frames=60,
                         waypoints=[(3.0, 3.0, 0.0), (7.0, 3.0, 0.0), (7.0, 7.0, 0.0)], **kw)

@@ -5,6 +5,10 @@
   along the corridor_easy trajectory.
 * ``tracking``     — configs[1]: box_easy room with the corridor.cfg desk
   calibration, 65,536 particles, 512-point scans.
+* ``kidnap``       — configs[3]: builder-defined outdoor world (280 x 200 x
+  30 m city grid, 10 pts/m^2, NNF 0.2 m / 2.0 m max query = 2.2e8 cells), a
+  street drive with a 20-frame scan blackout and a teleport (empty scans
+  exercise the kidnap branch of filter.cpp:174-187).
 
 Scans: 2,048 rays (256 azimuths x 8 elevations in [-30, 30] deg, 30 m range,
 1 cm range noise), voxel-downsampled at the reference's 5 cm leaf, then
@@ -25,6 +29,8 @@ def bench_sensor():
 
 
 def scan_of_points(pts, n_points, cfg):
+    if len(pts) < max(cfg.covariance_k + 1, 5):  # occluded frame: empty scan (filter.cpp:87-89)
+        return GaussianCloud(np.zeros((0, 3)), np.zeros((0, 9)))
     d = downsample_to(pts, 1 << 20, cfg.scan_voxel_leaf)
     if len(d) > n_points:
         d = d[np.linspace(0, len(d) - 1, n_points).astype(np.int64)]
@@ -49,6 +55,10 @@ def build(kind="global_init", n_particles=1 << 20, scan_points=512, n_frames=13,
     if kind == "global_init":
         sc = sim.scenario_preset("corridor_easy", seed=seed)
         cfg = make_config(n_particles=n_particles, seed=seed)
+    elif kind == "kidnap":
+        # configs[3]: outdoor world 280 x 200 x 30 m, NNF 0.2 m, max query 2.0 m
+        sc = sim.scenario_preset("outdoor_kidnap", seed=seed)
+        cfg = make_config(n_particles=n_particles, seed=seed, nnf_resolution=0.2, nnf_max_query_dist=2.0)
     elif kind == "tracking":
         sc = sim.scenario_preset("box_easy", seed=seed)
         cfg = make_config(n_particles=n_particles, seed=seed, **CORRIDOR_CFG)
