@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mode", default="auto", choices=["auto", "exact", "fast"])
     ap.add_argument("--profile-json", default="")
+    ap.add_argument("--no-reorder", action="store_true",
+                    help="reorder_particles = 0 (no cross-shard migration under torchrun)")
     return ap.parse_args()
 
 
@@ -223,7 +225,8 @@ def main():
     if pg:  # particle-index shards of the same N (strong scaling), NCCL all-gathers at the exchange points
         from paper_2404_16370_b200.comm import TorchComm, shard_range
         shard_range(args.particles, rank, world)
-        cfg.reorder_particles = 0
+        if args.no_reorder:  # v1 exchange plan: particles never migrate between shards
+            cfg.reorder_particles = 0
         comm = TorchComm()
     eng = FilterEngine(wl.map, cfg, device=local, comm=comm)
     eng.init_uniform(wl.bounds)
@@ -332,7 +335,8 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
         "config": {"workload": WORKLOAD_TEXT[args.workload].format(n=args.particles, s=S),
                    "n_particles": args.particles, "scan_points": S, "pp_per_step": pp,
-                   "parallelism": f"particle shards x{world} (NCCL all-gather)" if world > 1 else "single",
+                   "parallelism": (f"particle shards x{world} (NCCL all-gather, reorder_particles="
+                                   f"{int(cfg.reorder_particles)})") if world > 1 else "single",
                    "likelihood_path": "fast" if avg["fast_path"] else "exact",
                    "l2": "per-step working set > L2 (particle state ~0.5 GB at 1M), no flush",
                    "engine_setup_s": setup_s},

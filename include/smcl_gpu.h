@@ -146,7 +146,10 @@ typedef struct smcl_comm {
 /* Sharded engine: this rank owns the particles with global indices
  * [rank*N/world, (rank+1)*N/world) (N/world must be a multiple of 4096 so
  * reduction chunks never straddle shards); the map is replicated. Results are
- * bit-identical to a single engine with reorder_particles = 0 (required). */
+ * bit-identical to a single engine with the same config. With
+ * reorder_particles = 1 (the reference default) the LSH reorder migrates
+ * particle state across shards: rank r always holds storage positions
+ * [r*N/world, (r+1)*N/world) of the global sorted order. */
 int smcl_create_sharded(const smcl_cloud* map, const smcl_config* cfg, int device, const smcl_comm* comm,
                         smcl_engine** out);
 /* In-process loopback collectives for `world` engines driven by `world` host

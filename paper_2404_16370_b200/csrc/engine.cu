@@ -268,6 +268,11 @@ struct smcl_engine {
   DBuf<double> g_steps, g_p, g_part, g_part2;
   DBuf<uint64_t> g_keys;
   DBuf<int32_t> g_flag, pos_list;
+  // Sharded reorder: the full old particle state of every
+  // shard, gathered before each rank permutes its new index range.
+  DBuf<double> g_lp;
+  DBuf<int32_t> g_id, g_idx, g_count;
+  DBuf<float> g_kval;
   DBuf<unsigned long long> g_counts;
   DBuf<double> g_argv;
   DBuf<long long> g_argi;
@@ -447,7 +452,6 @@ struct smcl_engine {
     if (sharded) {
       if (n % world != 0 || (n / world) % kReduceChunk != 0)
         throw std::invalid_argument("sharded engine: N/world must be a multiple of 4096");
-      if (cfg.reorder_particles) throw std::invalid_argument("sharded engine requires reorder_particles = 0");
     }
     n_total = n;
     n_local = n / world;
@@ -474,6 +478,13 @@ struct smcl_engine {
       g_argi.ensure(w);
       g_rep.ensure(w);
       g_repid.ensure(w);
+      if (cfg.reorder_particles) {
+        g_lp.ensure(ug);
+        g_id.ensure(ug);
+        g_count.ensure(ug);
+        g_idx.ensure(ug * static_cast<size_t>(kk));
+        g_kval.ensure(ug * static_cast<size_t>(kk));
+      }
     }
     poses.ensure(un);
     poses2.ensure(un);
@@ -813,8 +824,25 @@ struct smcl_engine {
     const int32_t* members = member_of.p;
     if (cfg.reorder_particles) {
       launch_inverse_perm(member_of.p, n, new_of_old.p, st);
-      launch_reorder(member_of.p, new_of_old.p, n, k, poses.p, log_post.p, id.p, idx.p, kval.p, count.p, poses2.p,
-                     log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st);
+      if (sharded) {
+        // Cross-shard permutation (particle_set.cpp:7-47 over the global
+        // order): every rank owns the new positions [gbase, gbase + n_local)
+        // and pulls their old state from whichever shard held it. v1
+        // exchanges by all-gather (each rank receives the whole set, 272 B per
+        // particle at K = 20); an all-to-all would move 1/world of that.
+        const size_t nl = static_cast<size_t>(n_local), kk = static_cast<size_t>(k);
+        allgather(poses.p, g_poses.p, sizeof(Pose) * nl);
+        allgather(log_post.p, g_lp.p, sizeof(double) * nl);
+        allgather(id.p, g_id.p, sizeof(int32_t) * nl);
+        allgather(count.p, g_count.p, sizeof(int32_t) * nl);
+        allgather(idx.p, g_idx.p, sizeof(int32_t) * nl * kk);
+        allgather(kval.p, g_kval.p, sizeof(float) * nl * kk);
+        launch_reorder(member_of.p + gbase, new_of_old.p, n_local, k, g_poses.p, g_lp.p, g_id.p, g_idx.p, g_kval.p,
+                       g_count.p, poses2.p, log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st);
+      } else {
+        launch_reorder(member_of.p, new_of_old.p, n, k, poses.p, log_post.p, id.p, idx.p, kval.p, count.p, poses2.p,
+                       log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st);
+      }
       poses.swap(poses2);
       log_post.swap(log_post2);
       id.swap(id2);
@@ -1252,8 +1280,6 @@ int smcl_create_sharded(const smcl_cloud* map, const smcl_config* cfg, int devic
     e->rank = comm->rank;
     e->world = comm->world;
     e->sharded = comm->world > 1;
-    if (e->sharded && cfg->reorder_particles)
-      throw std::invalid_argument("sharded engine requires reorder_particles = 0");
     *out = e.release();
   });
 }
