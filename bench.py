@@ -194,9 +194,21 @@ def roofline(prof_avg, hbm_peak, peak_kind, ms_kernels):
         name = max(("gicp_gn (K1)", "gicp_ll (K2)"), key=lambda k: kernels[k][0])
         ms, nbytes = kernels[name]
     achieved = nbytes / (ms * 1e-3) / 1e9
+    # DRAM bytes per launch of the same kernel from the committed ncu --set full
+    # capture (profiles/r01_dram_traffic.json); the map records are L2-resident,
+    # so DRAM traffic is a small fraction of the algorithmic gather bytes.
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_dram_traffic.json")) as f:
+            t = json.load(f)["kernels"].get(name)
+        if t:
+            traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+    except Exception:
+        traffic = None
     return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-            "frac": achieved / hbm_peak, "traffic": None, "peak_source": peak_kind,
-            "algorithmic_bytes_per_launch": nbytes, "kernel_ms": ms}
+            "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_kind,
+            "algorithmic_bytes_per_launch": nbytes, "kernel_ms": ms,
+            "traffic_source": "profiles/r01_dram_traffic.json (ncu --set full, bytes per launch)"}
 
 
 def main():
