@@ -20,7 +20,7 @@ HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/host/*.hpp) include/smcl_gp
 CU_OBJ := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRC))
 CPP_OBJ := $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(CPP_SRC))
 
-all: $(LIB) oracle examples/facade_demo
+all: $(LIB) oracle examples/facade_demo build/tools/micro_peaks
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(dir $@)
@@ -48,3 +48,8 @@ clean:
 # C++ facade example (reference-shaped API over the C ABI).
 examples/facade_demo: examples/facade_demo.cpp include/steinmcl_b200.hpp include/smcl_gpu.h $(LIB)
 	$(HOSTCXX) -std=c++20 -O2 -Iinclude -o $@ examples/facade_demo.cpp -L$(PKG)/lib -lsmcl_gpu -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
+
+# Roofline microbenchmarks (FP32/FP64 FMA, random record gathers from L2 / HBM).
+build/tools/micro_peaks: $(CSRC)/tools/micro_peaks.cu
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -O3 -ccbin $(HOSTCXX) -o $@ $<

@@ -180,6 +180,28 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def gather_peaks():
+    """Random 32-byte record gather bandwidth (L2-resident / HBM tables) and
+    FP32/FP64 FMA peaks from build/tools/micro_peaks, measured live on this
+    box when the binary is present, else the committed r01 measurement."""
+    exe = os.path.join(ROOT, "build", "tools", "micro_peaks")
+    if os.path.exists(exe):
+        try:
+            out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout.strip().splitlines()
+            d = json.loads(out[-1])
+            d["source"] = "measured live (build/tools/micro_peaks)"
+            return d
+        except Exception:  # noqa: BLE001
+            pass
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_micro_peaks.json")) as f:
+            d = json.load(f)
+        d["source"] = "profiles/r01_micro_peaks.json"
+        return d
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def roofline(prof_avg, hbm_peak, peak_kind, ms_kernels):
     """Dominant-kernel roofline with BASELINE.md §3 algorithmic bytes."""
     kernels = {
@@ -340,6 +362,17 @@ def main():
     ms_kernels = {"lsh refresh+gather (K6/K7)": avg["refresh_gather_ms"], "svgd (K8)": avg["svgd_ms"],
                   "smooth (K12)": avg["smooth_ms"], "sort (CUB)": avg["sort_ms"]}
     roof = roofline(avg, hbm, kind, ms_kernels)
+    # The same kernel against the achievable random-gather bandwidth of its
+    # record table (L2-resident for the corridor map): the north-star's
+    # "fraction of achievable L2/HBM gather bandwidth".
+    gp = gather_peaks() if rank == 0 else None
+    roof_gather = None
+    if gp:
+        key = "gather_hbm_7GB_gbs" if args.workload == "kidnap" else "gather_l2_resident_49MB_gbs"
+        peak_g = gp.get(key)
+        if peak_g:
+            roof_gather = {"kernel": roof["kernel"], "achieved": roof["achieved"], "peak": peak_g, "unit": "GB/s",
+                           "frac": roof["achieved"] / peak_g, "peak_kind": key, "peaks": gp}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -361,6 +394,7 @@ def main():
         "scan_prep_ms": {"device": dev_prep_ms, "host": host_prep_ms, "raw_points": len(wl.raw[f0])},
         "gpu_launches": int(sum(p["kernel_launches"] for p in profs)),
         "roofline": roof,
+        "roofline_gather": roof_gather,
         "clocks": clk,
         "stage_ms": {k: avg[k] for k in keys},
         "mean_n_matched_last": res["mean_n_matched"],

@@ -1,0 +1,109 @@
+// Microbenchmarks for the roofline denominators MEASURED_PEAKS.json does not
+// carry: FP32 and FP64 FMA throughput, and the random 32-byte
+// record gather bandwidth of the likelihood kernels, from an L2-resident table
+// (the corridor map's 49 MB of NNF records) and from an HBM-sized table (the
+// outdoor map's 7 GB). Prints one JSON object.
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o micro_peaks micro_peaks.cu
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) {                                                    \
+      std::fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e_));             \
+      return 1;                                                                 \
+    }                                                                           \
+  } while (0)
+
+template <typename T, int ILP>
+__global__ void k_fma(T* out, int iters, T a, T b) {
+  T v[ILP];
+#pragma unroll
+  for (int j = 0; j < ILP; ++j) v[j] = static_cast<T>(threadIdx.x + j);
+  for (int i = 0; i < iters; ++i)
+#pragma unroll
+    for (int j = 0; j < ILP; ++j) v[j] = fma(v[j], a, b);
+  T s = 0;
+#pragma unroll
+  for (int j = 0; j < ILP; ++j) s += v[j];
+  if (s == static_cast<T>(-1.2345)) out[0] = s;
+}
+
+// Each thread gathers `per_thread` random 32-byte records (two 16-byte loads,
+// the K1/K2 record layout) from a table of n_rec records.
+__global__ void k_gather(const float4* __restrict__ rec, uint64_t n_rec, int per_thread, uint64_t seed,
+                         float* __restrict__ out) {
+  uint64_t s = seed ^ (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 0x9E3779B97F4A7C15ull;
+  float acc = 0.f;
+  for (int i = 0; i < per_thread; i += 8) {
+    float4 r[16];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s ^= s << 13;
+      s ^= s >> 7;
+      s ^= s << 17;
+      const uint64_t c = s % n_rec;
+      r[2 * u] = __ldg(rec + 2 * c);
+      r[2 * u + 1] = __ldg(rec + 2 * c + 1);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc += r[u].x + r[u].w;
+  }
+  if (acc == -1.2345f) out[0] = acc;
+}
+
+int main() {
+  int dev = 0, n_sm = 0, clk = 0;
+  CK(cudaSetDevice(dev));
+  CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  float* out;
+  CK(cudaMalloc(&out, 16));
+  auto time_ms = [&](auto launch) -> float {
+    launch();
+    cudaEventRecord(e0);
+    for (int r = 0; r < 5; ++r) launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms / 5.f;
+  };
+  const int blocks = n_sm * 8, threads = 256, iters = 4096;
+  const float ms32 = time_ms([&] { k_fma<float, 8><<<blocks, threads>>>(out, iters, 1.0000001f, 1e-7f); });
+  const double f32 = 2.0 * blocks * threads * 8.0 * iters / (ms32 * 1e-3) / 1e12;
+  const float ms64 = time_ms([&] {
+    k_fma<double, 8><<<blocks, threads>>>(reinterpret_cast<double*>(out), iters / 4, 1.0000001, 1e-7);
+  });
+  const double f64 = 2.0 * blocks * threads * 8.0 * (iters / 4) / (ms64 * 1e-3) / 1e12;
+  std::printf("{\"fp32_fma_tflops\": %.2f, \"fp64_fma_tflops\": %.2f", f32, f64);
+  const uint64_t tables[2] = {uint64_t(49) << 20, uint64_t(7) << 30};  // bytes
+  const char* names[2] = {"l2_resident_49MB", "hbm_7GB"};
+  for (int t = 0; t < 2; ++t) {
+    const uint64_t n_rec = tables[t] / 32;
+    float4* rec = nullptr;
+    if (cudaMalloc(&rec, n_rec * 32) != cudaSuccess) {
+      std::printf(", \"gather_%s_gbs\": null", names[t]);
+      cudaGetLastError();
+      continue;
+    }
+    CK(cudaMemset(rec, 0, n_rec * 32));
+    const int gblocks = n_sm * 8, gthreads = 256, per = 256;
+    const float ms = time_ms([&] { k_gather<<<gblocks, gthreads>>>(rec, n_rec, per, 12345ull, out); });
+    const double gbs = 32.0 * gblocks * gthreads * per / (ms * 1e-3) / 1e9;
+    std::printf(", \"gather_%s_gbs\": %.1f", names[t], gbs);
+    CK(cudaFree(rec));
+  }
+  CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev));
+  std::printf(", \"sm_count\": %d, \"note\": \"random 32-byte record gathers (two 16-B __ldg per record, 8 records "
+              "in flight per thread), %d CTAs x 256 threads\"}\n",
+              n_sm, n_sm * 8);
+  return 0;
+}
