@@ -302,6 +302,7 @@ struct smcl_engine {
   // map
   bool has_map = false;
   bool map_structured = false;
+  int map_brick = 0;  // fast-record table layout (MapFast::choose_brick)
   host::Aabb map_bounds{};
   NnfGeom geom{};
   int64_t n_cells = 0;
@@ -437,7 +438,8 @@ struct smcl_engine {
     if (ok) {
       DBuf<float4> d_plane;
       d_plane.upload(plane.data(), plane.size(), st);
-      map_fast.ensure(2 * static_cast<size_t>(n_cells));
+      map_brick = MapFast::choose_brick(g.dims);
+      map_fast.ensure(2 * static_cast<size_t>(MapFast::n_records(g.dims, map_brick)));
       CK(build_map_records_device(cells.p, n_cells, g.origin, g.dims, g.resolution, map_mu.p, d_plane.p, map_fast.p,
                                   st));
       sync();
@@ -747,7 +749,7 @@ struct smcl_engine {
     if (profiling) mark(gn ? E_GN0 : E_LL0);
     fast_used = use_fast(sd);
     if (fast_used) {
-      MapFast mf{geom, map_fast.p};
+      MapFast mf{geom, map_fast.p, map_brick};
       launch_gicp_fast(gn, poses.p, n_local, sv, mf, sys.p, nm.p, st);
     } else {
       MapExact me{geom, cells.p, map_mu.p, map_sigma.p};

@@ -35,9 +35,30 @@ struct MapExact {
 //   rec[2c+0] = (mu - corner(c)).xyz, beta      (beta < 0: empty cell)
 //   rec[2c+1] = u.xyz, s
 // with beta = a - s >= 0 (a: double eigenvalue, s: single eigenvalue, u its axis).
+// Record table layout: x-fastest cells (tables that fit in L2), or 4x4x4-cell
+// bricks (64 records = 2 KB contiguous, bricks x-fastest) for tables larger
+// than L2: scan points that land close together share bricks, so their
+// gathers share L2 lines and DRAM pages (outdoor map: 7 GB table, K1 4.1 ->
+// 2.5 ms; for the L2-resident corridor table the extra index math costs more
+// than it saves).
 struct MapFast {
   NnfGeom g;
   const float4* rec;
+  int brick = 0;
+  // Host-side / map-build slot; the likelihood kernels use rec_index<kBrick>.
+  // 32-bit index math: the NNF budget (2^30 cells) keeps every table < 2^32 records.
+  __host__ __device__ __forceinline__ uint32_t index(uint32_t ix, uint32_t iy, uint32_t iz) const {
+    const uint32_t nx = static_cast<uint32_t>(g.dims[0]), ny = static_cast<uint32_t>(g.dims[1]);
+    if (!brick) return (iz * ny + iy) * nx + ix;
+    const uint32_t b = ((iz >> 2) * ((ny + 3u) >> 2) + (iy >> 2)) * ((nx + 3u) >> 2) + (ix >> 2);
+    return (b << 6) | ((iz & 3u) << 4) | ((iy & 3u) << 2) | (ix & 3u);
+  }
+  static uint64_t n_records(const int dims[3], int brick) {
+    if (!brick) return static_cast<uint64_t>(dims[0]) * dims[1] * dims[2];
+    return static_cast<uint64_t>((dims[0] + 3) >> 2) * ((dims[1] + 3) >> 2) * ((dims[2] + 3) >> 2) * 64u;
+  }
+  // Brick layout when the linear table exceeds 64 MB (half the B200 L2).
+  static int choose_brick(const int dims[3]) { return n_records(dims, 0) * 32u > (uint64_t(64) << 20) ? 1 : 0; }
 };
 
 // Per-frame scan in both precisions. Fast records: (mu.xyz, gamma), (u.xyz, s).

@@ -169,6 +169,15 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// Record slot of cell (ix, iy, iz) for the table layout fixed at compile time.
+template <int kBrick>
+__device__ __forceinline__ uint32_t rec_index(const MapFast& m, uint32_t ix, uint32_t iy, uint32_t iz) {
+  const uint32_t nx = static_cast<uint32_t>(m.g.dims[0]), ny = static_cast<uint32_t>(m.g.dims[1]);
+  if (!kBrick) return (iz * ny + iy) * nx + ix;
+  const uint32_t b = ((iz >> 2) * ((ny + 3u) >> 2) + (iy >> 2)) * ((nx + 3u) >> 2) + (ix >> 2);
+  return (b << 6) | ((iz & 3u) << 4) | ((iy & 3u) << 2) | (ix & 3u);
+}
+
 __device__ __forceinline__ void transform_x(const double* R, const double* t, const double mu[3], double p[3]) {
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -183,7 +192,7 @@ __constant__ int c_sys_off[28] = {0,  6,  7,  12, 13, 14,                 // htl
                                   36, 37, 38, 39, 40, 41,                 // b
                                   42};                                    // ll
 
-template <bool GN, int kFastUnroll, int kWarps>
+template <bool GN, int kFastUnroll, int kWarps, int kBrick>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     k_gicp_fast(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, double* __restrict__ sys,
                 int32_t* __restrict__ nm_out) {
@@ -269,8 +278,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         const bool real = k < S;
         const bool resolve = amb && real;
         const bool stage = !amb && inb;  // padded points are NaN: never staged
-        const uint32_t cell = stage ? (static_cast<uint32_t>(ic[2]) * ny + ic[1]) * nx + ic[0] : 0u;
-        const float4* src = map.rec + 2 * static_cast<uint64_t>(cell);
+        const uint64_t cell = stage ? rec_index<kBrick>(map, ic[0], ic[1], ic[2]) : 0u;
+        const float4* src = map.rec + 2 * cell;
         cp_async16_pred(&ws.m0[slot], src, stage);
         cp_async16_pred(&ws.m1[slot], src + 1, stage);
         const uint32_t meta = static_cast<uint32_t>(k) | (stage ? kMetaStage : 0u) | (resolve ? kMetaResolve : 0u);
@@ -316,7 +325,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
               c3[ax] = valid ? static_cast<int>(fl) : 0;
               fr[ax] = __double2float_rn(xsub(x, fl));
             }
-            const int64_t c = (static_cast<int64_t>(c3[2]) * ny + c3[1]) * nx + c3[0];
+            const uint64_t c = rec_index<kBrick>(map, c3[0], c3[1], c3[2]);
             m0 = valid ? __ldg(map.rec + 2 * c) : make_float4(0.f, 0.f, 0.f, -1.f);
             m1 = valid ? __ldg(map.rec + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
           } else {
@@ -374,7 +383,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 // point is warp-uniform (broadcast shared-memory reads), each lane gathers its
 // own particle's cell record (U points per lane in flight through cp.async).
 // Costs are accumulated in fp64 per lane (~S terms, no warp reduction).
-template <int U, int kWarps>
+template <int U, int kWarps, int kBrick>
 __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __restrict__ poses, int64_t n,
                                                              ScanView scan, MapFast map, double* __restrict__ sys,
                                                              int32_t* __restrict__ nm_out) {
@@ -437,8 +446,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
       }
       const bool stg = real && !amb && inb;
       st[u] = (stg ? 1u : 0u) | (real && amb ? 2u : 0u);
-      const uint32_t cell = stg ? (static_cast<uint32_t>(ic[2]) * ny + ic[1]) * nx + ic[0] : 0u;
-      const float4* src = map.rec + 2 * static_cast<uint64_t>(cell);
+      const uint64_t cell = stg ? rec_index<kBrick>(map, ic[0], ic[1], ic[2]) : 0u;
+      const float4* src = map.rec + 2 * cell;
       cp_async16_pred(&ws[(u * 2) * 32 + lane], src, stg);
       cp_async16_pred(&ws[(u * 2 + 1) * 32 + lane], src + 1, stg);
     }
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
           c3[ax] = valid ? static_cast<int>(fl) : 0;
           fr[u][ax] = __double2float_rn(xsub(x, fl));
         }
-        const int64_t c = (static_cast<int64_t>(c3[2]) * ny + c3[1]) * nx + c3[0];
+        const uint64_t c = rec_index<kBrick>(map, c3[0], c3[1], c3[2]);
         m0 = valid ? __ldg(map.rec + 2 * c) : make_float4(0.f, 0.f, 0.f, -1.f);
         m1 = valid ? __ldg(map.rec + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -494,9 +503,14 @@ template <int U, int W>
 void launch_ll_lanes_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys, int32_t* nm,
                        cudaStream_t st) {
   const size_t smem = ll_lanes_smem<U, W>(scan.n);
-  cudaFuncSetAttribute(k_gicp_ll_lanes<U, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   const unsigned grid = static_cast<unsigned>((n + W * 32 - 1) / (W * 32));
-  k_gicp_ll_lanes<U, W><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+  if (map.brick) {
+    cudaFuncSetAttribute(k_gicp_ll_lanes<U, W, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_gicp_ll_lanes<U, W, 1><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+  } else {
+    cudaFuncSetAttribute(k_gicp_ll_lanes<U, W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_gicp_ll_lanes<U, W, 0><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+  }
 }
 
 template <int U, int W>
@@ -505,19 +519,26 @@ size_t fast_smem(int S) {
   return sizeof(WarpStage<32 * U>) * W + sizeof(float4) * 2 * Sp + sizeof(double) * 3 * Sp;
 }
 
-template <bool GN, int U, int W>
-void launch_fast_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys, int32_t* nm,
-                   cudaStream_t st) {
+template <bool GN, int U, int W, int B>
+void launch_fast_tb(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys, int32_t* nm,
+                    cudaStream_t st) {
   const size_t smem = fast_smem<U, W>(scan.n);
   int dev, n_sm, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(k_gicp_fast<GN, U, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gicp_fast<GN, U, W>, W * 32, smem);
+  cudaFuncSetAttribute(k_gicp_fast<GN, U, W, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gicp_fast<GN, U, W, B>, W * 32, smem);
   const int64_t want = (n + W - 1) / W;
   const unsigned grid =
       static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(n_sm) * std::max(per_sm, 1)));
-  k_gicp_fast<GN, U, W><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+  k_gicp_fast<GN, U, W, B><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+}
+
+template <bool GN, int U, int W>
+void launch_fast_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys, int32_t* nm,
+                   cudaStream_t st) {
+  map.brick ? launch_fast_tb<GN, U, W, 1>(poses, n, scan, map, sys, nm, st)
+            : launch_fast_tb<GN, U, W, 0>(poses, n, scan, map, sys, nm, st);
 }
 
 }  // namespace

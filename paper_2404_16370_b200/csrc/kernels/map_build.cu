@@ -144,28 +144,41 @@ __global__ void k_nnf_query(const uint8_t* __restrict__ reach, int64_t n_cells, 
   cells[c] = best;
 }
 
-// Fast-map record of every cell: ((mu - corner).xyz, beta), (u.xyz, s).
+// Fast-map record of every cell: ((mu - corner).xyz, beta), (u.xyz, s), at
+// its brick-layout slot (MapFast::index); padding slots of partial bricks
+// stay empty.
 __global__ void k_map_records(const int32_t* __restrict__ cells, int64_t n_cells, GridDev nnf,
-                              const double* __restrict__ mu, const float4* __restrict__ plane,
+                              const double* __restrict__ mu, const float4* __restrict__ plane, int brick,
                               float4* __restrict__ rec) {
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= n_cells) return;
-  const int32_t mi = cells[c];
-  if (mi < 0) {
-    rec[2 * c] = make_float4(0.f, 0.f, 0.f, -1.f);
-    rec[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
-    return;
-  }
   const int nx = nnf.dims[0], ny = nnf.dims[1];
   const int64_t ix = c % nx, iy = (c / nx) % ny, iz = c / (static_cast<int64_t>(nx) * ny);
+  MapFast mf;
+  mf.brick = brick;
+  for (int a = 0; a < 3; ++a) mf.g.dims[a] = nnf.dims[a];
+  const uint64_t slot = mf.index(static_cast<uint32_t>(ix), static_cast<uint32_t>(iy), static_cast<uint32_t>(iz));
+  const int32_t mi = cells[c];
+  if (mi < 0) {
+    rec[2 * slot] = make_float4(0.f, 0.f, 0.f, -1.f);
+    rec[2 * slot + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   const double corner[3] = {__dadd_rn(nnf.org[0], __dmul_rn(static_cast<double>(ix), nnf.cell)),
                             __dadd_rn(nnf.org[1], __dmul_rn(static_cast<double>(iy), nnf.cell)),
                             __dadd_rn(nnf.org[2], __dmul_rn(static_cast<double>(iz), nnf.cell))};
   const float4 p0 = plane[2 * mi], p1 = plane[2 * mi + 1];  // (beta, s, -, -), (u.xyz, -)
-  rec[2 * c] = make_float4(__double2float_rn(__dsub_rn(mu[3 * mi], corner[0])),
-                           __double2float_rn(__dsub_rn(mu[3 * mi + 1], corner[1])),
-                           __double2float_rn(__dsub_rn(mu[3 * mi + 2], corner[2])), p0.x);
-  rec[2 * c + 1] = make_float4(p1.x, p1.y, p1.z, p0.y);
+  rec[2 * slot] = make_float4(__double2float_rn(__dsub_rn(mu[3 * mi], corner[0])),
+                              __double2float_rn(__dsub_rn(mu[3 * mi + 1], corner[1])),
+                              __double2float_rn(__dsub_rn(mu[3 * mi + 2], corner[2])), p0.x);
+  rec[2 * slot + 1] = make_float4(p1.x, p1.y, p1.z, p0.y);
+}
+
+__global__ void k_fill_empty(float4* __restrict__ rec, uint64_t n) {
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  rec[2 * c] = make_float4(0.f, 0.f, 0.f, -1.f);
+  rec[2 * c + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 GridDev grid_dev(const double org[3], double cell, const int dims[3]) {
@@ -238,9 +251,14 @@ cudaError_t build_nnf_device(const double* d_mu, int64_t n, const double pg_org[
 
 cudaError_t build_map_records_device(const int32_t* d_cells, int64_t n_cells, const double nnf_org[3], const int nnf_dims[3],
                               double res, const double* d_mu, const float4* d_plane, float4* d_rec, cudaStream_t st) {
+  // partial bricks: every slot starts empty (beta = -1)
+  const int brick = MapFast::choose_brick(nnf_dims);
+  const uint64_t nrec = MapFast::n_records(nnf_dims, brick);
+  count_launch();
+  k_fill_empty<<<blocks_for(static_cast<int64_t>(nrec), 256), 256, 0, st>>>(d_rec, nrec);
   count_launch();
   k_map_records<<<blocks_for(n_cells, 256), 256, 0, st>>>(d_cells, n_cells, grid_dev(nnf_org, res, nnf_dims), d_mu,
-                                                          d_plane, d_rec);
+                                                          d_plane, brick, d_rec);
   return cudaGetLastError();
 }
 
