@@ -549,18 +549,25 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
                       int32_t* nm, cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
-  static const int cfg = [] {
-    const char* e = std::getenv("SMCL_FAST_CFG");
+  auto parse = [](const char* e) {
     if (!e) return 0;
     int u = 0, w = 0;
     if (std::sscanf(e, "L%dx%d", &u, &w) == 2) return 9000 + u * 100 + w;  // lane-per-particle likelihood
     return std::sscanf(e, "%dx%d", &u, &w) == 2 ? u * 100 + w : 0;
-  }();
+  };
+  static const int cfg_gn = parse(std::getenv("SMCL_FAST_CFG_GN") ? std::getenv("SMCL_FAST_CFG_GN")
+                                                                   : std::getenv("SMCL_FAST_CFG"));
+  static const int cfg_ll = parse(std::getenv("SMCL_FAST_CFG_LL") ? std::getenv("SMCL_FAST_CFG_LL")
+                                                                   : std::getenv("SMCL_FAST_CFG"));
+  const int cfg = gn ? cfg_gn : cfg_ll;
   // Measured on B200 at 1M x 512 (profiles/README.md): the GN pass is
   // register bound (128 regs, 16 warps); the likelihood-only pass needs 80
   // registers and gains from 24 warps of latency hiding.
+  // Likelihood pass: lane per particle when the record table is L2-resident;
+  // for bricked (HBM-sized) tables a warp walks one particle's scan so its
+  // gathers stay inside a few bricks (kidnap outdoor map: 4.8 -> 2.4 ms).
   int c = cfg;
-  if (!gn && c == 0) c = 9000;  // lane-per-particle likelihood pass
+  if (!gn && c == 0) c = map.brick ? 416 : 9000;
   if (c == 0) c = 416;
   if (c >= 9000) {  // SMCL_FAST_CFG=9UWW: lane-per-particle variants (9000 = default 8 points x 8 warps)
     const int u = c == 9000 ? 8 : (c / 100) % 10, w = c == 9000 ? 8 : c % 100;
