@@ -62,10 +62,16 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 // 16-byte async copy; when !pred nothing is read and the destination is zero-filled.
+// kL1: also allocate in L1 (.ca) — pays for bricked HBM-sized tables, where
+// neighbouring particles re-read the same records; L2-resident tables use .cg.
+template <bool kL1>
 __device__ __forceinline__ void cp_async16_pred(void* smem, const void* gmem, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   const int src_bytes = pred ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+  if (kL1)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -280,8 +286,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         const bool stage = !amb && inb;  // padded points are NaN: never staged
         const uint64_t cell = stage ? rec_index<kBrick>(map, ic[0], ic[1], ic[2]) : 0u;
         const float4* src = map.rec + 2 * cell;
-        cp_async16_pred(&ws.m0[slot], src, stage);
-        cp_async16_pred(&ws.m1[slot], src + 1, stage);
+        cp_async16_pred<kBrick != 0>(&ws.m0[slot], src, stage);
+        cp_async16_pred<kBrick != 0>(&ws.m1[slot], src + 1, stage);
         const uint32_t meta = static_cast<uint32_t>(k) | (stage ? kMetaStage : 0u) | (resolve ? kMetaResolve : 0u);
         ws.fq[slot] = make_float4(fr[0], fr[1], fr[2], __uint_as_float(meta));
       }
@@ -448,8 +454,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
       st[u] = (stg ? 1u : 0u) | (real && amb ? 2u : 0u);
       const uint64_t cell = stg ? rec_index<kBrick>(map, ic[0], ic[1], ic[2]) : 0u;
       const float4* src = map.rec + 2 * cell;
-      cp_async16_pred(&ws[(u * 2) * 32 + lane], src, stg);
-      cp_async16_pred(&ws[(u * 2 + 1) * 32 + lane], src + 1, stg);
+      cp_async16_pred<kBrick != 0>(&ws[(u * 2) * 32 + lane], src, stg);
+      cp_async16_pred<kBrick != 0>(&ws[(u * 2 + 1) * 32 + lane], src + 1, stg);
     }
     cp_async_wait_all();
 #pragma unroll
