@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "../engine.cuh"
 #include "../kernels.cuh"
@@ -242,10 +243,10 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
 
   int cnt = count[li];
   for (int s = 0; s < cnt; ++s) s_idx[s * BLOCK + t] = idx[li * k + s];
-  const Pose pi = all_poses[gi];
+  const Pose pi = ldg_pose(all_poses + gi);
   for (int s = 0; s < cnt; ++s) {  // refresh
     const int32_t j = s_idx[s * BLOCK + t];
-    s_kv[s * BLOCK + t] = (j == gi) ? 1.0f : kval_of(pi, all_poses[j], sr, st);
+    s_kv[s * BLOCK + t] = (j == gi) ? 1.0f : kval_of(pi, ldg_pose(all_poses + j), sr, st);
   }
   // Weakest non-self entry (first strict minimum, neighbor_graph.hpp:60-72).
   int weakest = -1;
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
     for (int s = 0; s < cnt; ++s) dup |= (s_idx[s * BLOCK + t] == j);
     if (dup) continue;
     if (cnt == k && weakest < 0) continue;  // self-only full list (k == 1): nothing evictable
-    const float kij = kval_of(pi, all_poses[j], sr, st);
+    const float kij = kval_of(pi, ldg_pose(all_poses + j), sr, st);
     if (cnt < k) {
       s_idx[cnt * BLOCK + t] = j;
       s_kv[cnt * BLOCK + t] = kij;
@@ -288,6 +289,152 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
   for (int s = 0; s < cnt; ++s) {
     idx[li * k + s] = s_idx[s * BLOCK + t];
     kval[li * k + s] = s_kv[s * BLOCK + t];
+  }
+}
+
+// Filtered variant of k_refresh_gather (same results). Once the list is full,
+// a candidate is inserted only if its float kernel value beats the weakest
+// entry wk, and wk never decreases during the window scan. The reference's
+// q = sr|w|^2 + st|V^-1 u|^2 (svgd.hpp:30-44) satisfies |w|^2 = theta^2 >=
+// 2(1 - cos theta) = 3 - tr(Ra^T Rb) and |V^-1 u| >= |u| = |tb - ta| (V^-1
+// scales the plane across w by (theta/2)/sin(theta/2) >= 1), so
+//   q >= L = sr (3 - tr(Ra^T Rb)) + st |tb - ta|^2
+// and L > -log(wk) (1e-6 margin) proves float(exp(-q)) <= wk: the offer
+// would be dropped whatever the list holds (a duplicate is dropped anyway).
+// Each lane filters its window into a chunk of up to kRgChunk survivors; the
+// warp evaluates all lanes' survivors together (full-width kval_of), then each
+// lane replays its offers in window order: values not above wk are dropped
+// before any list scan; the duplicate scan runs only for would-be inserts.
+constexpr int kRgChunk = 16;
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restrict__ all_poses, int64_t n,
+                                                            int64_t gbase, const int32_t* __restrict__ pos_list,
+                                                            const int32_t* __restrict__ member_of,
+                                                            const int32_t* __restrict__ seg_id,
+                                                            const int32_t* __restrict__ seg_start, int32_t n_seg,
+                                                            int64_t n_sorted, int32_t* __restrict__ idx,
+                                                            float* __restrict__ kval, int32_t* __restrict__ count,
+                                                            int k, int cap, double sr, double st) {
+  extern __shared__ __align__(16) unsigned char rg_smem[];
+  int32_t* s_idx = reinterpret_cast<int32_t*>(rg_smem);                  // [k][BLOCK]
+  float* s_kv = reinterpret_cast<float*>(s_idx + k * BLOCK);             // [k][BLOCK]
+  int32_t* s_cand = reinterpret_cast<int32_t*>(s_kv + k * BLOCK);        // [kRgChunk][BLOCK]
+  float* s_ckv = reinterpret_cast<float*>(s_cand + kRgChunk * BLOCK);    // [kRgChunk][BLOCK]
+  int32_t* s_gi = reinterpret_cast<int32_t*>(s_ckv + kRgChunk * BLOCK);  // [BLOCK]
+  uint16_t* s_flat = reinterpret_cast<uint16_t*>(s_gi + BLOCK);          // [BLOCK/32][32*kRgChunk]
+  const unsigned FULL = 0xffffffffu;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  uint16_t* w_flat = s_flat + wid * 32 * kRgChunk;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * BLOCK + t;
+  const bool active = r < n;
+  int32_t gi = -1;
+  int64_t li = 0, q = 0, q_end = 0;
+  int cnt = 0;
+  if (active) {
+    const int64_t gp = pos_list ? static_cast<int64_t>(pos_list[r]) : r;
+    gi = member_of[gp];
+    li = static_cast<int64_t>(gi) - gbase;
+    const int32_t seg = seg_id[gp] - 1;
+    const int64_t rb = seg_start[seg];
+    const int64_t re = seg + 1 < n_seg ? seg_start[seg + 1] : n_sorted;
+    q = rb;
+    q_end = re < rb + cap ? re : rb + cap;
+    cnt = count[li];
+    for (int s = 0; s < cnt; ++s) s_idx[s * BLOCK + t] = idx[li * k + s];
+    const Pose pi = ldg_pose(all_poses + gi);
+    for (int s = 0; s < cnt; ++s) {  // refresh (neighbor_graph.hpp:76-90)
+      const int32_t j = s_idx[s * BLOCK + t];
+      s_kv[s * BLOCK + t] = (j == gi) ? 1.0f : kval_of(pi, ldg_pose(all_poses + j), sr, st);
+    }
+  }
+  s_gi[t] = gi;
+  int weakest = -1;
+  float wk = __int_as_float(0x7f800000);
+  auto find_weakest = [&]() {  // first strict minimum (neighbor_graph.hpp:60-72)
+    weakest = -1;
+    wk = __int_as_float(0x7f800000);
+    for (int s = 0; s < cnt; ++s) {
+      if (s_idx[s * BLOCK + t] == gi) continue;
+      const float v = s_kv[s * BLOCK + t];
+      if (v < wk) {
+        wk = v;
+        weakest = s;
+      }
+    }
+  };
+  if (active && cnt == k) find_weakest();
+
+  while (__any_sync(FULL, q < q_end)) {
+    // ---- filter (no list access): up to kRgChunk survivors in window order
+    const bool full = cnt == k;
+    double thr = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    if (full && wk > 0.0f) thr = -log(static_cast<double>(wk));
+    int ns = 0;
+    if (active) {
+      const Pose pi = ldg_pose(all_poses + gi);
+      for (; q < q_end && ns < kRgChunk; ++q) {
+        const int32_t j = member_of[q];
+        if (j == gi) continue;
+        if (full) {
+          if (weakest < 0) continue;  // self-only full list (k == 1): nothing evictable
+          const Pose pj = ldg_pose(all_poses + j);
+          const double d0 = xsub(pj.t[0], pi.t[0]), d1 = xsub(pj.t[1], pi.t[1]), d2 = xsub(pj.t[2], pi.t[2]);
+          const double uu = xadd(xadd(xmul(d0, d0), xmul(d1, d1)), xmul(d2, d2));
+          if (xmul(st, uu) > 110.0) continue;  // kernel_underflows: k = 0 <= wk
+          double tr = 0.0;
+#pragma unroll
+          for (int e = 0; e < 9; ++e) tr = fma(pi.R[e], pj.R[e], tr);
+          const double L = fma(sr, 3.0 - tr, st * uu);
+          if (L * (1.0 - 1e-6) - 1e-6 > thr) continue;  // float(exp(-q)) <= wk: dropped
+        }
+        s_cand[ns * BLOCK + t] = j;
+        ++ns;
+      }
+    }
+    // ---- warp-wide evaluation of all lanes' survivors
+    int incl = ns;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    for (int s = 0, f = incl - ns; s < ns; ++s, ++f) w_flat[f] = static_cast<uint16_t>((lane << 5) | s);
+    __syncwarp();
+    for (int f = lane; f < total; f += 32) {
+      const int e = w_flat[f];
+      const int ot = (wid << 5) | (e >> 5), sl = e & 31;
+      s_ckv[sl * BLOCK + ot] = kval_of(ldg_pose(all_poses + s_gi[ot]), ldg_pose(all_poses + s_cand[sl * BLOCK + ot]), sr, st);
+    }
+    __syncwarp();
+    // ---- offers in window order (neighbor_graph.hpp:47-74)
+    for (int s = 0; s < ns; ++s) {
+      const float kij = s_ckv[s * BLOCK + t];
+      if (cnt == k && !(weakest >= 0 && kij > wk)) continue;  // dropped, listed or not
+      const int32_t j = s_cand[s * BLOCK + t];
+      bool dup = false;
+      for (int u = 0; u < cnt; ++u) dup |= (s_idx[u * BLOCK + t] == j);
+      if (dup) continue;  // duplicates are ignored
+      if (cnt < k) {
+        s_idx[cnt * BLOCK + t] = j;
+        s_kv[cnt * BLOCK + t] = kij;
+        ++cnt;
+        if (cnt == k) find_weakest();
+        continue;
+      }
+      s_idx[weakest * BLOCK + t] = j;
+      s_kv[weakest * BLOCK + t] = kij;
+      find_weakest();
+    }
+    __syncwarp();
+  }
+  if (active) {
+    count[li] = cnt;
+    for (int s = 0; s < cnt; ++s) {
+      idx[li * k + s] = s_idx[s * BLOCK + t];
+      kval[li * k + s] = s_kv[s * BLOCK + t];
+    }
   }
 }
 
@@ -387,9 +534,20 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                            cudaStream_t st, unsigned long long* /*dbg*/) {
   count_launch();
   constexpr int B = 64;
-  if (n > 0)
-    k_refresh_gather<B><<<blocks_for(n, B), B, static_cast<size_t>(k) * B * 8, st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, seg_start, n_seg,
-                                                         n_sorted, idx, kval, count, k, cap, sr, st_);
+  if (n <= 0) return;
+  static const bool filtered = std::getenv("SMCL_RG_PLAIN") == nullptr;
+  if (filtered) {
+    const size_t smem = static_cast<size_t>(k) * B * 8 + static_cast<size_t>(kRgChunk) * B * 8 + B * 4 +
+                        static_cast<size_t>(B) * kRgChunk * 2;
+    k_refresh_gather_f<B><<<blocks_for(n, B), B, smem, st>>>(all_poses, n, gbase, pos_list, member_of, seg_id,
+                                                             seg_start, n_seg, n_sorted, idx, kval, count, k, cap, sr,
+                                                             st_);
+    return;
+  }
+  k_refresh_gather<B><<<blocks_for(n, B), B, static_cast<size_t>(k) * B * 8, st>>>(all_poses, n, gbase, pos_list,
+                                                                                 member_of, seg_id, seg_start, n_seg,
+                                                                                 n_sorted, idx, kval, count, k, cap,
+                                                                                 sr, st_);
 }
 
 }  // namespace smcl

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(128, MINB) k_svgd(const Pose* __restrict__ all
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t gi = gbase + i;
-  const Pose pi = all_poses[gi];
+  const Pose pi = ldg_pose(all_poses + gi);
   double numer[6] = {0, 0, 0, 0, 0, 0};
   double denom = 0.0;
   const int cnt = count[i];
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(128, MINB) k_svgd(const Pose* __restrict__ all
       denom = denom + 1.0;
       continue;
     }
-    const Pose pj = all_poses[j];
+    const Pose pj = ldg_pose(all_poses + j);
     if (kernel_underflows(pi, pj, sp.sigma_t)) continue;
     double d[6];
     se3_log_rel_fast(pi, pj, d);

@@ -64,6 +64,20 @@ struct SMCL_ALIGN16 Pose {
   double t[3];
 };
 
+#ifdef __CUDACC__
+// Read-only 96-byte pose as six 128-bit loads (a plain struct copy compiles
+// to twelve 64-bit loads: twice the L1 wavefronts in the gather-heavy passes).
+__device__ __forceinline__ Pose ldg_pose(const Pose* p) {
+  const double2* v = reinterpret_cast<const double2*>(p);
+  const double2 a0 = __ldg(v), a1 = __ldg(v + 1), a2 = __ldg(v + 2), a3 = __ldg(v + 3), a4 = __ldg(v + 4),
+                a5 = __ldg(v + 5);
+  Pose q;
+  q.R[0] = a0.x, q.R[1] = a0.y, q.R[2] = a1.x, q.R[3] = a1.y, q.R[4] = a2.x, q.R[5] = a2.y;
+  q.R[6] = a3.x, q.R[7] = a3.y, q.R[8] = a4.x, q.t[0] = a4.y, q.t[1] = a5.x, q.t[2] = a5.y;
+  return q;
+}
+#endif
+
 SMCL_HD Pose pose_identity() {
   Pose p;
 #pragma unroll
