@@ -163,7 +163,7 @@ __device__ __forceinline__ float kval_fast(const Pose& a, const Pose& b, double 
   } else {
     const double ivs = rsqrt_nr(vv);  // 1 / |vee|
     const double s = 0.5 * (vv * ivs);
-    const double theta = atan2(s, c);
+    const double theta = atan2_pos(s, c);
     if (theta > 3.14159265358979323846 - 1e-2) {  // near the pi branch: reference path
       *ok = false;
       return 0.0f;

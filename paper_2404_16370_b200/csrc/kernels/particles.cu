@@ -82,7 +82,7 @@ __device__ __forceinline__ void se3_log_rel_fast(const Pose& a, const Pose& b, d
     ivs = rsqrt_nr(vv);
     s = 0.5 * (vv * ivs);
   }
-  const double theta = atan2(s, c);
+  const double theta = atan2_pos(s, c);
   if (theta > kPi - 1e-6) {  // reference pi branch
     se3_log(inv_compose_x(a, b), d);
     return;

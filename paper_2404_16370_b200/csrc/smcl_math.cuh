@@ -48,6 +48,54 @@ __device__ __forceinline__ double rcp_nr(double x) {
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
 }
+// atan2(s, c) for s >= 0 (angles in [0, pi]) at ~1 ulp: one division by a
+// Newton reciprocal, octant reduction to |u| <= tan(pi/8) + eps, and
+// atan(u) = u P(u^2) with a degree-11 near-minimax P on u^2 <= 0.18
+// (scratch/atan_poly.py: max relative error 1.5e-16). No special cases: the
+// callers pass finite (s, c) with s^2 + c^2 ~ 1.
+__device__ __forceinline__ double atan2_pos(double s, double c) {
+  constexpr double kT8 = 0.41421356237309504880;  // tan(pi/8)
+  const double ac = fabs(c);
+  double num, den, base;
+  if (s <= kT8 * ac) {  // near 0 (c > 0) or near pi (c < 0): u = s / c
+    num = s;
+    den = c;
+    base = c > 0.0 ? 0.0 : 3.14159265358979323846;
+  } else if (ac <= kT8 * s) {  // near pi/2: u = -c / s
+    num = -c;
+    den = s;
+    base = 1.57079632679489661923;
+  } else if (c > 0.0) {  // near pi/4: u = (s - c) / (s + c)
+    num = s - c;
+    den = s + c;
+    base = 0.78539816339744830962;
+  } else {  // near 3pi/4: u = (s + c) / (c - s)
+    num = s + c;
+    den = c - s;
+    base = 2.35619449019234492885;
+  }
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+  double e = fma(-den, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-den, r, 1.0);
+  r = fma(r, e, r);
+  double u = num * r;
+  u = fma(fma(-den, u, num), r, u);  // one correction step: u = num / den to ~1 ulp
+  const double y = u * u;
+  double p = -0.017085141492542092;
+  p = fma(p, y, 0.037299486849215);
+  p = fma(p, y, -0.05008578394066089);
+  p = fma(p, y, 0.058409193896630636);
+  p = fma(p, y, -0.06662122513410981);
+  p = fma(p, y, 0.07691971387624114);
+  p = fma(p, y, -0.09090892587575122);
+  p = fma(p, y, 0.11111110595175504);
+  p = fma(p, y, -0.14285714276163336);
+  p = fma(p, y, 0.19999999999908397);
+  p = fma(p, y, -0.3333333333333299);
+  return fma(u * y, p, u) + base;  // u (1 + y p(y)) + base
+}
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));

@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/gpu_tests.log
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+python -c "import json; d=json.load(open('gpurun_out/bench.json')); print('ms', d['ms_per_step']); print({k: round(v,3) for k,v in d['stage_ms'].items()})"
