@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
 // before any list scan; the duplicate scan runs only for would-be inserts.
 constexpr int kRgChunk = 16;
 
-template <int BLOCK>
+template <int BLOCK, int KMAX>
 __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restrict__ all_poses, int64_t n,
                                                             int64_t gbase, const int32_t* __restrict__ pos_list,
                                                             const int32_t* __restrict__ member_of,
@@ -349,15 +349,22 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
     }
   }
   s_gi[t] = gi;
+  // Self never leaves its slot (offers never evict it): locate it once, so the
+  // weakest-entry scan reads only values. Loops run over KMAX >= k slots,
+  // unrolled and predicated.
+  int self_slot = -1;
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s)
+    if (s < cnt && s_idx[s * BLOCK + t] == gi) self_slot = s;
   int weakest = -1;
   float wk = __int_as_float(0x7f800000);
   auto find_weakest = [&]() {  // first strict minimum (neighbor_graph.hpp:60-72)
     weakest = -1;
     wk = __int_as_float(0x7f800000);
-    for (int s = 0; s < cnt; ++s) {
-      if (s_idx[s * BLOCK + t] == gi) continue;
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
       const float v = s_kv[s * BLOCK + t];
-      if (v < wk) {
+      if (s < cnt && s != self_slot && v < wk) {
         wk = v;
         weakest = s;
       }
@@ -414,7 +421,8 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
       if (cnt == k && !(weakest >= 0 && kij > wk)) continue;  // dropped, listed or not
       const int32_t j = s_cand[s * BLOCK + t];
       bool dup = false;
-      for (int u = 0; u < cnt; ++u) dup |= (s_idx[u * BLOCK + t] == j);
+#pragma unroll
+      for (int u = 0; u < KMAX; ++u) dup |= (u < cnt && s_idx[u * BLOCK + t] == j);
       if (dup) continue;  // duplicates are ignored
       if (cnt < k) {
         s_idx[cnt * BLOCK + t] = j;
@@ -536,12 +544,20 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
   constexpr int B = 64;
   if (n <= 0) return;
   static const bool filtered = std::getenv("SMCL_RG_PLAIN") == nullptr;
-  if (filtered) {
+  if (filtered && k <= 32) {
     const size_t smem = static_cast<size_t>(k) * B * 8 + static_cast<size_t>(kRgChunk) * B * 8 + B * 4 +
                         static_cast<size_t>(B) * kRgChunk * 2;
-    k_refresh_gather_f<B><<<blocks_for(n, B), B, smem, st>>>(all_poses, n, gbase, pos_list, member_of, seg_id,
-                                                             seg_start, n_seg, n_sorted, idx, kval, count, k, cap, sr,
-                                                             st_);
+#define RGF(KM)                                                                                                   \
+  k_refresh_gather_f<B, KM><<<blocks_for(n, B), B, smem, st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, \
+                                                               seg_start, n_seg, n_sorted, idx, kval, count, k,   \
+                                                               cap, sr, st_)
+    if (k <= 8)
+      RGF(8);
+    else if (k <= 20)
+      RGF(20);
+    else
+      RGF(32);
+#undef RGF
     return;
   }
   k_refresh_gather<B><<<blocks_for(n, B), B, static_cast<size_t>(k) * B * 8, st>>>(all_poses, n, gbase, pos_list,
