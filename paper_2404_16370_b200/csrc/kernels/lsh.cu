@@ -100,6 +100,54 @@ __global__ void k_reorder(const int32_t* __restrict__ old_of_new, const int32_t*
   }
 }
 
+// K = 20 rows (80 B, 16-byte aligned): 128-bit row copies, all 20 remap
+// gathers issued together, 128-bit pose copy.
+template <int K>
+__global__ void __launch_bounds__(128) k_reorder_k(const int32_t* __restrict__ old_of_new,
+                                                   const int32_t* __restrict__ new_of_old, int64_t n,
+                                                   const Pose* __restrict__ poses, const double* __restrict__ lp,
+                                                   const int32_t* __restrict__ id, const int32_t* __restrict__ idx,
+                                                   const float* __restrict__ kval, const int32_t* __restrict__ count,
+                                                   Pose* __restrict__ poses2, double* __restrict__ lp2,
+                                                   int32_t* __restrict__ id2, int32_t* __restrict__ idx2,
+                                                   float* __restrict__ kval2, int32_t* __restrict__ count2) {
+  static_assert(K % 4 == 0, "rows must be whole 16-byte vectors");
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int64_t src = old_of_new[p];
+  const double2* ps = reinterpret_cast<const double2*>(poses + src);
+  double2* pd = reinterpret_cast<double2*>(poses2 + p);
+#pragma unroll
+  for (int v = 0; v < 6; ++v) pd[v] = __ldg(ps + v);
+  lp2[p] = lp[src];
+  id2[p] = id[src];
+  const int c = count[src];
+  count2[p] = c;
+  const int4* ir = reinterpret_cast<const int4*>(idx + src * K);
+  const float4* kr = reinterpret_cast<const float4*>(kval + src * K);
+  int j[K];
+  float w[K];
+#pragma unroll
+  for (int v = 0; v < K / 4; ++v) {
+    const int4 a = __ldg(ir + v);
+    const float4 b = __ldg(kr + v);
+    j[4 * v] = a.x, j[4 * v + 1] = a.y, j[4 * v + 2] = a.z, j[4 * v + 3] = a.w;
+    w[4 * v] = b.x, w[4 * v + 1] = b.y, w[4 * v + 2] = b.z, w[4 * v + 3] = b.w;
+  }
+#pragma unroll
+  for (int s = 0; s < K; ++s) {  // particle_set.cpp:17-19 value-initialises the unused slots
+    j[s] = s < c ? __ldg(new_of_old + j[s]) : 0;
+    w[s] = s < c ? w[s] : 0.0f;
+  }
+  int4* io = reinterpret_cast<int4*>(idx2 + p * K);
+  float4* ko = reinterpret_cast<float4*>(kval2 + p * K);
+#pragma unroll
+  for (int v = 0; v < K / 4; ++v) {
+    io[v] = make_int4(j[4 * v], j[4 * v + 1], j[4 * v + 2], j[4 * v + 3]);
+    ko[v] = make_float4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+  }
+}
+
 __global__ void k_segments(const int32_t* __restrict__ head, const int32_t* __restrict__ seg_id, int64_t n,
                            int32_t* __restrict__ seg_start) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -516,6 +564,11 @@ void launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_
                     Pose* poses2, double* lp2, int32_t* id2, int32_t* idx2, float* kval2, int32_t* count2,
                     cudaStream_t st) {
   count_launch();
+  if (n > 0 && k == 20) {
+    k_reorder_k<20><<<blocks_for(n, 128), 128, 0, st>>>(old_of_new, new_of_old, n, poses, lp, id, idx, kval, count,
+                                                        poses2, lp2, id2, idx2, kval2, count2);
+    return;
+  }
   if (n > 0)
     k_reorder<<<blocks_for(n, 128), 128, 0, st>>>(old_of_new, new_of_old, n, k, poses, lp, id, idx, kval, count, poses2,
                                                   lp2, id2, idx2, kval2, count2);
