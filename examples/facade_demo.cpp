@@ -50,7 +50,9 @@ int main() {
     int64_t n_pts = 0;
     detail::check(smcl_sim_scan(rects, n_rects, pose, &sensor, &rng, pts.data(), &n_pts));
     pts.resize(static_cast<size_t>(n_pts) * 3);
-    r = engine.step(make_scan_cloud(pts, cfg), odo);
+    // frames 0-1: host make_scan_cloud + step(); frame 2: raw points, scan
+    // preparation on the device (step_points)
+    r = f < 2 ? engine.step(make_scan_cloud(pts, cfg), odo) : engine.step_points(pts.data(), n_pts, odo);
   }
   const ParticleSet& ps = engine.particles();
   if (ps.size() != 4096) return 1;

@@ -127,6 +127,21 @@ class FilterEngine {
     return r;
   }
 
+  // Scenario-runner frame (scenario.cpp:315-338): make_scan_cloud on the
+  // device from raw sensor points (x, y, z triples), then step().
+  FrameResult step_points(const double* points_xyz, std::int64_t n_points, const OdometryInput& odo) {
+    flush();
+    smcl_odom o;
+    std::memcpy(o.delta, odo.delta.R, sizeof(odo.delta.R));
+    std::memcpy(o.delta + 9, odo.delta.t, sizeof(odo.delta.t));
+    std::memcpy(o.cov, odo.cov, sizeof(o.cov));
+    o.valid = odo.valid ? 1 : 0;
+    FrameResult r;
+    detail::check(smcl_step_points(h_, points_xyz, n_points, &o, &r));
+    mirror_valid_ = false;
+    return r;
+  }
+
   const ParticleSet& particles() {
     if (!mirror_valid_) download();
     return mirror_;
