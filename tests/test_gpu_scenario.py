@@ -53,3 +53,30 @@ def test_c8_no_resampling_invariant():
         fr = e.step_points(sim.scan_points_for_frame(sc, rects, truth, f), d, c, v)
         assert fr["n_particles"] == 3000
         assert np.array_equal(np.sort(e.particles().id), np.arange(3000))
+
+
+def test_c4_lsh_recall_at_20():
+    """acceptance.cpp:169-220: 1,000 particles (rotations <= 0.2 rad, positions
+    in a 10 m cube), default LSH, 10 passes: recall@20 against the brute-force
+    kernel kNN >= 0.9, with the GPU neighbour pass."""
+    import oracle as O
+    from helpers import random_cube_set
+    n, k = 1000, 20
+    g = random_cube_set(n, 10.0, 0.2, k, 404)
+    truth = O.brute_force_kernel_knn(g.poses, k)
+    e = FilterEngine(None, make_config(k_neighbors=k))
+    e.set_particles(g)
+    for p in range(10):
+        e.update_neighbors(O.mix_seed(405, p), [0, 0, 0, 10, 10, 10])
+    got = e.particles()
+    slot_of_id = np.empty(n, np.int64)
+    slot_of_id[got.id] = np.arange(n)
+    hit = total = 0
+    for orig in range(n):
+        s = slot_of_id[orig]
+        have = {int(got.id[j]) for j in got.idx[s, : got.count[s]]}
+        for want in truth[orig]:
+            total += 1
+            hit += int(want) in have
+    print(f"C4: recall@20 = {hit / total:.4f}")
+    assert hit / total >= 0.9
