@@ -257,11 +257,16 @@ def main():
     t_setup = time.perf_counter()
     comm = None
     if pg:  # particle-index shards of the same N (strong scaling), NCCL all-gathers at the exchange points
-        from paper_2404_16370_b200.comm import TorchComm, shard_range
+        from paper_2404_16370_b200.comm import NcclComm, TorchComm, shard_range
         shard_range(args.particles, rank, world)
         if args.no_reorder:  # v1 exchange plan: particles never migrate between shards
             cfg.reorder_particles = 0
-        comm = TorchComm()
+        # native NCCL on the engine stream (fallback: torch.distributed trampoline)
+        try:
+            comm = NcclComm.from_torch()
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] native NCCL comm unavailable ({e}); using TorchComm", file=sys.stderr)
+            comm = TorchComm()
     eng = FilterEngine(wl.map, cfg, device=local, comm=comm)
     eng.init_uniform(wl.bounds)
     setup_s = time.perf_counter() - t_setup

@@ -156,6 +156,14 @@ int smcl_create_sharded(const smcl_cloud* map, const smcl_config* cfg, int devic
  * threads (shard-count invariance tests on one device): fills comms[world]. */
 int smcl_comm_loopback_create(int32_t world, smcl_comm* comms);
 void smcl_comm_loopback_destroy(smcl_comm* comms);
+/* Native NCCL communicator (libnccl.so.2 loaded at run time): the engine's
+ * all-gathers become ncclAllGather on the engine stream over NVLink/NVSwitch.
+ * Rank 0 calls smcl_nccl_get_unique_id and distributes the 128 bytes (any
+ * host channel); every rank then calls smcl_comm_nccl_create with its CUDA
+ * device current. The reference has no distributed backend. */
+int smcl_nccl_get_unique_id(uint8_t id[128]);
+int smcl_comm_nccl_create(const uint8_t id[128], int32_t rank, int32_t world, smcl_comm* out);
+void smcl_comm_nccl_destroy(smcl_comm* comm);
 int smcl_destroy(smcl_engine* h);
 
 /* FilterEngine::init_uniform(const Aabb&) (filter.cpp:108-116). */

@@ -25,6 +25,9 @@ SIGNATURES = {
     "smcl_create_sharded": (_int, [_P(SmclCloud), _P(SmclConfig), _int, _P(SmclComm), _P(C.c_void_p)]),
     "smcl_comm_loopback_create": (_int, [_i32, _P(SmclComm)]),
     "smcl_comm_loopback_destroy": (None, [_P(SmclComm)]),
+    "smcl_nccl_get_unique_id": (_int, [_P(C.c_uint8)]),
+    "smcl_comm_nccl_create": (_int, [_P(C.c_uint8), _i32, _i32, _P(SmclComm)]),
+    "smcl_comm_nccl_destroy": (None, [_P(SmclComm)]),
     "smcl_destroy": (_int, [C.c_void_p]),
     "smcl_init_uniform": (_int, [C.c_void_p, _P(_d)]),
     "smcl_init_uniform_seeded": (_int, [C.c_void_p, _i64, _P(_d), _int, _u64]),

@@ -12,6 +12,10 @@ Backends:
 
 * ``LoopbackComms`` — in-process, ``world`` engines driven by ``world`` host
   threads (one device or several); implemented in C (engine.cu).
+* ``NcclComm`` — native NCCL (``smcl_comm_nccl_create``): the engine calls
+  ``ncclAllGather`` on its own stream, no Python on the data path. The
+  128-byte unique id travels over any host channel (``NcclComm.from_torch``
+  uses the torch.distributed group bench.py already has).
 * ``TorchComm`` — ``torch.distributed`` over NCCL (device buffers, one process
   per GPU) or gloo (host buffers; used by the CPU tests of this layer).
 
@@ -50,6 +54,42 @@ class LoopbackComms:
         if self.structs is not None:
             _lib.lib().smcl_comm_loopback_destroy(self.structs)
             self.structs = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NcclComm:
+    """Native NCCL communicator for one rank (libnccl.so.2, NVLink/NVSwitch)."""
+
+    @staticmethod
+    def unique_id():
+        buf = (C.c_uint8 * 128)()
+        _lib.check(_lib.lib().smcl_nccl_get_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, uid, rank, world):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self.struct = SmclComm()
+        _lib.check(_lib.lib().smcl_comm_nccl_create(buf, rank, world, C.byref(self.struct)))
+        self.rank, self.world = rank, world
+
+    @classmethod
+    def from_torch(cls, group=None):
+        """Rank 0 makes the id, torch.distributed broadcasts it, every rank joins
+        (call with this rank's CUDA device current)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        return cls(obj[0], rank, world)
+
+    def close(self):
+        if getattr(self, "struct", None) is not None and self.struct.ctx:
+            _lib.lib().smcl_comm_nccl_destroy(C.byref(self.struct))
 
     def __del__(self):
         try:
