@@ -127,10 +127,17 @@ __global__ void k_list_sums(const float* __restrict__ kval, const int32_t* __res
 // values at a time in shared memory (coalesced) and lane 0 adds them serially
 // in index order, so every chunk partial is bit-identical to the reference's.
 constexpr int kStage = 1024;
-__global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ v, int64_t n,
-                                                     double* __restrict__ partial) {
+// Two independent vectors per launch (blocks [0, chunks) sum v0, [chunks,
+// 2*chunks) sum v1). The serial chain is DADD-latency bound: lane 0 reads
+// the staged values 8 at a time ahead of the adds.
+__global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ v0, const double* __restrict__ v1,
+                                                     int64_t n, int64_t chunks, double* __restrict__ p0,
+                                                     double* __restrict__ p1) {
   __shared__ double s[kStage];
-  const int64_t c = blockIdx.x;
+  const bool second = blockIdx.x >= chunks;
+  const double* __restrict__ v = second ? v1 : v0;
+  double* __restrict__ partial = second ? p1 : p0;
+  const int64_t c = second ? blockIdx.x - chunks : blockIdx.x;
   const int64_t begin = c * kReduceChunk;
   const int64_t end = begin + kReduceChunk < n ? begin + kReduceChunk : n;
   double acc = 0.0;
@@ -138,8 +145,17 @@ __global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ 
     const int64_t m = end - b < kStage ? end - b : kStage;
     for (int q = threadIdx.x; q < m; q += 32) s[q] = v[b + q];
     __syncwarp();
-    if (threadIdx.x == 0)
-      for (int q = 0; q < m; ++q) acc = xadd(acc, s[q]);
+    if (threadIdx.x == 0) {
+      int q = 0;
+      for (; q + 8 <= m; q += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = s[q + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = xadd(acc, x[u]);
+      }
+      for (; q < m; ++q) acc = xadd(acc, s[q]);
+    }
     __syncwarp();
   }
   if (threadIdx.x == 0) partial[c] = acc;
@@ -268,7 +284,12 @@ void launch_max_of_partials(const double* pv, const long long* pi, int64_t n, do
 static void chunk_serial(const double* v, int64_t n, double* partial, cudaStream_t st) {
   count_launch();
   const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
-  if (chunks > 0) k_chunk_serial<<<static_cast<unsigned>(chunks), 32, 0, st>>>(v, n, partial);
+  if (chunks > 0) k_chunk_serial<<<static_cast<unsigned>(chunks), 32, 0, st>>>(v, v, n, chunks, partial, partial);
+}
+static void chunk_serial2(const double* a, const double* b, int64_t n, double* pa, double* pb, cudaStream_t st) {
+  count_launch();
+  const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
+  if (chunks > 0) k_chunk_serial<<<static_cast<unsigned>(2 * chunks), 32, 0, st>>>(a, b, n, chunks, pa, pb);
 }
 void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* scratch, double* partial,
                           cudaStream_t st) {
@@ -282,8 +303,7 @@ void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n,
   count_launch();
   if (n <= 0) return;
   k_list_sums<<<blocks_for(n, 256), 256, 0, st>>>(kval, count, n, k, s1, s2);
-  chunk_serial(s1, n, pk, st);
-  chunk_serial(s2, n, pc, st);
+  chunk_serial2(s1, s2, n, pk, pc, st);
 }
 void launch_finish_lse(const double* partial, int64_t n_chunks, const double* m, double* lse, cudaStream_t st) {
   count_launch();
