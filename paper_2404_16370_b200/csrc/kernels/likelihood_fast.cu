@@ -573,7 +573,9 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
   // for bricked (HBM-sized) tables a warp walks one particle's scan so its
   // gathers stay inside a few bricks (kidnap outdoor map: 4.8 -> 2.4 ms).
   int c = cfg;
-  if (!gn && c == 0) c = map.brick ? 416 : 9000;
+  // The lane kernel needs two resident CTAs per SM (16 warps): scans too large
+  // for that (S > ~900 points) take the warp-per-particle kernel as well.
+  if (!gn && c == 0) c = (map.brick || 2 * ll_lanes_smem<8, 8>(scan.n) > 227 * 1024) ? 416 : 9000;
   if (c == 0) c = 416;
   if (c >= 9000) {  // SMCL_FAST_CFG=9UWW: lane-per-particle variants (9000 = default 8 points x 8 warps)
     const int u = c == 9000 ? 8 : (c / 100) % 10, w = c == 9000 ? 8 : c % 100;
