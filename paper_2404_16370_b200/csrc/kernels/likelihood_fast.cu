@@ -128,19 +128,26 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
     acc.b[3] -= gx;  // b_bot -= g
     acc.b[4] -= gy;
     acc.b[5] -= gz;
-    const float pm[3] = {P * mx, P * my, P * mz};
-    const float qn[3] = {Q * nx, Q * ny, Q * nz};
-    const float tm[3] = {T * mx, T * my, T * mz};
-    const float tn[3] = {T * nx, T * ny, T * nz};
+    // Omega' = invA (I + P m m^T + Q n n^T + T (m n^T + n m^T))
+    //        = invA I + alpha m^T + beta_ n^T,  alpha = invA (P m + T n),
+    //                                           beta_ = invA (Q n + T m)
+    // (symmetric: alpha_r m_q + beta_r n_q = invA (P m_r m_q + Q n_r n_q + T (n_r m_q + m_r n_q))).
+    const float Pa = P * invA, Qa = Q * invA, Ta = T * invA;
     const float mv[3] = {mx, my, mz}, nv[3] = {nx, ny, nz};
+    float al[3], be[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      al[r] = fmaf(Pa, mv[r], Ta * nv[r]);
+      be[r] = fmaf(Qa, nv[r], Ta * mv[r]);
+    }
     float O[3][3];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int q = 0; q <= r; ++q) {
-        float v = pm[r] * mv[q] + qn[r] * nv[q] + tm[r] * nv[q] + tn[r] * mv[q];
-        if (r == q) v += 1.0f;
-        O[r][q] = O[q][r] = v * invA;
+        float v = fmaf(al[r], mv[q], be[r] * nv[q]);
+        if (r == q) v += invA;
+        O[r][q] = O[q][r] = v;
       }
     acc.hbr[0] += O[0][0];
     acc.hbr[1] += O[1][0];
@@ -159,13 +166,13 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int q = 0; q < 3; ++q) acc.htr[r * 3 + q] += W[r][q];
-    // H_tl -= W [mu]x (lower triangle)
-    acc.htl[0] -= W[0][1] * uz - W[0][2] * uy;
-    acc.htl[1] -= W[1][1] * uz - W[1][2] * uy;
-    acc.htl[2] -= W[1][2] * ux - W[1][0] * uz;
-    acc.htl[3] -= W[2][1] * uz - W[2][2] * uy;
-    acc.htl[4] -= W[2][2] * ux - W[2][0] * uz;
-    acc.htl[5] -= W[2][0] * uy - W[2][1] * ux;
+    // H_tl -= W [mu]x (lower triangle), two FMAs per entry
+    acc.htl[0] = fmaf(W[0][2], uy, fmaf(-W[0][1], uz, acc.htl[0]));
+    acc.htl[1] = fmaf(W[1][2], uy, fmaf(-W[1][1], uz, acc.htl[1]));
+    acc.htl[2] = fmaf(W[1][0], uz, fmaf(-W[1][2], ux, acc.htl[2]));
+    acc.htl[3] = fmaf(W[2][2], uy, fmaf(-W[2][1], uz, acc.htl[3]));
+    acc.htl[4] = fmaf(W[2][0], uz, fmaf(-W[2][2], ux, acc.htl[4]));
+    acc.htl[5] = fmaf(W[2][1], ux, fmaf(-W[2][0], uy, acc.htl[5]));
   }
 }
 
