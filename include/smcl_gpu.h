@@ -184,6 +184,11 @@ int smcl_step_slot(smcl_engine* h, int slot, const smcl_odom* odo, smcl_frame_re
  * covariances + sensor noise, staged into a device slot. Bit-identical to
  * smcl_make_scan_cloud. */
 int smcl_scan_prepare(smcl_engine* h, int slot, const double* points, int64_t n);
+/* Same preparation, asynchronous: the points are copied and prepared by the
+ * engine's preparation thread on its own stream while other slots are being
+ * stepped (2-stage pipeline); smcl_step_slot / smcl_scan_get on the slot wait
+ * for it. Do not re-prepare a slot that a running step is using. */
+int smcl_scan_prepare_async(smcl_engine* h, int slot, const double* points, int64_t n);
 /* Prepared scan of a slot (mu_out n*3, sigma_out n*9; NULL pointers: count only). */
 int smcl_scan_get(smcl_engine* h, int slot, double* mu_out, double* sigma_out, int64_t* n_out);
 /* Scenario-runner frame (scenario.cpp:315-338): make_scan_cloud + step on raw

@@ -35,6 +35,7 @@ SIGNATURES = {
     "smcl_scan_upload": (_int, [C.c_void_p, _int, _P(SmclCloud)]),
     "smcl_step_slot": (_int, [C.c_void_p, _int, _P(SmclOdom), _P(SmclFrameResult)]),
     "smcl_scan_prepare": (_int, [C.c_void_p, _int, _P(_d), _i64]),
+    "smcl_scan_prepare_async": (_int, [C.c_void_p, _int, _P(_d), _i64]),
     "smcl_scan_get": (_int, [C.c_void_p, _int, _P(_d), _P(_d), _P(_i64)]),
     "smcl_step_points": (_int, [C.c_void_p, _P(_d), _i64, _P(SmclOdom), _P(SmclFrameResult)]),
     "smcl_last_step_profile": (_int, [C.c_void_p, _P(SmclStepProfile)]),

@@ -123,6 +123,12 @@ class FilterEngine:
         pts = _a(points, (-1, 3))
         check(_lib.lib().smcl_scan_prepare(self.h, slot, f64ptr(pts), pts.shape[0]))
 
+    def scan_prepare_async(self, slot, points):
+        """Queue make_scan_cloud for a slot on the engine's preparation stream
+        (overlaps the step running on another slot); step_slot waits for it."""
+        pts = _a(points, (-1, 3))
+        check(_lib.lib().smcl_scan_prepare_async(self.h, slot, f64ptr(pts), pts.shape[0]))
+
     def scan_get(self, slot):
         """Prepared scan of a slot as a GaussianCloud."""
         n = C.c_int64()

@@ -12,6 +12,9 @@
 #include <atomic>
 #include <bit>
 #include <condition_variable>
+#include <deque>
+#include <exception>
+#include <thread>
 #include <mutex>
 #include <cmath>
 #include <cstring>
@@ -347,6 +350,7 @@ struct smcl_engine {
     ScanDev full, gn;
     bool gn_alias = true;  // stride 1: the GN scan is the full scan
     bool valid = false;
+    long long upload_bytes = 0;  // H2D bytes of the slot's last preparation
     const ScanDev& gn_view() const { return gn_alias ? full : gn; }
   };
   std::vector<std::unique_ptr<ScanSlot>> slots;
@@ -382,6 +386,18 @@ struct smcl_engine {
   }
 
   ~smcl_engine() {
+    if (prep_thread.joinable()) {
+      {
+        std::lock_guard<std::mutex> lk(prep_m);
+        prep_stop = true;
+      }
+      prep_cv.notify_all();
+      prep_thread.join();
+    }
+    if (prep_st) {
+      cudaStreamSynchronize(prep_st);
+      cudaStreamDestroy(prep_st);
+    }
     if (st) cudaStreamSynchronize(st);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -538,11 +554,11 @@ struct smcl_engine {
   }
 
   // ------------------------------------------------------------ scans
-  void upload_scan(ScanDev& sd, const double* mu, const double* sigma, int n) {
+  void upload_scan(ScanDev& sd, const double* mu, const double* sigma, int n, cudaStream_t us) {
     if (n > kMaxScan) throw std::invalid_argument("scan exceeds the device scan capacity");
     sd.n = n;
-    sd.mu.upload(mu, static_cast<size_t>(n) * 3, st);
-    sd.sigma.upload(sigma, static_cast<size_t>(n) * 9, st);
+    sd.mu.upload(mu, static_cast<size_t>(n) * 3, us);
+    sd.sigma.upload(sigma, static_cast<size_t>(n) * 9, us);
     std::vector<float4> rec(2 * static_cast<size_t>(std::max(n, 1)));
     bool ok = true;
     for (int q = 0; q < n && ok; ++q) {
@@ -556,26 +572,106 @@ struct smcl_engine {
     sd.l1max = 0.0;
     for (int q = 0; q < n; ++q)
       sd.l1max = std::max(sd.l1max, std::fabs(mu[3 * q]) + std::fabs(mu[3 * q + 1]) + std::fabs(mu[3 * q + 2]));
-    if (ok) sd.rec.upload(rec.data(), rec.size(), st);
+    if (ok) sd.rec.upload(rec.data(), rec.size(), us);
   }
 
-  ScanSlot& slot_at(int i) {
+  ScanSlot& slot_at(int i) {  // slots are created with the engine: safe from the preparation thread
     if (i < 0 || i >= SMCL_MAX_SCAN_SLOTS) throw std::invalid_argument("scan slot out of range");
-    while (static_cast<int>(slots.size()) <= i) slots.push_back(std::make_unique<ScanSlot>());
     return *slots[static_cast<size_t>(i)];
+  }
+
+  // ------------------------------------------------------------ scan pipeline
+  // smcl_scan_prepare_async: a preparation thread with its own stream runs
+  // make_scan_cloud for slot f+1 while the engine stream runs the step on
+  // slot f (the 2-stage stream pipeline of SURVEY §8f next-2). step_slot(i)
+  // waits for slot i's pending preparation; synchronous preparations wait for
+  // the queue to drain (they share the scratch buffers).
+  struct PrepJob {
+    int slot;
+    std::vector<double> pts;
+  };
+  std::thread prep_thread;
+  std::mutex prep_m;
+  std::condition_variable prep_cv;
+  std::deque<PrepJob> prep_q;
+  int prep_pending[SMCL_MAX_SCAN_SLOTS] = {};
+  bool prep_stop = false;
+  std::exception_ptr prep_err;
+  cudaStream_t prep_st = nullptr;
+
+  void prep_worker() {
+    cudaSetDevice(device);
+    for (;;) {
+      PrepJob job;
+      {
+        std::unique_lock<std::mutex> lk(prep_m);
+        prep_cv.wait(lk, [&] { return prep_stop || !prep_q.empty(); });
+        if (prep_q.empty()) return;
+        job = std::move(prep_q.front());
+        prep_q.pop_front();
+      }
+      try {
+        prepare_slot(job.slot, job.pts.data(), static_cast<int64_t>(job.pts.size() / 3), prep_st);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(prep_m);
+        if (!prep_err) prep_err = std::current_exception();
+      }
+      {
+        std::lock_guard<std::mutex> lk(prep_m);
+        --prep_pending[job.slot];
+      }
+      prep_cv.notify_all();
+    }
+  }
+  void prepare_async(int slot, const double* points, int64_t n) {
+    slot_at(slot);
+    if (n < 0 || (n > 0 && !points)) throw std::invalid_argument("scan_prepare: null points");
+    if (!prep_thread.joinable()) {
+      CK(cudaStreamCreateWithFlags(&prep_st, cudaStreamNonBlocking));
+      prep_thread = std::thread([this] { prep_worker(); });
+    }
+    PrepJob job{slot, std::vector<double>(points, points + 3 * n)};  // the caller may reuse its buffer
+    {
+      std::lock_guard<std::mutex> lk(prep_m);
+      ++prep_pending[slot];
+      prep_q.push_back(std::move(job));
+    }
+    prep_cv.notify_all();
+  }
+  void rethrow_prep_error() {
+    if (prep_err) {
+      std::exception_ptr e = prep_err;
+      prep_err = nullptr;
+      std::rethrow_exception(e);
+    }
+  }
+  void wait_slot(int slot) {
+    if (!prep_thread.joinable()) return;
+    std::unique_lock<std::mutex> lk(prep_m);
+    prep_cv.wait(lk, [&] { return prep_pending[slot] == 0; });
+    rethrow_prep_error();
+  }
+  void wait_prep_all() {
+    if (!prep_thread.joinable()) return;
+    std::unique_lock<std::mutex> lk(prep_m);
+    prep_cv.wait(lk, [&] { return prep_q.empty() && std::all_of(std::begin(prep_pending), std::end(prep_pending), [](int v) { return v == 0; }); });
+    rethrow_prep_error();
   }
 
   // Host scan preparation + H2D into a device slot (filter.cpp:154-165 for
   // the strided Gauss-Newton subset).
-  long long last_upload_bytes = 0;  // H2D bytes of the most recent set_slot
   void set_slot(int i, const smcl_cloud* scan) {
+    wait_slot(i);
+    set_slot_impl(i, scan, st);
+  }
+  void set_slot_impl(int i, const smcl_cloud* scan, cudaStream_t us) {
     const long long h2d0 = g_h2d.load();
+    ScanSlot& sl = slot_at(i);
     struct Tally {
       long long h0;
       long long& out;
       ~Tally() { out = g_h2d.load() - h0; }
-    } tally{h2d0, last_upload_bytes};
-    ScanSlot& sl = slot_at(i);
+    } tally{h2d0, sl.upload_bytes};
     const int S = static_cast<int>(scan ? scan->n : 0);
     sl.valid = true;
     if (S == 0) {
@@ -583,7 +679,7 @@ struct smcl_engine {
       sl.gn_alias = true;
       return;
     }
-    upload_scan(sl.full, scan->mu, scan->sigma, S);
+    upload_scan(sl.full, scan->mu, scan->sigma, S, us);
     const int stride = cfg.gn_scan_stride;
     if (stride > 1 && S > 2 * stride) {
       std::vector<double> mu, sg;
@@ -591,18 +687,19 @@ struct smcl_engine {
         mu.insert(mu.end(), scan->mu + 3 * q, scan->mu + 3 * q + 3);
         sg.insert(sg.end(), scan->sigma + 9 * q, scan->sigma + 9 * q + 9);
       }
-      upload_scan(sl.gn, mu.data(), sg.data(), static_cast<int>(mu.size() / 3));
+      upload_scan(sl.gn, mu.data(), sg.data(), static_cast<int>(mu.size() / 3), us);
       sl.gn_alias = false;
     } else {
       sl.gn_alias = true;
     }
+    CK(cudaStreamSynchronize(us));  // host staging vectors die here
   }
 
   // make_scan_cloud (filter.cpp:86-100) on the device into slot i: raw
   // points in, prepared Gaussian scan + fast records out, no host math on the
   // data path. Falls back to the host preparation only for inputs outside the
   // device path's envelope (voxel keys beyond 21 bits, k + 1 > 16).
-  void prepare_slot(int i, const double* points, int64_t n) {
+  void prepare_slot(int i, const double* points, int64_t n, cudaStream_t ps) {
     if (n < 0 || (n > 0 && !points)) throw std::invalid_argument("scan_prepare: null points");
     ScanSlot& sl = slot_at(i);
     const long long h2d0 = g_h2d.load();
@@ -622,7 +719,7 @@ struct smcl_engine {
       c.n = m;
       c.mu = mu.data();
       c.sigma = sg.data();
-      set_slot(i, &c);
+      set_slot_impl(i, &c, ps);
     };
     if (cfg.covariance_k + 1 > 16) return host_fallback();
     // SMCL_PREP_STATS=1: per-phase host-timed breakdown on stderr (diagnostics only).
@@ -630,12 +727,12 @@ struct smcl_engine {
     auto t_prev = std::chrono::steady_clock::now();
     auto lap = [&](const char* what) {
       if (!prep_stats) return;
-      sync();
+      CK(cudaStreamSynchronize(ps));
       const auto t = std::chrono::steady_clock::now();
       std::fprintf(stderr, "[prep] %s %.1f us\n", what, std::chrono::duration<double, std::micro>(t - t_prev).count());
       t_prev = t;
     };
-    raw_pts.upload(points, static_cast<size_t>(n) * 3, st);
+    raw_pts.upload(points, static_cast<size_t>(n) * 3, ps);
     if (!prep_work) prep_work.reset(scan_prep_create());
     lap("upload");
     const int ni = static_cast<int>(n);
@@ -648,14 +745,14 @@ struct smcl_engine {
       bool overflow = false;
       if (n <= 4096) {  // one block, leaf doubling on the device
         CK(scan_downsample_block(prep_work.get(), raw_pts.p, ni, cfg.scan_voxel_leaf, cfg.n_scan_max, down_pts.p, &m,
-                                 &overflow, b, st));
+                                 &overflow, b, ps));
         have_bounds = true;
       } else {
         double leaf = cfg.scan_voxel_leaf;
-        CK(scan_voxel_downsample(prep_work.get(), raw_pts.p, ni, leaf, down_pts.p, &m, &overflow, st));
+        CK(scan_voxel_downsample(prep_work.get(), raw_pts.p, ni, leaf, down_pts.p, &m, &overflow, ps));
         while (!overflow && m > cfg.n_scan_max) {
           leaf *= 2.0;
-          CK(scan_voxel_downsample(prep_work.get(), raw_pts.p, ni, leaf, down_pts.p, &m, &overflow, st));
+          CK(scan_voxel_downsample(prep_work.get(), raw_pts.p, ni, leaf, down_pts.p, &m, &overflow, ps));
         }
       }
       if (overflow) return host_fallback();
@@ -668,7 +765,7 @@ struct smcl_engine {
     // kNN grid (point_grid.cpp:10-49 over the downsampled points,
     // gaussian_cloud.cpp:24-32 cell size) — scalars on the host.
     if (!have_bounds) {
-      CK(scan_bounds(prep_work.get(), d_down, m, b, st));
+      CK(scan_bounds(prep_work.get(), d_down, m, b, ps));
       lap("bounds");
     }
     double ext[3];
@@ -688,10 +785,10 @@ struct smcl_engine {
     sd.sigma.ensure(static_cast<size_t>(m) * 9);
     sd.rec.ensure(2 * static_cast<size_t>(m));
     scan_l1.ensure(static_cast<size_t>(m));
-    CK(cudaMemcpyAsync(sd.mu.p, d_down, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(sd.mu.p, d_down, sizeof(double) * 3 * m, cudaMemcpyDeviceToDevice, ps));
     const double nv = cfg.sensor_noise_sigma * cfg.sensor_noise_sigma;
     CK(scan_knn_cov_records(prep_work.get(), sd.mu.p, m, k, cfg.epsilon_plane, nv > 0.0 ? nv : 0.0, b, cell, dims,
-                            sd.sigma.p, sd.rec.p, &sd.structured, &sd.l1max, st));
+                            sd.sigma.p, sd.rec.p, &sd.structured, &sd.l1max, ps));
     lap("knn+cov+records");
     const int stride = cfg.gn_scan_stride;
     if (stride > 1 && m > 2 * stride) {  // filter.cpp:154-165 strided GN subset
@@ -702,19 +799,20 @@ struct smcl_engine {
       g.sigma.ensure(static_cast<size_t>(ng) * 9);
       g.rec.ensure(2 * static_cast<size_t>(ng));
       scan_l1.ensure(static_cast<size_t>(std::max(m, ng)));
-      CK(scan_gather_stride(sd.mu.p, sd.sigma.p, ng, stride, g.mu.p, g.sigma.p, st));
-      CK(scan_records(prep_work.get(), g.mu.p, g.sigma.p, ng, g.rec.p, scan_l1.p, &g.structured, &g.l1max, st));
+      CK(scan_gather_stride(sd.mu.p, sd.sigma.p, ng, stride, g.mu.p, g.sigma.p, ps));
+      CK(scan_records(prep_work.get(), g.mu.p, g.sigma.p, ng, g.rec.p, scan_l1.p, &g.structured, &g.l1max, ps));
       sl.gn_alias = false;
     } else {
       sl.gn_alias = true;
     }
     sl.valid = true;
-    last_upload_bytes = g_h2d.load() - h2d0;
+    sl.upload_bytes = g_h2d.load() - h2d0;
   }
 
   void step_points(const double* points, int64_t n, const smcl_odom* odo, smcl_frame_result* out) {
     if (n_total == 0) throw std::logic_error("FilterEngine::step: not initialized");
-    prepare_slot(0, points, n);
+    wait_prep_all();
+    prepare_slot(0, points, n, st);
     step_slot(0, odo, out);
   }
 
@@ -1076,6 +1174,7 @@ struct smcl_engine {
   void step_slot(int slot_i, const smcl_odom* odo, smcl_frame_result* out) {
     if (n_total == 0) throw std::logic_error("FilterEngine::step: not initialized");
     if (!has_map) throw std::invalid_argument("engine has no map");
+    wait_slot(slot_i);
     ScanSlot& sl = slot_at(slot_i);
     if (!sl.valid) throw std::invalid_argument("scan slot not uploaded");
     profiling = true;
@@ -1185,7 +1284,7 @@ struct smcl_engine {
     prof.n_svgd_iters = cfg.n_svgd_iters;
     prof.kernel_launches = launch_count() - launches0;
     prof.d2h_bytes = g_d2h.load() - d2h0;
-    prof.h2d_bytes = last_upload_bytes;
+    prof.h2d_bytes = sl.upload_bytes;
     profiling = false;
     *out = r;
     ++frame;
@@ -1211,6 +1310,7 @@ smcl_engine* make_engine(const smcl_cloud* map, const smcl_config* cfg, int devi
     CK(cudaGetDevice(&e->device));
   }
   CK(cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking));
+  for (int q = 0; q < SMCL_MAX_SCAN_SLOTS; ++q) e->slots.push_back(std::make_unique<smcl_engine::ScanSlot>());
   e->k = cfg->k_neighbors;
   if (map) e->setup_map(map);
   return e.release();
@@ -1403,14 +1503,23 @@ int smcl_step_slot(smcl_engine* h, int slot, const smcl_odom* odo, smcl_frame_re
 int smcl_scan_prepare(smcl_engine* h, int slot, const double* points, int64_t n) {
   return guard([&] {
     use_dev(h);
-    h->prepare_slot(slot, points, n);
+    h->wait_prep_all();
+    h->prepare_slot(slot, points, n, h->st);
     h->sync();
+  });
+}
+
+int smcl_scan_prepare_async(smcl_engine* h, int slot, const double* points, int64_t n) {
+  return guard([&] {
+    use_dev(h);
+    h->prepare_async(slot, points, n);
   });
 }
 
 int smcl_scan_get(smcl_engine* h, int slot, double* mu_out, double* sigma_out, int64_t* n_out) {
   return guard([&] {
     use_dev(h);
+    h->wait_slot(slot);
     if (!n_out) throw std::invalid_argument("smcl_scan_get: null count");
     auto& sl = h->slot_at(slot);
     if (!sl.valid) throw std::invalid_argument("smcl_scan_get: empty slot");
@@ -1536,7 +1645,7 @@ int smcl_evaluate_all(smcl_engine* h, const smcl_cloud* scan, double* step_out, 
   return guard([&] {
     use_dev(h);
     if (!scan || scan->n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
-    h->upload_scan(h->scan_tmp, scan->mu, scan->sigma, static_cast<int>(scan->n));
+    h->upload_scan(h->scan_tmp, scan->mu, scan->sigma, static_cast<int>(scan->n), h->st);
     h->run_likelihood(true, h->scan_tmp);
     const size_t n = static_cast<size_t>(h->n_local);
     if (step_out) h->steps.download(step_out, n * 6, h->st);
@@ -1564,7 +1673,7 @@ int smcl_evaluate_likelihoods(smcl_engine* h, const smcl_cloud* scan, double* ll
   return guard([&] {
     use_dev(h);
     if (!scan || scan->n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
-    h->upload_scan(h->scan_tmp, scan->mu, scan->sigma, static_cast<int>(scan->n));
+    h->upload_scan(h->scan_tmp, scan->mu, scan->sigma, static_cast<int>(scan->n), h->st);
     h->run_likelihood(false, h->scan_tmp);
     const size_t n = static_cast<size_t>(h->n_local);
     if (ll_out) h->ll.download(ll_out, n, h->st);
