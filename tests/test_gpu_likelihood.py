@@ -144,3 +144,32 @@ def test_empty_scan_rejected(scene):
     e = _engine(mapc, parts, 0)
     with pytest.raises(ValueError):
         e.evaluate_all(GaussianCloud(np.zeros((0, 3)), np.zeros((0, 9))))
+
+
+@pytest.mark.parametrize("S", [1, 7, 33, 129, 1100])
+def test_fast_paths_ragged_scan_sizes(scene, S):
+    """Scan sizes off the kernels' step multiples (1 point, partial warps,
+    one past a step, beyond the lane kernel's two-CTA limit) and particles far
+    outside the map: n_matched exact, ll within tolerance, gating exact."""
+    mapc, scan, parts, om = scene
+    idx = np.arange(S) % len(scan)
+    sc = GaussianCloud(scan.mu[idx], scan.sigma[idx])
+    p = parts.copy() if hasattr(parts, "copy") else parts
+    poses = p.poses.copy()
+    poses[:50, 9] += 500.0  # every point out of bounds: n = 0, ll = -1e30
+    from paper_2404_16370_b200.abi import Particles
+    q = Particles.from_poses(poses, p.k)
+    for gn in (False, True):
+        e = _engine(mapc, q, 2)
+        if gn:
+            _, ll, nm = e.evaluate_all(sc)
+            _, ll2, nm2 = O.evaluate_all(om, sc.mu, sc.sigma, poses, config())
+        else:
+            ll, nm = e.evaluate_likelihoods(sc)
+            ll2, nm2 = O.evaluate_likelihoods(om, sc.mu, sc.sigma, poses, config())
+        assert np.array_equal(nm, nm2)
+        assert np.all(nm[:50] == 0) and np.all(ll[:50] == -1e30)
+        m = ll2 > -1e29
+        assert np.array_equal(ll[~m], ll2[~m])
+        if m.any():
+            assert np.all(np.abs(ll[m] - ll2[m]) <= TOL_LL * np.abs(ll2[m]))
