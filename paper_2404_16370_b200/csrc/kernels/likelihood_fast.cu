@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     // Pose in voxel units x = Rv mu + tv (Rv = R/res, tv = (t - o)/res) in
     // fp64 registers; Rf = R (fp32) for the body-frame algebra.
     float Rf[9];
+    bool huge;
     {
       const Pose P = poses[i];
 #pragma unroll
@@ -253,6 +254,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
       for (int a = 0; a < 3; ++a)
         if (lane == 9 + a) ws.pose_v[9 + a] = (P.t[a] - g.origin[a]) * g.inv_res;
+      // |x| <= max|Rv| |mu|_1 + max|tv|: below 2^40 the round-down floor is
+      // exact for every point; otherwise (or NaN) every point resolves.
+      double mr = 0.0, mt = 0.0;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) mr = fmax(mr, fabs(P.R[q]));
+#pragma unroll
+      for (int a = 0; a < 3; ++a) mt = fmax(mt, fabs(P.t[a] - g.origin[a]));
+      huge = !((mr * scan.mu_l1_max + mt) * g.inv_res < 1.0995e12);
     }
     __syncwarp();
     Acc acc;
@@ -276,7 +285,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         const double m0 = s_mu[3 * k], m1 = s_mu[3 * k + 1], m2 = s_mu[3 * k + 2];
         float fr[3];
         int ic[3];
-        bool amb = false, inb = true;
+        bool amb = huge, inb = true;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
           const double x = fma(Rv[ax * 3 + 2], m2, fma(Rv[ax * 3 + 1], m1, fma(Rv[ax * 3 + 0], m0, tv[ax])));
@@ -284,7 +293,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           const double f = x - (y - kMagic);
           ic[ax] = __double2loint(y);
           // |x| < 2^40 and f at least 1e-9 from a face (NaN fails both)
-          amb = amb || !(fabs(x) < 1.0995e12) || !(fabs(f - 0.5) < 0.5 - 1e-9);
+          amb = amb || !(fabs(f - 0.5) < 0.5 - 1e-9);
           inb = inb && static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz));
           fr[ax] = __double2float_rn(f);
         }
@@ -424,6 +433,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
   constexpr double kMagic = 6755399441055744.0;
   double Rv[9], tv[3];
   float Rf[9];
+  bool huge;
   {
     const Pose P = poses[active ? i : 0];
 #pragma unroll
@@ -433,6 +443,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) tv[a] = (P.t[a] - g.origin[a]) * g.inv_res;
+    double mr = 0.0, mt = 0.0;  // |x| bound, as in k_gicp_fast
+#pragma unroll
+    for (int q = 0; q < 9; ++q) mr = fmax(mr, fabs(P.R[q]));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) mt = fmax(mt, fabs(P.t[a] - g.origin[a]));
+    huge = !((mr * scan.mu_l1_max + mt) * g.inv_res < 1.0995e12);
   }
   double cost = 0.0;
   int nmatch = 0;
@@ -446,14 +462,14 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
       const double m0 = s_mu[3 * (k < S ? k : 0)], m1 = s_mu[3 * (k < S ? k : 0) + 1],
                    m2 = s_mu[3 * (k < S ? k : 0) + 2];
       int ic[3];
-      bool amb = false, inb = true;
+      bool amb = huge, inb = true;
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         const double x = fma(Rv[ax * 3 + 2], m2, fma(Rv[ax * 3 + 1], m1, fma(Rv[ax * 3 + 0], m0, tv[ax])));
         const double y = __dadd_rd(x, kMagic);
         const double f = x - (y - kMagic);
         ic[ax] = __double2loint(y);
-        amb = amb || !(fabs(x) < 1.0995e12) || !(fabs(f - 0.5) < 0.5 - 1e-9);
+        amb = amb || !(fabs(f - 0.5) < 0.5 - 1e-9);
         inb = inb && static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz));
         fr[u][ax] = __double2float_rn(f);
       }
