@@ -80,3 +80,25 @@ def test_c4_lsh_recall_at_20():
             hit += int(want) in have
     print(f"C4: recall@20 = {hit / total:.4f}")
     assert hit / total >= 0.9
+
+
+def test_outdoor_kidnap_1m_particles():
+    """The paper's outdoor kidnap experiment at its scale (BASELINE configs[3]):
+    1,048,576 particles on the builder-defined 280 x 200 x 30 m city map (NNF
+    0.2 m, 2.2e8 cells built on the device), a 20-frame scan blackout during
+    which the vehicle is teleported to another street. The filter (acceptance
+    calibration) must localize globally, lose the pose during the blackout
+    and re-localize right after it."""
+    sc = sim.scenario_preset("outdoor_kidnap", seed=7)
+    sc.sensor = sim.sensor_spec(n_azimuth=256, elevations_deg=list(np.linspace(-30.0, 30.0, 8)), max_range=60.0)
+    cfg = S.localization_config(11, n_particles=1 << 20)
+    cfg.nnf_resolution, cfg.nnf_max_query_dist, cfg.n_scan_max = 0.2, 2.0, 512
+    res = S.run_scenario(sc, cfg)
+    rep = res.report
+    terr = rep.terr
+    print(f"outdoor kidnap 1M: convergence={rep.convergence_frame} recovery={rep.recovery_frames} "
+          f"mean_total_ms={rep.mean_times['total_ms']:.2f} final terr={terr[-10:].max():.3f}")
+    assert 0 <= rep.convergence_frame < 20
+    assert rep.recovery_frames and rep.recovery_frames[0] >= 0
+    assert terr[-10:].max() < 0.5
+    assert terr[45] > 10.0  # the teleport inside the blackout really displaced the vehicle
