@@ -267,7 +267,7 @@ struct smcl_engine {
   // exchange points. Unsharded engines alias them to the local arrays.
   smcl_comm comm{};
   bool sharded = false;
-  DBuf<Pose> g_poses;
+  DBuf<Pose> g_poses, g_poses2;
   DBuf<double> g_steps, g_p, g_part, g_part2;
   DBuf<uint64_t> g_keys;
   DBuf<int32_t> g_flag, pos_list;
@@ -291,9 +291,17 @@ struct smcl_engine {
     if (comm.allgather(comm.ctx, send, recv, static_cast<uint64_t>(bytes), st) != 0)
       throw std::runtime_error("smcl_comm allgather failed");
   }
+  // Gathered poses of every particle, cached until this rank's poses change
+  // (predict, SVGD apply, init, set_particles): the neighbour pass and SVGD
+  // share one gather per step; a sharded reorder permutes it locally.
+  bool g_poses_valid = false;
+  void poses_changed() { g_poses_valid = false; }
   const Pose* all_poses() {  // current poses of every particle
     if (!sharded) return poses.p;
-    allgather(poses.p, g_poses.p, sizeof(Pose) * static_cast<size_t>(n_local));
+    if (!g_poses_valid) {
+      allgather(poses.p, g_poses.p, sizeof(Pose) * static_cast<size_t>(n_local));
+      g_poses_valid = true;
+    }
     return g_poses.p;
   }
   const double* all_steps() {
@@ -497,6 +505,7 @@ struct smcl_engine {
       g_rep.ensure(w);
       g_repid.ensure(w);
       if (cfg.reorder_particles) {
+        g_poses2.ensure(ug);
         g_lp.ensure(ug);
         g_id.ensure(ug);
         g_count.ensure(ug);
@@ -878,6 +887,7 @@ struct smcl_engine {
     if (!noiseless) covariance_sqrt(cov, pp.L);
     pp.frame_seed = frame_seed;
     launch_predict(poses.p, n_local, gbase, pp, st);
+    poses_changed();
     CK(cudaGetLastError());
   }
 
@@ -931,7 +941,7 @@ struct smcl_engine {
         // exchanges by all-gather (each rank receives the whole set, 272 B per
         // particle at K = 20); an all-to-all would move 1/world of that.
         const size_t nl = static_cast<size_t>(n_local), kk = static_cast<size_t>(k);
-        allgather(poses.p, g_poses.p, sizeof(Pose) * nl);
+        all_poses();  // old poses of every particle (cached gather)
         allgather(log_post.p, g_lp.p, sizeof(double) * nl);
         allgather(id.p, g_id.p, sizeof(int32_t) * nl);
         allgather(count.p, g_count.p, sizeof(int32_t) * nl);
@@ -939,6 +949,10 @@ struct smcl_engine {
         allgather(kval.p, g_kval.p, sizeof(float) * nl * kk);
         launch_reorder(member_of.p + gbase, new_of_old.p, n_local, k, g_poses.p, g_lp.p, g_id.p, g_idx.p, g_kval.p,
                        g_count.p, poses2.p, log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st);
+        // The new global pose order is a permutation of the gathered old one:
+        // every rank applies it locally instead of gathering again.
+        launch_permute_poses(member_of.p, n, g_poses.p, g_poses2.p, st);
+        g_poses.swap(g_poses2);
       } else {
         launch_reorder(member_of.p, new_of_old.p, n, k, poses.p, log_post.p, id.p, idx.p, kval.p, count.p, poses2.p,
                        log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st);
@@ -951,6 +965,7 @@ struct smcl_engine {
       count.swap(count2);
       members = iota.p;
       steps_valid = phis_valid = ll_valid = false;  // storage order changed
+      g_poses_valid = sharded;  // sharded: g_poses already holds the permuted global array
     }
     const Pose* poses_all = all_poses();  // after the reorder: candidates read the current storage
     if (profiling) mark(E_REORDER);
@@ -1029,6 +1044,7 @@ struct smcl_engine {
     if (fused_apply) {
       launch_svgd(pa, sa, n_local, gbase, idx.p, count.p, k, sp, nullptr, poses2.p, st);
       poses.swap(poses2);
+      poses_changed();
     } else {
       launch_svgd(pa, sa, n_local, gbase, idx.p, count.p, k, sp, phis.p, nullptr, st);
       phis_valid = true;
@@ -1167,6 +1183,7 @@ struct smcl_engine {
     ip.log_post0 = -std::log(static_cast<double>(n));
     ip.full_rotation = full_rotation ? 1 : 0;
     launch_init_uniform(poses.p, log_post.p, id.p, idx.p, kval.p, count.p, n_local, gbase, k, ip, st);
+    poses_changed();
     CK(cudaGetLastError());
     sync();
   }
@@ -1596,6 +1613,7 @@ int smcl_set_particles(smcl_engine* h, const smcl_particles_view* v) {
     std::vector<Pose> ps(n);
     for (size_t i = 0; i < n; ++i) ps[i] = load_pose(v->poses + 12 * i);
     h->poses.upload(ps.data(), n, h->st);
+    h->poses_changed();
     h->log_post.upload(v->log_post, n, h->st);
     h->id.upload(v->id, n, h->st);
     h->idx.upload(v->idx, n * k, h->st);
@@ -1707,6 +1725,7 @@ int smcl_apply_updates(smcl_engine* h, const double* phis) {
     }
     if (!h->phis_valid) throw std::logic_error("apply_updates: one phi per particle required");
     launch_apply(h->poses.p, h->phis.p, h->n_local, h->st);
+    h->poses_changed();
     CK(cudaGetLastError());
     h->sync();
   });

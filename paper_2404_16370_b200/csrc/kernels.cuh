@@ -62,6 +62,7 @@ void sort_keys(const uint64_t* in, uint64_t* out, int64_t n, int end_bit, void* 
 void launch_members(const uint64_t* skeys, int64_t n, uint64_t idx_mask, int shift, int32_t* member_of, int32_t* head,
                     cudaStream_t st);
 void inclusive_sum_i32(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t st);
+void launch_permute_poses(const int32_t* perm, int64_t n, const Pose* src, Pose* dst, cudaStream_t st);
 void launch_inverse_perm(const int32_t* member_of, int64_t n, int32_t* new_of_old, cudaStream_t st);
 void launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_t n, int k, const Pose* poses,
                     const double* lp, const int32_t* id, const int32_t* idx, const float* kval, const int32_t* count,

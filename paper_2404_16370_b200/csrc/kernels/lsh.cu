@@ -148,6 +148,17 @@ __global__ void __launch_bounds__(128) k_reorder_k(const int32_t* __restrict__ o
   }
 }
 
+// dst[p] = src[perm[p]] for whole 96-byte poses (128-bit copies).
+__global__ void k_permute_poses(const int32_t* __restrict__ perm, int64_t n, const Pose* __restrict__ src,
+                                Pose* __restrict__ dst) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const double2* a = reinterpret_cast<const double2*>(src + perm[p]);
+  double2* b = reinterpret_cast<double2*>(dst + p);
+#pragma unroll
+  for (int v = 0; v < 6; ++v) b[v] = __ldg(a + v);
+}
+
 __global__ void k_segments(const int32_t* __restrict__ head, const int32_t* __restrict__ seg_id, int64_t n,
                            int32_t* __restrict__ seg_start) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -572,6 +583,11 @@ void launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_
   if (n > 0)
     k_reorder<<<blocks_for(n, 128), 128, 0, st>>>(old_of_new, new_of_old, n, k, poses, lp, id, idx, kval, count, poses2,
                                                   lp2, id2, idx2, kval2, count2);
+}
+
+void launch_permute_poses(const int32_t* perm, int64_t n, const Pose* src, Pose* dst, cudaStream_t st) {
+  count_launch();
+  if (n > 0) k_permute_poses<<<blocks_for(n, 128), 128, 0, st>>>(perm, n, src, dst);
 }
 
 void launch_segments(const int32_t* head, const int32_t* seg_id, int64_t n, int32_t* seg_start, cudaStream_t st) {
