@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SMCL_ABI_VERSION 1
+#define SMCL_ABI_VERSION 2
 #define SMCL_MAX_HIST 1026
 
 enum {
@@ -136,11 +136,20 @@ int smcl_create(const smcl_cloud* map, const smcl_config* cfg, int device, smcl_
  * engine's device); `recv` (device, world*bytes) receives the contributions in
  * rank order. `stream` is the engine's cudaStream_t: the callee must order its
  * work after everything already enqueued on it and before anything enqueued
- * after the call returns (e.g. NCCL on that stream). Returns 0 on success. */
+ * after the call returns (e.g. NCCL on that stream). Returns 0 on success.
+ * alltoallv (optional, may be NULL): rank r sends send_bytes[d] bytes to
+ * every rank d (chunks packed in rank order at `send`) and receives
+ * recv_bytes[s] bytes from every rank s (packed in rank order at `recv`);
+ * send_bytes / recv_bytes are host arrays of `world` entries, same stream
+ * contract. A sharded engine with reorder_particles = 1 migrates particle
+ * state with it (1/world of the all-gather volume); without it the engine
+ * falls back to all-gathering the state. */
 typedef struct smcl_comm {
   void* ctx;
   int32_t rank, world;
   int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes, void* stream);
+  int (*alltoallv)(void* ctx, const void* send, const uint64_t* send_bytes, void* recv, const uint64_t* recv_bytes,
+                   void* stream);
 } smcl_comm;
 
 /* Sharded engine: this rank owns the particles with global indices

@@ -179,11 +179,14 @@ class SmclSensorSpec(C.Structure):
 
 # int (*allgather)(void* ctx, const void* send, void* recv, uint64_t bytes, void* stream)
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p,
+                           C.POINTER(C.c_uint64), C.c_void_p)
 
 
 class SmclComm(C.Structure):
     """smcl_comm: the collective backend of a sharded engine."""
-    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32), ("allgather", ALLGATHER_FN)]
+    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32), ("allgather", ALLGATHER_FN),
+                ("alltoallv", ALLTOALLV_FN)]
 
 
 def f64ptr(a):

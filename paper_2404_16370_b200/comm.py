@@ -1,8 +1,9 @@
 """Collective backends for sharded engines.
 
 A sharded engine (``smcl_create_sharded``) owns the particles with global
-indices ``[rank*N/world, (rank+1)*N/world)`` and calls ONE collective, an
-all-gather on its own CUDA stream, at the exchange points of
+indices ``[rank*N/world, (rank+1)*N/world)`` and calls an all-gather on its
+own CUDA stream (plus, with ``reorder_particles``, an alltoallv of the
+particle records that change shard) at the exchange points of
 ``FilterEngine::step`` (filter.cpp:118-213): LSH keys before the global sort,
 poses/steps before each SVGD iteration, per-chunk partial sums and argmax
 partials of the posterior reductions, the per-round probabilities of the
@@ -13,7 +14,8 @@ Backends:
 * ``LoopbackComms`` — in-process, ``world`` engines driven by ``world`` host
   threads (one device or several); implemented in C (engine.cu).
 * ``NcclComm`` — native NCCL (``smcl_comm_nccl_create``): the engine calls
-  ``ncclAllGather`` on its own stream, no Python on the data path. The
+  ``ncclAllGather`` / grouped ``ncclSend``+``ncclRecv`` on its own stream,
+  no Python on the data path. The
   128-byte unique id travels over any host channel (``NcclComm.from_torch``
   uses the torch.distributed group bench.py already has).
 * ``TorchComm`` — ``torch.distributed`` over NCCL (device buffers, one process
@@ -24,7 +26,7 @@ torch is plumbing here: it is imported lazily and only by ``TorchComm``.
 import ctypes as C
 
 from . import _lib
-from .abi import ALLGATHER_FN, SmclComm
+from .abi import ALLGATHER_FN, ALLTOALLV_FN, SmclComm
 
 SHARD_ALIGN = 4096  # reduce.hpp chunk: no posterior reduction chunk straddles two shards
 
@@ -122,8 +124,9 @@ class TorchComm:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.error = None
-        self._fn = ALLGATHER_FN(self._allgather)  # keep the trampoline alive
-        self.struct = SmclComm(None, self.rank, self.world, self._fn)
+        self._fn = ALLGATHER_FN(self._allgather)  # keep the trampolines alive
+        self._fn_a2a = ALLTOALLV_FN(self._alltoallv)
+        self.struct = SmclComm(None, self.rank, self.world, self._fn, self._fn_a2a)
 
     def _allgather(self, ctx, send, recv, nbytes, stream):
         try:
@@ -144,5 +147,32 @@ class TorchComm:
                 dist.all_gather(list(r.split(nbytes)), s.clone(), group=self.group)
             return 0
         except Exception as e:  # surfaced by the engine as an SMCL error
+            self.error = e
+            return 1
+
+    def _alltoallv(self, ctx, send, send_bytes, recv, recv_bytes, stream):
+        try:
+            import torch
+            import torch.distributed as dist
+            sb = [int(send_bytes[i]) for i in range(self.world)]
+            rb = [int(recv_bytes[i]) for i in range(self.world)]
+            ns, nr = sum(sb), sum(rb)
+            if self.device:
+                dev = torch.device("cuda", torch.cuda.current_device())
+                s = torch.as_tensor(_DeviceBytes(send, ns), device=dev) if ns else torch.empty(0, dtype=torch.uint8,
+                                                                                                device=dev)
+                r = torch.as_tensor(_DeviceBytes(recv, nr), device=dev) if nr else torch.empty(0, dtype=torch.uint8,
+                                                                                                device=dev)
+                with torch.cuda.stream(torch.cuda.ExternalStream(int(stream or 0), device=dev)):
+                    dist.all_to_all_single(r, s, output_split_sizes=rb, input_split_sizes=sb, group=self.group)
+            else:
+                s = (torch.frombuffer((C.c_uint8 * ns).from_address(send), dtype=torch.uint8).clone() if ns
+                     else torch.empty(0, dtype=torch.uint8))
+                r = torch.empty(nr, dtype=torch.uint8)
+                dist.all_to_all_single(r, s, output_split_sizes=rb, input_split_sizes=sb, group=self.group)
+                if nr:
+                    C.memmove(recv, r.data_ptr(), nr)
+            return 0
+        except Exception as e:
             self.error = e
             return 1

@@ -276,6 +276,11 @@ struct smcl_engine {
   DBuf<double> g_lp;
   DBuf<int32_t> g_id, g_idx, g_count;
   DBuf<float> g_kval;
+  // ... or, when the communicator has alltoallv, only the migrating records
+  // (count matrix + per-destination cursors, packed send and received records).
+  DBuf<unsigned int> mig_mat;
+  DBuf<unsigned char> mig_send, mig_recv;
+  std::vector<unsigned int> mig_host;
   DBuf<unsigned long long> g_counts;
   DBuf<double> g_argv;
   DBuf<long long> g_argi;
@@ -290,6 +295,31 @@ struct smcl_engine {
     }
     if (comm.allgather(comm.ctx, send, recv, static_cast<uint64_t>(bytes), st) != 0)
       throw std::runtime_error("smcl_comm allgather failed");
+  }
+  void alltoallv(const void* send, const uint64_t* send_bytes, void* recv, const uint64_t* recv_bytes) {
+    if (comm.alltoallv(comm.ctx, send, send_bytes, recv, recv_bytes, st) != 0)
+      throw std::runtime_error("smcl_comm alltoallv failed");
+  }
+  // Sharded reorder, non-pose state: count matrix from the replicated
+  // member_of (one small device->host read), pack this rank's outgoing
+  // records, alltoallv, scatter the received ones to their new positions.
+  void migrate_reorder() {
+    const size_t w = static_cast<size_t>(world), rec = migrate_record_bytes(k);
+    CK(cudaMemsetAsync(mig_mat.p, 0, sizeof(unsigned int) * (w * w + w), st));
+    launch_migrate_counts(member_of.p, n_total, n_local, world, mig_mat.p, st);
+    mig_host.resize(w * w);
+    CK(cudaMemcpyAsync(mig_host.data(), mig_mat.p, sizeof(unsigned int) * w * w, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<uint64_t> sb(w), rb(w);
+    for (size_t d = 0; d < w; ++d) {
+      sb[d] = rec * mig_host[d * w + static_cast<size_t>(rank)];
+      rb[d] = rec * mig_host[static_cast<size_t>(rank) * w + d];
+    }
+    launch_migrate_pack(member_of.p, n_total, n_local, world, rank, mig_mat.p, mig_mat.p + w * w, log_post.p, id.p,
+                        count.p, idx.p, kval.p, k, mig_send.p, st);
+    alltoallv(mig_send.p, sb.data(), mig_recv.p, rb.data());
+    launch_migrate_unpack(mig_recv.p, n_local, gbase, k, new_of_old.p, log_post2.p, id2.p, count2.p, idx2.p, kval2.p,
+                          st);
   }
   // Gathered poses of every particle, cached until this rank's poses change
   // (predict, SVGD apply, init, set_particles): the neighbour pass and SVGD
@@ -506,11 +536,17 @@ struct smcl_engine {
       g_repid.ensure(w);
       if (cfg.reorder_particles) {
         g_poses2.ensure(ug);
-        g_lp.ensure(ug);
-        g_id.ensure(ug);
-        g_count.ensure(ug);
-        g_idx.ensure(ug * static_cast<size_t>(kk));
-        g_kval.ensure(ug * static_cast<size_t>(kk));
+        if (comm.alltoallv) {
+          mig_mat.ensure(w * w + w);
+          mig_send.ensure(un * migrate_record_bytes(kk));
+          mig_recv.ensure(un * migrate_record_bytes(kk));
+        } else {
+          g_lp.ensure(ug);
+          g_id.ensure(ug);
+          g_count.ensure(ug);
+          g_idx.ensure(ug * static_cast<size_t>(kk));
+          g_kval.ensure(ug * static_cast<size_t>(kk));
+        }
       }
     }
     poses.ensure(un);
@@ -937,22 +973,28 @@ struct smcl_engine {
       if (sharded) {
         // Cross-shard permutation (particle_set.cpp:7-47 over the global
         // order): every rank owns the new positions [gbase, gbase + n_local)
-        // and pulls their old state from whichever shard held it. v1
-        // exchanges by all-gather (each rank receives the whole set, 272 B per
-        // particle at K = 20); an all-to-all would move 1/world of that.
+        // and pulls their old state from whichever shard held it. Poses: the
+        // new global order is a permutation of the gathered old one, applied
+        // locally by every rank (no second gather). The rest of the state
+        // (16 + 8K B per particle) moves by alltoallv, only the particles
+        // that change shard; without alltoallv, by all-gather of everything.
         const size_t nl = static_cast<size_t>(n_local), kk = static_cast<size_t>(k);
         all_poses();  // old poses of every particle (cached gather)
-        allgather(log_post.p, g_lp.p, sizeof(double) * nl);
-        allgather(id.p, g_id.p, sizeof(int32_t) * nl);
-        allgather(count.p, g_count.p, sizeof(int32_t) * nl);
-        allgather(idx.p, g_idx.p, sizeof(int32_t) * nl * kk);
-        allgather(kval.p, g_kval.p, sizeof(float) * nl * kk);
-        launch_reorder(member_of.p + gbase, new_of_old.p, n_local, k, g_poses.p, g_lp.p, g_id.p, g_idx.p, g_kval.p,
-                       g_count.p, poses2.p, log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st);
-        // The new global pose order is a permutation of the gathered old one:
-        // every rank applies it locally instead of gathering again.
+        if (comm.alltoallv) {
+          migrate_reorder();
+        } else {
+          allgather(log_post.p, g_lp.p, sizeof(double) * nl);
+          allgather(id.p, g_id.p, sizeof(int32_t) * nl);
+          allgather(count.p, g_count.p, sizeof(int32_t) * nl);
+          allgather(idx.p, g_idx.p, sizeof(int32_t) * nl * kk);
+          allgather(kval.p, g_kval.p, sizeof(float) * nl * kk);
+          launch_reorder(member_of.p + gbase, new_of_old.p, n_local, k, g_poses.p, g_lp.p, g_id.p, g_idx.p, g_kval.p,
+                         g_count.p, poses2.p, log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st);
+        }
         launch_permute_poses(member_of.p, n, g_poses.p, g_poses2.p, st);
         g_poses.swap(g_poses2);
+        if (comm.alltoallv)
+          CK(cudaMemcpyAsync(poses2.p, g_poses.p + gbase, sizeof(Pose) * nl, cudaMemcpyDeviceToDevice, st));
       } else {
         launch_reorder(member_of.p, new_of_old.p, n, k, poses.p, log_post.p, id.p, idx.p, kval.p, count.p, poses2.p,
                        log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st);
@@ -1412,6 +1454,7 @@ struct LoopShared {
   int arrived = 0;
   long long generation = 0;
   std::vector<const void*> send;
+  std::vector<std::vector<uint64_t>> send_bytes;  // alltoallv: per rank, bytes to each destination
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
     const long long gen = generation;
@@ -1448,6 +1491,35 @@ int loopback_allgather(void* ctx, const void* send, void* recv, uint64_t bytes, 
   sh.barrier();  // no rank reuses its send buffer before every rank has read it
   return 0;
 }
+// alltoallv: every rank posts its packed send buffer and per-destination
+// sizes; each rank then copies the chunk addressed to it out of every peer's
+// buffer (the chunk's offset = the peer's bytes to lower ranks).
+int loopback_alltoallv(void* ctx, const void* send, const uint64_t* send_bytes, void* recv, const uint64_t* recv_bytes,
+                       void* stream) {
+  auto* lr = static_cast<LoopRank*>(ctx);
+  LoopShared& sh = *lr->shared;
+  auto st = static_cast<cudaStream_t>(stream);
+  const size_t w = static_cast<size_t>(sh.world), me = static_cast<size_t>(lr->rank);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return 1;
+  sh.send[me] = send;
+  sh.send_bytes[me].assign(send_bytes, send_bytes + w);
+  sh.barrier();
+  int rc = 0;
+  uint64_t roff = 0;
+  for (size_t s = 0; s < w && rc == 0; ++s) {
+    const std::vector<uint64_t>& sb = sh.send_bytes[s];
+    uint64_t soff = 0;
+    for (size_t d = 0; d < me; ++d) soff += sb[d];
+    if (sb[me] != recv_bytes[s]) rc = 1;  // sender and receiver disagree on the chunk size
+    else if (sb[me] && cudaMemcpyAsync(static_cast<char*>(recv) + roff, static_cast<const char*>(sh.send[s]) + soff,
+                                       sb[me], cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      rc = 1;
+    roff += recv_bytes[s];
+  }
+  if (cudaStreamSynchronize(st) != cudaSuccess) rc = 1;
+  sh.barrier();  // always reached by every rank: no deadlock on a failed rank
+  return rc;
+}
 }  // namespace
 
 int smcl_comm_loopback_create(int32_t world, smcl_comm* comms) {
@@ -1456,11 +1528,13 @@ int smcl_comm_loopback_create(int32_t world, smcl_comm* comms) {
     auto sh = std::make_shared<LoopShared>();
     sh->world = world;
     sh->send.assign(static_cast<size_t>(world), nullptr);
+    sh->send_bytes.assign(static_cast<size_t>(world), {});
     for (int r = 0; r < world; ++r) {
       comms[r].ctx = new LoopRank{sh, r};
       comms[r].rank = r;
       comms[r].world = world;
       comms[r].allgather = loopback_allgather;
+      comms[r].alltoallv = loopback_alltoallv;
     }
   });
 }

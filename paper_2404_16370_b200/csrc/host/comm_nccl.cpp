@@ -33,6 +33,10 @@ struct NcclApi {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, int, ncclComm_t, void*) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, int, int, ncclComm_t, void*) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, int, int, ncclComm_t, void*) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -50,6 +54,10 @@ NcclApi& api() {
     a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(a.h, "ncclAllGather"));
     a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(a.h, "ncclCommDestroy"));
     a.getErrorString = reinterpret_cast<decltype(a.getErrorString)>(dlsym(a.h, "ncclGetErrorString"));
+    a.send = reinterpret_cast<decltype(a.send)>(dlsym(a.h, "ncclSend"));  // NCCL >= 2.7
+    a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(a.h, "ncclRecv"));
+    a.groupStart = reinterpret_cast<decltype(a.groupStart)>(dlsym(a.h, "ncclGroupStart"));
+    a.groupEnd = reinterpret_cast<decltype(a.groupEnd)>(dlsym(a.h, "ncclGroupEnd"));
   });
   if (!a.getUniqueId || !a.commInitRank || !a.allGather || !a.commDestroy)
     throw std::runtime_error("NCCL (libnccl.so.2) not available");
@@ -63,6 +71,7 @@ std::string nccl_err(ncclResult_t r) {
 
 struct NcclCtx {
   ncclComm_t comm = nullptr;
+  int world = 1;
 };
 
 // smcl_comm::allgather: `bytes` from every rank, rank-ordered into recv.
@@ -70,6 +79,28 @@ int nccl_allgather(void* ctx, const void* send, void* recv, uint64_t bytes, void
   auto* c = static_cast<NcclCtx*>(ctx);
   if (bytes == 0) return 0;
   return api().allGather(send, recv, static_cast<size_t>(bytes), kNcclUint8, c->comm, stream) == 0 ? 0 : 1;
+}
+
+// smcl_comm::alltoallv as one NCCL group of point-to-point sends and receives
+// (chunks packed in rank order on both sides).
+int nccl_alltoallv(void* ctx, const void* send, const uint64_t* send_bytes, void* recv, const uint64_t* recv_bytes,
+                   void* stream) {
+  auto* c = static_cast<NcclCtx*>(ctx);
+  const NcclApi& a = api();
+  const int world = c->world;
+  if (a.groupStart() != 0) return 1;
+  int rc = 0;
+  uint64_t so = 0, ro = 0;
+  for (int p = 0; p < world; ++p) {
+    if (send_bytes[p] && a.send(static_cast<const char*>(send) + so, send_bytes[p], kNcclUint8, p, c->comm, stream))
+      rc = 1;
+    if (recv_bytes[p] && a.recv(static_cast<char*>(recv) + ro, recv_bytes[p], kNcclUint8, p, c->comm, stream))
+      rc = 1;
+    so += send_bytes[p];
+    ro += recv_bytes[p];
+  }
+  if (a.groupEnd() != 0) rc = 1;
+  return rc;
 }
 
 template <class F>
@@ -105,6 +136,7 @@ int smcl_comm_nccl_create(const uint8_t id[128], int32_t rank, int32_t world, sm
     ncclUniqueId u;
     std::memcpy(u.internal, id, sizeof(u.internal));
     auto* c = new NcclCtx();
+    c->world = world;
     const ncclResult_t r = api().commInitRank(&c->comm, world, u, rank);  // on the current CUDA device
     if (r != 0) {
       delete c;
@@ -114,6 +146,8 @@ int smcl_comm_nccl_create(const uint8_t id[128], int32_t rank, int32_t world, sm
     out->rank = rank;
     out->world = world;
     out->allgather = nccl_allgather;
+    const NcclApi& a = api();
+    out->alltoallv = (a.send && a.recv && a.groupStart && a.groupEnd) ? nccl_alltoallv : nullptr;
   });
 }
 

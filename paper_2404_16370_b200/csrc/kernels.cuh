@@ -63,6 +63,14 @@ void launch_members(const uint64_t* skeys, int64_t n, uint64_t idx_mask, int shi
                     cudaStream_t st);
 void inclusive_sum_i32(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t st);
 void launch_permute_poses(const int32_t* perm, int64_t n, const Pose* src, Pose* dst, cudaStream_t st);
+size_t migrate_record_bytes(int k);
+void launch_migrate_counts(const int32_t* member_of, int64_t n, int64_t nl, int world, unsigned int* mat,
+                           cudaStream_t st);
+void launch_migrate_pack(const int32_t* member_of, int64_t n, int64_t nl, int world, int rank, const unsigned int* mat,
+                         unsigned int* cursor, const double* lp, const int32_t* id, const int32_t* count,
+                         const int32_t* idx, const float* kval, int k, void* send, cudaStream_t st);
+void launch_migrate_unpack(const void* recv, int64_t nl, int64_t gbase, int k, const int32_t* new_of_old, double* lp2,
+                           int32_t* id2, int32_t* count2, int32_t* idx2, float* kval2, cudaStream_t st);
 void launch_inverse_perm(const int32_t* member_of, int64_t n, int32_t* new_of_old, cudaStream_t st);
 void launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_t n, int k, const Pose* poses,
                     const double* lp, const int32_t* id, const int32_t* idx, const float* kval, const int32_t* count,

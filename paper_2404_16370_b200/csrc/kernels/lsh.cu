@@ -159,6 +159,109 @@ __global__ void k_permute_poses(const int32_t* __restrict__ perm, int64_t n, con
   for (int v = 0; v < 6; ++v) b[v] = __ldg(a + v);
 }
 
+// ---- Cross-shard reorder by all-to-all (the permutation
+// of particle_set.cpp:7-47 over the global sorted order). New position p
+// belongs to shard p / n_local; its old state lives on shard member_of[p] /
+// n_local. Every rank holds the global member_of, so the shard-to-shard count
+// matrix is computed locally (no count exchange) and only the non-pose state
+// moves, one record per migrating particle (poses are permuted from the
+// gathered pose array instead).
+struct MigHeader {
+  double lp;
+  int32_t id, count, pnew, pad;
+};
+static_assert(sizeof(MigHeader) == 24, "record header");
+
+// mat[d * world + s] = number of new positions on shard d whose old state is on shard s.
+__global__ void k_migrate_counts(const int32_t* __restrict__ member_of, int64_t n, int64_t nl, int world,
+                                 unsigned int* __restrict__ mat) {
+  extern __shared__ unsigned int hist[];
+  const int cells = world * world;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int d = static_cast<int>(p / nl), src = static_cast<int>(member_of[p] / nl);
+    atomicAdd(&hist[d * world + src], 1u);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < cells; c += blockDim.x)
+    if (hist[c]) atomicAdd(&mat[c], hist[c]);
+}
+
+// Packs the records this rank sends, grouped by destination shard in rank
+// order (offsets from the count matrix); order inside a destination's chunk
+// is immaterial because each record carries its new position. Blocks of 256
+// never straddle two destinations (n_local is a multiple of 4096).
+__global__ void __launch_bounds__(256) k_migrate_pack(const int32_t* __restrict__ member_of, int64_t n, int64_t nl,
+                                                      int world, int rank, const unsigned int* __restrict__ mat,
+                                                      unsigned int* __restrict__ cursor, const double* __restrict__ lp,
+                                                      const int32_t* __restrict__ id,
+                                                      const int32_t* __restrict__ count,
+                                                      const int32_t* __restrict__ idx,
+                                                      const float* __restrict__ kval, int k,
+                                                      unsigned char* __restrict__ send) {
+  __shared__ unsigned int warp_n[8];
+  __shared__ unsigned int base;
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+  const int64_t o = p < n ? static_cast<int64_t>(member_of[p]) - static_cast<int64_t>(rank) * nl : -1;
+  const bool mine = p < n && o >= 0 && o < nl;
+  const unsigned int bal = __ballot_sync(0xffffffffu, mine);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) warp_n[w] = __popc(bal);
+  __syncthreads();
+  const int d = static_cast<int>((static_cast<int64_t>(blockIdx.x) * 256) / nl);
+  if (threadIdx.x == 0) {
+    unsigned int tot = 0;
+    for (int i = 0; i < 8; ++i) tot += warp_n[i];
+    unsigned int off = 0;  // records this rank sends to shards before d
+    for (int e = 0; e < d; ++e) off += mat[e * world + rank];
+    base = off + (tot ? atomicAdd(&cursor[d], tot) : 0u);
+  }
+  __syncthreads();
+  if (!mine) return;
+  unsigned int pos = base + __popc(bal & ((1u << lane) - 1u));
+  for (int i = 0; i < w; ++i) pos += warp_n[i];
+  const size_t rec = sizeof(MigHeader) + 8 * static_cast<size_t>(k);
+  unsigned char* r = send + static_cast<size_t>(pos) * rec;
+  MigHeader h;
+  h.lp = lp[o];
+  h.id = id[o];
+  h.count = count[o];
+  h.pnew = static_cast<int32_t>(p);
+  h.pad = 0;
+  *reinterpret_cast<MigHeader*>(r) = h;
+  int32_t* ri = reinterpret_cast<int32_t*>(r + sizeof(MigHeader));
+  float* rk = reinterpret_cast<float*>(ri + k);
+  for (int s = 0; s < k; ++s) {
+    ri[s] = idx[o * k + s];
+    rk[s] = kval[o * k + s];
+  }
+}
+
+// Scatters the received records to their new local positions, remapping the
+// neighbour ids to new global indices (particle_set.cpp:17-19 as k_reorder).
+__global__ void k_migrate_unpack(const unsigned char* __restrict__ recv, int64_t nl, int64_t gbase, int k,
+                                 const int32_t* __restrict__ new_of_old, double* __restrict__ lp2,
+                                 int32_t* __restrict__ id2, int32_t* __restrict__ count2,
+                                 int32_t* __restrict__ idx2, float* __restrict__ kval2) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= nl) return;
+  const size_t rec = sizeof(MigHeader) + 8 * static_cast<size_t>(k);
+  const unsigned char* r = recv + static_cast<size_t>(j) * rec;
+  const MigHeader h = *reinterpret_cast<const MigHeader*>(r);
+  const int32_t* ri = reinterpret_cast<const int32_t*>(r + sizeof(MigHeader));
+  const float* rk = reinterpret_cast<const float*>(ri + k);
+  const int64_t p = h.pnew - gbase;
+  lp2[p] = h.lp;
+  id2[p] = h.id;
+  count2[p] = h.count;
+  for (int s = 0; s < k; ++s) {
+    idx2[p * k + s] = s < h.count ? new_of_old[ri[s]] : 0;
+    kval2[p * k + s] = s < h.count ? rk[s] : 0.0f;
+  }
+}
+
 __global__ void k_segments(const int32_t* __restrict__ head, const int32_t* __restrict__ seg_id, int64_t n,
                            int32_t* __restrict__ seg_start) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -588,6 +691,33 @@ void launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_
 void launch_permute_poses(const int32_t* perm, int64_t n, const Pose* src, Pose* dst, cudaStream_t st) {
   count_launch();
   if (n > 0) k_permute_poses<<<blocks_for(n, 128), 128, 0, st>>>(perm, n, src, dst);
+}
+
+size_t migrate_record_bytes(int k) { return sizeof(MigHeader) + 8 * static_cast<size_t>(k); }
+
+void launch_migrate_counts(const int32_t* member_of, int64_t n, int64_t nl, int world, unsigned int* mat,
+                           cudaStream_t st) {
+  count_launch();
+  const int blocks = static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 4 * 148));
+  if (n > 0)
+    k_migrate_counts<<<blocks, 256, sizeof(unsigned int) * world * world, st>>>(member_of, n, nl, world, mat);
+}
+
+void launch_migrate_pack(const int32_t* member_of, int64_t n, int64_t nl, int world, int rank, const unsigned int* mat,
+                         unsigned int* cursor, const double* lp, const int32_t* id, const int32_t* count,
+                         const int32_t* idx, const float* kval, int k, void* send, cudaStream_t st) {
+  count_launch();
+  if (n > 0)
+    k_migrate_pack<<<blocks_for(n, 256), 256, 0, st>>>(member_of, n, nl, world, rank, mat, cursor, lp, id, count, idx,
+                                                       kval, k, static_cast<unsigned char*>(send));
+}
+
+void launch_migrate_unpack(const void* recv, int64_t nl, int64_t gbase, int k, const int32_t* new_of_old, double* lp2,
+                           int32_t* id2, int32_t* count2, int32_t* idx2, float* kval2, cudaStream_t st) {
+  count_launch();
+  if (nl > 0)
+    k_migrate_unpack<<<blocks_for(nl, 128), 128, 0, st>>>(static_cast<const unsigned char*>(recv), nl, gbase, k,
+                                                          new_of_old, lp2, id2, count2, idx2, kval2);
 }
 
 void launch_segments(const int32_t* head, const int32_t* seg_id, int64_t n, int32_t* seg_start, cudaStream_t st) {

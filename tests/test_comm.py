@@ -10,7 +10,7 @@ import pytest
 import torch.multiprocessing as mp
 
 from paper_2404_16370_b200 import comm as CM
-from paper_2404_16370_b200.abi import ALLGATHER_FN
+from paper_2404_16370_b200.abi import ALLGATHER_FN, ALLTOALLV_FN
 
 
 def test_shard_range_contiguous_and_aligned():
@@ -28,7 +28,7 @@ def test_loopback_comms_fill_rank_and_world():
     c = CM.LoopbackComms(3)
     assert [c[r].rank for r in range(3)] == [0, 1, 2]
     assert all(c[r].world == 3 and c[r].ctx for r in range(3))
-    assert all(bool(c[r].allgather) for r in range(3))
+    assert all(bool(c[r].allgather) and bool(c[r].alltoallv) for r in range(3))
     c.close()
     c.close()  # idempotent
 
@@ -58,6 +58,16 @@ def _worker(rank, world, port, out):
                 exp = (np.arange(nbytes, dtype=np.uint64) * 7 + r * 1000003).astype(np.uint8)
                 assert np.array_equal(recv[r * nbytes:(r + 1) * nbytes], exp)
         assert fn(None, None, None, 0, None) == 0  # empty all-gather is a no-op
+        # alltoallv: rank r sends (r + 1) * (d + 1) * 3 bytes to rank d (one chunk empty)
+        a2a = C.cast(tc.struct.alltoallv, ALLTOALLV_FN)
+        size = lambda s, d: 0 if (s, d) == (1, 0) else (s + 1) * (d + 1) * 3
+        sb = (C.c_uint64 * world)(*[size(rank, d) for d in range(world)])
+        rb = (C.c_uint64 * world)(*[size(s, rank) for s in range(world)])
+        send = np.concatenate([np.full(size(rank, d), 16 * rank + d, np.uint8) for d in range(world)])
+        recv = np.zeros(sum(rb), np.uint8)
+        assert a2a(None, send.ctypes.data, sb, recv.ctypes.data, rb, None) == 0, tc.error
+        exp = np.concatenate([np.full(size(s, rank), 16 * s + rank, np.uint8) for s in range(world)])
+        assert np.array_equal(recv, exp)
         out.put((rank, "ok"))
     except Exception as e:  # pragma: no cover
         out.put((rank, repr(e)))

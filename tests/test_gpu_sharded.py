@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 from paper_2404_16370_b200 import sim
-from paper_2404_16370_b200.abi import Particles, identity_pose, make_config
+from paper_2404_16370_b200.abi import ALLTOALLV_FN, Particles, identity_pose, make_config
 from paper_2404_16370_b200.api import FilterEngine, make_scan_cloud
 from paper_2404_16370_b200.comm import LoopbackComms
 
@@ -52,9 +52,12 @@ def run_single(world, cfg, frames):
     return res, eng.particles()
 
 
-def run_sharded(world, cfg, frames, G):
+def run_sharded(world, cfg, frames, G, alltoallv=True):
     scans_, delta, cov = frames
     comms = LoopbackComms(G)
+    if not alltoallv:  # a communicator without alltoallv: the reorder all-gathers the state
+        for r in range(G):
+            comms[r].alltoallv = ALLTOALLV_FN()
     engines = [FilterEngine(world[1], cfg, comm=comms[r]) for r in range(G)]
     results = [None] * G
     errors = []
@@ -85,15 +88,17 @@ def run_sharded(world, cfg, frames, G):
     return results, cat
 
 
-@pytest.mark.parametrize("G,mode,reorder", [(2, 2, 0), (4, 2, 0), (2, 1, 0), (2, 2, 1), (4, 2, 1), (2, 1, 1)])
-def test_sharded_engine_is_bit_identical_to_single(world, G, mode, reorder):
+@pytest.mark.parametrize("G,mode,reorder,a2a", [(2, 2, 0, 1), (4, 2, 0, 1), (2, 1, 0, 1), (2, 2, 1, 1), (4, 2, 1, 1),
+                                                (2, 1, 1, 1), (4, 2, 1, 0), (2, 1, 1, 0)])
+def test_sharded_engine_is_bit_identical_to_single(world, G, mode, reorder, a2a):
     """reorder = 1: the LSH reorder migrates particle state across shards
-    (particle_set.cpp:7-47 on the global order)."""
+    (particle_set.cpp:7-47 on the global order), by
+    alltoallv of the migrating records (a2a = 1) or by all-gather (a2a = 0)."""
     n = 16384 if mode == 2 else 8192
     cfg = make_config(n_particles=n, seed=7, nnf_resolution=0.2, likelihood_mode=mode, reorder_particles=reorder)
     frames = scans(world, cfg, 3)
     ref_res, ref_p = run_single(world, cfg, frames)
-    sh_res, sh_p = run_sharded(world, cfg, frames, G)
+    sh_res, sh_p = run_sharded(world, cfg, frames, G, alltoallv=bool(a2a))
     for r in range(G):  # every rank reports the same global frame result
         for a, b in zip(sh_res[r], ref_res):
             assert a["rep_id"] == b["rep_id"] and a["rep_index"] == b["rep_index"]
