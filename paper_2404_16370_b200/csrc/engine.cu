@@ -365,7 +365,7 @@ struct smcl_engine {
 
   // lsh
   DBuf<uint64_t> keys, skeys;
-  DBuf<int32_t> member_of, head, seg_id, seg_start, new_of_old, iota;
+  DBuf<int32_t> member_of, head, seg_id, seg_start, new_of_old, iota, pos_of_buf;
   DBuf<unsigned char> temp;
   size_t temp_bytes = 0;
   DBuf<unsigned long long> d_hist, d_counts;
@@ -1026,25 +1026,17 @@ struct smcl_engine {
     }
     if (profiling) mark(E_SEG);
     sync();
-    // SMCL_RG_STATS=1: per-pass candidate / survivor / evaluation counters on stderr (diagnostics only).
-    static const bool rg_stats = std::getenv("SMCL_RG_STATS") != nullptr;
-    unsigned long long* dbg = nullptr;
-    if (rg_stats) {
-      CK(cudaMallocAsync(reinterpret_cast<void**>(&dbg), 5 * sizeof(unsigned long long), st));
-      CK(cudaMemsetAsync(dbg, 0, 5 * sizeof(unsigned long long), st));
+    // Sorted position of every particle, for the neighbour pass's duplicate
+    // test: the identity after a reorder, else the inverse of member_of.
+    const int32_t* pos_of = nullptr;
+    if (members != iota.p) {
+      pos_of_buf.ensure(static_cast<size_t>(n));
+      launch_inverse_perm(members, n, pos_of_buf.p, st);
+      pos_of = pos_of_buf.p;
     }
-    launch_refresh_gather(poses_all, n_local, gbase, owned, members, seg_id.p, seg_start.p, n_seg, n, idx.p, kval.p,
-                          count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, st,
-                          dbg);
+    launch_refresh_gather(poses_all, n_local, gbase, owned, members, seg_id.p, seg_start.p, n_seg, n, pos_of, idx.p,
+                          kval.p, count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, st);
     CK(cudaGetLastError());
-    if (rg_stats) {
-      unsigned long long c[5];
-      CK(cudaMemcpyAsync(c, dbg, sizeof(c), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      CK(cudaFree(dbg));
-      std::fprintf(stderr, "[rg] n=%lld window=%llu survivors=%llu evaluated=%llu lazy=%llu refresh=%llu\n",
-                   static_cast<long long>(n_local), c[0], c[1], c[2], c[3], c[4]);
-    }
     if (profiling) mark(E_RG);
     // statistics
     const int hist_len = cfg.lsh_bucket_capacity + 2;

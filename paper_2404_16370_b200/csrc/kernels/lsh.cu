@@ -463,10 +463,16 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
 //   q >= L = sr (3 - tr(Ra^T Rb)) + st |tb - ta|^2
 // and L > -log(wk) (1e-6 margin) proves float(exp(-q)) <= wk: the offer
 // would be dropped whatever the list holds (a duplicate is dropped anyway).
+// Duplicates: offer() ignores a candidate already listed. Window members are
+// unique, so a member inserted during the scan is never offered again, and a
+// member listed at the start that gets evicted before its turn is never
+// re-inserted (it was the weakest, kv = wk_then <= wk_now, and an insert needs
+// kij > wk_now with kij = the same float). Hence "duplicate" = "listed before
+// the window scan": a 64-bit mask over window offsets (cap <= 64) marks those
+// members and the filter drops them before any evaluation.
 // Each lane filters its window into a chunk of up to kRgChunk survivors; the
 // warp evaluates all lanes' survivors together (full-width kval_of), then each
-// lane replays its offers in window order: values not above wk are dropped
-// before any list scan; the duplicate scan runs only for would-be inserts.
+// lane replays its offers in window order.
 constexpr int kRgChunk = 16;
 
 template <int BLOCK, int KMAX>
@@ -475,7 +481,8 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
                                                             const int32_t* __restrict__ member_of,
                                                             const int32_t* __restrict__ seg_id,
                                                             const int32_t* __restrict__ seg_start, int32_t n_seg,
-                                                            int64_t n_sorted, int32_t* __restrict__ idx,
+                                                            int64_t n_sorted, const int32_t* __restrict__ pos_of,
+                                                            int32_t* __restrict__ idx,
                                                             float* __restrict__ kval, int32_t* __restrict__ count,
                                                             int k, int cap, double sr, double st) {
   extern __shared__ __align__(16) unsigned char rg_smem[];
@@ -491,19 +498,26 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
   const int64_t r = static_cast<int64_t>(blockIdx.x) * BLOCK + t;
   const bool active = r < n;
   int32_t gi = -1;
-  int64_t li = 0, q = 0, q_end = 0;
+  int64_t li = 0, q = 0, q_end = 0, rb = 0;
   int cnt = 0;
+  unsigned long long listed = 0ull;  // window offsets (q - rb) of the members listed before the scan
   if (active) {
     const int64_t gp = pos_list ? static_cast<int64_t>(pos_list[r]) : r;
     gi = member_of[gp];
     li = static_cast<int64_t>(gi) - gbase;
     const int32_t seg = seg_id[gp] - 1;
-    const int64_t rb = seg_start[seg];
+    rb = seg_start[seg];
     const int64_t re = seg + 1 < n_seg ? seg_start[seg + 1] : n_sorted;
     q = rb;
     q_end = re < rb + cap ? re : rb + cap;
     cnt = count[li];
-    for (int s = 0; s < cnt; ++s) s_idx[s * BLOCK + t] = idx[li * k + s];
+    for (int s = 0; s < cnt; ++s) {
+      const int32_t e = idx[li * k + s];
+      s_idx[s * BLOCK + t] = e;
+      // sorted position of the listed particle (identity after a reorder)
+      const int64_t o = static_cast<int64_t>(pos_of ? pos_of[e] : e) - rb;
+      if (o >= 0 && o < q_end - rb) listed |= 1ull << o;
+    }
     const Pose pi = ldg_pose(all_poses + gi);
     for (int s = 0; s < cnt; ++s) {  // refresh (neighbor_graph.hpp:76-90)
       const int32_t j = s_idx[s * BLOCK + t];
@@ -543,6 +557,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
     if (active) {
       const Pose pi = ldg_pose(all_poses + gi);
       for (; q < q_end && ns < kRgChunk; ++q) {
+        if ((listed >> (q - rb)) & 1ull) continue;  // listed: a duplicate offer (also self)
         const int32_t j = member_of[q];
         if (j == gi) continue;
         if (full) {
@@ -580,12 +595,8 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
     // ---- offers in window order (neighbor_graph.hpp:47-74)
     for (int s = 0; s < ns; ++s) {
       const float kij = s_ckv[s * BLOCK + t];
-      if (cnt == k && !(weakest >= 0 && kij > wk)) continue;  // dropped, listed or not
+      if (cnt == k && !(weakest >= 0 && kij > wk)) continue;  // dropped
       const int32_t j = s_cand[s * BLOCK + t];
-      bool dup = false;
-#pragma unroll
-      for (int u = 0; u < KMAX; ++u) dup |= (u < cnt && s_idx[u * BLOCK + t] == j);
-      if (dup) continue;  // duplicates are ignored
       if (cnt < k) {
         s_idx[cnt * BLOCK + t] = j;
         s_kv[cnt * BLOCK + t] = kij;
@@ -737,18 +748,19 @@ void launch_seg_stats(const int32_t* seg_start, int32_t n_seg, int64_t n, int ca
 void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, const int32_t* pos_list,
                            const int32_t* member_of,
                            const int32_t* seg_id, const int32_t* seg_start, int32_t n_seg, int64_t n_sorted,
-                           int32_t* idx, float* kval, int32_t* count, int k, int cap, double sr, double st_,
-                           cudaStream_t st, unsigned long long* /*dbg*/) {
+                           const int32_t* pos_of, int32_t* idx, float* kval, int32_t* count, int k, int cap,
+                           double sr, double st_, cudaStream_t st) {
   count_launch();
   constexpr int B = 64;
   if (n <= 0) return;
   static const bool filtered = std::getenv("SMCL_RG_PLAIN") == nullptr;
-  if (filtered && k <= 32) {
+  if (filtered && k <= 32 && cap <= 64) {
     const size_t smem = static_cast<size_t>(k) * B * 8 + static_cast<size_t>(kRgChunk) * B * 8 + B * 4 +
                         static_cast<size_t>(B) * kRgChunk * 2;
 #define RGF(KM)                                                                                                   \
   k_refresh_gather_f<B, KM><<<blocks_for(n, B), B, smem, st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, \
-                                                               seg_start, n_seg, n_sorted, idx, kval, count, k,   \
+                                                               seg_start, n_seg, n_sorted, pos_of, idx, kval,     \
+                                                               count, k,                                          \
                                                                cap, sr, st_)
     if (k <= 8)
       RGF(8);
