@@ -113,15 +113,21 @@ struct SMCL_ALIGN16 Pose {
 };
 
 #ifdef __CUDACC__
-// Read-only 96-byte pose as six 128-bit loads (a plain struct copy compiles
-// to twelve 64-bit loads: twice the L1 wavefronts in the gather-heavy passes).
+// Read-only 96-byte pose as three 256-bit loads (sm_100 LDG.256; poses sit
+// at 96-byte strides from a 256-byte aligned base, so every one is 32-byte
+// aligned). A plain struct copy compiles to twelve 64-bit loads; the gather-
+// heavy passes (neighbour pass, SVGD) are L1-wavefront bound.
+__device__ __forceinline__ void ldg_v4d(const double* p, double& a, double& b, double& c, double& d) {
+  // volatile: a non-volatile asm is a pure function to the compiler, which may
+  // then hoist the load above the guard that makes the address valid.
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
 __device__ __forceinline__ Pose ldg_pose(const Pose* p) {
-  const double2* v = reinterpret_cast<const double2*>(p);
-  const double2 a0 = __ldg(v), a1 = __ldg(v + 1), a2 = __ldg(v + 2), a3 = __ldg(v + 3), a4 = __ldg(v + 4),
-                a5 = __ldg(v + 5);
+  const double* v = reinterpret_cast<const double*>(p);
   Pose q;
-  q.R[0] = a0.x, q.R[1] = a0.y, q.R[2] = a1.x, q.R[3] = a1.y, q.R[4] = a2.x, q.R[5] = a2.y;
-  q.R[6] = a3.x, q.R[7] = a3.y, q.R[8] = a4.x, q.t[0] = a4.y, q.t[1] = a5.x, q.t[2] = a5.y;
+  ldg_v4d(v, q.R[0], q.R[1], q.R[2], q.R[3]);
+  ldg_v4d(v + 4, q.R[4], q.R[5], q.R[6], q.R[7]);
+  ldg_v4d(v + 8, q.R[8], q.t[0], q.t[1], q.t[2]);
   return q;
 }
 #endif
