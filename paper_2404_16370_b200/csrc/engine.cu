@@ -423,6 +423,42 @@ struct smcl_engine {
     return ms;
   }
 
+  // Neighbour-pass statistics (neighbor_search.cpp:172-190) run on a side
+  // stream, overlapped with the rest of the step, into their own buffers; the
+  // host copy lands in pinned memory and fills the caller's struct after the
+  // call's final sync (finish_nb_stats). Sharded engines keep them on the
+  // engine stream (their all-gathers are stream-ordered there).
+  struct NbHost {
+    unsigned long long hist[SMCL_MAX_HIST];
+    unsigned long long overflow;
+    double sums[2];
+    int32_t n_seg;
+  };
+  cudaStream_t aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  NbHost* nb_host = nullptr;
+  DBuf<unsigned long long> nb_hist;
+  DBuf<double> nb_s1, nb_s2, nb_p1, nb_p2, nb_sum;
+  smcl_neighbor_stats* nb_out = nullptr;
+  int32_t nb_buckets = 0;
+  int nb_hist_len = 0;
+  bool aux_pending = false;
+  void join_aux() {  // engine stream waits for the side-stream statistics
+    if (aux_pending) CK(cudaStreamWaitEvent(st, ev_join, 0));
+    aux_pending = false;
+  }
+  void finish_nb_stats() {  // after the call's final sync
+    if (!nb_out) return;
+    smcl_neighbor_stats* out = nb_out;
+    nb_out = nullptr;
+    out->n_buckets = nb_buckets;
+    out->buckets_used = nb_host->n_seg;
+    out->overflow_dropped = static_cast<int64_t>(nb_host->overflow);
+    out->mean_kernel = nb_host->sums[1] > 0 ? nb_host->sums[0] / nb_host->sums[1] : 0.0;
+    out->hist_len = std::min(nb_hist_len, SMCL_MAX_HIST);
+    for (int q = 0; q < out->hist_len; ++q) out->occupancy_hist[q] = static_cast<int64_t>(nb_host->hist[q]);
+  }
+
   ~smcl_engine() {
     if (prep_thread.joinable()) {
       {
@@ -437,6 +473,13 @@ struct smcl_engine {
       cudaStreamDestroy(prep_st);
     }
     if (st) cudaStreamSynchronize(st);
+    if (aux) {
+      cudaStreamSynchronize(aux);
+      cudaStreamDestroy(aux);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (nb_host) cudaFreeHost(nb_host);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : timer)
@@ -571,7 +614,13 @@ struct smcl_engine {
     member_of.ensure(ug);
     head.ensure(ug);
     seg_id.ensure(ug);
-    seg_start.ensure(ug);
+    seg_start.ensure(ug + 1);  // + sentinel
+    nb_hist.ensure(SMCL_MAX_HIST + 1);  // + overflow count
+    nb_s1.ensure(un);
+    nb_s2.ensure(un);
+    nb_p1.ensure((un + kReduceChunk - 1) / kReduceChunk);
+    nb_p2.ensure((un + kReduceChunk - 1) / kReduceChunk);
+    nb_sum.ensure(2);
     new_of_old.ensure(ug);
     iota.ensure(ug);
     {
@@ -929,6 +978,8 @@ struct smcl_engine {
 
   void update_neighbors(uint64_t pass_seed, const double* bounds, smcl_neighbor_stats* out) {
     const int64_t n = n_total;
+    join_aux();
+    nb_out = nullptr;
     if (out) std::memset(out, 0, sizeof(*out));
     if (n == 0) return;
     if (k != cfg.k_neighbors) throw std::invalid_argument("update_neighbors: graph not initialized for this set");
@@ -1013,9 +1064,7 @@ struct smcl_engine {
     if (profiling) mark(E_REORDER);
     inclusive_sum_i32(head.p, seg_id.p, n, temp.p, temp_bytes, st);
     launch_segments(head.p, seg_id.p, n, seg_start.p, st);
-    int32_t n_seg = 0;
-    CK(cudaMemcpyAsync(&n_seg, seg_id.p + (n - 1), sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    g_d2h += sizeof(int32_t);
+    const int32_t* n_seg = seg_id.p + (n - 1);  // number of buckets (device)
     // Sorted positions of this shard's particles, in sorted order.
     const int32_t* owned = nullptr;
     if (sharded) {
@@ -1025,7 +1074,6 @@ struct smcl_engine {
       owned = pos_list.p;
     }
     if (profiling) mark(E_SEG);
-    sync();
     // Sorted position of every particle, for the neighbour pass's duplicate
     // test: the identity after a reorder, else the inverse of member_of.
     const int32_t* pos_of = nullptr;
@@ -1034,39 +1082,45 @@ struct smcl_engine {
       launch_inverse_perm(members, n, pos_of_buf.p, st);
       pos_of = pos_of_buf.p;
     }
-    launch_refresh_gather(poses_all, n_local, gbase, owned, members, seg_id.p, seg_start.p, n_seg, n, pos_of, idx.p,
+    launch_refresh_gather(poses_all, n_local, gbase, owned, members, seg_id.p, seg_start.p, n, pos_of, idx.p,
                           kval.p, count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, st);
     CK(cudaGetLastError());
     if (profiling) mark(E_RG);
-    // statistics
+    // statistics (neighbor_search.cpp:172-190)
     const int hist_len = cfg.lsh_bucket_capacity + 2;
-    CK(cudaMemsetAsync(d_hist.p, 0, sizeof(unsigned long long) * hist_len, st));
-    CK(cudaMemsetAsync(d_counts.p, 0, sizeof(unsigned long long) * 2, st));
-    launch_seg_stats(seg_start.p, n_seg, n, cfg.lsh_bucket_capacity, d_hist.p, d_counts.p, st);
+    if (hist_len > SMCL_MAX_HIST) throw std::invalid_argument("lsh_bucket_capacity too large for the statistics");
+    cudaStream_t ss = st;
+    if (!sharded) {  // overlapped with the rest of the step
+      CK(cudaEventRecord(ev_fork, st));
+      CK(cudaStreamWaitEvent(aux, ev_fork, 0));
+      ss = aux;
+    }
+    CK(cudaMemsetAsync(nb_hist.p, 0, sizeof(unsigned long long) * (SMCL_MAX_HIST + 1), ss));
+    launch_seg_stats(seg_start.p, n_seg, n, cfg.lsh_bucket_capacity, nb_hist.p, nb_hist.p + SMCL_MAX_HIST, ss);
     const int64_t chunks = (n_local + kReduceChunk - 1) / kReduceChunk;
-    launch_chunk_sum_kernel(kval.p, count.p, n_local, k, pbuf.p, qbuf.p, partial.p, partial2.p, st);
+    launch_chunk_sum_kernel(kval.p, count.p, n_local, k, nb_s1.p, nb_s2.p, nb_p1.p, nb_p2.p, ss);
     if (sharded) {  // chunk partials of every shard, combined in global chunk order
-      allgather(partial.p, g_part.p, sizeof(double) * static_cast<size_t>(chunks));
-      allgather(partial2.p, g_part2.p, sizeof(double) * static_cast<size_t>(chunks));
-      launch_finish_sum2(g_part.p, g_part2.p, chunks * world, scal.p, st);
+      allgather(nb_p1.p, g_part.p, sizeof(double) * static_cast<size_t>(chunks));
+      allgather(nb_p2.p, g_part2.p, sizeof(double) * static_cast<size_t>(chunks));
+      launch_finish_sum2(g_part.p, g_part2.p, chunks * world, nb_sum.p, ss);
     } else {
-      launch_finish_sum2(partial.p, partial2.p, chunks, scal.p, st);
+      launch_finish_sum2(nb_p1.p, nb_p2.p, chunks, nb_sum.p, ss);
     }
     CK(cudaGetLastError());
-    if (out) {
-      std::vector<unsigned long long> hist(static_cast<size_t>(hist_len));
-      unsigned long long ov[2];
-      double sums[2];
-      d_hist.download(hist.data(), hist.size(), st);
-      d_counts.download(ov, 2, st);
-      scal.download(sums, 2, st);
-      sync();
-      out->n_buckets = nb;
-      out->buckets_used = n_seg;
-      out->overflow_dropped = static_cast<int64_t>(ov[0]);
-      out->mean_kernel = sums[1] > 0 ? sums[0] / sums[1] : 0.0;
-      out->hist_len = std::min(hist_len, SMCL_MAX_HIST);
-      for (int q = 0; q < out->hist_len; ++q) out->occupancy_hist[q] = static_cast<int64_t>(hist[static_cast<size_t>(q)]);
+    if (out) {  // read back after the call's final sync (finish_nb_stats)
+      CK(cudaMemcpyAsync(nb_host->hist, nb_hist.p, sizeof(unsigned long long) * (SMCL_MAX_HIST + 1),
+                         cudaMemcpyDeviceToHost, ss));
+      CK(cudaMemcpyAsync(nb_host->sums, nb_sum.p, sizeof(double) * 2, cudaMemcpyDeviceToHost, ss));
+      CK(cudaMemcpyAsync(&nb_host->n_seg, n_seg, sizeof(int32_t), cudaMemcpyDeviceToHost, ss));
+      g_d2h += static_cast<long long>(sizeof(unsigned long long) * (SMCL_MAX_HIST + 1) + 2 * sizeof(double) +
+                                      sizeof(int32_t));
+      nb_out = out;
+      nb_buckets = nb;
+      nb_hist_len = hist_len;
+    }
+    if (!sharded) {
+      CK(cudaEventRecord(ev_join, aux));
+      aux_pending = true;
     }
   }
 
@@ -1290,10 +1344,12 @@ struct smcl_engine {
     double v;
     representative(&ix, r.representative, &v);
     unsigned long long cnt[6];
+    join_aux();
     d_counts.download(cnt, 6, st);
     const int32_t rid = rep_id;
     cnt[1] = last_nm_sum;  // global sum of n_matched (bayes)
     sync();
+    finish_nb_stats();
     if (!empty) {  // last (or only) Gauss-Newton iteration
       t_gn += since(E_GN0, E_GN1);
       t_solve += since(E_GN1, E_SOLVE);
@@ -1361,6 +1417,10 @@ smcl_engine* make_engine(const smcl_cloud* map, const smcl_config* cfg, int devi
     CK(cudaGetDevice(&e->device));
   }
   CK(cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&e->aux, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
+  CK(cudaMallocHost(reinterpret_cast<void**>(&e->nb_host), sizeof(smcl_engine::NbHost)));
   for (int q = 0; q < SMCL_MAX_SCAN_SLOTS; ++q) e->slots.push_back(std::make_unique<smcl_engine::ScanSlot>());
   e->k = cfg->k_neighbors;
   if (map) e->setup_map(map);
@@ -1720,7 +1780,9 @@ int smcl_update_neighbors(smcl_engine* h, uint64_t pass_seed, const double bound
   return guard([&] {
     use_dev(h);
     h->update_neighbors(pass_seed, bounds, stats);
+    h->join_aux();
     h->sync();
+    h->finish_nb_stats();
   });
 }
 

@@ -77,13 +77,13 @@ void launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_
                     Pose* poses2, double* lp2, int32_t* id2, int32_t* idx2, float* kval2, int32_t* count2,
                     cudaStream_t st);
 void launch_segments(const int32_t* head, const int32_t* seg_id, int64_t n, int32_t* seg_start, cudaStream_t st);
-void launch_seg_stats(const int32_t* seg_start, int32_t n_seg, int64_t n, int cap, unsigned long long* hist,
+void launch_seg_stats(const int32_t* seg_start, const int32_t* n_seg, int64_t n, int cap, unsigned long long* hist,
                       unsigned long long* overflow, cudaStream_t st);
 void launch_owned_flags(const int32_t* member_of, int64_t n, int64_t gbase, int64_t n_local, int32_t* flag,
                         cudaStream_t st);
 void launch_owned_scatter(const int32_t* flag, const int32_t* incl, int64_t n, int32_t* pos_list, cudaStream_t st);
 void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, const int32_t* pos_list,
-                           const int32_t* member_of, const int32_t* seg_id, const int32_t* seg_start, int32_t n_seg,
+                           const int32_t* member_of, const int32_t* seg_id, const int32_t* seg_start,
                            int64_t n_sorted, const int32_t* pos_of, int32_t* idx, float* kval, int32_t* count, int k,
                            int cap, double sr, double st_, cudaStream_t st);
 

@@ -266,19 +266,21 @@ __global__ void k_segments(const int32_t* __restrict__ head, const int32_t* __re
                            int32_t* __restrict__ seg_start) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p < n && head[p]) seg_start[seg_id[p] - 1] = static_cast<int32_t>(p);
+  if (p == n - 1) seg_start[seg_id[p]] = static_cast<int32_t>(n);  // sentinel: seg_start[n_seg] = n
 }
 
 // Bucket-size statistics (neighbor_search.cpp:172-181); integer atomics are
 // order independent, so the histogram is exact.
-__global__ void k_seg_stats(const int32_t* __restrict__ seg_start, int32_t n_seg, int64_t n, int cap,
+__global__ void k_seg_stats(const int32_t* __restrict__ seg_start, const int32_t* __restrict__ n_seg_ptr, int cap,
                             unsigned long long* __restrict__ hist, unsigned long long* __restrict__ overflow) {
   // Block-private histogram in shared memory, one global atomic per bin per block.
   extern __shared__ unsigned long long s_hist[];  // cap + 3 (last = overflow)
   for (int b = threadIdx.x; b < cap + 3; b += blockDim.x) s_hist[b] = 0ull;
   __syncthreads();
+  const int64_t n_seg = *n_seg_ptr;
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < n_seg;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t end = s + 1 < n_seg ? seg_start[s + 1] : n;
+    const int64_t end = seg_start[s + 1];
     const int64_t size = end - seg_start[s];
     const int64_t bin = size < cap + 1 ? size : cap + 1;
     atomicAdd(s_hist + bin, 1ull);
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
                                                           int64_t gbase, const int32_t* __restrict__ pos_list,
                                                           const int32_t* __restrict__ member_of,
                                                           const int32_t* __restrict__ seg_id,
-                                                          const int32_t* __restrict__ seg_start, int32_t n_seg,
+                                                          const int32_t* __restrict__ seg_start,
                                                           int64_t n_sorted, int32_t* __restrict__ idx,
                                                           float* __restrict__ kval, int32_t* __restrict__ count, int k,
                                                           int cap, double sr, double st) {
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
   const int64_t li = static_cast<int64_t>(gi) - gbase;    // local storage slot
   const int32_t seg = seg_id[gp] - 1;
   const int64_t rb = seg_start[seg];
-  const int64_t re = seg + 1 < n_seg ? seg_start[seg + 1] : n_sorted;
+  const int64_t re = seg_start[seg + 1];  // sentinel seg_start[n_seg] = n
   const int64_t vis_end = re < rb + cap ? re : rb + cap;
 
   int cnt = count[li];
@@ -480,7 +482,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
                                                             int64_t gbase, const int32_t* __restrict__ pos_list,
                                                             const int32_t* __restrict__ member_of,
                                                             const int32_t* __restrict__ seg_id,
-                                                            const int32_t* __restrict__ seg_start, int32_t n_seg,
+                                                            const int32_t* __restrict__ seg_start,
                                                             int64_t n_sorted, const int32_t* __restrict__ pos_of,
                                                             int32_t* __restrict__ idx,
                                                             float* __restrict__ kval, int32_t* __restrict__ count,
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
     li = static_cast<int64_t>(gi) - gbase;
     const int32_t seg = seg_id[gp] - 1;
     rb = seg_start[seg];
-    const int64_t re = seg + 1 < n_seg ? seg_start[seg + 1] : n_sorted;
+    const int64_t re = seg_start[seg + 1];  // sentinel seg_start[n_seg] = n
     q = rb;
     q_end = re < rb + cap ? re : rb + cap;
     cnt = count[li];
@@ -736,18 +738,18 @@ void launch_segments(const int32_t* head, const int32_t* seg_id, int64_t n, int3
   if (n > 0) k_segments<<<blocks_for(n, 256), 256, 0, st>>>(head, seg_id, n, seg_start);
 }
 
-void launch_seg_stats(const int32_t* seg_start, int32_t n_seg, int64_t n, int cap, unsigned long long* hist,
+void launch_seg_stats(const int32_t* seg_start, const int32_t* n_seg, int64_t n, int cap, unsigned long long* hist,
                       unsigned long long* overflow, cudaStream_t st) {
   count_launch();
-  if (n_seg > 0) {
-    const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(n_seg, 256), 296));
-    k_seg_stats<<<g, 256, sizeof(unsigned long long) * (cap + 3), st>>>(seg_start, n_seg, n, cap, hist, overflow);
+  if (n > 0) {
+    const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(n, 256), 296));
+    k_seg_stats<<<g, 256, sizeof(unsigned long long) * (cap + 3), st>>>(seg_start, n_seg, cap, hist, overflow);
   }
 }
 
 void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, const int32_t* pos_list,
                            const int32_t* member_of,
-                           const int32_t* seg_id, const int32_t* seg_start, int32_t n_seg, int64_t n_sorted,
+                           const int32_t* seg_id, const int32_t* seg_start, int64_t n_sorted,
                            const int32_t* pos_of, int32_t* idx, float* kval, int32_t* count, int k, int cap,
                            double sr, double st_, cudaStream_t st) {
   count_launch();
@@ -759,7 +761,7 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                         static_cast<size_t>(B) * kRgChunk * 2;
 #define RGF(KM)                                                                                                   \
   k_refresh_gather_f<B, KM><<<blocks_for(n, B), B, smem, st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, \
-                                                               seg_start, n_seg, n_sorted, pos_of, idx, kval,     \
+                                                               seg_start, n_sorted, pos_of, idx, kval,            \
                                                                count, k,                                          \
                                                                cap, sr, st_)
     if (k <= 8)
@@ -772,7 +774,7 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
     return;
   }
   k_refresh_gather<B><<<blocks_for(n, B), B, static_cast<size_t>(k) * B * 8, st>>>(all_poses, n, gbase, pos_list,
-                                                                                 member_of, seg_id, seg_start, n_seg,
+                                                                                 member_of, seg_id, seg_start,
                                                                                  n_sorted, idx, kval, count, k, cap,
                                                                                  sr, st_);
 }

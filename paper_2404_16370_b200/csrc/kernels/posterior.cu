@@ -123,42 +123,50 @@ __global__ void k_list_sums(const float* __restrict__ kval, const int32_t* __res
   csum[i] = static_cast<double>(cnt);
 }
 
-// reduce.hpp:22-27: one warp per 4096-element chunk; the warp stages 1024
-// values at a time in shared memory (coalesced) and lane 0 adds them serially
-// in index order, so every chunk partial is bit-identical to the reference's.
-constexpr int kStage = 1024;
-// Two independent vectors per launch (blocks [0, chunks) sum v0, [chunks,
-// 2*chunks) sum v1). The serial chain is DADD-latency bound: lane 0 reads
-// the staged values 8 at a time ahead of the adds.
+// reduce.hpp:22-27: one warp per 4096-element chunk. The warp stages the
+// whole chunk in shared memory with coalesced 128-bit loads (one round trip),
+// then lane 0 adds it serially in index order, so every chunk partial is
+// bit-identical to the reference's. Two independent vectors per launch
+// (blocks [0, chunks) sum v0, [chunks, 2*chunks) sum v1). The serial chain
+// is DADD-latency bound: lane 0 reads the staged values 16 at a time (LDS.128)
+// ahead of the adds.
 __global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ v0, const double* __restrict__ v1,
                                                      int64_t n, int64_t chunks, double* __restrict__ p0,
                                                      double* __restrict__ p1) {
-  __shared__ double s[kStage];
+  __shared__ __align__(16) double s[kReduceChunk];
   const bool second = blockIdx.x >= chunks;
   const double* __restrict__ v = second ? v1 : v0;
   double* __restrict__ partial = second ? p1 : p0;
   const int64_t c = second ? blockIdx.x - chunks : blockIdx.x;
   const int64_t begin = c * kReduceChunk;
-  const int64_t end = begin + kReduceChunk < n ? begin + kReduceChunk : n;
-  double acc = 0.0;
-  for (int64_t b = begin; b < end; b += kStage) {
-    const int64_t m = end - b < kStage ? end - b : kStage;
-    for (int q = threadIdx.x; q < m; q += 32) s[q] = v[b + q];
-    __syncwarp();
-    if (threadIdx.x == 0) {
-      int q = 0;
-      for (; q + 8 <= m; q += 8) {
-        double x[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = s[q + u];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc = xadd(acc, x[u]);
-      }
-      for (; q < m; ++q) acc = xadd(acc, s[q]);
-    }
-    __syncwarp();
+  const int m = static_cast<int>(begin + kReduceChunk < n ? kReduceChunk : n - begin);
+  const bool vec = (reinterpret_cast<uintptr_t>(v + begin) & 15u) == 0;
+  if (vec) {
+    const double2* src = reinterpret_cast<const double2*>(v + begin);
+    double2* dst = reinterpret_cast<double2*>(s);
+#pragma unroll 8
+    for (int q = threadIdx.x; q < m / 2; q += 32) dst[q] = __ldg(src + q);
+    if ((m & 1) && threadIdx.x == 0) s[m - 1] = v[begin + m - 1];
+  } else {
+    for (int q = threadIdx.x; q < m; q += 32) s[q] = v[begin + q];
   }
-  if (threadIdx.x == 0) partial[c] = acc;
+  __syncwarp();
+  if (threadIdx.x != 0) return;
+  double acc = 0.0;
+  int q = 0;
+  const double2* s2 = reinterpret_cast<const double2*>(s);
+  for (; q + 16 <= m; q += 16) {
+    double2 x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = s2[q / 2 + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      acc = xadd(acc, x[u].x);
+      acc = xadd(acc, x[u].y);
+    }
+  }
+  for (; q < m; ++q) acc = xadd(acc, s[q]);
+  partial[c] = acc;
 }
 
 // Serial combine of chunk partials (single thread): lse = m + log(sum).
