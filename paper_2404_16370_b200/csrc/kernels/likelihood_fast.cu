@@ -10,7 +10,7 @@
 // shared memory as fp32 (its 1e-8 m resolution is below the fp32 map record
 // precision). x differs from the reference's ((R mu + t) - o) * inv_res
 // (nnf.hpp:24-35) by < 1e-12 voxel, so the cell is the reference's unless f is
-// within 1e-9 of a face: such points "resolve" in phase B through the
+// within ~5e-8 of a face (frac_clear_of_faces): such points "resolve" in phase B through the
 // reference-order fp64 transform. In-bounds points start a cp.async of their
 // 32-byte cell record into the warp's stage, so U x 2 16-byte gathers per lane
 // are in flight (the global-init gathers are random L2 hits).
@@ -38,7 +38,7 @@ namespace smcl {
 namespace {
 
 constexpr uint32_t kMetaStage = 1u << 16;    // fq.w: record staged (in bounds, cell proven)
-constexpr uint32_t kMetaResolve = 1u << 17;  // fq.w: fraction within 1e-9 of a cell face: reference-order path
+constexpr uint32_t kMetaResolve = 1u << 17;  // fq.w: fraction within ~5e-8 of a cell face: reference-order path
 
 template <int kStep>
 struct WarpStage {
@@ -112,15 +112,17 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
   // physical covariance, well inside __fdividef's range.
   const float invD = rcp_approx(fmaf(A, Ssum, bg * w));
   const float invA = rcp_approx(A);
-  const float P = beta * AmG * invD, Q = gam * AmB * invD, T = c * bg * invD;
+  // P, Q, T pre-scaled by 1/A: Omega' = invA I + Pa m m^T + Qa n n^T + Ta (m n^T + n m^T)
+  const float invDA = invD * invA;
+  const float Pa = beta * AmG * invDA, Qa = gam * AmB * invDA, Ta = c * bg * invDA;
   const float x = mx * ex + my * ey + mz * ez;
   const float y = nx * ex + ny * ey + nz * ez;
-  const float am = fmaf(P, x, T * y), an = fmaf(Q, y, T * x);
-  acc.cost += (ex * ex + ey * ey + ez * ez + am * x + an * y) * invA;
+  const float am = fmaf(Pa, x, Ta * y), an = fmaf(Qa, y, Ta * x);  // (Omega' - invA I) e = am m + an n
+  acc.cost += fmaf(ex * ex + ey * ey + ez * ez, invA, fmaf(am, x, an * y));
   if (GN) {
-    const float gx = (ex + am * mx + an * nx) * invA;
-    const float gy = (ey + am * my + an * ny) * invA;
-    const float gz = (ez + am * mz + an * nz) * invA;
+    const float gx = fmaf(ex, invA, fmaf(am, mx, an * nx));  // g = Omega' e
+    const float gy = fmaf(ey, invA, fmaf(am, my, an * ny));
+    const float gz = fmaf(ez, invA, fmaf(am, mz, an * nz));
     const float ux = s0.x, uy = s0.y, uz = s0.z;  // scan mean (body frame)
     acc.b[0] += gy * uz - gz * uy;  // b_top += g x mu
     acc.b[1] += gz * ux - gx * uz;
@@ -128,11 +130,8 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
     acc.b[3] -= gx;  // b_bot -= g
     acc.b[4] -= gy;
     acc.b[5] -= gz;
-    // Omega' = invA (I + P m m^T + Q n n^T + T (m n^T + n m^T))
-    //        = invA I + alpha m^T + beta_ n^T,  alpha = invA (P m + T n),
-    //                                           beta_ = invA (Q n + T m)
+    // Omega' = invA I + alpha m^T + beta_ n^T,  alpha = Pa m + Ta n, beta_ = Qa n + Ta m
     // (symmetric: alpha_r m_q + beta_r n_q = invA (P m_r m_q + Q n_r n_q + T (n_r m_q + m_r n_q))).
-    const float Pa = P * invA, Qa = Q * invA, Ta = T * invA;
     const float mv[3] = {mx, my, mz}, nv[3] = {nx, ny, nz};
     float al[3], be[3];
 #pragma unroll
@@ -145,8 +144,7 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
     for (int r = 0; r < 3; ++r)
 #pragma unroll
       for (int q = 0; q <= r; ++q) {
-        float v = fmaf(al[r], mv[q], be[r] * nv[q]);
-        if (r == q) v += invA;
+        const float v = fmaf(al[r], mv[q], fmaf(be[r], nv[q], r == q ? invA : 0.f));
         O[r][q] = O[q][r] = v;
       }
     acc.hbr[0] += O[0][0];
@@ -174,6 +172,14 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
     acc.htl[4] = fmaf(W[2][0], uz, fmaf(-W[2][2], ux, acc.htl[4]));
     acc.htl[5] = fmaf(W[2][1], ux, fmaf(-W[2][0], uy, acc.htl[5]));
   }
+}
+
+// f = x - floor(x) at least ~5e-8 from both cell faces: 2^-24 <= f < 1 - 2^-21,
+// decided on the high word of f with one unsigned range test (integer pipe;
+// NaN and negative values fail). The transform differs from the reference's
+// by < 1e-12 voxel, so such a point's cell is the reference's.
+__device__ __forceinline__ bool frac_clear_of_faces(double f) {
+  return static_cast<unsigned>(__double2hiint(f)) - 0x3E700000u < 0x3FEFFFFFu - 0x3E700000u;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -285,18 +291,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         const double m0 = s_mu[3 * k], m1 = s_mu[3 * k + 1], m2 = s_mu[3 * k + 2];
         float fr[3];
         int ic[3];
-        bool amb = huge, inb = true;
+        bool safe = !huge, inb = true;
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
           const double x = fma(Rv[ax * 3 + 2], m2, fma(Rv[ax * 3 + 1], m1, fma(Rv[ax * 3 + 0], m0, tv[ax])));
           const double y = __dadd_rd(x, kMagic);
           const double f = x - (y - kMagic);
           ic[ax] = __double2loint(y);
-          // |x| < 2^40 and f at least 1e-9 from a face (NaN fails both)
-          amb = amb || !(fabs(f - 0.5) < 0.5 - 1e-9);
-          inb = inb && static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz));
+          inb = inb & (static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz)));
           fr[ax] = __double2float_rn(f);
+          safe = safe & frac_clear_of_faces(f);
         }
+        const bool amb = !safe;
         const bool real = k < S;
         const bool resolve = amb && real;
         const bool stage = !amb && inb;  // padded points are NaN: never staged
@@ -315,7 +321,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       for (int u = 0; u < kFastUnroll; ++u) {
         const int slot = u * 32 + lane;
         const uint32_t meta = __float_as_uint(ws.fq[slot].w);
-        const bool keep = (meta & kMetaResolve) || ((meta & kMetaStage) && ws.m0[slot].w >= 0.f);
+        const float mw = ws.m0[slot].w;  // unstaged slots were zero-filled: the meta bit decides
+        const bool keep = ((meta & kMetaResolve) != 0u) | (((meta & kMetaStage) != 0u) & (mw >= 0.f));
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
         if (keep) ws.q[n_cand + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(slot);
         n_cand += __popc(mask);
@@ -462,17 +469,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
       const double m0 = s_mu[3 * (k < S ? k : 0)], m1 = s_mu[3 * (k < S ? k : 0) + 1],
                    m2 = s_mu[3 * (k < S ? k : 0) + 2];
       int ic[3];
-      bool amb = huge, inb = true;
+      bool safe = !huge, inb = true;
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         const double x = fma(Rv[ax * 3 + 2], m2, fma(Rv[ax * 3 + 1], m1, fma(Rv[ax * 3 + 0], m0, tv[ax])));
         const double y = __dadd_rd(x, kMagic);
         const double f = x - (y - kMagic);
         ic[ax] = __double2loint(y);
-        amb = amb || !(fabs(f - 0.5) < 0.5 - 1e-9);
-        inb = inb && static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz));
+        inb = inb & (static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz)));
         fr[u][ax] = __double2float_rn(f);
+        safe = safe & frac_clear_of_faces(f);
       }
+      const bool amb = !safe;
       const bool stg = real && !amb && inb;
       st[u] = (stg ? 1u : 0u) | (real && amb ? 2u : 0u);
       const uint64_t cell = stg ? rec_index<kBrick>(map, ic[0], ic[1], ic[2]) : 0u;
