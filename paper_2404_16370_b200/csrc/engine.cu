@@ -1015,7 +1015,9 @@ struct smcl_engine {
       keys_all = g_keys.p;
     }
     if (profiling) mark(E_KEYS);
-    sort_keys(keys_all, skeys.p, n, 64, temp.p, temp_bytes, st);
+    // The keys are in global index order with the index in the low idx_bits
+    // (neighbor_search.cpp:86-103): a stable sort of the upper bits suffices.
+    sort_keys(keys_all, skeys.p, n, lp.idx_bits, 64, temp.p, temp_bytes, st);
     if (profiling) mark(E_SORT);
     launch_members(skeys.p, n, idx_mask, shift, member_of.p, head.p, st);
     const int32_t* members = member_of.p;

@@ -57,7 +57,7 @@ void launch_kernel_batch(const Pose* a, const Pose* b, int64_t n, double sr, dou
 void launch_lsh_keys(const Pose* poses, int64_t n, int64_t gbase, const LshPass& lp, uint64_t* keys, cudaStream_t st);
 void launch_hash_batch(const Pose* poses, int64_t n, const LshPass& lp, uint64_t* out, cudaStream_t st);
 size_t sort_temp_bytes(int64_t n);
-void sort_keys(const uint64_t* in, uint64_t* out, int64_t n, int end_bit, void* temp, size_t temp_bytes,
+void sort_keys(const uint64_t* in, uint64_t* out, int64_t n, int begin_bit, int end_bit, void* temp, size_t temp_bytes,
                cudaStream_t st);
 void launch_members(const uint64_t* skeys, int64_t n, uint64_t idx_mask, int shift, int32_t* member_of, int32_t* head,
                     cudaStream_t st);

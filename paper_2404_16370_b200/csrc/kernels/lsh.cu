@@ -666,9 +666,12 @@ size_t sort_temp_bytes(int64_t n) {
   return a > b ? a : b;
 }
 
-void sort_keys(const uint64_t* in, uint64_t* out, int64_t n, int end_bit, void* temp, size_t temp_bytes,
+// Keys [begin_bit, end_bit) with a stable LSD radix sort: when the low bits
+// hold the particle index and the input is in index order, sorting only the
+// bits above them gives the order of the full 64-bit sort.
+void sort_keys(const uint64_t* in, uint64_t* out, int64_t n, int begin_bit, int end_bit, void* temp, size_t temp_bytes,
                cudaStream_t st) {
-  cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, static_cast<int>(n), 0, end_bit, st);
+  cub::DeviceRadixSort::SortKeys(temp, temp_bytes, in, out, static_cast<int>(n), begin_bit, end_bit, st);
 }
 
 void launch_members(const uint64_t* skeys, int64_t n, uint64_t idx_mask, int shift, int32_t* member_of, int32_t* head,
