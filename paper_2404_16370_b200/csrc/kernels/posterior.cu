@@ -130,9 +130,11 @@ __global__ void k_list_sums(const float* __restrict__ kval, const int32_t* __res
 // (blocks [0, chunks) sum v0, [chunks, 2*chunks) sum v1). The serial chain
 // is DADD-latency bound: lane 0 reads the staged values 16 at a time (LDS.128)
 // ahead of the adds.
+// m_ptr != nullptr: the staged values are exp(v - *m_ptr) (posterior.cpp:17,
+// as k_exp_shift), computed by the 32 lanes while staging.
 __global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ v0, const double* __restrict__ v1,
                                                      int64_t n, int64_t chunks, double* __restrict__ p0,
-                                                     double* __restrict__ p1) {
+                                                     double* __restrict__ p1, const double* __restrict__ m_ptr) {
   __shared__ __align__(16) double s[kReduceChunk];
   const bool second = blockIdx.x >= chunks;
   const double* __restrict__ v = second ? v1 : v0;
@@ -141,7 +143,11 @@ __global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ 
   const int64_t begin = c * kReduceChunk;
   const int m = static_cast<int>(begin + kReduceChunk < n ? kReduceChunk : n - begin);
   const bool vec = (reinterpret_cast<uintptr_t>(v + begin) & 15u) == 0;
-  if (vec) {
+  if (m_ptr) {
+    const double mv = *m_ptr;
+#pragma unroll 4
+    for (int q = threadIdx.x; q < m; q += 32) s[q] = exp(xsub(__ldg(v + begin + q), mv));
+  } else if (vec) {
     const double2* src = reinterpret_cast<const double2*>(v + begin);
     double2* dst = reinterpret_cast<double2*>(s);
 #pragma unroll 8
@@ -170,22 +176,47 @@ __global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ 
 }
 
 // Serial combine of chunk partials (single thread): lse = m + log(sum).
-__global__ void k_finish_lse(const double* __restrict__ partial, int64_t n_chunks, const double* __restrict__ m_ptr,
-                             double* __restrict__ lse_out) {
+// Serial combines of the chunk partials (reduce.hpp order) by lane 0 of one
+// warp, after the warp has staged the partials in shared memory (coalesced).
+constexpr int kFinStage = 2048;
+__device__ __forceinline__ double serial_sum_staged(const double* __restrict__ a, int64_t n, double* s) {
   double t = 0.0;
-  for (int64_t c = 0; c < n_chunks; ++c) t = xadd(t, partial[c]);
-  *lse_out = xadd(*m_ptr, log(t));
+  for (int64_t b = 0; b < n; b += kFinStage) {
+    const int m = static_cast<int>(n - b < kFinStage ? n - b : kFinStage);
+    for (int q = threadIdx.x; q < m; q += 32) s[q] = a[b + q];
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      int q = 0;
+      for (; q + 8 <= m; q += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = s[q + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t = xadd(t, x[u]);
+      }
+      for (; q < m; ++q) t = xadd(t, s[q]);
+    }
+    __syncwarp();
+  }
+  return t;
 }
 
-__global__ void k_finish_sum2(const double* __restrict__ a, const double* __restrict__ b, int64_t n_chunks,
-                              double* __restrict__ out) {
-  double ta = 0.0, tb = 0.0;
-  for (int64_t c = 0; c < n_chunks; ++c) {
-    ta = xadd(ta, a[c]);
-    tb = xadd(tb, b[c]);
+__global__ void __launch_bounds__(32) k_finish_lse(const double* __restrict__ partial, int64_t n_chunks,
+                                                   const double* __restrict__ m_ptr, double* __restrict__ lse_out) {
+  __shared__ double s[kFinStage];
+  const double t = serial_sum_staged(partial, n_chunks, s);
+  if (threadIdx.x == 0) *lse_out = xadd(*m_ptr, log(t));
+}
+
+__global__ void __launch_bounds__(32) k_finish_sum2(const double* __restrict__ a, const double* __restrict__ b,
+                                                    int64_t n_chunks, double* __restrict__ out) {
+  __shared__ double s[kFinStage];
+  const double ta = serial_sum_staged(a, n_chunks, s);
+  const double tb = serial_sum_staged(b, n_chunks, s);
+  if (threadIdx.x == 0) {
+    out[0] = ta;
+    out[1] = tb;
   }
-  out[0] = ta;
-  out[1] = tb;
 }
 
 __global__ void k_apply_lse(double* __restrict__ v, int64_t n, const double* __restrict__ lse_ptr, double floor_v) {
@@ -292,19 +323,21 @@ void launch_max_of_partials(const double* pv, const long long* pi, int64_t n, do
 static void chunk_serial(const double* v, int64_t n, double* partial, cudaStream_t st) {
   count_launch();
   const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
-  if (chunks > 0) k_chunk_serial<<<static_cast<unsigned>(chunks), 32, 0, st>>>(v, v, n, chunks, partial, partial);
+  if (chunks > 0)
+    k_chunk_serial<<<static_cast<unsigned>(chunks), 32, 0, st>>>(v, v, n, chunks, partial, partial, nullptr);
 }
 static void chunk_serial2(const double* a, const double* b, int64_t n, double* pa, double* pb, cudaStream_t st) {
   count_launch();
   const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
-  if (chunks > 0) k_chunk_serial<<<static_cast<unsigned>(2 * chunks), 32, 0, st>>>(a, b, n, chunks, pa, pb);
+  if (chunks > 0) k_chunk_serial<<<static_cast<unsigned>(2 * chunks), 32, 0, st>>>(a, b, n, chunks, pa, pb, nullptr);
 }
 void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* scratch, double* partial,
                           cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
-  k_exp_shift<<<blocks_for(n, 256), 256, 0, st>>>(v, n, m, scratch);
-  chunk_serial(scratch, n, partial, st);
+  (void)scratch;  // exp(v - m) is computed while staging each chunk
+  const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
+  k_chunk_serial<<<static_cast<unsigned>(chunks), 32, 0, st>>>(v, v, n, chunks, partial, partial, m);
 }
 void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n, int k, double* s1, double* s2,
                              double* pk, double* pc, cudaStream_t st) {
@@ -315,11 +348,11 @@ void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n,
 }
 void launch_finish_lse(const double* partial, int64_t n_chunks, const double* m, double* lse, cudaStream_t st) {
   count_launch();
-  k_finish_lse<<<1, 1, 0, st>>>(partial, n_chunks, m, lse);
+  k_finish_lse<<<1, 32, 0, st>>>(partial, n_chunks, m, lse);
 }
 void launch_finish_sum2(const double* a, const double* b, int64_t n_chunks, double* out, cudaStream_t st) {
   count_launch();
-  k_finish_sum2<<<1, 1, 0, st>>>(a, b, n_chunks, out);
+  k_finish_sum2<<<1, 32, 0, st>>>(a, b, n_chunks, out);
 }
 void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, cudaStream_t st) {
   count_launch();
