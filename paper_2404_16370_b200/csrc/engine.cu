@@ -359,7 +359,8 @@ struct smcl_engine {
   DBuf<float> kval, kval2;
 
   // per-stage work
-  DBuf<double> sys, steps, phis, ll;
+  DBuf<double> sys, steps, phis, ll, raw_ll;  // sys: exact-path GN records (allocated on first use)
+  DBuf<float> sysf;                           // fast-path GN records (kSysF floats per particle)
   DBuf<int32_t> nm;
   bool steps_valid = false, phis_valid = false, ll_valid = false;
 
@@ -604,7 +605,8 @@ struct smcl_engine {
     idx2.ensure(un * kk);
     kval.ensure(un * kk);
     kval2.ensure(un * kk);
-    sys.ensure(un * kSysStride);
+    sysf.ensure(un * kSysF);
+    raw_ll.ensure(un);
     steps.ensure(un * 6);
     phis.ensure(un * 6);
     ll.ensure(un);
@@ -942,10 +944,11 @@ struct smcl_engine {
     fast_used = use_fast(sd);
     if (fast_used) {
       MapFast mf{geom, map_fast.p, map_brick};
-      launch_gicp_fast(gn, poses.p, n_local, sv, mf, sys.p, nm.p, st);
+      launch_gicp_fast(gn, poses.p, n_local, sv, mf, sysf.p, raw_ll.p, nm.p, st);
     } else {
       MapExact me{geom, cells.p, map_mu.p, map_sigma.p};
-      launch_gicp_exact(gn, poses.p, n_local, sv, me, sys.p, nm.p, st);
+      if (gn) sys.ensure(static_cast<size_t>(std::max<int64_t>(n_local, 1)) * kSysStride);
+      launch_gicp_exact(gn, poses.p, n_local, sv, me, sys.p, raw_ll.p, nm.p, st);
     }
     CK(cudaGetLastError());
     if (profiling) {
@@ -954,9 +957,10 @@ struct smcl_engine {
     }
     const GicpParamsDev gp = gicp_params(sd.n);
     if (gn)
-      launch_solve(sys.p, nm.p, n_local, gp, steps.p, ll.p, st);
+      launch_solve(fast_used ? nullptr : sys.p, fast_used ? sysf.p : nullptr, raw_ll.p, nm.p, n_local, gp, steps.p,
+                   ll.p, st);
     else
-      launch_gate_ll(sys.p, nm.p, n_local, gp, ll.p, st);
+      launch_gate_ll(raw_ll.p, nm.p, n_local, gp, ll.p, st);
     CK(cudaGetLastError());
     ll_valid = true;
     if (gn) steps_valid = true;
@@ -1801,15 +1805,24 @@ int smcl_evaluate_all(smcl_engine* h, const smcl_cloud* scan, double* step_out, 
     if (nm_out) h->nm.download(nm_out, n, h->st);
     if (H_out || b_out) {
       std::vector<double> sys(n * kSysStride);
-      h->sys.download(sys.data(), sys.size(), h->st);
-      h->sync();
-      for (size_t i = 0; i < n; ++i) {
-        if (H_out) {
-          std::memcpy(H_out + 36 * i, &sys[i * kSysStride], 36 * sizeof(double));
-          if (h->fast_used)  // the fast kernel writes the (authoritative) lower triangle only
-            for (int r = 0; r < 6; ++r)
-              for (int c = r + 1; c < 6; ++c) H_out[36 * i + r * 6 + c] = H_out[36 * i + c * 6 + r];
+      if (h->fast_used) {  // widen the fp32 record (lower triangle of H, b), mirror H
+        std::vector<float> f(n * kSysF);
+        h->sysf.download(f.data(), f.size(), h->st);
+        h->sync();
+        constexpr int off[27] = SMCL_FAST_SYS_OFF;
+        for (size_t i = 0; i < n; ++i) {
+          double* r = &sys[i * kSysStride];
+          for (int q = 0; q < kSysStride; ++q) r[q] = 0.0;
+          for (int q = 0; q < 27; ++q) r[off[q]] = static_cast<double>(f[i * kSysF + q]);
+          for (int a = 0; a < 6; ++a)
+            for (int c = a + 1; c < 6; ++c) r[a * 6 + c] = r[c * 6 + a];
         }
+      } else {
+        h->sys.download(sys.data(), sys.size(), h->st);
+        h->sync();
+      }
+      for (size_t i = 0; i < n; ++i) {
+        if (H_out) std::memcpy(H_out + 36 * i, &sys[i * kSysStride], 36 * sizeof(double));
         if (b_out) std::memcpy(b_out + 6 * i, &sys[i * kSysStride + 36], 6 * sizeof(double));
       }
     }

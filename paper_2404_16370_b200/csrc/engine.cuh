@@ -70,9 +70,17 @@ struct ScanView {
   double mu_l1_max;     // max_k |mu_k|_1, for the fp32 prefilter error bound
 };
 
-// Particle-point GN system accumulators as written by the likelihood kernels:
-// 36 (H row-major, lower triangle authoritative) + 6 (b) + ll_raw.
-constexpr int kSysStride = 43;
+// Per-particle GN system as written by the exact likelihood kernel: 36 (H
+// row-major) + 6 (b), fp64. The raw log-likelihood goes to its own array.
+constexpr int kSysStride = 42;
+// The fast kernel's record: its 27 fp32 accumulators (H lower triangle, b) and
+// the cost in lane order, padded to one 128-byte line per particle; the solve
+// widens them to fp64 exactly as the kernel's own conversion would.
+constexpr int kSysF = 32;
+// Lane q of the fast record -> offset in the 42-entry (H row-major, b) system.
+// htl -> H(r, c), c <= r < 3; htr(r, c) -> H(c+3, r); hbr -> H(r+3, c+3); b.
+#define SMCL_FAST_SYS_OFF                                                                                   \
+  {0, 6, 7, 12, 13, 14, 18, 24, 30, 19, 25, 31, 20, 26, 32, 21, 27, 28, 33, 34, 35, 36, 37, 38, 39, 40, 41}
 
 struct GicpParamsDev {
   double damping_scale, omega_max, v_max, miss_cost;
@@ -83,12 +91,13 @@ struct GicpParamsDev {
 // ---------------------------------------------------------------- launchers
 // likelihood.cu
 void launch_gicp_exact(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapExact& map,
-                       double* sys, int32_t* nm, cudaStream_t st);
-void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys,
-                      int32_t* nm, cudaStream_t st);
-void launch_solve(const double* sys, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* steps, double* ll,
-                  cudaStream_t st);
-void launch_gate_ll(const double* sys, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* ll,
+                       double* sys, double* raw_ll, int32_t* nm, cudaStream_t st);
+void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
+                      double* raw_ll, int32_t* nm, cudaStream_t st);
+// Exactly one of sys (exact record) / sysf (fast record) is non-null.
+void launch_solve(const double* sys, const float* sysf, const double* raw_ll, const int32_t* nm, int64_t n,
+                  const GicpParamsDev& p, double* steps, double* ll, cudaStream_t st);
+void launch_gate_ll(const double* raw_ll, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* ll,
                     cudaStream_t st);
 void launch_solve_batch(const double* H, const double* b, const double* lam, int64_t n, double omax, double vmax,
                         double* out, cudaStream_t st);

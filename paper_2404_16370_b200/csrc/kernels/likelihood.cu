@@ -101,7 +101,7 @@ __device__ __forceinline__ void transform_x(const Pose& P, const double mu[3], d
 template <bool GN>
 __global__ void __launch_bounds__(128) k_gicp_exact(const Pose* __restrict__ poses, int64_t n, ScanView scan,
                                                     MapExact map, double* __restrict__ sys,
-                                                    int32_t* __restrict__ nm_out) {
+                                                    double* __restrict__ raw_ll, int32_t* __restrict__ nm_out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const Pose P = poses[i];
@@ -163,8 +163,8 @@ __global__ void __launch_bounds__(128) k_gicp_exact(const Pose* __restrict__ pos
     ll = xsub(ll, xadd(xadd(xmul(e[0], oe[0]), xmul(e[1], oe[1])), xmul(e[2], oe[2])));
     ++nmatch;
   }
-  double* out = sys + i * kSysStride;
   if (GN) {
+    double* out = sys + i * kSysStride;
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(128) k_gicp_exact(const Pose* __restrict__ pos
 #pragma unroll
     for (int q = 0; q < 6; ++q) out[36 + q] = b[q];
   }
-  out[42] = nmatch == 0 ? -1e30 : ll;
+  raw_ll[i] = nmatch == 0 ? -1e30 : ll;
   nm_out[i] = nmatch;
 }
 
@@ -278,35 +278,53 @@ __device__ __forceinline__ double gated(const GicpParamsDev& p, double raw, int 
   return xsub(raw, xmul(p.miss_cost, xsub(static_cast<double>(p.scan_size), static_cast<double>(nm))));
 }
 
-__global__ void k_solve(const double* __restrict__ sys, const int32_t* __restrict__ nm, int64_t n, GicpParamsDev p,
-                        double* __restrict__ steps, double* __restrict__ ll) {
+// F32: the fast kernel's fp32 record (kSysF lanes), widened to fp64 as the
+// kernel's own conversion would; else the exact kernel's fp64 record. Only
+// the lower triangle of H is read (LLT, trace).
+template <bool F32>
+__global__ void k_solve(const double* __restrict__ sys, const float* __restrict__ sysf,
+                        const double* __restrict__ raw_ll, const int32_t* __restrict__ nm, int64_t n,
+                        GicpParamsDev p, double* __restrict__ steps, double* __restrict__ ll) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  const double* s = sys + i * kSysStride;
   const int m = nm[i];
-  ll[i] = gated(p, s[42], m);
+  ll[i] = gated(p, raw_ll[i], m);
   double step[6] = {0, 0, 0, 0, 0, 0};
   if (m != 0) {
-    double H[36], b[6];
+    double Hb[42];  // H row-major, b
+    if (F32) {
+      constexpr int off[27] = SMCL_FAST_SYS_OFF;
 #pragma unroll
-    for (int q = 0; q < 36; ++q) H[q] = s[q];
+      for (int q = 0; q < 42; ++q) Hb[q] = 0.0;
+      const float4* r = reinterpret_cast<const float4*>(sysf + i * kSysF);
+      float v[28];
 #pragma unroll
-    for (int q = 0; q < 6; ++q) b[q] = s[36 + q];
+      for (int q = 0; q < 7; ++q) {
+        const float4 a = __ldg(r + q);
+        v[4 * q] = a.x, v[4 * q + 1] = a.y, v[4 * q + 2] = a.z, v[4 * q + 3] = a.w;
+      }
+#pragma unroll
+      for (int q = 0; q < 27; ++q) Hb[off[q]] = static_cast<double>(v[q]);
+    } else {
+      const double* s = sys + i * kSysStride;
+#pragma unroll
+      for (int q = 0; q < 42; ++q) Hb[q] = s[q];
+    }
     double tr = 0.0;
 #pragma unroll
-    for (int q = 0; q < 6; ++q) tr = xadd(tr, H[q * 7]);
+    for (int q = 0; q < 6; ++q) tr = xadd(tr, Hb[q * 7]);
     const double lambda = xmul(p.damping_scale, tr) / 6.0;
-    solve_step_dev(H, b, lambda, p.omega_max, p.v_max, step);
+    solve_step_dev(Hb, Hb + 36, lambda, p.omega_max, p.v_max, step);
   }
 #pragma unroll
   for (int q = 0; q < 6; ++q) steps[6 * i + q] = step[q];
 }
 
-__global__ void k_gate(const double* __restrict__ sys, const int32_t* __restrict__ nm, int64_t n, GicpParamsDev p,
+__global__ void k_gate(const double* __restrict__ raw_ll, const int32_t* __restrict__ nm, int64_t n, GicpParamsDev p,
                        double* __restrict__ ll) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  ll[i] = gated(p, sys[i * kSysStride + 42], nm[i]);
+  ll[i] = gated(p, raw_ll[i], nm[i]);
 }
 
 __global__ void k_solve_batch(const double* __restrict__ H, const double* __restrict__ b,
@@ -326,27 +344,30 @@ inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n +
 }  // namespace
 
 void launch_gicp_exact(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapExact& map, double* sys,
-                       int32_t* nm, cudaStream_t st) {
+                       double* raw_ll, int32_t* nm, cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
   if (gn)
-    k_gicp_exact<true><<<blocks_for(n, 128), 128, 0, st>>>(poses, n, scan, map, sys, nm);
+    k_gicp_exact<true><<<blocks_for(n, 128), 128, 0, st>>>(poses, n, scan, map, sys, raw_ll, nm);
   else
-    k_gicp_exact<false><<<blocks_for(n, 128), 128, 0, st>>>(poses, n, scan, map, sys, nm);
+    k_gicp_exact<false><<<blocks_for(n, 128), 128, 0, st>>>(poses, n, scan, map, sys, raw_ll, nm);
 }
 
-void launch_solve(const double* sys, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* steps, double* ll,
-                  cudaStream_t st) {
+void launch_solve(const double* sys, const float* sysf, const double* raw_ll, const int32_t* nm, int64_t n,
+                  const GicpParamsDev& p, double* steps, double* ll, cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
-  k_solve<<<blocks_for(n, 128), 128, 0, st>>>(sys, nm, n, p, steps, ll);
+  if (sysf)
+    k_solve<true><<<blocks_for(n, 128), 128, 0, st>>>(nullptr, sysf, raw_ll, nm, n, p, steps, ll);
+  else
+    k_solve<false><<<blocks_for(n, 128), 128, 0, st>>>(sys, nullptr, raw_ll, nm, n, p, steps, ll);
 }
 
-void launch_gate_ll(const double* sys, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* ll,
+void launch_gate_ll(const double* raw_ll, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* ll,
                     cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
-  k_gate<<<blocks_for(n, 256), 256, 0, st>>>(sys, nm, n, p, ll);
+  k_gate<<<blocks_for(n, 256), 256, 0, st>>>(raw_ll, nm, n, p, ll);
 }
 
 void launch_solve_batch(const double* H, const double* b, const double* lam, int64_t n, double omax, double vmax,

@@ -203,18 +203,10 @@ __device__ __forceinline__ void transform_x(const double* R, const double* t, co
     p[i] = xadd(xadd(xadd(xmul(R[i * 3 + 0], mu[0]), xmul(R[i * 3 + 1], mu[1])), xmul(R[i * 3 + 2], mu[2])), t[i]);
 }
 
-// Lower-triangle / b / ll offsets of the 28 per-lane accumulators in the
-// per-particle system record (kSysStride layout: H row-major, b, ll).
-__constant__ int c_sys_off[28] = {0,  6,  7,  12, 13, 14,                 // htl -> H(r, c), c <= r < 3
-                                  18, 24, 30, 19, 25, 31, 20, 26, 32,     // htr(r, c) -> H(c+3, r)
-                                  21, 27, 28, 33, 34, 35,                 // hbr -> H(r+3, c+3)
-                                  36, 37, 38, 39, 40, 41,                 // b
-                                  42};                                    // ll
-
 template <bool GN, int kFastUnroll, int kWarps, int kBrick>
 __global__ void __launch_bounds__(kWarps * 32, 1)
-    k_gicp_fast(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, double* __restrict__ sys,
-                int32_t* __restrict__ nm_out) {
+    k_gicp_fast(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, float* __restrict__ sysf,
+                double* __restrict__ raw_ll, int32_t* __restrict__ nm_out) {
   constexpr int kStep = 32 * kFastUnroll;
   using Stage = WarpStage<kStep>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -370,7 +362,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     }
 
     // ---- epilogue: lane q ends up with the warp total of accumulator q
-    double* out = sys + i * kSysStride;
     if (GN) {
       float v[32];
 #pragma unroll
@@ -395,11 +386,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
         }
       }
-      if (lane < 27) out[c_sys_off[lane]] = static_cast<double>(v[0]);
-      if (lane == 27) out[42] = nmatch == 0 ? -1e30 : -static_cast<double>(v[0]);
+      // One 128-byte line per particle (lanes 28-31 hold zeros), widened to
+      // fp64 by the solve (SMCL_FAST_SYS_OFF).
+      sysf[i * kSysF + lane] = v[0];
+      if (lane == 27) raw_ll[i] = nmatch == 0 ? -1e30 : -static_cast<double>(v[0]);
     } else {
       const float cost = warp_sum(acc.cost);
-      if (lane == 0) out[42] = nmatch == 0 ? -1e30 : -static_cast<double>(cost);
+      if (lane == 0) raw_ll[i] = nmatch == 0 ? -1e30 : -static_cast<double>(cost);
     }
     if (lane == 0) nm_out[i] = nmatch;
     __syncwarp();
@@ -414,7 +407,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 // Costs are accumulated in fp64 per lane (~S terms, no warp reduction).
 template <int U, int kWarps, int kBrick>
 __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __restrict__ poses, int64_t n,
-                                                             ScanView scan, MapFast map, double* __restrict__ sys,
+                                                             ScanView scan, MapFast map,
+                                                             double* __restrict__ raw_ll,
                                                              int32_t* __restrict__ nm_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float4* stage = reinterpret_cast<float4*>(smem_raw);  // [kWarps][U][2][32]
@@ -525,7 +519,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
     __syncwarp();
   }
   if (active) {
-    sys[i * kSysStride + 42] = nmatch == 0 ? -1e30 : -cost;
+    raw_ll[i] = nmatch == 0 ? -1e30 : -cost;
     nm_out[i] = nmatch;
   }
 }
@@ -537,16 +531,16 @@ size_t ll_lanes_smem(int S) {
 }
 
 template <int U, int W>
-void launch_ll_lanes_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys, int32_t* nm,
-                       cudaStream_t st) {
+void launch_ll_lanes_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* raw_ll,
+                       int32_t* nm, cudaStream_t st) {
   const size_t smem = ll_lanes_smem<U, W>(scan.n);
   const unsigned grid = static_cast<unsigned>((n + W * 32 - 1) / (W * 32));
   if (map.brick) {
     cudaFuncSetAttribute(k_gicp_ll_lanes<U, W, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_gicp_ll_lanes<U, W, 1><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+    k_gicp_ll_lanes<U, W, 1><<<grid, W * 32, smem, st>>>(poses, n, scan, map, raw_ll, nm);
   } else {
     cudaFuncSetAttribute(k_gicp_ll_lanes<U, W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_gicp_ll_lanes<U, W, 0><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+    k_gicp_ll_lanes<U, W, 0><<<grid, W * 32, smem, st>>>(poses, n, scan, map, raw_ll, nm);
   }
 }
 
@@ -557,8 +551,8 @@ size_t fast_smem(int S) {
 }
 
 template <bool GN, int U, int W, int B>
-void launch_fast_tb(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys, int32_t* nm,
-                    cudaStream_t st) {
+void launch_fast_tb(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
+                    double* raw_ll, int32_t* nm, cudaStream_t st) {
   const size_t smem = fast_smem<U, W>(scan.n);
   int dev, n_sm, per_sm = 0;
   cudaGetDevice(&dev);
@@ -568,22 +562,22 @@ void launch_fast_tb(const Pose* poses, int64_t n, const ScanView& scan, const Ma
   const int64_t want = (n + W - 1) / W;
   const unsigned grid =
       static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(n_sm) * std::max(per_sm, 1)));
-  k_gicp_fast<GN, U, W, B><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sys, nm);
+  k_gicp_fast<GN, U, W, B><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sysf, raw_ll, nm);
 }
 
 template <bool GN, int U, int W>
-void launch_fast_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys, int32_t* nm,
-                   cudaStream_t st) {
-  map.brick ? launch_fast_tb<GN, U, W, 1>(poses, n, scan, map, sys, nm, st)
-            : launch_fast_tb<GN, U, W, 0>(poses, n, scan, map, sys, nm, st);
+void launch_fast_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf, double* raw_ll,
+                   int32_t* nm, cudaStream_t st) {
+  map.brick ? launch_fast_tb<GN, U, W, 1>(poses, n, scan, map, sysf, raw_ll, nm, st)
+            : launch_fast_tb<GN, U, W, 0>(poses, n, scan, map, sysf, raw_ll, nm, st);
 }
 
 }  // namespace
 
 // U points per lane in flight x W warps per SM (one CTA per SM).
 // SMCL_FAST_CFG=UxW overrides the default (tuning sweeps only).
-void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* sys,
-                      int32_t* nm, cudaStream_t st) {
+void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
+                      double* raw_ll, int32_t* nm, cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
   auto parse = [](const char* e) {
@@ -611,15 +605,15 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
   if (c >= 9000) {  // SMCL_FAST_CFG=9UWW: lane-per-particle variants (9000 = default 8 points x 8 warps)
     const int u = c == 9000 ? 8 : (c / 100) % 10, w = c == 9000 ? 8 : c % 100;
     if (!gn && u == 8 && w == 8 && ll_lanes_smem<8, 8>(scan.n) <= 227 * 1024) {
-      launch_ll_lanes_t<8, 8>(poses, n, scan, map, sys, nm, st);
+      launch_ll_lanes_t<8, 8>(poses, n, scan, map, raw_ll, nm, st);
       return;
     }
     if (!gn && u == 4 && w == 8 && ll_lanes_smem<4, 8>(scan.n) <= 227 * 1024) {
-      launch_ll_lanes_t<4, 8>(poses, n, scan, map, sys, nm, st);
+      launch_ll_lanes_t<4, 8>(poses, n, scan, map, raw_ll, nm, st);
       return;
     }
     if (!gn && u == 8 && w == 4 && ll_lanes_smem<8, 4>(scan.n) <= 227 * 1024) {
-      launch_ll_lanes_t<8, 4>(poses, n, scan, map, sys, nm, st);
+      launch_ll_lanes_t<8, 4>(poses, n, scan, map, raw_ll, nm, st);
       return;
     }
     c = gn ? 416 : 424;
@@ -627,8 +621,8 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
 #define FAST_CASE(U, W)                                                                    \
   case U * 100 + W:                                                                        \
     if (fast_smem<U, W>(scan.n) <= 227 * 1024) {                                           \
-      gn ? launch_fast_t<true, U, W>(poses, n, scan, map, sys, nm, st)                     \
-         : launch_fast_t<false, U, W>(poses, n, scan, map, sys, nm, st);                   \
+      gn ? launch_fast_t<true, U, W>(poses, n, scan, map, sysf, raw_ll, nm, st)            \
+         : launch_fast_t<false, U, W>(poses, n, scan, map, sysf, raw_ll, nm, st);          \
       return;                                                                              \
     }                                                                                      \
     break;
@@ -643,8 +637,8 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
       break;
   }
 #undef FAST_CASE
-  gn ? launch_fast_t<true, 4, 16>(poses, n, scan, map, sys, nm, st)
-     : launch_fast_t<false, 4, 16>(poses, n, scan, map, sys, nm, st);
+  gn ? launch_fast_t<true, 4, 16>(poses, n, scan, map, sysf, raw_ll, nm, st)
+     : launch_fast_t<false, 4, 16>(poses, n, scan, map, sysf, raw_ll, nm, st);
 }
 
 }  // namespace smcl
