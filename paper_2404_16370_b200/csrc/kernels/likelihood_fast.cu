@@ -243,23 +243,30 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     float Rf[9];
     bool huge;
     {
-      const Pose P = poses[i];
+      // Lane q < 12 loads pose word q (R row-major, then t) and writes its
+      // voxel-unit value; the fp32 rotation and the |x| bound are shared by
+      // shuffles.
+      const double pv = __ldg(reinterpret_cast<const double*>(poses + i) + (lane < 12 ? lane : 0));
+      const bool isR = lane < 9, isT = lane >= 9 && lane < 12;
+      const double o = lane == 9 ? g.origin[0] : (lane == 10 ? g.origin[1] : (lane == 11 ? g.origin[2] : 0.0));
+      const double centered = pv - o;
+      if (lane < 12) ws.pose_v[lane] = centered * g.inv_res;
+      const float rf = static_cast<float>(pv);
 #pragma unroll
-      for (int q = 0; q < 9; ++q) {
-        if (lane == q) ws.pose_v[q] = P.R[q] * g.inv_res;
-        Rf[q] = static_cast<float>(P.R[q]);
-      }
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-        if (lane == 9 + a) ws.pose_v[9 + a] = (P.t[a] - g.origin[a]) * g.inv_res;
+      for (int q = 0; q < 9; ++q) Rf[q] = __shfl_sync(0xffffffffu, rf, q);
       // |x| <= max|Rv| |mu|_1 + max|tv|: below 2^40 the round-down floor is
       // exact for every point; otherwise (or NaN) every point resolves.
-      double mr = 0.0, mt = 0.0;
+      float mr = isR ? fabsf(rf) : 0.f, mt = isT ? fabsf(static_cast<float>(centered)) : 0.f;
 #pragma unroll
-      for (int q = 0; q < 9; ++q) mr = fmax(mr, fabs(P.R[q]));
-#pragma unroll
-      for (int a = 0; a < 3; ++a) mt = fmax(mt, fabs(P.t[a] - g.origin[a]));
-      huge = !((mr * scan.mu_l1_max + mt) * g.inv_res < 1.0995e12);
+      for (int m = 8; m > 0; m >>= 1) {
+        mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, m));
+        mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, m));
+      }
+      mr = __shfl_sync(0xffffffffu, mr, 0);
+      mt = __shfl_sync(0xffffffffu, mt, 0);
+      huge = !((static_cast<double>(mr) * scan.mu_l1_max + static_cast<double>(mt)) * g.inv_res < 1.0995e12) ||
+             !(pv == pv);
+      huge = __any_sync(0xffffffffu, huge);
     }
     __syncwarp();
     Acc acc;
