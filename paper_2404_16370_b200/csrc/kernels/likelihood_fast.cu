@@ -598,9 +598,8 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
   static const int cfg_ll = parse(std::getenv("SMCL_FAST_CFG_LL") ? std::getenv("SMCL_FAST_CFG_LL")
                                                                    : std::getenv("SMCL_FAST_CFG"));
   const int cfg = gn ? cfg_gn : cfg_ll;
-  // Measured on B200 at 1M x 512 (profiles/README.md): the GN pass is
-  // register bound (128 regs, 16 warps); the likelihood-only pass needs 80
-  // registers and gains from 24 warps of latency hiding.
+  // Measured on B200 at 1M x 512 (profiles/README.md): GN pass 4.77 ms with
+  // 16 warps per SM, 4.57 ms with 24 (4x20: 4.63, 4x28 / 4x32 spill).
   // Likelihood pass: lane per particle when the record table is L2-resident;
   // for bricked (HBM-sized) tables a warp walks one particle's scan so its
   // gathers stay inside a few bricks (kidnap outdoor map: 4.8 -> 2.4 ms).
@@ -608,7 +607,9 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
   // The lane kernel needs two resident CTAs per SM (16 warps): scans too large
   // for that (S > ~900 points) take the warp-per-particle kernel as well.
   if (!gn && c == 0) c = (map.brick || 2 * ll_lanes_smem<8, 8>(scan.n) > 227 * 1024) ? 416 : 9000;
-  if (c == 0) c = 416;
+  // GN pass: 24 warps per SM (80 registers) where the scan fits in shared
+  // memory next to 24 warp stages (S <= ~1300), else 16.
+  if (c == 0) c = (gn && fast_smem<4, 24>(scan.n) <= 227 * 1024) ? 424 : 416;
   if (c >= 9000) {  // SMCL_FAST_CFG=9UWW: lane-per-particle variants (9000 = default 8 points x 8 warps)
     const int u = c == 9000 ? 8 : (c / 100) % 10, w = c == 9000 ? 8 : c % 100;
     if (!gn && u == 8 && w == 8 && ll_lanes_smem<8, 8>(scan.n) <= 227 * 1024) {
