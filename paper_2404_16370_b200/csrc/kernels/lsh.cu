@@ -489,8 +489,12 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
                                                             int k, int cap, double sr, double st) {
   extern __shared__ __align__(16) unsigned char rg_smem[];
   int32_t* s_idx = reinterpret_cast<int32_t*>(rg_smem);                  // [k][BLOCK]
-  float* s_kv = reinterpret_cast<float*>(s_idx + k * BLOCK);             // [k][BLOCK]
-  int32_t* s_cand = reinterpret_cast<int32_t*>(s_kv + k * BLOCK);        // [kRgChunk][BLOCK]
+  // List values per thread row [BLOCK][KMAX] (16-byte aligned rows: the
+  // weakest-entry scan reads them with 128-bit loads). Empty slots and the
+  // self slot hold +inf while the window is scanned, so the scan is a plain
+  // first-strict-minimum; self's 1.0f is restored on write-out.
+  float* s_kv = reinterpret_cast<float*>(s_idx + k * BLOCK);             // [BLOCK][KMAX]
+  int32_t* s_cand = reinterpret_cast<int32_t*>(s_kv + KMAX * BLOCK);     // [kRgChunk][BLOCK]
   float* s_ckv = reinterpret_cast<float*>(s_cand + kRgChunk * BLOCK);    // [kRgChunk][BLOCK]
   int32_t* s_gi = reinterpret_cast<int32_t*>(s_ckv + kRgChunk * BLOCK);  // [BLOCK]
   uint16_t* s_flat = reinterpret_cast<uint16_t*>(s_gi + BLOCK);          // [BLOCK/32][32*kRgChunk]
@@ -521,9 +525,11 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
       if (o >= 0 && o < q_end - rb) listed |= 1ull << o;
     }
     const Pose pi = ldg_pose(all_poses + gi);
-    for (int s = 0; s < cnt; ++s) {  // refresh (neighbor_graph.hpp:76-90)
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) s_kv[t * KMAX + s] = __int_as_float(0x7f800000);
+    for (int s = 0; s < cnt; ++s) {  // refresh (neighbor_graph.hpp:76-90); self stays +inf (see above)
       const int32_t j = s_idx[s * BLOCK + t];
-      s_kv[s * BLOCK + t] = (j == gi) ? 1.0f : kval_of(pi, ldg_pose(all_poses + j), sr, st);
+      if (j != gi) s_kv[t * KMAX + s] = kval_of(pi, ldg_pose(all_poses + j), sr, st);
     }
   }
   s_gi[t] = gi;
@@ -539,13 +545,17 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
   auto find_weakest = [&]() {  // first strict minimum (neighbor_graph.hpp:60-72)
     weakest = -1;
     wk = __int_as_float(0x7f800000);
+    const float4* row = reinterpret_cast<const float4*>(s_kv + t * KMAX);
 #pragma unroll
-    for (int s = 0; s < KMAX; ++s) {
-      const float v = s_kv[s * BLOCK + t];
-      if (s < cnt && s != self_slot && v < wk) {
-        wk = v;
-        weakest = s;
-      }
+    for (int v4 = 0; v4 < KMAX / 4; ++v4) {
+      const float4 a = row[v4];
+      const float vals[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (vals[u] < wk) {
+          wk = vals[u];
+          weakest = 4 * v4 + u;
+        }
     }
   };
   if (active && cnt == k) find_weakest();
@@ -601,13 +611,13 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
       const int32_t j = s_cand[s * BLOCK + t];
       if (cnt < k) {
         s_idx[cnt * BLOCK + t] = j;
-        s_kv[cnt * BLOCK + t] = kij;
+        s_kv[t * KMAX + cnt] = kij;
         ++cnt;
         if (cnt == k) find_weakest();
         continue;
       }
       s_idx[weakest * BLOCK + t] = j;
-      s_kv[weakest * BLOCK + t] = kij;
+      s_kv[t * KMAX + weakest] = kij;
       find_weakest();
     }
     __syncwarp();
@@ -616,7 +626,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
     count[li] = cnt;
     for (int s = 0; s < cnt; ++s) {
       idx[li * k + s] = s_idx[s * BLOCK + t];
-      kval[li * k + s] = s_kv[s * BLOCK + t];
+      kval[li * k + s] = s == self_slot ? 1.0f : s_kv[t * KMAX + s];
     }
   }
 }
@@ -760,10 +770,11 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
   if (n <= 0) return;
   static const bool filtered = std::getenv("SMCL_RG_PLAIN") == nullptr;
   if (filtered && k <= 32 && cap <= 64) {
-    const size_t smem = static_cast<size_t>(k) * B * 8 + static_cast<size_t>(kRgChunk) * B * 8 + B * 4 +
-                        static_cast<size_t>(B) * kRgChunk * 2;
 #define RGF(KM)                                                                                                   \
-  k_refresh_gather_f<B, KM><<<blocks_for(n, B), B, smem, st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, \
+  k_refresh_gather_f<B, KM><<<blocks_for(n, B), B,                                                                 \
+                              static_cast<size_t>(k) * B * 4 + static_cast<size_t>(KM) * B * 4 +                   \
+                                  static_cast<size_t>(kRgChunk) * B * 8 + B * 4 + static_cast<size_t>(B) * kRgChunk * 2, \
+                              st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, \
                                                                seg_start, n_sorted, pos_of, idx, kval,            \
                                                                count, k,                                          \
                                                                cap, sr, st_)
