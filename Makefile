@@ -11,7 +11,7 @@ LIB := $(PKG)/lib/libsmcl_gpu.so
 
 # -ffp-contract=off on the host side; device exact paths use __dmul_rn/__dadd_rn.
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++20 -ccbin $(HOSTCXX) --expt-relaxed-constexpr \
-           -Xcompiler -fPIC,-ffp-contract=off,-fopenmp -Xptxas -v
+           -Xcompiler -fPIC,-ffp-contract=off,-fopenmp -Xptxas -v $(EXTRA_NVFLAGS)
 CXXFLAGS := -std=c++20 -O3 -fPIC -fopenmp -ffp-contract=off -Wall -Wextra -Wno-unknown-pragmas
 
 CU_SRC := $(wildcard $(CSRC)/*.cu) $(wildcard $(CSRC)/kernels/*.cu)

@@ -115,10 +115,7 @@ __global__ void __launch_bounds__(128) k_reorder_k(const int32_t* __restrict__ o
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int64_t src = old_of_new[p];
-  const double2* ps = reinterpret_cast<const double2*>(poses + src);
-  double2* pd = reinterpret_cast<double2*>(poses2 + p);
-#pragma unroll
-  for (int v = 0; v < 6; ++v) pd[v] = __ldg(ps + v);
+  poses2[p] = ldg_pose(poses + src);
   lp2[p] = lp[src];
   id2[p] = id[src];
   const int c = count[src];

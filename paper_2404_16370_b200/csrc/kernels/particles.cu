@@ -222,12 +222,13 @@ void launch_svgd(const Pose* all_poses, const double* all_steps, int64_t n, int6
                  cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
-  // 5 CTAs x 4 warps per SM (96 registers): measured best on B200 (0.85 ms at 1M).
+  // 7 CTAs x 4 warps per SM (72 registers): measured best on B200 at 1M
+  // (MINB 4 / 5 / 6 / 7 / 8: 0.86 / 0.80 / 0.79 / 0.77 / 0.85 ms).
   if (poses_out)
-    k_svgd<true, 5><<<blocks_for(n, 128), 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out,
+    k_svgd<true, 7><<<blocks_for(n, 128), 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out,
                                                          poses_out);
   else
-    k_svgd<false, 5><<<blocks_for(n, 128), 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out,
+    k_svgd<false, 7><<<blocks_for(n, 128), 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out,
                                                           nullptr);
 }
 void launch_apply(Pose* poses, const double* phis, int64_t n, cudaStream_t st) {
