@@ -73,6 +73,20 @@ __device__ __forceinline__ void cp_async16_pred(void* smem, const void* gmem, bo
   else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
 }
+// One 32-byte record as a single 256-bit load (sm_100 LDG.256), predicated:
+// when !pred nothing is read and the record reads as empty (beta = -1).
+// One L1TEX request per record instead of two: random record gathers from
+// the L2-resident table reach 8.1 TB/s this way against 3.2 (two 16-byte
+// loads) or 4.6 (two 16-byte cp.async) — build/tools/micro_peaks.
+__device__ __forceinline__ void ldg_rec_pred(const float4* src, bool pred, float4& m0, float4& m1) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = -1.f, b0 = 0.f, b1 = 0.f, b2 = 0.f, b3 = 0.f;
+  asm("{\n .reg .pred p;\n setp.ne.u32 p, %9, 0;\n"
+      " @p ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n}"
+      : "+f"(a0), "+f"(a1), "+f"(a2), "+f"(a3), "+f"(b0), "+f"(b1), "+f"(b2), "+f"(b3)
+      : "l"(src), "r"(static_cast<unsigned>(pred)));
+  m0 = make_float4(a0, a1, a2, a3);
+  m1 = make_float4(b0, b1, b2, b3);
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -412,15 +426,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 // point is warp-uniform (broadcast shared-memory reads), each lane gathers its
 // own particle's cell record (U points per lane in flight through cp.async).
 // Costs are accumulated in fp64 per lane (~S terms, no warp reduction).
-template <int U, int kWarps, int kBrick>
-__global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __restrict__ poses, int64_t n,
+// kLdg: records gathered straight into registers with one predicated 256-bit
+// load each (no shared-memory stage); else two 16-byte cp.async per record.
+template <int U, int kWarps, int kBrick, bool kLdg, int kMinB = 1>
+__global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose* __restrict__ poses, int64_t n,
                                                              ScanView scan, MapFast map,
                                                              double* __restrict__ raw_ll,
                                                              int32_t* __restrict__ nm_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float4* stage = reinterpret_cast<float4*>(smem_raw);  // [kWarps][U][2][32]
+  float4* stage = reinterpret_cast<float4*>(smem_raw);  // [kWarps][U][2][32] (cp.async variant)
   const int S = scan.n;
-  float4* s_r0 = stage + kWarps * U * 2 * 32;  // S: mu.xyz, gamma
+  float4* s_r0 = stage + (kLdg ? 0 : kWarps * U * 2 * 32);  // S: mu.xyz, gamma
   float4* s_r1 = s_r0 + S;                     // S: u.xyz, s
   double* s_mu = reinterpret_cast<double*>(s_r1 + S);
   for (int q = threadIdx.x; q < S; q += blockDim.x) {
@@ -463,6 +479,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
   for (int base = 0; base < S; base += U) {
     float fr[U][3];
     uint32_t st[U];  // bit 0 staged, bit 1 resolve
+    float4 rm0[kLdg ? U : 1], rm1[kLdg ? U : 1];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int k = base + u;
@@ -486,14 +503,19 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
       st[u] = (stg ? 1u : 0u) | (real && amb ? 2u : 0u);
       const uint64_t cell = stg ? rec_index<kBrick>(map, ic[0], ic[1], ic[2]) : 0u;
       const float4* src = map.rec + 2 * cell;
-      cp_async16_pred<kBrick != 0>(&ws[(u * 2) * 32 + lane], src, stg);
-      cp_async16_pred<kBrick != 0>(&ws[(u * 2 + 1) * 32 + lane], src + 1, stg);
+      if (kLdg) {
+        ldg_rec_pred(src, stg, rm0[kLdg ? u : 0], rm1[kLdg ? u : 0]);
+      } else {
+        cp_async16_pred<kBrick != 0>(&ws[(u * 2) * 32 + lane], src, stg);
+        cp_async16_pred<kBrick != 0>(&ws[(u * 2 + 1) * 32 + lane], src + 1, stg);
+      }
     }
-    cp_async_wait_all();
+    if (!kLdg) cp_async_wait_all();
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int k = base + u;
-      float4 m0 = ws[(u * 2) * 32 + lane], m1 = ws[(u * 2 + 1) * 32 + lane];
+      float4 m0 = kLdg ? rm0[kLdg ? u : 0] : ws[(u * 2) * 32 + lane];
+      float4 m1 = kLdg ? rm1[kLdg ? u : 0] : ws[(u * 2 + 1) * 32 + lane];
       bool valid = (st[u] & 1u) != 0;
       if (st[u] & 2u) {  // reference-order transform, floor and bounds (nnf.hpp:24-35)
         const Pose P = poses[i];
@@ -531,23 +553,25 @@ __global__ void __launch_bounds__(kWarps * 32) k_gicp_ll_lanes(const Pose* __res
   }
 }
 
-template <int U, int W>
+template <int U, int W, bool kLdg = false>
 size_t ll_lanes_smem(int S) {
-  return sizeof(float4) * (static_cast<size_t>(W) * U * 2 * 32 + 2 * static_cast<size_t>(S)) +
+  return sizeof(float4) * ((kLdg ? 0 : static_cast<size_t>(W) * U * 2 * 32) + 2 * static_cast<size_t>(S)) +
          sizeof(double) * 3 * static_cast<size_t>(S);
 }
 
-template <int U, int W>
+template <int U, int W, bool kLdg, int kMinB = 1>
 void launch_ll_lanes_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* raw_ll,
                        int32_t* nm, cudaStream_t st) {
-  const size_t smem = ll_lanes_smem<U, W>(scan.n);
+  const size_t smem = ll_lanes_smem<U, W, kLdg>(scan.n);
   const unsigned grid = static_cast<unsigned>((n + W * 32 - 1) / (W * 32));
   if (map.brick) {
-    cudaFuncSetAttribute(k_gicp_ll_lanes<U, W, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_gicp_ll_lanes<U, W, 1><<<grid, W * 32, smem, st>>>(poses, n, scan, map, raw_ll, nm);
+    cudaFuncSetAttribute(k_gicp_ll_lanes<U, W, 1, kLdg, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    k_gicp_ll_lanes<U, W, 1, kLdg, kMinB><<<grid, W * 32, smem, st>>>(poses, n, scan, map, raw_ll, nm);
   } else {
-    cudaFuncSetAttribute(k_gicp_ll_lanes<U, W, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_gicp_ll_lanes<U, W, 0><<<grid, W * 32, smem, st>>>(poses, n, scan, map, raw_ll, nm);
+    cudaFuncSetAttribute(k_gicp_ll_lanes<U, W, 0, kLdg, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    k_gicp_ll_lanes<U, W, 0, kLdg, kMinB><<<grid, W * 32, smem, st>>>(poses, n, scan, map, raw_ll, nm);
   }
 }
 
@@ -606,23 +630,45 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
   int c = cfg;
   // The lane kernel needs two resident CTAs per SM (16 warps): scans too large
   // for that (S > ~900 points) take the warp-per-particle kernel as well.
-  if (!gn && c == 0) c = (map.brick || 2 * ll_lanes_smem<8, 8>(scan.n) > 227 * 1024) ? 416 : 9000;
+  if (!gn && c == 0) c = (map.brick || 4 * ll_lanes_smem<1, 8, true>(scan.n) > 227 * 1024) ? 416 : 9000;
   // GN pass: 24 warps per SM (80 registers) where the scan fits in shared
   // memory next to 24 warp stages (S <= ~1300), else 16.
   if (c == 0) c = (gn && fast_smem<4, 24>(scan.n) <= 227 * 1024) ? 424 : 416;
-  if (c >= 9000) {  // SMCL_FAST_CFG=9UWW: lane-per-particle variants (9000 = default 8 points x 8 warps)
-    const int u = c == 9000 ? 8 : (c / 100) % 10, w = c == 9000 ? 8 : c % 100;
-    if (!gn && u == 8 && w == 8 && ll_lanes_smem<8, 8>(scan.n) <= 227 * 1024) {
-      launch_ll_lanes_t<8, 8>(poses, n, scan, map, raw_ll, nm, st);
+  if (c >= 9000) {  // SMCL_FAST_CFG=LUxW: lane-per-particle variants (9000 = default)
+    static const bool ldg = std::getenv("SMCL_LL_CPASYNC") == nullptr;
+    // Default: one record in flight per lane, 8-warp CTAs, 4 CTAs (32 warps)
+    // per SM: 2.79 ms at 1M x 512 (cp.async 8 x 8: 3.43; LDG 2 x 8: 2.91;
+    // 4 x 8: 3.23; 1 x 8 at 5 / 6 CTAs spills: 3.33 / 3.42).
+    if (c == 9000) {
+      launch_ll_lanes_t<1, 8, true, 4>(poses, n, scan, map, raw_ll, nm, st);
       return;
     }
-    if (!gn && u == 4 && w == 8 && ll_lanes_smem<4, 8>(scan.n) <= 227 * 1024) {
-      launch_ll_lanes_t<4, 8>(poses, n, scan, map, raw_ll, nm, st);
-      return;
+    const int u = (c / 100) % 10, w = c % 100;
+#define LL_CASE(UU, WW)                                                                         \
+    if (!gn && u == UU && w == WW && ll_lanes_smem<UU, WW>(scan.n) <= 227 * 1024) {            \
+      ldg ? launch_ll_lanes_t<UU, WW, true>(poses, n, scan, map, raw_ll, nm, st)               \
+          : launch_ll_lanes_t<UU, WW, false>(poses, n, scan, map, raw_ll, nm, st);             \
+      return;                                                                                  \
     }
-    if (!gn && u == 8 && w == 4 && ll_lanes_smem<8, 4>(scan.n) <= 227 * 1024) {
-      launch_ll_lanes_t<8, 4>(poses, n, scan, map, raw_ll, nm, st);
-      return;
+    LL_CASE(8, 8)
+    LL_CASE(4, 8)
+    LL_CASE(2, 8)
+    LL_CASE(2, 16)
+    LL_CASE(3, 8)
+#undef LL_CASE
+    if (!gn && (u == 2 || u == 1) && w >= 80) {  // SMCL_FAST_CFG_LL=L2x84 / L1x84: 8 warps, >= 4 CTAs per SM
+      const int mb = w - 80;
+      if (u == 2 && mb == 4) return launch_ll_lanes_t<2, 8, true, 4>(poses, n, scan, map, raw_ll, nm, st);
+      if (u == 2 && mb == 5) return launch_ll_lanes_t<2, 8, true, 5>(poses, n, scan, map, raw_ll, nm, st);
+      if (u == 1 && mb == 4) return launch_ll_lanes_t<1, 8, true, 4>(poses, n, scan, map, raw_ll, nm, st);
+      if (u == 1 && mb == 5) return launch_ll_lanes_t<1, 8, true, 5>(poses, n, scan, map, raw_ll, nm, st);
+      if (u == 1 && mb == 6) return launch_ll_lanes_t<1, 8, true, 6>(poses, n, scan, map, raw_ll, nm, st);
+    }
+    if (!gn && u == 1 && w >= 40 && w < 80) {  // L1x4M: 4 warps per CTA, >= M CTAs per SM
+      const int mb = w - 40;
+      if (mb == 8) return launch_ll_lanes_t<1, 4, true, 8>(poses, n, scan, map, raw_ll, nm, st);
+      if (mb == 10) return launch_ll_lanes_t<1, 4, true, 10>(poses, n, scan, map, raw_ll, nm, st);
+      if (mb == 12) return launch_ll_lanes_t<1, 4, true, 12>(poses, n, scan, map, raw_ll, nm, st);
     }
     c = gn ? 416 : 424;
   }

@@ -57,6 +57,55 @@ __global__ void k_gather(const float4* __restrict__ rec, uint64_t n_rec, int per
   if (acc == -1.2345f) out[0] = acc;
 }
 
+// Same access, one 256-bit load per record (sm_100 LDG.256).
+__global__ void k_gather256(const double* __restrict__ rec, uint64_t n_rec, int per_thread, uint64_t seed,
+                            float* __restrict__ out) {
+  uint64_t s = seed ^ (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 0x9E3779B97F4A7C15ull;
+  double acc = 0.0;
+  for (int i = 0; i < per_thread; i += 8) {
+    double r[8][4];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s ^= s << 13;
+      s ^= s >> 7;
+      s ^= s << 17;
+      const uint64_t c = s % n_rec;
+      asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                   : "=d"(r[u][0]), "=d"(r[u][1]), "=d"(r[u][2]), "=d"(r[u][3])
+                   : "l"(rec + 4 * c));
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += r[u][0] + r[u][3];
+  }
+  if (acc == -1.2345) out[0] = static_cast<float>(acc);
+}
+
+// Same access through cp.async (two 16-byte async copies per record into a
+// per-thread shared-memory stage), as the likelihood kernels issue it.
+__global__ void k_gather_cpasync(const float4* __restrict__ rec, uint64_t n_rec, int per_thread, uint64_t seed,
+                                 float* __restrict__ out) {
+  __shared__ float4 stage[128 * 16];  // launched with 128 threads
+  uint64_t s = seed ^ (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 0x9E3779B97F4A7C15ull;
+  float acc = 0.f;
+  for (int i = 0; i < per_thread; i += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s ^= s << 13;
+      s ^= s >> 7;
+      s ^= s << 17;
+      const uint64_t c = s % n_rec;
+      const unsigned d0 = static_cast<unsigned>(__cvta_generic_to_shared(&stage[(2 * u) * 128 + threadIdx.x]));
+      const unsigned d1 = static_cast<unsigned>(__cvta_generic_to_shared(&stage[(2 * u + 1) * 128 + threadIdx.x]));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d0), "l"(rec + 2 * c) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d1), "l"(rec + 2 * c + 1) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += stage[(2 * u) * 128 + threadIdx.x].x + stage[(2 * u + 1) * 128 + threadIdx.x].w;
+  }
+  if (acc == -1.2345f) out[0] = acc;
+}
+
 int main() {
   int dev = 0, n_sm = 0, clk = 0;
   CK(cudaSetDevice(dev));
@@ -99,6 +148,12 @@ int main() {
     const float ms = time_ms([&] { k_gather<<<gblocks, gthreads>>>(rec, n_rec, per, 12345ull, out); });
     const double gbs = 32.0 * gblocks * gthreads * per / (ms * 1e-3) / 1e9;
     std::printf(", \"gather_%s_gbs\": %.1f", names[t], gbs);
+    const float ms2 = time_ms([&] {
+      k_gather256<<<gblocks, gthreads>>>(reinterpret_cast<const double*>(rec), n_rec, per, 12345ull, out);
+    });
+    std::printf(", \"gather256_%s_gbs\": %.1f", names[t], 32.0 * gblocks * gthreads * per / (ms2 * 1e-3) / 1e9);
+    const float ms3 = time_ms([&] { k_gather_cpasync<<<2 * gblocks, 128>>>(rec, n_rec, per, 12345ull, out); });
+    std::printf(", \"gather_cpasync_%s_gbs\": %.1f", names[t], 32.0 * gblocks * gthreads * per / (ms3 * 1e-3) / 1e9);
     CK(cudaFree(rec));
   }
   CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev));
