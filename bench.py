@@ -381,8 +381,12 @@ def main():
     gp = gather_peaks() if rank == 0 else None
     roof_gather = None
     if gp:
-        key = "gather_hbm_7GB_gbs" if args.workload == "kidnap" else "gather_l2_resident_49MB_gbs"
-        peak_g = gp.get(key)
+        # The best measured access method (two 16-B loads, one 256-bit load,
+        # two 16-B cp.async) is the achievable roof.
+        table = "hbm_7GB" if args.workload == "kidnap" else "l2_resident_49MB"
+        cands = {k: v for k, v in gp.items() if isinstance(v, (int, float)) and k.endswith(table + "_gbs")}
+        key = max(cands, key=cands.get) if cands else None
+        peak_g = cands.get(key) if key else None
         if peak_g:
             roof_gather = {"kernel": roof["kernel"], "achieved": roof["achieved"], "peak": peak_g, "unit": "GB/s",
                            "frac": roof["achieved"] / peak_g, "peak_kind": key, "peaks": gp}

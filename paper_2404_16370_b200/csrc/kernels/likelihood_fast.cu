@@ -217,7 +217,7 @@ __device__ __forceinline__ void transform_x(const double* R, const double* t, co
     p[i] = xadd(xadd(xadd(xmul(R[i * 3 + 0], mu[0]), xmul(R[i * 3 + 1], mu[1])), xmul(R[i * 3 + 2], mu[2])), t[i]);
 }
 
-template <bool GN, int kFastUnroll, int kWarps, int kBrick>
+template <bool GN, int kFastUnroll, int kWarps, int kBrick, bool kLdg = false>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     k_gicp_fast(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, float* __restrict__ sysf,
                 double* __restrict__ raw_ll, int32_t* __restrict__ nm_out) {
@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     for (int base = 0; base < S; base += kStep) {
       // ---- phase A: fp64 cell + exact fraction, predicated async gather
       double Rv[9], tv[3];
+      float4 rm0[kLdg ? kFastUnroll : 1], rm1[kLdg ? kFastUnroll : 1];  // kLdg: records in flight
 #pragma unroll
       for (int q = 0; q < 9; ++q) Rv[q] = ws.pose_v[q];
 #pragma unroll
@@ -321,12 +322,24 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         const bool stage = !amb && inb;  // padded points are NaN: never staged
         const uint64_t cell = stage ? rec_index<kBrick>(map, ic[0], ic[1], ic[2]) : 0u;
         const float4* src = map.rec + 2 * cell;
-        cp_async16_pred<kBrick != 0>(&ws.m0[slot], src, stage);
-        cp_async16_pred<kBrick != 0>(&ws.m1[slot], src + 1, stage);
+        if (kLdg) {
+          ldg_rec_pred(src, stage, rm0[kLdg ? u : 0], rm1[kLdg ? u : 0]);
+        } else {
+          cp_async16_pred<kBrick != 0>(&ws.m0[slot], src, stage);
+          cp_async16_pred<kBrick != 0>(&ws.m1[slot], src + 1, stage);
+        }
         const uint32_t meta = static_cast<uint32_t>(k) | (stage ? kMetaStage : 0u) | (resolve ? kMetaResolve : 0u);
         ws.fq[slot] = make_float4(fr[0], fr[1], fr[2], __uint_as_float(meta));
       }
-      cp_async_wait_all();
+      if (kLdg) {
+#pragma unroll
+        for (int u = 0; u < kFastUnroll; ++u) {
+          ws.m0[u * 32 + lane] = rm0[kLdg ? u : 0];
+          ws.m1[u * 32 + lane] = rm1[kLdg ? u : 0];
+        }
+      } else {
+        cp_async_wait_all();
+      }
       __syncwarp();
       // ---- compaction of the candidate slots (records stay in place)
       int n_cand = 0;
@@ -581,19 +594,32 @@ size_t fast_smem(int S) {
   return sizeof(WarpStage<32 * U>) * W + sizeof(float4) * 2 * Sp + sizeof(double) * 3 * Sp;
 }
 
-template <bool GN, int U, int W, int B>
-void launch_fast_tb(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
+template <bool GN, int U, int W, int B, bool L>
+void launch_fast_tbl(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
                     double* raw_ll, int32_t* nm, cudaStream_t st) {
   const size_t smem = fast_smem<U, W>(scan.n);
   int dev, n_sm, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(k_gicp_fast<GN, U, W, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gicp_fast<GN, U, W, B>, W * 32, smem);
+  cudaFuncSetAttribute(k_gicp_fast<GN, U, W, B, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gicp_fast<GN, U, W, B, L>, W * 32, smem);
   const int64_t want = (n + W - 1) / W;
   const unsigned grid =
       static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(n_sm) * std::max(per_sm, 1)));
-  k_gicp_fast<GN, U, W, B><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sysf, raw_ll, nm);
+  k_gicp_fast<GN, U, W, B, L><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sysf, raw_ll, nm);
+}
+
+template <bool GN, int U, int W, int B>
+void launch_fast_tb(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
+                    double* raw_ll, int32_t* nm, cudaStream_t st) {
+  // Record gathers: the GN pass keeps cp.async (issue bound: 4.57 ms against
+  // 5.25 with 256-bit loads + shared stores); the likelihood-only warp variant
+  // (bricked HBM-sized tables) gathers with 256-bit loads (outdoor kidnap LL
+  // 2.49-2.72 ms against 2.82-2.88; HBM cp.async gathers measure 0.73 TB/s
+  // against 1.34 for loads).
+  static const bool ldg = GN ? std::getenv("SMCL_K1_LDG") != nullptr : std::getenv("SMCL_K2W_CPASYNC") == nullptr;
+  ldg ? launch_fast_tbl<GN, U, W, B, true>(poses, n, scan, map, sysf, raw_ll, nm, st)
+      : launch_fast_tbl<GN, U, W, B, false>(poses, n, scan, map, sysf, raw_ll, nm, st);
 }
 
 template <bool GN, int U, int W>

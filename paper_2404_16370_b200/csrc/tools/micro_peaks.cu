@@ -2,7 +2,8 @@
 // carry: FP32 and FP64 FMA throughput, and the random 32-byte
 // record gather bandwidth of the likelihood kernels, from an L2-resident table
 // (the corridor map's 49 MB of NNF records) and from an HBM-sized table (the
-// outdoor map's 7 GB). Prints one JSON object.
+// outdoor map's 7 GB), for three ways of issuing the gather (two 16-byte
+// loads, one 256-bit load, two 16-byte cp.async). Prints one JSON object.
 //
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o micro_peaks micro_peaks.cu
 #include <cuda_runtime.h>
@@ -157,8 +158,9 @@ int main() {
     CK(cudaFree(rec));
   }
   CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev));
-  std::printf(", \"sm_count\": %d, \"note\": \"random 32-byte record gathers (two 16-B __ldg per record, 8 records "
-              "in flight per thread), %d CTAs x 256 threads\"}\n",
+  std::printf(", \"sm_count\": %d, \"note\": \"random 32-byte record gathers, 8 records in flight per thread, %d "
+              "CTAs x 256 threads: gather_ = two 16-B __ldg per record, gather256_ = one 256-bit ld.global.nc.v4.f64, "
+              "gather_cpasync_ = two 16-B cp.async.cg into shared memory\"}\n",
               n_sm, n_sm * 8);
   return 0;
 }
