@@ -220,6 +220,7 @@ def roofline(prof_avg, hbm_peak, peak_kind, ms_kernels, workload="global_init"):
     # capture (profiles/r01_dram_traffic.json); the map records are L2-resident,
     # so DRAM traffic is a small fraction of the algorithmic gather bytes.
     traffic = None
+    issue = None
     try:
         if workload != "global_init":  # the committed capture is of the global_init workload
             raise LookupError
@@ -227,12 +228,16 @@ def roofline(prof_avg, hbm_peak, peak_kind, ms_kernels, workload="global_init"):
             t = json.load(f)["kernels"].get(name)
         if t:
             traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+            if "ipc_issued" in t:  # the kernel's actual limiter: instruction issue (4 per SM per cycle)
+                issue = {"kernel": name, "achieved_ipc": t["ipc_issued"], "peak_ipc": 4.0,
+                         "frac": t["issue_pct_of_peak"] / 100.0,
+                         "source": "profiles/r01_dram_traffic.json (ncu --set full, sm__inst_issued)"}
     except Exception:
         traffic = None
     return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_kind,
             "algorithmic_bytes_per_launch": nbytes, "kernel_ms": ms,
-            "traffic_source": "profiles/r01_dram_traffic.json (ncu --set full, bytes per launch)"}
+            "traffic_source": "profiles/r01_dram_traffic.json (ncu --set full, bytes per launch)", "issue": issue}
 
 
 def main():

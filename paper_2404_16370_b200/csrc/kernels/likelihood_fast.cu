@@ -656,7 +656,7 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
   int c = cfg;
   // The lane kernel needs two resident CTAs per SM (16 warps): scans too large
   // for that (S > ~900 points) take the warp-per-particle kernel as well.
-  if (!gn && c == 0) c = (map.brick || 4 * ll_lanes_smem<1, 8, true>(scan.n) > 227 * 1024) ? 416 : 9000;
+  if (!gn && c == 0) c = (map.brick || 3 * ll_lanes_smem<1, 8, true>(scan.n) > 227 * 1024) ? 416 : 9000;
   // GN pass: 24 warps per SM (80 registers) where the scan fits in shared
   // memory next to 24 warp stages (S <= ~1300), else 16.
   if (c == 0) c = (gn && fast_smem<4, 24>(scan.n) <= 227 * 1024) ? 424 : 416;
@@ -665,8 +665,11 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
     // Default: one record in flight per lane, 8-warp CTAs, 4 CTAs (32 warps)
     // per SM: 2.79 ms at 1M x 512 (cp.async 8 x 8: 3.43; LDG 2 x 8: 2.91;
     // 4 x 8: 3.23; 1 x 8 at 5 / 6 CTAs spills: 3.33 / 3.42).
-    if (c == 9000) {
-      launch_ll_lanes_t<1, 8, true, 4>(poses, n, scan, map, raw_ll, nm, st);
+    if (c == 9000) {  // 3 CTAs per SM when 4 do not fit next to the scan (S > ~1000)
+      if (4 * ll_lanes_smem<1, 8, true>(scan.n) <= 227 * 1024)
+        launch_ll_lanes_t<1, 8, true, 4>(poses, n, scan, map, raw_ll, nm, st);
+      else
+        launch_ll_lanes_t<1, 8, true, 3>(poses, n, scan, map, raw_ll, nm, st);
       return;
     }
     const int u = (c / 100) % 10, w = c % 100;

@@ -107,6 +107,44 @@ __global__ void k_gather_cpasync(const float4* __restrict__ rec, uint64_t n_rec,
   if (acc == -1.2345f) out[0] = acc;
 }
 
+// Same access through the bulk-copy (TMA) engine: one 32-byte
+// cp.async.bulk per record into shared memory, completion counted by a
+// per-thread mbarrier (expect-tx of the 8 records' bytes).
+__global__ void k_gather_bulk(const float4* __restrict__ rec, uint64_t n_rec, int per_thread, uint64_t seed,
+                              float* __restrict__ out) {
+  __shared__ __align__(16) float4 stage[128 * 16];  // launched with 128 threads
+  __shared__ __align__(8) unsigned long long bar[128];
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(&bar[threadIdx.x]));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  uint64_t s = seed ^ (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 0x9E3779B97F4A7C15ull;
+  float acc = 0.f;
+  unsigned phase = 0;
+  for (int i = 0; i < per_thread; i += 8) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(8 * 32) : "memory");
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s ^= s << 13;
+      s ^= s >> 7;
+      s ^= s << 17;
+      const uint64_t c = s % n_rec;
+      const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(&stage[(threadIdx.x * 8 + u) * 2]));
+      asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], 32, [%2];" ::"r"(d),
+                   "l"(rec + 2 * c), "r"(b)
+                   : "memory");
+    }
+    asm volatile(
+        "{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra WAIT_%=;\n}" ::"r"(b),
+        "r"(phase)
+        : "memory");
+    phase ^= 1u;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += stage[(threadIdx.x * 8 + u) * 2].x;
+  }
+  if (acc == -1.2345f) out[0] = acc;
+}
+
 int main() {
   int dev = 0, n_sm = 0, clk = 0;
   CK(cudaSetDevice(dev));
@@ -155,12 +193,15 @@ int main() {
     std::printf(", \"gather256_%s_gbs\": %.1f", names[t], 32.0 * gblocks * gthreads * per / (ms2 * 1e-3) / 1e9);
     const float ms3 = time_ms([&] { k_gather_cpasync<<<2 * gblocks, 128>>>(rec, n_rec, per, 12345ull, out); });
     std::printf(", \"gather_cpasync_%s_gbs\": %.1f", names[t], 32.0 * gblocks * gthreads * per / (ms3 * 1e-3) / 1e9);
+    const float ms4 = time_ms([&] { k_gather_bulk<<<2 * gblocks, 128>>>(rec, n_rec, per, 12345ull, out); });
+    std::printf(", \"gather_bulk_%s_gbs\": %.1f", names[t], 32.0 * gblocks * gthreads * per / (ms4 * 1e-3) / 1e9);
     CK(cudaFree(rec));
   }
   CK(cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev));
   std::printf(", \"sm_count\": %d, \"note\": \"random 32-byte record gathers, 8 records in flight per thread, %d "
               "CTAs x 256 threads: gather_ = two 16-B __ldg per record, gather256_ = one 256-bit ld.global.nc.v4.f64, "
-              "gather_cpasync_ = two 16-B cp.async.cg into shared memory\"}\n",
+              "gather_cpasync_ = two 16-B cp.async.cg into shared memory, gather_bulk_ = one 32-B "
+              "cp.async.bulk (TMA) per record\"}\n",
               n_sm, n_sm * 8);
   return 0;
 }

@@ -29,7 +29,9 @@ def traffic(rep, out, src):
     rows = list(csv.reader(raw.splitlines()))
     h = rows[0]
     ki = h.index("Kernel Name")
-    cols = {m: h.index(m) for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum")}
+    cols = {m: h.index(m) for m in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+                                    "sm__inst_issued.avg.per_cycle_active",
+                                    "sm__inst_issued.avg.pct_of_peak_sustained_active")}
     units = rows[1]
     res = {}
     names = {"k_refresh_gather": "refresh_gather", "k_gicp_fast": "gicp_gn (K1)", "k_gicp_ll": "gicp_ll (K2)"}
@@ -44,7 +46,11 @@ def traffic(rep, out, src):
             if pat in r[ki] and nm not in res:
                 res[nm] = {"dram_read_bytes": val(r, "dram__bytes_read.sum"),
                            "dram_write_bytes": val(r, "dram__bytes_write.sum"),
-                           "ncu_duration_ms": val(r, "gpu__time_duration.sum"), "kernel": r[ki][:80]}
+                           "ncu_duration_ms": val(r, "gpu__time_duration.sum"),
+                           "ipc_issued": float(r[cols["sm__inst_issued.avg.per_cycle_active"]].replace(",", "")),
+                           "issue_pct_of_peak": float(
+                               r[cols["sm__inst_issued.avg.pct_of_peak_sustained_active"]].replace(",", "")),
+                           "kernel": r[ki][:80]}
     json.dump({"source": src, "kernels": res}, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
