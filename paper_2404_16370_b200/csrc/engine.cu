@@ -367,6 +367,8 @@ struct smcl_engine {
   // lsh
   DBuf<uint64_t> keys, skeys;
   DBuf<int32_t> member_of, head, seg_id, seg_start, new_of_old, iota, pos_of_buf;
+  DBuf<float4> pose_mirror;        // fp32 poses for the neighbour-pass window filter
+  DBuf<unsigned int> mirror_tmax;  // max |t - anchor| (float bits) of that mirror
   DBuf<unsigned char> temp;
   size_t temp_bytes = 0;
   DBuf<unsigned long long> d_hist, d_counts;
@@ -1088,8 +1090,13 @@ struct smcl_engine {
       launch_inverse_perm(members, n, pos_of_buf.p, st);
       pos_of = pos_of_buf.p;
     }
+    pose_mirror.ensure(3 * static_cast<size_t>(n));
+    mirror_tmax.ensure(1);
+    const double anchor[3] = {0.5 * (bounds[0] + bounds[3]), 0.5 * (bounds[1] + bounds[4]),
+                              0.5 * (bounds[2] + bounds[5])};
     launch_refresh_gather(poses_all, n_local, gbase, owned, members, seg_id.p, seg_start.p, n, pos_of, idx.p,
-                          kval.p, count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, st);
+                          kval.p, count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, anchor,
+                          pose_mirror.p, mirror_tmax.p, st);
     CK(cudaGetLastError());
     if (profiling) mark(E_RG);
     // statistics (neighbor_search.cpp:172-190)

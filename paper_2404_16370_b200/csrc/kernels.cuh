@@ -85,7 +85,8 @@ void launch_owned_scatter(const int32_t* flag, const int32_t* incl, int64_t n, i
 void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, const int32_t* pos_list,
                            const int32_t* member_of, const int32_t* seg_id, const int32_t* seg_start,
                            int64_t n_sorted, const int32_t* pos_of, int32_t* idx, float* kval, int32_t* count, int k,
-                           int cap, double sr, double st_, cudaStream_t st);
+                           int cap, double sr, double st_, const double anchor[3], float4* mir,
+                           unsigned int* tmax_bits, cudaStream_t st);
 
 // map_build.cu (device map load: NNF + fast-map records)
 cudaError_t build_nnf_device(const double* d_mu, int64_t n, const double pg_org[3], const int pg_dims[3],

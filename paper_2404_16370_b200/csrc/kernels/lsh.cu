@@ -453,6 +453,28 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather(const Pose* __restrict
   }
 }
 
+// fp32 mirror of the poses for the window filter: (R0..R3), (R4..R7),
+// (R8, t - c) with c a per-pass anchor, plus max |t - c|_inf of all particles
+// (float bits, atomicMax) that sizes the filter's rounding margin.
+__global__ void k_pose_mirror(const Pose* __restrict__ poses, int64_t n, double3 c, float4* __restrict__ mir,
+                              unsigned int* __restrict__ tmax_bits) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  float tm = 0.f;
+  if (i < n) {
+    const Pose p = ldg_pose(poses + i);
+    const float t0 = static_cast<float>(p.t[0] - c.x), t1 = static_cast<float>(p.t[1] - c.y),
+                t2 = static_cast<float>(p.t[2] - c.z);
+    mir[3 * i] = make_float4(p.R[0], p.R[1], p.R[2], p.R[3]);
+    mir[3 * i + 1] = make_float4(p.R[4], p.R[5], p.R[6], p.R[7]);
+    mir[3 * i + 2] = make_float4(p.R[8], t0, t1, t2);
+    tm = fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2)));
+    if (!(tm <= 3.0e38f)) tm = 3.0e38f;  // NaN / inf poses: the margin becomes useless (filter passes all)
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+  if ((threadIdx.x & 31) == 0 && tm > 0.f) atomicMax(tmax_bits, __float_as_uint(tm));
+}
+
 // Filtered variant of k_refresh_gather (same results). Once the list is full,
 // a candidate is inserted only if its float kernel value beats the weakest
 // entry wk, and wk never decreases during the window scan. The reference's
@@ -483,7 +505,9 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
                                                             int64_t n_sorted, const int32_t* __restrict__ pos_of,
                                                             int32_t* __restrict__ idx,
                                                             float* __restrict__ kval, int32_t* __restrict__ count,
-                                                            int k, int cap, double sr, double st) {
+                                                            int k, int cap, double sr, double st,
+                                                            const float4* __restrict__ mir,
+                                                            const unsigned int* __restrict__ tmax_bits) {
   extern __shared__ __align__(16) unsigned char rg_smem[];
   int32_t* s_idx = reinterpret_cast<int32_t*>(rg_smem);                  // [k][BLOCK]
   // List values per thread row [BLOCK][KMAX] (16-byte aligned rows: the
@@ -530,6 +554,21 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
     }
   }
   s_gi[t] = gi;
+  // Rounding margins of the fp32 filter. Mirror rotations carry 2^-24 relative
+  // error per entry: |tr32 - tr| <= 4e-6. Mirror translations (|t - c| <=
+  // tmax) carry tmax 2^-24 each: |dt32 - dt| <= eps = tmax 2^-22 per axis;
+  // where the bound can matter (st |dt|^2 <= 110 + margin) |dt| <= D =
+  // sqrt(120 / st), so |uu32 - uu| <= 2 sqrt(3) D eps + 3 eps^2 + 3 D^2 2^-22.
+  const float sr32 = static_cast<float>(sr), st32 = static_cast<float>(st);
+  float mt, mL;
+  {
+    const double tmax = static_cast<double>(__uint_as_float(*tmax_bits));
+    const double eps = tmax * 0x1p-22, D = sqrt(120.0 / st);
+    const double duu = 2.0 * 1.7320508075688772 * D * eps + 3.0 * eps * eps + 3.0 * D * D * 0x1p-22;
+    mt = static_cast<float>(st * duu * 1.01 + 1e-6);
+    mL = static_cast<float>(sr * 4e-6 + st * duu * 1.01 + 1e-5);
+    if (!(mL < 1e30f)) mt = mL = 3.0e38f;  // huge or non-finite poses: filter off
+  }
   // Self never leaves its slot (offers never evict it): locate it once, so the
   // weakest-entry scan reads only values. Loops run over KMAX >= k slots,
   // unrolled and predicated.
@@ -564,22 +603,24 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
     if (full && wk > 0.0f) thr = -log(static_cast<double>(wk));
     int ns = 0;
     if (active) {
-      const Pose pi = ldg_pose(all_poses + gi);
+      // fp32 bound on the mirror: L32 - margin > thr proves L > thr (and
+      // st |dt|^2 - margin_t > 110 proves the translation underflow).
+      const float thr32 = static_cast<float>(thr);
+      const float4 a0 = __ldg(mir + 3 * gi), a1 = __ldg(mir + 3 * gi + 1), a2 = __ldg(mir + 3 * gi + 2);
       for (; q < q_end && ns < kRgChunk; ++q) {
         if ((listed >> (q - rb)) & 1ull) continue;  // listed: a duplicate offer (also self)
         const int32_t j = member_of[q];
         if (j == gi) continue;
         if (full) {
           if (weakest < 0) continue;  // self-only full list (k == 1): nothing evictable
-          const Pose pj = ldg_pose(all_poses + j);
-          const double d0 = xsub(pj.t[0], pi.t[0]), d1 = xsub(pj.t[1], pi.t[1]), d2 = xsub(pj.t[2], pi.t[2]);
-          const double uu = xadd(xadd(xmul(d0, d0), xmul(d1, d1)), xmul(d2, d2));
-          if (xmul(st, uu) > 110.0) continue;  // kernel_underflows: k = 0 <= wk
-          double tr = 0.0;
-#pragma unroll
-          for (int e = 0; e < 9; ++e) tr = fma(pi.R[e], pj.R[e], tr);
-          const double L = fma(sr, 3.0 - tr, st * uu);
-          if (L * (1.0 - 1e-6) - 1e-6 > thr) continue;  // float(exp(-q)) <= wk: dropped
+          const float4 b0 = __ldg(mir + 3 * j), b1 = __ldg(mir + 3 * j + 1), b2 = __ldg(mir + 3 * j + 2);
+          const float d0 = b2.y - a2.y, d1 = b2.z - a2.z, d2 = b2.w - a2.w;
+          const float uu = fmaf(d0, d0, fmaf(d1, d1, d2 * d2));
+          if (fmaf(st32, uu, -mt) > 110.0f) continue;  // kernel_underflows: k = 0 <= wk
+          const float tr = fmaf(a0.x, b0.x, fmaf(a0.y, b0.y, fmaf(a0.z, b0.z, a0.w * b0.w))) +
+                           fmaf(a1.x, b1.x, fmaf(a1.y, b1.y, fmaf(a1.z, b1.z, a1.w * b1.w))) + a2.x * b2.x;
+          const float L = fmaf(sr32, 3.0f - tr, st32 * uu);
+          if (L * (1.0f - 1e-5f) - mL > thr32) continue;  // float(exp(-q)) <= wk: dropped
         }
         s_cand[ns * BLOCK + t] = j;
         ++ns;
@@ -761,12 +802,19 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                            const int32_t* member_of,
                            const int32_t* seg_id, const int32_t* seg_start, int64_t n_sorted,
                            const int32_t* pos_of, int32_t* idx, float* kval, int32_t* count, int k, int cap,
-                           double sr, double st_, cudaStream_t st) {
+                           double sr, double st_, const double anchor[3], float4* mir, unsigned int* tmax_bits,
+                           cudaStream_t st) {
   count_launch();
   constexpr int B = 64;
   if (n <= 0) return;
   static const bool filtered = std::getenv("SMCL_RG_PLAIN") == nullptr;
   if (filtered && k <= 32 && cap <= 64) {
+    // fp32 pose mirror of every particle (the window members may be any shard's)
+    count_launch();
+    cudaMemsetAsync(tmax_bits, 0, sizeof(unsigned int), st);
+    k_pose_mirror<<<blocks_for(n_sorted, 256), 256, 0, st>>>(all_poses, n_sorted,
+                                                            make_double3(anchor[0], anchor[1], anchor[2]), mir,
+                                                            tmax_bits);
 #define RGF(KM)                                                                                                   \
   k_refresh_gather_f<B, KM><<<blocks_for(n, B), B,                                                                 \
                               static_cast<size_t>(k) * B * 4 + static_cast<size_t>(KM) * B * 4 +                   \
@@ -774,7 +822,7 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                               st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, \
                                                                seg_start, n_sorted, pos_of, idx, kval,            \
                                                                count, k,                                          \
-                                                               cap, sr, st_)
+                                                               cap, sr, st_, mir, tmax_bits)
     if (k <= 8)
       RGF(8);
     else if (k <= 20)
