@@ -472,7 +472,14 @@ __global__ void k_pose_mirror(const Pose* __restrict__ poses, int64_t n, double3
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
-  if ((threadIdx.x & 31) == 0 && tm > 0.f) atomicMax(tmax_bits, __float_as_uint(tm));
+  __shared__ float wmax[8];  // launched with 256 threads: one atomic per block
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = tm;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = 0.f;
+    for (int w = 0; w < 8; ++w) b = fmaxf(b, wmax[w]);
+    if (b > 0.f) atomicMax(tmax_bits, __float_as_uint(b));
+  }
 }
 
 // Filtered variant of k_refresh_gather (same results). Once the list is full,
