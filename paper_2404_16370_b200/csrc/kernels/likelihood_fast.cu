@@ -658,8 +658,10 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
   // for that (S > ~900 points) take the warp-per-particle kernel as well.
   if (!gn && c == 0) c = (map.brick || 3 * ll_lanes_smem<1, 8, true>(scan.n) > 227 * 1024) ? 416 : 9000;
   // GN pass: 24 warps per SM (80 registers) where the scan fits in shared
-  // memory next to 24 warp stages (S <= ~1300), else 16.
-  if (c == 0) c = (gn && fast_smem<4, 24>(scan.n) <= 227 * 1024) ? 424 : 416;
+  // memory next to 24 warp stages (S <= ~1300), else 16. Bricked (HBM-sized)
+  // tables keep 16 warps: their L1-allocating gathers need the L1 that 8 more
+  // warp stages would take (outdoor kidnap GN 2.43 -> 2.31 ms, LL 2.55 -> 2.32).
+  if (c == 0) c = (gn && !map.brick && fast_smem<4, 24>(scan.n) <= 227 * 1024) ? 424 : 416;
   if (c >= 9000) {  // SMCL_FAST_CFG=LUxW: lane-per-particle variants (9000 = default)
     static const bool ldg = std::getenv("SMCL_LL_CPASYNC") == nullptr;
     // Default: one record in flight per lane, 8-warp CTAs, 4 CTAs (32 warps)
