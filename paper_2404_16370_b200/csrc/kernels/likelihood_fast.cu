@@ -9,7 +9,8 @@
 // add of 1.5*2^52, the exact fractional coordinate f = x - floor(x) goes to
 // shared memory as fp32 (its 1e-8 m resolution is below the fp32 map record
 // precision). x differs from the reference's ((R mu + t) - o) * inv_res
-// (nnf.hpp:24-35) by < 1e-12 voxel, so the cell is the reference's unless f is
+// (nnf.hpp:24-35) by < 2.2e-8 voxel (coordinates below 2^26 voxels; beyond,
+// every point resolves), so the cell is the reference's unless f is
 // within ~5e-8 of a face (frac_clear_of_faces): such points "resolve" in phase B through the
 // reference-order fp64 transform. In-bounds points start a cp.async of their
 // 32-byte cell record into the warp's stage, so U x 2 16-byte gathers per lane
@@ -191,7 +192,8 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
 // f = x - floor(x) at least ~5e-8 from both cell faces: 2^-24 <= f < 1 - 2^-21,
 // decided on the high word of f with one unsigned range test (integer pipe;
 // NaN and negative values fail). The transform differs from the reference's
-// by < 1e-12 voxel, so such a point's cell is the reference's.
+// by < 2.2e-8 voxel (the per-particle resolve bound), so such a point's cell
+// is the reference's.
 __device__ __forceinline__ bool frac_clear_of_faces(double f) {
   return static_cast<unsigned>(__double2hiint(f)) - 0x3E700000u < 0x3FEFFFFFu - 0x3E700000u;
 }
@@ -268,9 +270,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       const float rf = static_cast<float>(pv);
 #pragma unroll
       for (int q = 0; q < 9; ++q) Rf[q] = __shfl_sync(0xffffffffu, rf, q);
-      // |x| <= max|Rv| |mu|_1 + max|tv|: below 2^40 the round-down floor is
-      // exact for every point; otherwise (or NaN) every point resolves.
-      float mr = isR ? fabsf(rf) : 0.f, mt = isT ? fabsf(static_cast<float>(centered)) : 0.f;
+      // Resolve every point (NaN too) unless (max|R| |mu|_1 + max(|t| + |o|))
+      // / res < 2^26: the reference forms p = R mu + t in world coordinates,
+      // whose rounding (~3 ulp of |t| + |R mu|, plus p - o) stays below 2.2e-8
+      // voxel there, inside the 5e-8 face margin; the round-down floor needs
+      // |x| < 2^40 (implied).
+      float mr = isR ? fabsf(rf) : 0.f,
+            mt = isT ? fabsf(static_cast<float>(pv)) + fabsf(static_cast<float>(o)) : 0.f;
 #pragma unroll
       for (int m = 8; m > 0; m >>= 1) {
         mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, m));
@@ -278,7 +284,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       }
       mr = __shfl_sync(0xffffffffu, mr, 0);
       mt = __shfl_sync(0xffffffffu, mt, 0);
-      huge = !((static_cast<double>(mr) * scan.mu_l1_max + static_cast<double>(mt)) * g.inv_res < 1.0995e12) ||
+      huge = !((static_cast<double>(mr) * scan.mu_l1_max + static_cast<double>(mt)) * g.inv_res < 6.7e7) ||
              !(pv == pv);
       huge = __any_sync(0xffffffffu, huge);
     }
@@ -480,12 +486,12 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) tv[a] = (P.t[a] - g.origin[a]) * g.inv_res;
-    double mr = 0.0, mt = 0.0;  // |x| bound, as in k_gicp_fast
+    double mr = 0.0, mt = 0.0;  // resolve bound, as in k_gicp_fast
 #pragma unroll
     for (int q = 0; q < 9; ++q) mr = fmax(mr, fabs(P.R[q]));
 #pragma unroll
-    for (int a = 0; a < 3; ++a) mt = fmax(mt, fabs(P.t[a] - g.origin[a]));
-    huge = !((mr * scan.mu_l1_max + mt) * g.inv_res < 1.0995e12);
+    for (int a = 0; a < 3; ++a) mt = fmax(mt, fabs(P.t[a]) + fabs(g.origin[a]));
+    huge = !((mr * scan.mu_l1_max + mt) * g.inv_res < 6.7e7);
   }
   double cost = 0.0;
   int nmatch = 0;

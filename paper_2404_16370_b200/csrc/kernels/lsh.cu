@@ -353,8 +353,17 @@ __device__ __forceinline__ float kval_fast(const Pose& a, const Pose& b, double 
     *ok = false;
     return 0.0f;
   }
+  // The reference forms u as Ra^T tb + (-Ra^T ta) (se3.hpp inverse, compose):
+  // both products are of size |t|, so its u carries up to ~10 ulp(|t|) of
+  // cancellation error that this u = Ra^T (tb - ta) does not. The guard grows
+  // with it: |dq| <= st F (2 |u| du sqrt 3 + 3 du^2), F = |V^-1|^2 <= pi^2/4,
+  // du = 4e-15 (|ta| + |tb|), |u| <= (1 + |u|^2) / 2.
+  const double T = fmax(fmax(fabs(a.t[0]), fabs(a.t[1])), fabs(a.t[2])) +
+                   fmax(fmax(fabs(b.t[0]), fabs(b.t[1])), fabs(b.t[2]));
+  const double du = 4e-15 * T;
+  const double gq = 4e-12 + st * 2.5 * fma(3.5 * du, 0.5 * (1.0 + uu), 3.0 * du * du);
   const double k = exp(-q);
-  const float lo = __double2float_rn(k * (1.0 - 4e-12)), hi = __double2float_rn(k * (1.0 + 4e-12));
+  const float lo = __double2float_rn(k * (1.0 - gq)), hi = __double2float_rn(k * (1.0 + gq));
   *ok = lo == hi;
   return hi;
 }

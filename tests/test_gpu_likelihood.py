@@ -173,3 +173,28 @@ def test_fast_paths_ragged_scan_sizes(scene, S):
         assert np.array_equal(ll[~m], ll2[~m])
         if m.any():
             assert np.all(np.abs(ll[m] - ll2[m]) <= TOL_LL * np.abs(ll2[m]))
+
+
+@pytest.mark.parametrize("offset", [2.0e4, 3.0e6])
+def test_fast_paths_far_from_origin(scene, offset):
+    """The same room and particles translated far from the origin (e.g. a map
+    in UTM coordinates): the reference's world-frame rounding grows with |t|,
+    so the fast kernels must still pick the reference's cells (n_matched exact)
+    — at 3e6 m every point takes the resolve path."""
+    mapc, scan, parts, om = scene
+    from paper_2404_16370_b200.abi import Particles
+    m2 = GaussianCloud(mapc.mu + offset, mapc.sigma, mapc.bounds + offset)
+    om2 = O.OracleMap(m2.mu, m2.sigma, m2.bounds, 0.2, 0.5, 1.0)
+    poses = parts.poses.copy()
+    poses[:, 9:] += offset
+    q = Particles.from_poses(poses, parts.k)
+    e = FilterEngine(m2, config(nnf_resolution=0.2, likelihood_mode=2))
+    e.set_particles(q)
+    ll, nm = e.evaluate_likelihoods(scan)
+    ll2, nm2 = O.evaluate_likelihoods(om2, scan.mu, scan.sigma, poses, config())
+    assert np.array_equal(nm, nm2) and (nm > 0).sum() > 100
+    _, llg, nmg = e.evaluate_all(scan)
+    _, llg2, nmg2 = O.evaluate_all(om2, scan.mu, scan.sigma, poses, config())
+    assert np.array_equal(nmg, nmg2)
+    m = ll2 > -1e29
+    assert np.all(np.abs(ll[m] - ll2[m]) <= TOL_LL * np.abs(ll2[m]))

@@ -166,6 +166,31 @@ def test_update_neighbors_matches_oracle(reorder):
     assert np.array_equal(got.poses, r.poses)
 
 
+@pytest.mark.parametrize("case", ["offset", "outliers", "dense"])
+def test_update_neighbors_filter_margins(case):
+    """The window filter runs in fp32 on a pose mirror with a rounding margin
+    sized by the largest translation: lists stay bit-identical to the oracle
+    far from the origin, with outliers that blow the margin up, and in dense
+    buckets where most offers compete (small rotation spread, 2 m cube)."""
+    n, side, ang, off = {"offset": (600, 6.0, 0.3, 5000.0), "outliers": (600, 6.0, 0.3, 0.0),
+                         "dense": (800, 2.0, 0.05, 0.0)}[case]
+    g = random_cube_set(n, side, ang, 20, 71)
+    g.poses[:, 9:] += off
+    if case == "outliers":
+        g.poses[:3, 9] = [1e6, -2e6, 3e7]
+    bounds = [off, off, off, off + side, off + side, off + side]
+    cfg = make_config(lsh_bucket_capacity=32 if case == "dense" else 64)
+    r = g.copy()
+    e = _stage_engine(g, lsh_bucket_capacity=cfg.lsh_bucket_capacity)
+    for p in range(4):
+        seed = O.mix_seed(73, p)
+        e.update_neighbors(seed, bounds)
+        O.update_neighbors(r, cfg, seed, bounds)
+    got = e.particles()
+    assert np.array_equal(got.idx, r.idx) and np.array_equal(got.kval, r.kval)
+    assert np.array_equal(got.count, r.count) and np.array_equal(got.id, r.id)
+
+
 def test_update_neighbors_oracle_serial_twin():
     """test_neighbor_search.cpp:234-257 on the oracle itself (parallel == serial)."""
     cfg = make_config()
