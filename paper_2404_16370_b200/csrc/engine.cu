@@ -285,6 +285,7 @@ struct smcl_engine {
   DBuf<double> g_argv;
   DBuf<long long> g_argi;
   DBuf<Pose> g_rep;
+  DBuf<double> rep_stage;  // representative: value, index, pose, id
   DBuf<int32_t> g_repid;
 
   // All-gather `bytes` per rank from send (device) into recv (device).
@@ -440,6 +441,11 @@ struct smcl_engine {
   cudaStream_t aux = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   NbHost* nb_host = nullptr;
+  struct StepHost {  // end-of-step reads (pinned)
+    double rep[16];
+    unsigned long long cnt[6];
+  };
+  StepHost* step_host = nullptr;
   DBuf<unsigned long long> nb_hist;
   DBuf<double> nb_s1, nb_s2, nb_p1, nb_p2, nb_sum;
   smcl_neighbor_stats* nb_out = nullptr;
@@ -483,6 +489,7 @@ struct smcl_engine {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (nb_host) cudaFreeHost(nb_host);
+    if (step_host) cudaFreeHost(step_host);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : timer)
@@ -1237,34 +1244,42 @@ struct smcl_engine {
   }
 
   void representative(int64_t* index, double* pose, double* value) {
+    representative_enqueue();
+    sync();
+    representative_read(index, pose, value);
+  }
+  // Value, index, pose and id of the winner gathered on the device into one
+  // staging record, read back into pinned memory (no host round trip until
+  // the caller's sync).
+  void representative_enqueue() {
     if (n_local == 0) throw std::invalid_argument("representative: empty or mismatched particle set");
     global_argmax(4, 1);
-    double v;
-    long long ix;
-    CK(cudaMemcpyAsync(&v, scal.p + 4, sizeof(double), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&ix, scal_i.p + 1, sizeof(long long), cudaMemcpyDeviceToHost, st));
-    g_d2h += sizeof(double) + sizeof(long long);
-    sync();
-    *index = ix;
-    *value = v;
-    // The owner rank publishes the winner's pose and id (one slot per rank).
-    const int64_t owner = sharded ? ix / n_local : 0;
-    const int64_t li = ix - owner * n_local;
-    if (sharded) {
-      const int64_t mine = owner == rank ? li : 0;
-      CK(cudaMemcpyAsync(g_rep.p + rank, poses.p + mine, sizeof(Pose), cudaMemcpyDeviceToDevice, st));
-      CK(cudaMemcpyAsync(g_repid.p + rank, id.p + mine, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    rep_stage.ensure(16);
+    if (sharded) {  // the owner rank publishes the winner's pose and id (one slot per rank)
+      launch_rep_local(scal.p + 4, scal_i.p + 1, n_local, rank, true, poses.p, id.p, g_rep.p + rank,
+                       g_repid.p + rank, nullptr, st);
       allgather(g_rep.p + rank, g_rep.p, sizeof(Pose));
       allgather(g_repid.p + rank, g_repid.p, sizeof(int32_t));
+      launch_rep_select(scal.p + 4, scal_i.p + 1, n_local, world, g_rep.p, g_repid.p, rep_stage.p, st);
+    } else {
+      launch_rep_local(scal.p + 4, scal_i.p + 1, n_local, 0, false, poses.p, id.p, nullptr, nullptr, rep_stage.p, st);
     }
-    const Pose* src_pose = sharded ? g_rep.p + owner : poses.p + li;
-    const int32_t* src_id = sharded ? g_repid.p + owner : id.p + li;
-    Pose p;
-    CK(cudaMemcpyAsync(&p, src_pose, sizeof(Pose), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(&rep_id, src_id, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    g_d2h += sizeof(Pose) + sizeof(int32_t);
-    sync();
-    if (pose) store_pose(p, pose);
+    CK(cudaMemcpyAsync(step_host->rep, rep_stage.p, sizeof(double) * 15, cudaMemcpyDeviceToHost, st));
+    g_d2h += sizeof(double) * 15;
+  }
+  void representative_read(int64_t* index, double* pose, double* value) {  // after a sync
+    const double* h = step_host->rep;
+    *value = h[0];
+    long long ix;
+    std::memcpy(&ix, &h[1], sizeof(ix));
+    *index = ix;
+    rep_id = static_cast<int32_t>(h[14]);
+    if (pose) {
+      Pose p;
+      for (int q = 0; q < 9; ++q) p.R[q] = h[2 + q];
+      for (int a = 0; a < 3; ++a) p.t[a] = h[11 + a];
+      store_pose(p, pose);
+    }
   }
 
   void init_uniform(int64_t n, const double* b, bool full_rotation, uint64_t seed) {
@@ -1355,13 +1370,16 @@ struct smcl_engine {
     mark(E_END);
     int64_t ix;
     double v;
-    representative(&ix, r.representative, &v);
-    unsigned long long cnt[6];
+    representative_enqueue();
     join_aux();
-    d_counts.download(cnt, 6, st);
+    CK(cudaMemcpyAsync(step_host->cnt, d_counts.p, sizeof(unsigned long long) * 6, cudaMemcpyDeviceToHost, st));
+    g_d2h += sizeof(unsigned long long) * 6;
+    sync();  // the step's one end-of-frame host synchronisation
+    representative_read(&ix, r.representative, &v);
+    unsigned long long cnt[6];
+    std::memcpy(cnt, step_host->cnt, sizeof(cnt));
     const int32_t rid = rep_id;
     cnt[1] = last_nm_sum;  // global sum of n_matched (bayes)
-    sync();
     finish_nb_stats();
     if (!empty) {  // last (or only) Gauss-Newton iteration
       t_gn += since(E_GN0, E_GN1);
@@ -1434,6 +1452,7 @@ smcl_engine* make_engine(const smcl_cloud* map, const smcl_config* cfg, int devi
   CK(cudaEventCreateWithFlags(&e->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&e->ev_join, cudaEventDisableTiming));
   CK(cudaMallocHost(reinterpret_cast<void**>(&e->nb_host), sizeof(smcl_engine::NbHost)));
+  CK(cudaMallocHost(reinterpret_cast<void**>(&e->step_host), sizeof(smcl_engine::StepHost)));
   for (int q = 0; q < SMCL_MAX_SCAN_SLOTS; ++q) e->slots.push_back(std::make_unique<smcl_engine::ScanSlot>());
   e->k = cfg->k_neighbors;
   if (map) e->setup_map(map);

@@ -289,7 +289,54 @@ __global__ void __launch_bounds__(128) k_smooth_round_k(const double* __restrict
   q[i] = num / den;
 }
 
+// Representative (posterior.cpp:99-108) without a host round trip: the
+// winning index is read on the device. Stage layout: [0] value, [1] index
+// (bits), [2..13] pose, [14] id (as double).
+__global__ void k_rep_local(const double* __restrict__ v_ptr, const long long* __restrict__ ix_ptr, int64_t n_local,
+                            int rank, int sharded, const Pose* __restrict__ poses, const int32_t* __restrict__ id,
+                            Pose* __restrict__ dst_pose, int32_t* __restrict__ dst_id, double* __restrict__ stage) {
+  const long long ix = *ix_ptr;
+  const long long owner = sharded ? ix / n_local : 0;
+  const long long li = ix - owner * n_local;
+  const long long mine = (owner == rank && li >= 0 && li < n_local) ? li : 0;
+  if (sharded) {  // this rank's slot of the all-gathered candidates
+    *dst_pose = poses[mine];
+    *dst_id = id[mine];
+    return;
+  }
+  stage[0] = *v_ptr;
+  stage[1] = __longlong_as_double(ix);
+  const Pose p = poses[mine];
+  for (int q = 0; q < 9; ++q) stage[2 + q] = p.R[q];
+  for (int a = 0; a < 3; ++a) stage[11 + a] = p.t[a];
+  stage[14] = static_cast<double>(id[mine]);
+}
+__global__ void k_rep_select(const double* __restrict__ v_ptr, const long long* __restrict__ ix_ptr, int64_t n_local,
+                             int world, const Pose* __restrict__ g_rep, const int32_t* __restrict__ g_repid,
+                             double* __restrict__ stage) {
+  const long long ix = *ix_ptr;
+  long long owner = ix / n_local;
+  owner = owner < 0 ? 0 : (owner >= world ? world - 1 : owner);
+  stage[0] = *v_ptr;
+  stage[1] = __longlong_as_double(ix);
+  const Pose p = g_rep[owner];
+  for (int q = 0; q < 9; ++q) stage[2 + q] = p.R[q];
+  for (int a = 0; a < 3; ++a) stage[11 + a] = p.t[a];
+  stage[14] = static_cast<double>(g_repid[owner]);
+}
+
 }  // namespace
+
+void launch_rep_local(const double* v, const long long* ix, int64_t n_local, int rank, bool sharded, const Pose* poses,
+                      const int32_t* id, Pose* dst_pose, int32_t* dst_id, double* stage, cudaStream_t st) {
+  count_launch();
+  k_rep_local<<<1, 1, 0, st>>>(v, ix, n_local, rank, sharded ? 1 : 0, poses, id, dst_pose, dst_id, stage);
+}
+void launch_rep_select(const double* v, const long long* ix, int64_t n_local, int world, const Pose* g_rep,
+                       const int32_t* g_repid, double* stage, cudaStream_t st) {
+  count_launch();
+  k_rep_select<<<1, 1, 0, st>>>(v, ix, n_local, world, g_rep, g_repid, stage);
+}
 
 void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta, cudaStream_t st) {
   count_launch();
