@@ -372,7 +372,7 @@ struct smcl_engine {
   DBuf<unsigned int> mirror_tmax;  // max |t - anchor| (float bits) of that mirror
   DBuf<unsigned char> temp;
   size_t temp_bytes = 0;
-  DBuf<unsigned long long> d_hist, d_counts;
+  DBuf<unsigned long long> d_counts;
 
   // posterior
   DBuf<double> pbuf, qbuf, partial, partial2, scal;
@@ -653,7 +653,6 @@ struct smcl_engine {
     scal_i.ensure(8);
     argv.ensure(static_cast<size_t>(argmax_partials(static_cast<int64_t>(un))));
     argi.ensure(static_cast<size_t>(argmax_partials(static_cast<int64_t>(un))));
-    d_hist.ensure(SMCL_MAX_HIST);
     d_counts.ensure(8);
     steps_valid = phis_valid = ll_valid = false;
   }
@@ -1175,7 +1174,7 @@ struct smcl_engine {
     const int64_t n = n_local;
     if (n == 0) return;
     global_argmax(2, 0);
-    launch_chunk_sum_exp(log_post.p, n, scal.p + 2, pbuf.p, partial.p, st);
+    launch_chunk_sum_exp(log_post.p, n, scal.p + 2, partial.p, st);
     const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
     if (sharded) {  // reduce.hpp order: every chunk partial, in global chunk order
       allgather(partial.p, g_part.p, sizeof(double) * static_cast<size_t>(chunks));

@@ -130,8 +130,7 @@ void launch_argmax(const double* v, int64_t n, int64_t gbase, double* scratch_v,
 void launch_max_of_partials(const double* pv, const long long* pi, int64_t n, double* out_v, long long* out_i,
                             cudaStream_t st);
 // Chunked (4096) serial sums, reduce.hpp order; scratch arrays hold n doubles.
-void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* scratch, double* partial,
-                          cudaStream_t st);
+void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* partial, cudaStream_t st);
 void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n, int k, double* s1, double* s2,
                              double* pk, double* pc, cudaStream_t st);
 void launch_finish_lse(const double* partial, int64_t n_chunks, const double* m, double* lse, cudaStream_t st);

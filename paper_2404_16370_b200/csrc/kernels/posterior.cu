@@ -103,12 +103,6 @@ __global__ void k_argmax(const double* __restrict__ v, const long long* __restri
   }
 }
 
-// exp(v - m), elementwise (the value_at of posterior.cpp:17).
-__global__ void k_exp_shift(const double* __restrict__ v, int64_t n, const double* __restrict__ m_ptr,
-                            double* __restrict__ out) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = exp(xsub(v[i], *m_ptr));
-}
 
 // Per-particle list sums for mean_kernel (neighbor_search.cpp:182-190): the
 // kval sum in slot order and the entry count.
@@ -130,8 +124,8 @@ __global__ void k_list_sums(const float* __restrict__ kval, const int32_t* __res
 // (blocks [0, chunks) sum v0, [chunks, 2*chunks) sum v1). The serial chain
 // is DADD-latency bound: lane 0 reads the staged values 16 at a time (LDS.128)
 // ahead of the adds.
-// m_ptr != nullptr: the staged values are exp(v - *m_ptr) (posterior.cpp:17,
-// as k_exp_shift), computed by the 32 lanes while staging.
+// m_ptr != nullptr: the staged values are exp(v - *m_ptr) (the value_at of
+// posterior.cpp:17), computed by the 32 lanes while staging.
 __global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ v0, const double* __restrict__ v1,
                                                      int64_t n, int64_t chunks, double* __restrict__ p0,
                                                      double* __restrict__ p1, const double* __restrict__ m_ptr) {
@@ -367,22 +361,14 @@ void launch_max_of_partials(const double* pv, const long long* pi, int64_t n, do
   count_launch();
   k_argmax<<<1, 256, 0, st>>>(pv, pi, n, 0, out_v, out_i);
 }
-static void chunk_serial(const double* v, int64_t n, double* partial, cudaStream_t st) {
-  count_launch();
-  const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
-  if (chunks > 0)
-    k_chunk_serial<<<static_cast<unsigned>(chunks), 32, 0, st>>>(v, v, n, chunks, partial, partial, nullptr);
-}
 static void chunk_serial2(const double* a, const double* b, int64_t n, double* pa, double* pb, cudaStream_t st) {
   count_launch();
   const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
   if (chunks > 0) k_chunk_serial<<<static_cast<unsigned>(2 * chunks), 32, 0, st>>>(a, b, n, chunks, pa, pb, nullptr);
 }
-void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* scratch, double* partial,
-                          cudaStream_t st) {
+void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* partial, cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
-  (void)scratch;  // exp(v - m) is computed while staging each chunk
   const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
   k_chunk_serial<<<static_cast<unsigned>(chunks), 32, 0, st>>>(v, v, n, chunks, partial, partial, m);
 }
