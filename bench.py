@@ -168,9 +168,9 @@ def run_reference(args):
               f"{args.steps} timed steps after {args.warmup} warm-up, OpenMP on {threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: corridor_world 100 pts/m2 NNF 0.1 m, uniform SO3 init",
+        "config": {"workload": WORKLOAD_TEXT[args.workload].format(n=args.particles, s=args.scan_points),
                    "n_particles_sampled": args.cpu_sample, "scan_points": args.scan_points,
                    "parallelism": "host OpenMP"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
