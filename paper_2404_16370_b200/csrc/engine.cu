@@ -1170,7 +1170,7 @@ struct smcl_engine {
     }
   }
 
-  void normalize(double floor_v) {
+  void normalize(double floor_v, const unsigned long long* skip_if_zero = nullptr) {
     const int64_t n = n_local;
     if (n == 0) return;
     global_argmax(2, 0);
@@ -1182,7 +1182,7 @@ struct smcl_engine {
     } else {
       launch_finish_lse(partial.p, chunks, scal.p + 2, scal.p + 3, st);
     }
-    launch_apply_lse(log_post.p, n, scal.p + 3, floor_v, st);
+    launch_apply_lse(log_post.p, n, scal.p + 3, floor_v, st, skip_if_zero);
     CK(cudaGetLastError());
   }
 
@@ -1217,9 +1217,26 @@ struct smcl_engine {
       launch_fill(log_post.p, n, -std::log(static_cast<double>(n_total)), st);
       return true;
     }
-    launch_bayes_numer(log_post.p, ll.p, nm.p, n, beta, st);
+    launch_bayes_numer(log_post.p, ll.p, nm.p, n, beta, nullptr, 0.0, st);
     normalize(floor_v);
     return false;
+  }
+
+  // bayes() without the host round trip (the step's form): the match counts
+  // stay in d_counts[0..1], the uniform reset and the skipped normalization of
+  // a rejected observation are decided on the device; the caller reads the
+  // counts with its end-of-step sync.
+  void bayes_async(double beta, double floor_v) {
+    if (!(beta >= 0.0)) throw std::invalid_argument("bayes_update: beta must be >= 0");
+    const int64_t n = n_local;
+    if (n == 0) return;
+    launch_match_counts(ll.p, nm.p, n_local, d_counts.p, st);
+    if (sharded) {
+      allgather(d_counts.p, g_counts.p, 2 * sizeof(unsigned long long));
+      launch_sum_pairs(g_counts.p, world, d_counts.p, st);
+    }
+    launch_bayes_numer(log_post.p, ll.p, nm.p, n, beta, d_counts.p, -std::log(static_cast<double>(n_total)), st);
+    normalize(floor_v, d_counts.p);
   }
 
   void smooth(int iters, double floor_v) {
@@ -1358,7 +1375,7 @@ struct smcl_engine {
       }
       run_likelihood(false, sl.full);
       mark(E_BAYES);
-      r.observation_rejected = bayes(cfg.beta, cfg.log_post_floor) ? 1 : 0;
+      bayes_async(cfg.beta, cfg.log_post_floor);  // rejection flag read at the end of the step
     } else {
       mark(E_LL0);
       mark(E_LL1);
@@ -1378,7 +1395,10 @@ struct smcl_engine {
     unsigned long long cnt[6];
     std::memcpy(cnt, step_host->cnt, sizeof(cnt));
     const int32_t rid = rep_id;
-    cnt[1] = last_nm_sum;  // global sum of n_matched (bayes)
+    if (!empty) {  // bayes_async: global (matched particles, sum of n_matched)
+      r.observation_rejected = cnt[0] == 0 ? 1 : 0;
+      last_nm_sum = cnt[1];
+    }
     finish_nb_stats();
     if (!empty) {  // last (or only) Gauss-Newton iteration
       t_gn += since(E_GN0, E_GN1);

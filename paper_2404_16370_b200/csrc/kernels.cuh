@@ -121,7 +121,9 @@ void launch_rep_local(const double* v, const long long* ix, int64_t n_local, int
                       const int32_t* id, Pose* dst_pose, int32_t* dst_id, double* stage, cudaStream_t st);
 void launch_rep_select(const double* v, const long long* ix, int64_t n_local, int world, const Pose* g_rep,
                        const int32_t* g_repid, double* stage, cudaStream_t st);
-void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta, cudaStream_t st);
+void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta,
+                        const unsigned long long* matched, double fill, cudaStream_t st);
+void launch_sum_pairs(const unsigned long long* g, int world, unsigned long long* out, cudaStream_t st);
 void launch_fill(double* v, int64_t n, double value, cudaStream_t st);
 void launch_match_counts(const double* ll, const int32_t* nm, int64_t n, unsigned long long* out, cudaStream_t st);
 int argmax_partials(int64_t n);
@@ -135,7 +137,8 @@ void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n,
                              double* pk, double* pc, cudaStream_t st);
 void launch_finish_lse(const double* partial, int64_t n_chunks, const double* m, double* lse, cudaStream_t st);
 void launch_finish_sum2(const double* a, const double* b, int64_t n_chunks, double* out, cudaStream_t st);
-void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, cudaStream_t st);
+void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, cudaStream_t st,
+                      const unsigned long long* skip_if_zero = nullptr);
 void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st);
 void launch_log(const double* p, double* lp, int64_t n, cudaStream_t st);
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,

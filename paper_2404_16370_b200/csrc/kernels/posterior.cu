@@ -21,12 +21,29 @@ namespace {
 inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
 // log_post += beta * ll / max(nm, 1)   (posterior.cpp:50-56)
+// matched != nullptr (device branch of posterior.cpp:29-41): when no particle
+// matched, every value becomes fill (the uniform reset) instead.
 __global__ void k_bayes_numer(double* __restrict__ lp, const double* __restrict__ ll, const int32_t* __restrict__ nm,
-                              int64_t n, double beta) {
+                              int64_t n, double beta, const unsigned long long* __restrict__ matched,
+                              double fill) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (matched && *matched == 0ull) {
+    lp[i] = fill;
+    return;
+  }
   const double denom = static_cast<double>(nm[i] > 1 ? nm[i] : 1);
   lp[i] = xadd(lp[i], xmul(beta, ll[i]) / denom);
+}
+// Sum of the per-shard (matched, sum n_matched) pairs, in rank order.
+__global__ void k_sum_pairs(const unsigned long long* __restrict__ g, int world, unsigned long long* __restrict__ out) {
+  unsigned long long a = 0, b = 0;
+  for (int r = 0; r < world; ++r) {
+    a += g[2 * r];
+    b += g[2 * r + 1];
+  }
+  out[0] = a;
+  out[1] = b;
 }
 
 __global__ void k_fill(double* __restrict__ v, int64_t n, double value) {
@@ -213,9 +230,13 @@ __global__ void __launch_bounds__(32) k_finish_sum2(const double* __restrict__ a
   }
 }
 
-__global__ void k_apply_lse(double* __restrict__ v, int64_t n, const double* __restrict__ lse_ptr, double floor_v) {
+// skip_if_zero != nullptr and *skip_if_zero == 0: leave v unchanged (the
+// rejected observation of posterior.cpp:29-33 returns before normalizing).
+__global__ void k_apply_lse(double* __restrict__ v, int64_t n, const double* __restrict__ lse_ptr, double floor_v,
+                            const unsigned long long* __restrict__ skip_if_zero) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (skip_if_zero && *skip_if_zero == 0ull) return;
   const double r = xsub(v[i], *lse_ptr);
   v[i] = r < floor_v ? floor_v : r;  // std::max(v - lse, floor)
 }
@@ -332,9 +353,14 @@ void launch_rep_select(const double* v, const long long* ix, int64_t n_local, in
   k_rep_select<<<1, 1, 0, st>>>(v, ix, n_local, world, g_rep, g_repid, stage);
 }
 
-void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta, cudaStream_t st) {
+void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta,
+                        const unsigned long long* matched, double fill, cudaStream_t st) {
   count_launch();
-  if (n > 0) k_bayes_numer<<<blocks_for(n, 256), 256, 0, st>>>(lp, ll, nm, n, beta);
+  if (n > 0) k_bayes_numer<<<blocks_for(n, 256), 256, 0, st>>>(lp, ll, nm, n, beta, matched, fill);
+}
+void launch_sum_pairs(const unsigned long long* g, int world, unsigned long long* out, cudaStream_t st) {
+  count_launch();
+  k_sum_pairs<<<1, 1, 0, st>>>(g, world, out);
 }
 void launch_fill(double* v, int64_t n, double value, cudaStream_t st) {
   count_launch();
@@ -387,9 +413,10 @@ void launch_finish_sum2(const double* a, const double* b, int64_t n_chunks, doub
   count_launch();
   k_finish_sum2<<<1, 32, 0, st>>>(a, b, n_chunks, out);
 }
-void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, cudaStream_t st) {
+void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, cudaStream_t st,
+                      const unsigned long long* skip_if_zero) {
   count_launch();
-  if (n > 0) k_apply_lse<<<blocks_for(n, 256), 256, 0, st>>>(v, n, lse, floor_v);
+  if (n > 0) k_apply_lse<<<blocks_for(n, 256), 256, 0, st>>>(v, n, lse, floor_v, skip_if_zero);
 }
 void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st) {
   count_launch();

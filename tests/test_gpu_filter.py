@@ -162,3 +162,31 @@ def test_ids_fixed_and_timings(world):
         stage += sum(res[k] for k in ("predict_ms", "neighbor_ms", "likelihood_ms", "update_ms", "posterior_ms"))
         total += res["total_ms"]
     assert abs(stage - total) / total < 0.05
+
+
+def test_rejected_observation_resets_uniformly(world):
+    """posterior.cpp:29-33: when no particle matches, the Bayes update resets
+    log_post to uniform and reports the observation rejected (decided on the
+    device in the step); the following smoothing runs as usual."""
+    for mode in (1, 2):
+        cfg = make_config(n_particles=500, seed=42, nnf_resolution=0.2, likelihood_mode=mode)
+        g = FilterEngine(world.map, cfg)
+        r = O.FilterEngine(world.map.mu, world.map.sigma, cfg, world.map.bounds)
+        g.init_uniform(world.map.bounds)
+        r.init_uniform(world.map.bounds)
+        gt = I12.copy()
+        gt[9:] = [5.0, 4.0, 1.5]
+        scan = world.scan_at(gt, cfg)
+        far = GaussianCloud(scan.mu + 1000.0, scan.sigma)  # matches nothing anywhere
+        cov = np.diag([1e-4] * 6).reshape(36)
+        for sc in (scan, far, scan):
+            a = g.step(sc, I12, cov, True)
+            b = r.step(sc.mu, sc.sigma, I12, cov, True)
+            assert a["observation_rejected"] == b["observation_rejected"]
+            assert a["mean_n_matched"] == b["mean_n_matched"] or mode == 2
+        assert a["observation_rejected"] == 0
+        rej = g.step(far, I12, cov, True)
+        assert rej["observation_rejected"] == 1 and rej["mean_n_matched"] == 0.0
+        if mode == 1:
+            r.step(far.mu, far.sigma, I12, cov, True)
+            assert np.abs(g.particles().log_post - r.particles().log_post).max() < 1e-9
