@@ -191,6 +191,26 @@ def test_update_neighbors_filter_margins(case):
     assert np.array_equal(got.count, r.count) and np.array_equal(got.id, r.id)
 
 
+@pytest.mark.parametrize("k", [1, 8, 24, 32])
+def test_update_neighbors_list_sizes(k):
+    """List sizes off the default 20: self-only lists (k = 1: nothing is ever
+    evictable), the 8- and 32-slot kernel variants and a 24-entry list in the
+    32-slot variant (unused slots stay empty)."""
+    bounds = [0, 0, 0, 4, 4, 4]
+    g = random_cube_set(400, 4.0, 0.2, k, 5)
+    cfg = make_config(k_neighbors=k)
+    r = g.copy()
+    e = _stage_engine(g, k_neighbors=k)
+    for p in range(4):
+        seed = O.mix_seed(81, p)
+        e.update_neighbors(seed, bounds)
+        O.update_neighbors(r, cfg, seed, bounds)
+    got = e.particles()
+    assert np.array_equal(got.idx, r.idx) and np.array_equal(got.kval, r.kval)
+    assert np.array_equal(got.count, r.count) and np.array_equal(got.id, r.id)
+    assert got.count.max() == k
+
+
 def test_update_neighbors_oracle_serial_twin():
     """test_neighbor_search.cpp:234-257 on the oracle itself (parallel == serial)."""
     cfg = make_config()
