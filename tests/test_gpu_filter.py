@@ -190,3 +190,21 @@ def test_rejected_observation_resets_uniformly(world):
         if mode == 1:
             r.step(far.mu, far.sigma, I12, cov, True)
             assert np.abs(g.particles().log_post - r.particles().log_post).max() < 1e-9
+
+
+@pytest.mark.parametrize("k", [8, 32])
+def test_step_exact_mode_other_list_sizes(world, k):
+    """Whole steps with lists off the default 20 (generic reorder and
+    smoothing kernels, the 8- / 32-slot neighbour-pass variants)."""
+    cfg = make_config(n_particles=400, seed=7, nnf_resolution=0.2, likelihood_mode=1, k_neighbors=k)
+    g, fg = run_frames(world, cfg, 4)
+    r, fr = run_frames(world, cfg, 4, oracle=True)
+    for a, b in zip(fg, fr):
+        assert a["rep_id"] == b["rep_id"] and a["mean_n_matched"] == b["mean_n_matched"]
+        assert abs(a["rep_log_post"] - b["rep_log_post"]) < 1e-9
+    pg, pr = g.particles(), r.particles()
+    assert np.array_equal(pg.id, pr.id)
+    assert np.array_equal(pg.idx, pr.idx) and np.array_equal(pg.count, pr.count)
+    assert np.array_equal(pg.kval, pr.kval)
+    assert np.abs(pg.poses - pr.poses).max() < 1e-9
+    assert np.abs(pg.log_post - pr.log_post).max() < 1e-9
