@@ -89,12 +89,12 @@ def run_sharded(world, cfg, frames, G, alltoallv=True):
 
 
 @pytest.mark.parametrize("G,mode,reorder,a2a", [(2, 2, 0, 1), (4, 2, 0, 1), (2, 1, 0, 1), (2, 2, 1, 1), (4, 2, 1, 1),
-                                                (2, 1, 1, 1), (4, 2, 1, 0), (2, 1, 1, 0)])
+                                                (2, 1, 1, 1), (4, 2, 1, 0), (2, 1, 1, 0), (8, 2, 1, 1)])
 def test_sharded_engine_is_bit_identical_to_single(world, G, mode, reorder, a2a):
     """reorder = 1: the LSH reorder migrates particle state across shards
     (particle_set.cpp:7-47 on the global order), by
     alltoallv of the migrating records (a2a = 1) or by all-gather (a2a = 0)."""
-    n = 16384 if mode == 2 else 8192
+    n = max(16384 if mode == 2 else 8192, 4096 * G)
     cfg = make_config(n_particles=n, seed=7, nnf_resolution=0.2, likelihood_mode=mode, reorder_particles=reorder)
     frames = scans(world, cfg, 3)
     ref_res, ref_p = run_single(world, cfg, frames)
