@@ -1,4 +1,9 @@
-for c in 4x24 4x16 8x14; do
-SMCL_FAST_CFG_LL=$c timeout 600 python bench.py --particles 4194304 --scan-points 1024 --steps 3 --no-cpu-baseline > gpurun_out/b4_$c.json 2> /dev/null
-python -c "import json; d=json.load(open('gpurun_out/b4_$c.json')); print('$c', d['ms_per_step'], d['stage_ms']['ll_kernel_ms'])"
-done
+run() {
+  timeout 900 python bench.py --particles 4194304 --scan-points 1024 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/b4.json 2> gpurun_out/b4.err
+  python -c "
+import json
+d=json.loads(open('gpurun_out/b4.json').read().strip().splitlines()[-1])
+print('$1', d['ms_per_step'], {k: round(v,2) for k,v in d['stage_ms'].items()})" || tail -3 gpurun_out/b4.err
+}
+run default
+SMCL_FAST_CFG_LL=416 run ll416

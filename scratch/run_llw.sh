@@ -5,5 +5,5 @@ import json
 d=json.loads(open('gpurun_out/bench_ll.json').read().strip().splitlines()[-1])
 print('$1', d['ms_per_step'], d['stage_ms']['ll_kernel_ms'])" || tail -3 gpurun_out/bench_ll.err
 }
-
-for c in L1x84 L1x85 L1x48 L1x50 L1x52; do SMCL_FAST_CFG_LL=$c run $c; done
+run default
+for c in 4x16 4x24 4x32; do SMCL_FAST_CFG_LL=$c run w$c; done
