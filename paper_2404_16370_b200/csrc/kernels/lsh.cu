@@ -498,8 +498,9 @@ __global__ void k_pose_mirror(const Pose* __restrict__ poses, int64_t n, double3
 // 2(1 - cos theta) = 3 - tr(Ra^T Rb) and |V^-1 u| >= |u| = |tb - ta| (V^-1
 // scales the plane across w by (theta/2)/sin(theta/2) >= 1), so
 //   q >= L = sr (3 - tr(Ra^T Rb)) + st |tb - ta|^2
-// and L > -log(wk) (1e-6 margin) proves float(exp(-q)) <= wk: the offer
-// would be dropped whatever the list holds (a duplicate is dropped anyway).
+// and L > -log(wk) proves float(exp(-q)) <= wk: the offer would be dropped
+// whatever the list holds. L is evaluated in fp32 on the pose mirror
+// (k_pose_mirror) and only trusted beyond its rounding margin (kernel prologue).
 // Duplicates: offer() ignores a candidate already listed. Window members are
 // unique, so a member inserted during the scan is never offered again, and a
 // member listed at the start that gets evicted before its turn is never
