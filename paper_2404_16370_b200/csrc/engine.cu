@@ -282,11 +282,9 @@ struct smcl_engine {
   DBuf<unsigned char> mig_send, mig_recv;
   std::vector<unsigned int> mig_host;
   DBuf<unsigned long long> g_counts;
-  DBuf<double> g_argv;
-  DBuf<long long> g_argi;
-  DBuf<Pose> g_rep;
+  DBuf<double> g_argv, arg_pair;
+  DBuf<double> g_rep;  // per rank: representative pose (12 doubles) + id, 14-double (16-B aligned) records
   DBuf<double> rep_stage;  // representative: value, index, pose, id
-  DBuf<int32_t> g_repid;
 
   // All-gather `bytes` per rank from send (device) into recv (device).
   void allgather(const void* send, void* recv, size_t bytes) {
@@ -583,10 +581,9 @@ struct smcl_engine {
       g_part.ensure(w * ((un + kReduceChunk - 1) / kReduceChunk));
       g_part2.ensure(w * ((un + kReduceChunk - 1) / kReduceChunk));
       g_counts.ensure(w * 2);
-      g_argv.ensure(w);
-      g_argi.ensure(w);
-      g_rep.ensure(w);
-      g_repid.ensure(w);
+      g_argv.ensure(2 * w);  // (value, index) pairs
+      arg_pair.ensure(2);
+      g_rep.ensure(w * 14);   // per rank: pose (12 doubles) + id + pad
       if (cfg.reorder_particles) {
         g_poses2.ensure(ug);
         if (comm.alltoallv) {
@@ -1162,11 +1159,13 @@ struct smcl_engine {
   // Global argmax (value, index; ties -> lowest index) of log_post into
   // scal[slot], scal_i[slot_i]: per-shard partial, all-gathered, merged.
   void global_argmax(int slot, int slot_i) {
-    launch_argmax(log_post.p, n_local, gbase, argv.p, argi.p, scal.p + slot, scal_i.p + slot_i, st);
-    if (sharded) {
-      allgather(scal.p + slot, g_argv.p, sizeof(double));
-      allgather(scal_i.p + slot_i, g_argi.p, sizeof(long long));
-      launch_max_of_partials(g_argv.p, g_argi.p, world, scal.p + slot, scal_i.p + slot_i, st);
+    if (sharded) {  // this shard's (value, index) as one 16-byte pair: one all-gather
+      launch_argmax(log_post.p, n_local, gbase, argv.p, argi.p, arg_pair.p,
+                    reinterpret_cast<long long*>(arg_pair.p + 1), st);
+      allgather(arg_pair.p, g_argv.p, 2 * sizeof(double));
+      launch_merge_pairs(g_argv.p, world, scal.p + slot, scal_i.p + slot_i, st);
+    } else {
+      launch_argmax(log_post.p, n_local, gbase, argv.p, argi.p, scal.p + slot, scal_i.p + slot_i, st);
     }
   }
 
@@ -1272,11 +1271,11 @@ struct smcl_engine {
     global_argmax(4, 1);
     rep_stage.ensure(16);
     if (sharded) {  // the owner rank publishes the winner's pose and id (one slot per rank)
-      launch_rep_local(scal.p + 4, scal_i.p + 1, n_local, rank, true, poses.p, id.p, g_rep.p + rank,
-                       g_repid.p + rank, nullptr, st);
-      allgather(g_rep.p + rank, g_rep.p, sizeof(Pose));
-      allgather(g_repid.p + rank, g_repid.p, sizeof(int32_t));
-      launch_rep_select(scal.p + 4, scal_i.p + 1, n_local, world, g_rep.p, g_repid.p, rep_stage.p, st);
+      double* mine = g_rep.p + 14 * static_cast<size_t>(rank);
+      launch_rep_local(scal.p + 4, scal_i.p + 1, n_local, rank, true, poses.p, id.p, reinterpret_cast<Pose*>(mine),
+                       nullptr, nullptr, st);
+      allgather(mine, g_rep.p, 14 * sizeof(double));
+      launch_rep_select(scal.p + 4, scal_i.p + 1, n_local, world, g_rep.p, rep_stage.p, st);
     } else {
       launch_rep_local(scal.p + 4, scal_i.p + 1, n_local, 0, false, poses.p, id.p, nullptr, nullptr, rep_stage.p, st);
     }

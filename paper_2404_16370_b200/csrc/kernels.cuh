@@ -119,8 +119,9 @@ cudaError_t scan_gather_stride(const double* d_mu, const double* d_sigma, int n_
 // posterior.cu
 void launch_rep_local(const double* v, const long long* ix, int64_t n_local, int rank, bool sharded, const Pose* poses,
                       const int32_t* id, Pose* dst_pose, int32_t* dst_id, double* stage, cudaStream_t st);
-void launch_rep_select(const double* v, const long long* ix, int64_t n_local, int world, const Pose* g_rep,
-                       const int32_t* g_repid, double* stage, cudaStream_t st);
+void launch_rep_select(const double* v, const long long* ix, int64_t n_local, int world, const double* g_rec,
+                       double* stage, cudaStream_t st);
+void launch_merge_pairs(const double* g, int world, double* out_v, long long* out_i, cudaStream_t st);
 void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta,
                         const unsigned long long* matched, double fill, cudaStream_t st);
 void launch_sum_pairs(const unsigned long long* g, int world, unsigned long long* out, cudaStream_t st);

@@ -304,6 +304,17 @@ __global__ void __launch_bounds__(128) k_smooth_round_k(const double* __restrict
   q[i] = num / den;
 }
 
+// Merge of the per-shard (value, index) argmax pairs gathered as
+// [v0, i0, v1, i1, ...] (ties -> lowest index, as argmax_merge).
+__global__ void k_merge_pairs(const double* __restrict__ g, int world, double* __restrict__ out_v,
+                              long long* __restrict__ out_i) {
+  double v = -INFINITY;
+  long long ix = -1;
+  for (int r = 0; r < world; ++r) argmax_merge(v, ix, g[2 * r], __double_as_longlong(g[2 * r + 1]));
+  *out_v = v;
+  *out_i = ix;
+}
+
 // Representative (posterior.cpp:99-108) without a host round trip: the
 // winning index is read on the device. Stage layout: [0] value, [1] index
 // (bits), [2..13] pose, [14] id (as double).
@@ -314,9 +325,9 @@ __global__ void k_rep_local(const double* __restrict__ v_ptr, const long long* _
   const long long owner = sharded ? ix / n_local : 0;
   const long long li = ix - owner * n_local;
   const long long mine = (owner == rank && li >= 0 && li < n_local) ? li : 0;
-  if (sharded) {  // this rank's slot of the all-gathered candidates
+  if (sharded) {  // this rank's slot of the all-gathered candidates (pose, then id, one record)
     *dst_pose = poses[mine];
-    *dst_id = id[mine];
+    *reinterpret_cast<int32_t*>(dst_pose + 1) = id[mine];
     return;
   }
   stage[0] = *v_ptr;
@@ -326,18 +337,17 @@ __global__ void k_rep_local(const double* __restrict__ v_ptr, const long long* _
   for (int a = 0; a < 3; ++a) stage[11 + a] = p.t[a];
   stage[14] = static_cast<double>(id[mine]);
 }
+// g_rec: per rank one record of 14 doubles (pose, the id in the 13th, pad).
 __global__ void k_rep_select(const double* __restrict__ v_ptr, const long long* __restrict__ ix_ptr, int64_t n_local,
-                             int world, const Pose* __restrict__ g_rep, const int32_t* __restrict__ g_repid,
-                             double* __restrict__ stage) {
+                             int world, const double* __restrict__ g_rec, double* __restrict__ stage) {
   const long long ix = *ix_ptr;
   long long owner = ix / n_local;
   owner = owner < 0 ? 0 : (owner >= world ? world - 1 : owner);
   stage[0] = *v_ptr;
   stage[1] = __longlong_as_double(ix);
-  const Pose p = g_rep[owner];
-  for (int q = 0; q < 9; ++q) stage[2 + q] = p.R[q];
-  for (int a = 0; a < 3; ++a) stage[11 + a] = p.t[a];
-  stage[14] = static_cast<double>(g_repid[owner]);
+  const double* r = g_rec + 14 * owner;
+  for (int q = 0; q < 12; ++q) stage[2 + q] = r[q];
+  stage[14] = static_cast<double>(*reinterpret_cast<const int32_t*>(r + 12));
 }
 
 }  // namespace
@@ -347,10 +357,14 @@ void launch_rep_local(const double* v, const long long* ix, int64_t n_local, int
   count_launch();
   k_rep_local<<<1, 1, 0, st>>>(v, ix, n_local, rank, sharded ? 1 : 0, poses, id, dst_pose, dst_id, stage);
 }
-void launch_rep_select(const double* v, const long long* ix, int64_t n_local, int world, const Pose* g_rep,
-                       const int32_t* g_repid, double* stage, cudaStream_t st) {
+void launch_rep_select(const double* v, const long long* ix, int64_t n_local, int world, const double* g_rec,
+                       double* stage, cudaStream_t st) {
   count_launch();
-  k_rep_select<<<1, 1, 0, st>>>(v, ix, n_local, world, g_rep, g_repid, stage);
+  k_rep_select<<<1, 1, 0, st>>>(v, ix, n_local, world, g_rec, stage);
+}
+void launch_merge_pairs(const double* g, int world, double* out_v, long long* out_i, cudaStream_t st) {
+  count_launch();
+  k_merge_pairs<<<1, 1, 0, st>>>(g, world, out_v, out_i);
 }
 
 void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t n, double beta,
