@@ -1250,10 +1250,11 @@ struct smcl_engine {
         allgather(pbuf.p, g_p.p, sizeof(double) * static_cast<size_t>(n));
         p_all = g_p.p;
       }
-      launch_smooth_round(p_all, qbuf.p, n, idx.p, kval.p, count.p, k, st);
+      // the last round writes log(q) straight into log_post (posterior.cpp:94)
+      const bool last = r + 1 == iters;
+      launch_smooth_round(p_all, last ? log_post.p : qbuf.p, n, idx.p, kval.p, count.p, k, st, last);
       pbuf.swap(qbuf);
     }
-    launch_log(pbuf.p, log_post.p, n, st);
     CK(cudaGetLastError());
     normalize(floor_v);
   }

@@ -143,6 +143,6 @@ void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, c
 void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st);
 void launch_log(const double* p, double* lp, int64_t n, cudaStream_t st);
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
-                         const int32_t* count, int k, cudaStream_t st);
+                         const int32_t* count, int k, cudaStream_t st, bool take_log = false);
 
 }  // namespace smcl

@@ -253,7 +253,7 @@ __global__ void k_log(const double* __restrict__ p, double* __restrict__ lp, int
 // One Jacobi round of posterior.cpp:75-90 (q_i = sum_s w_s p[idx_s] / sum_s w_s).
 __global__ void k_smooth_round(const double* __restrict__ p_all, double* __restrict__ q, int64_t n,
                                const int32_t* __restrict__ idx, const float* __restrict__ kval,
-                               const int32_t* __restrict__ count, int k) {
+                               const int32_t* __restrict__ count, int k, int take_log) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double num = 0.0, den = 0.0;
@@ -263,7 +263,8 @@ __global__ void k_smooth_round(const double* __restrict__ p_all, double* __restr
     num = xadd(num, xmul(w, p_all[idx[i * k + s]]));
     den = xadd(den, w);
   }
-  q[i] = num / den;
+  const double r = num / den;
+  q[i] = take_log ? log(r) : r;  // last round: posterior.cpp's log pass fused
 }
 
 // K = 20 (the default list size): the particle's idx / kval rows (80 B
@@ -273,7 +274,7 @@ template <int K>
 __global__ void __launch_bounds__(128) k_smooth_round_k(const double* __restrict__ p_all, double* __restrict__ q,
                                                         int64_t n, const int32_t* __restrict__ idx,
                                                         const float* __restrict__ kval,
-                                                        const int32_t* __restrict__ count) {
+                                                        const int32_t* __restrict__ count, int take_log) {
   static_assert(K % 4 == 0, "rows must be whole 16-byte vectors");
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -301,7 +302,8 @@ __global__ void __launch_bounds__(128) k_smooth_round_k(const double* __restrict
       den = xadd(den, ws);
     }
   }
-  q[i] = num / den;
+  const double r = num / den;
+  q[i] = take_log ? log(r) : r;  // last round: posterior.cpp's log pass fused
 }
 
 // Merge of the per-shard (value, index) argmax pairs gathered as
@@ -441,13 +443,13 @@ void launch_log(const double* p, double* lp, int64_t n, cudaStream_t st) {
   if (n > 0) k_log<<<blocks_for(n, 256), 256, 0, st>>>(p, lp, n);
 }
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
-                         const int32_t* count, int k, cudaStream_t st) {
+                         const int32_t* count, int k, cudaStream_t st, bool take_log) {
   count_launch();
   if (n <= 0) return;
   if (k == 20)
-    k_smooth_round_k<20><<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count);
+    k_smooth_round_k<20><<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count, take_log ? 1 : 0);
   else
-    k_smooth_round<<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count, k);
+    k_smooth_round<<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count, k, take_log ? 1 : 0);
 }
 
 }  // namespace smcl
