@@ -141,7 +141,6 @@ void launch_finish_sum2(const double* a, const double* b, int64_t n_chunks, doub
 void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, cudaStream_t st,
                       const unsigned long long* skip_if_zero = nullptr);
 void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st);
-void launch_log(const double* p, double* lp, int64_t n, cudaStream_t st);
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
                          const int32_t* count, int k, cudaStream_t st, bool take_log = false);
 

@@ -245,10 +245,6 @@ __global__ void k_exp(const double* __restrict__ lp, double* __restrict__ p, int
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) p[i] = exp(lp[i]);
 }
-__global__ void k_log(const double* __restrict__ p, double* __restrict__ lp, int64_t n) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) lp[i] = log(p[i]);
-}
 
 // One Jacobi round of posterior.cpp:75-90 (q_i = sum_s w_s p[idx_s] / sum_s w_s).
 __global__ void k_smooth_round(const double* __restrict__ p_all, double* __restrict__ q, int64_t n,
@@ -437,10 +433,6 @@ void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, c
 void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st) {
   count_launch();
   if (n > 0) k_exp<<<blocks_for(n, 256), 256, 0, st>>>(lp, p, n);
-}
-void launch_log(const double* p, double* lp, int64_t n, cudaStream_t st) {
-  count_launch();
-  if (n > 0) k_log<<<blocks_for(n, 256), 256, 0, st>>>(p, lp, n);
 }
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
                          const int32_t* count, int k, cudaStream_t st, bool take_log) {
