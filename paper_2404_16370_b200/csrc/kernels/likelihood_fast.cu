@@ -101,9 +101,43 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 
+// Likelihood only: e^T Omega e is basis independent, and with n_w = R n the
+// scalars the cost needs are world-frame dot/cross products (u.e = m'.e',
+// n_w.e = n.e', u.n_w = m'.n, |u x n_w| = |m' x n|): one rotation (n) per
+// point instead of two (e, u).
+__device__ __forceinline__ float fast_cost(const float Rf[9], const float fr[3], float res, const float4 m0,
+                                           const float4 m1, const float4 s0, const float4 s1) {
+  const float ex = fmaf(-fr[0], res, m0.x), ey = fmaf(-fr[1], res, m0.y), ez = fmaf(-fr[2], res, m0.z);
+  const float mx = m1.x, my = m1.y, mz = m1.z;  // map plane direction u (world)
+  const float nx = Rf[0] * s1.x + Rf[1] * s1.y + Rf[2] * s1.z;  // R n (row-major R)
+  const float ny = Rf[3] * s1.x + Rf[4] * s1.y + Rf[5] * s1.z;
+  const float nz = Rf[6] * s1.x + Rf[7] * s1.y + Rf[8] * s1.z;
+  const float beta = m0.w, sM = m1.w, gam = s0.w, sS = s1.w;
+  const float A = (beta + sM) + (gam + sS);
+  const float Ssum = sM + sS;
+  const float AmB = sM + gam + sS;   // A - beta
+  const float AmG = beta + sM + sS;  // A - gamma
+  const float c = mx * nx + my * ny + mz * nz;
+  const float cx = my * nz - mz * ny, cy = mz * nx - mx * nz, cz = mx * ny - my * nx;
+  const float w = cx * cx + cy * cy + cz * cz;
+  const float bg = beta * gam;
+  const float invD = rcp_approx(fmaf(A, Ssum, bg * w));
+  const float invA = rcp_approx(A);
+  const float invDA = invD * invA;
+  const float Pa = beta * AmG * invDA, Qa = gam * AmB * invDA, Ta = c * bg * invDA;
+  const float x = mx * ex + my * ey + mz * ez;
+  const float y = nx * ex + ny * ey + nz * ez;
+  const float am = fmaf(Pa, x, Ta * y), an = fmaf(Qa, y, Ta * x);
+  return fmaf(ex * ex + ey * ey + ez * ez, invA, fmaf(am, x, an * y));
+}
+
 template <bool GN>
 __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const float fr[3], float res, const float4 m0,
                                           const float4 m1, const float4 s0, const float4 s1) {
+  if (!GN) {
+    acc.cost += fast_cost(Rf, fr, res, m0, m1, s0, s1);
+    return;
+  }
   // World residual e = mu_M - p = (mu_M - corner) - frac*res.
   const float ewx = fmaf(-fr[0], res, m0.x), ewy = fmaf(-fr[1], res, m0.y), ewz = fmaf(-fr[2], res, m0.z);
   // Body frame: e' = R^T e_w, m' = R^T u_M, n' = u_s, mu = scan mean.
