@@ -123,12 +123,12 @@ __device__ __forceinline__ float fast_cost(const float Rf[9], const float fr[3],
   const float bg = beta * gam;
   const float invD = rcp_approx(fmaf(A, Ssum, bg * w));
   const float invA = rcp_approx(A);
-  const float invDA = invD * invA;
-  const float Pa = beta * AmG * invDA, Qa = gam * AmB * invDA, Ta = c * bg * invDA;
   const float x = mx * ex + my * ey + mz * ez;
   const float y = nx * ex + ny * ey + nz * ez;
-  const float am = fmaf(Pa, x, Ta * y), an = fmaf(Qa, y, Ta * x);
-  return fmaf(ex * ex + ey * ey + ez * ez, invA, fmaf(am, x, an * y));
+  // e^T Omega e = |e|^2 / A + (beta AmG x^2 + gamma AmB y^2 + 2 c beta gamma x y) / (A Delta)
+  const float bx = beta * x, gy = gam * y;
+  const float inner = fmaf(AmG * bx, x, fmaf(AmB * gy, y, (c + c) * bx * gy));
+  return fmaf(ex * ex + ey * ey + ez * ez, invA, inner * (invD * invA));
 }
 
 template <bool GN>
