@@ -98,15 +98,21 @@ class ClockSampler:
 
     def __init__(self, device):
         self.device, self.rows, self.proc = device, [], None
+        self.t0 = self.t1 = None
 
     def start(self):
+        """Start polling (call before the warm-up: nvidia-smi needs a moment
+        to produce its first sample); mark() / stop() bracket the timed region."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                 text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
+            deadline = time.monotonic() + 3.0
+            while not self.rows and time.monotonic() < deadline:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
@@ -114,17 +120,26 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == len(self.FIELDS):
-                self.rows.append(parts)
+                self.rows.append((time.monotonic(), parts))
+
+    def mark(self):
+        self.t0 = time.monotonic()
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        self.t1 = time.monotonic()
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
+        t0 = self.t0 if self.t0 is not None else 0.0
+        inside = [r for t, r in self.rows if t0 <= t <= self.t1 + 0.05]
+        if not inside and self.rows:  # a region shorter than the poll interval: the nearest sample
+            inside = [min(self.rows, key=lambda tr: abs(tr[0] - self.t1))[1]]
+        self.rows = inside
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -284,6 +299,8 @@ def main():
     # ---- device-resident value: scans staged in HBM slots
     for f in range(args.warmup + args.steps):
         eng.scan_upload(f, wl.scans[f])
+    clocks = ClockSampler(local)
+    clocks.start()  # polling runs through the warm-up; only the timed region's samples are kept
     for f in range(args.warmup):
         d, c, v = wl.odometry[f]
         eng.step_slot(f, d, c, v)
@@ -293,9 +310,8 @@ def main():
             pg.barrier()
 
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     profs = []
+    clocks.mark()
     eng.timer_start()
     for f in range(args.warmup, args.warmup + args.steps):
         d, c, v = wl.odometry[f]
