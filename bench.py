@@ -23,8 +23,9 @@ particle-index shards (smcl_create_sharded, NCCL all-gathers at the
 exchange points), so scaling is strong: value = N_total pp / max-rank time.
 
 --impl reference runs the reference algorithm on the host cores (the oracle
-port: /root/reference cannot be built here, Eigen3 is absent) on a bounded
-sample of the same workload.
+port: /root/reference cannot be built here, Eigen3 is absent) on the same
+full workload (all particles). The cpu_baseline object of our own line times
+the same port on a bounded 65,536-particle sample (a few seconds).
 """
 import argparse
 import json
@@ -171,6 +172,10 @@ def cpu_reference(wl, n_sample, steps, warmup, threads):
 
 
 def run_reference(args):
+    """--impl reference: the reference algorithm (the oracle port; the reference
+    itself needs Eigen3, absent here) on the host cores, on the SAME workload
+    as our arm: all args.particles particles (1,048,576 by default), the same
+    map, scans, odometry, seeds and config. Each step is one full frame."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
@@ -178,15 +183,15 @@ def run_reference(args):
     wl = workload.build(args.workload, n_particles=args.particles, scan_points=args.scan_points,
                         n_frames=args.warmup + args.steps)
     threads = os.cpu_count()
-    val, ms = cpu_reference(wl, args.cpu_sample, args.steps, args.warmup, threads)
-    sample = (f"{args.cpu_sample} particles x {args.scan_points}-pt scans of the {args.workload} workload, "
-              f"{args.steps} timed steps after {args.warmup} warm-up, OpenMP on {threads} threads")
+    val, ms = cpu_reference(wl, args.particles, args.steps, args.warmup, threads)
+    sample = (f"the full workload: {args.particles} particles x {args.scan_points}-pt scans of the {args.workload} "
+              f"workload, {args.steps} timed steps after {args.warmup} warm-up, OpenMP on {threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD_TEXT[args.workload].format(n=args.particles, s=args.scan_points),
-                   "n_particles_sampled": args.cpu_sample, "scan_points": args.scan_points,
+                   "n_particles": args.particles, "scan_points": args.scan_points,
                    "parallelism": "host OpenMP"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -217,11 +222,15 @@ def gather_peaks():
         return None
 
 
-def roofline(prof_avg, hbm_peak, peak_kind, ms_kernels, workload="global_init"):
-    """Dominant-kernel roofline with BASELINE.md §3 algorithmic bytes."""
+def roofline(prof_avg, hbm_peak, peak_kind, ms_kernels, workload="global_init", world=1):
+    """Dominant-kernel roofline with BASELINE.md §3 algorithmic bytes, per
+    shard: the kernel times are this rank's, gn/ll_points count all shards
+    (divided by world), gn/ll_matched count this shard's matches."""
     kernels = {
-        "gicp_gn (K1)": (prof_avg["gn_kernel_ms"], 4.0 * prof_avg["gn_points"] + 36.0 * prof_avg["gn_matched"]),
-        "gicp_ll (K2)": (prof_avg["ll_kernel_ms"], 4.0 * prof_avg["ll_points"] + 36.0 * prof_avg["ll_matched"]),
+        "gicp_gn (K1)": (prof_avg["gn_kernel_ms"],
+                         4.0 * prof_avg["gn_points"] / world + 36.0 * prof_avg["gn_matched"]),
+        "gicp_ll (K2)": (prof_avg["ll_kernel_ms"],
+                         4.0 * prof_avg["ll_points"] / world + 36.0 * prof_avg["ll_matched"]),
     }
     for name, ms in ms_kernels.items():
         kernels.setdefault(name, (ms, None))
@@ -327,8 +336,9 @@ def main():
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         ms_step = float(t.item())
     # Particle-point evaluations actually performed (empty scans of the kidnap
-    # blackout contribute none), summed over shards.
-    pp = world * float(np.mean([p["gn_points"] + p["ll_points"] for p in profs]))
+    # blackout contribute none). The engine already counts gn_points/ll_points
+    # over ALL shards (n_total), so no world factor here.
+    pp = float(np.mean([p["gn_points"] + p["ll_points"] for p in profs]))
     value = pp / (ms_step * 1e-3)
 
     # ---- end to end through the public step call with host scan buffers
@@ -340,7 +350,7 @@ def main():
         d, c, v = wl.odometry[f]
         res = eng.step(wl.scans[f], d, c, v)
         p = eng.last_step_profile()
-        pp_e2e += world * (p["gn_points"] + p["ll_points"])
+        pp_e2e += p["gn_points"] + p["ll_points"]  # all shards
         h2d += p["h2d_bytes"] + 12 * 8 + 36 * 8 + 4  # scan arrays + odometry struct
         d2h += p["d2h_bytes"]
         assert math.isfinite(res["rep_log_post"])
@@ -377,7 +387,7 @@ def main():
         t = torch.tensor([raw_ms], device=f"cuda:{local}", dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         raw_ms = float(t.item())
-    pp_raw_step = pp_raw / args.steps * (world if pg else 1)
+    pp_raw_step = pp_raw / args.steps  # all shards
     # scan preparation alone: device pipeline vs the host product path
     from paper_2404_16370_b200.api import make_scan_cloud
     f0 = args.warmup
@@ -395,7 +405,7 @@ def main():
     hbm, kind = peaks()
     ms_kernels = {"lsh refresh+gather (K6/K7)": avg["refresh_gather_ms"], "svgd (K8)": avg["svgd_ms"],
                   "smooth (K12)": avg["smooth_ms"], "sort (CUB)": avg["sort_ms"]}
-    roof = roofline(avg, hbm, kind, ms_kernels, args.workload)
+    roof = roofline(avg, hbm, kind, ms_kernels, args.workload, world)
     # The same kernel against the achievable random-gather bandwidth of its
     # record table (L2-resident for the corridor map): the north-star's
     # "fraction of achievable L2/HBM gather bandwidth".

@@ -164,8 +164,12 @@ class FilterEngine:
     def num_particles(self):
         return _lib.lib().smcl_num_particles(self.h)
 
+    def num_local_particles(self):
+        """Particles held by this engine (its shard; all of them when unsharded)."""
+        return self.num_particles() // self.world
+
     def particles(self):
-        n = self.num_particles() // self.world
+        n = self.num_local_particles()
         p = Particles(n, self.cfg.k_neighbors)
         v = p.view()
         check(_lib.lib().smcl_get_particles(self.h, C.byref(v)))
@@ -197,7 +201,7 @@ class FilterEngine:
         return st.to_dict()
 
     def evaluate_all(self, scan, want_system=False):
-        n = self.num_particles()
+        n = self.num_local_particles()  # the ABI reads / writes this shard's rows
         sc, keep = scan.struct()
         steps, ll, nm = np.empty((n, 6)), np.empty(n), np.empty(n, np.int32)
         H = np.empty((n, 6, 6)) if want_system else None
@@ -208,7 +212,7 @@ class FilterEngine:
         return (steps, ll, nm, H, b) if want_system else (steps, ll, nm)
 
     def evaluate_likelihoods(self, scan):
-        n = self.num_particles()
+        n = self.num_local_particles()  # the ABI reads / writes this shard's rows
         sc, keep = scan.struct()
         ll, nm = np.empty(n), np.empty(n, np.int32)
         check(_lib.lib().smcl_evaluate_likelihoods(self.h, C.byref(sc), f64ptr(ll), i32ptr(nm)))
@@ -216,14 +220,14 @@ class FilterEngine:
         return ll, nm
 
     def compute_phis(self, steps=None):
-        n = self.num_particles()
+        n = self.num_local_particles()  # the ABI reads / writes this shard's rows
         out = np.empty((n, 6))
         sp = None if steps is None else f64ptr(_a(steps, (n, 6)))
         check(_lib.lib().smcl_compute_phis(self.h, sp, f64ptr(out)))
         return out
 
     def apply_updates(self, phis=None):
-        n = self.num_particles()
+        n = self.num_local_particles()  # the ABI reads / writes this shard's rows
         pp = None if phis is None else f64ptr(_a(phis, (n, 6)))
         check(_lib.lib().smcl_apply_updates(self.h, pp))
 

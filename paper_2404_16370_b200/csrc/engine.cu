@@ -404,11 +404,24 @@ struct smcl_engine {
   ScanDev scan_tmp;  // stage-API scans
 
   // Step profile: one event per boundary, read after the step's final sync.
-  enum Ev {
-    E_START, E_PRED, E_KEYS, E_SORT, E_REORDER, E_SEG, E_RG, E_NB, E_GN0, E_GN1, E_SOLVE, E_SVGD, E_LL0, E_LL1,
-    E_BAYES, E_SMOOTH, E_END, E_COUNT
-  };
+  enum Ev { E_START, E_PRED, E_KEYS, E_SORT, E_REORDER, E_SEG, E_RG, E_NB, E_LL0, E_LL1, E_BAYES, E_SMOOTH, E_END, E_COUNT };
   cudaEvent_t ev[E_COUNT] = {};
+  // One (GN start, GN end, solve end, SVGD end) quadruple per SVGD iteration,
+  // all read after the step's single end-of-frame sync.
+  enum ItEv { I_GN0, I_GN1, I_SOLVE, I_SVGD, I_COUNT };
+  std::vector<cudaEvent_t> it_ev;
+  int gn_iter = 0;  // SVGD iteration of the running step (event slot)
+  void mark_it(int it, ItEv e) {
+    const size_t q = static_cast<size_t>(it) * I_COUNT + e;
+    if (it_ev.size() <= q) it_ev.resize(q + 1, nullptr);
+    if (!it_ev[q]) CK(cudaEventCreate(&it_ev[q]));
+    CK(cudaEventRecord(it_ev[q], st));
+  }
+  float since_it(int it, ItEv a, ItEv b) const {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, it_ev[static_cast<size_t>(it) * I_COUNT + a], it_ev[static_cast<size_t>(it) * I_COUNT + b]);
+    return ms;
+  }
   cudaEvent_t timer[2] = {};
   smcl_step_profile prof{};
   bool fast_used = false;
@@ -489,6 +502,8 @@ struct smcl_engine {
     if (nb_host) cudaFreeHost(nb_host);
     if (step_host) cudaFreeHost(step_host);
     for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& e : it_ev)
       if (e) cudaEventDestroy(e);
     for (auto& e : timer)
       if (e) cudaEventDestroy(e);
@@ -945,7 +960,7 @@ struct smcl_engine {
     if (!has_map) throw std::invalid_argument("engine has no map");
     if (sd.n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
     ScanView sv{sd.n, sd.mu.p, sd.sigma.p, sd.structured ? sd.rec.p : nullptr, sd.l1max};
-    if (profiling) mark(gn ? E_GN0 : E_LL0);
+    if (profiling) gn ? mark_it(gn_iter, I_GN0) : mark(E_LL0);
     fast_used = use_fast(sd);
     if (fast_used) {
       MapFast mf{geom, map_fast.p, map_brick};
@@ -956,9 +971,9 @@ struct smcl_engine {
       launch_gicp_exact(gn, poses.p, n_local, sv, me, sys.p, raw_ll.p, nm.p, st);
     }
     CK(cudaGetLastError());
-    if (profiling) {
-      mark(gn ? E_GN1 : E_LL1);
-      launch_match_counts(ll.p /*unused for the sum*/, nm.p, n_local, d_counts.p + (gn ? 2 : 4), st);
+    if (profiling) {  // matched particle-points of this pass, summed over the step's passes (counts only)
+      gn ? mark_it(gn_iter, I_GN1) : mark(E_LL1);
+      launch_match_counts(nullptr, nm.p, n_local, d_counts.p + (gn ? 2 : 4), st, /*zero=*/false);
     }
     const GicpParamsDev gp = gicp_params(sd.n);
     if (gn)
@@ -1327,6 +1342,10 @@ struct smcl_engine {
     ScanSlot& sl = slot_at(slot_i);
     if (!sl.valid) throw std::invalid_argument("scan slot not uploaded");
     profiling = true;
+    struct ProfilingOff {  // cleared on every exit path (a throwing stage must not leave the step's events armed)
+      bool& f;
+      ~ProfilingOff() { f = false; }
+    } profiling_off{profiling};
     const long long launches0 = launch_count();
     const long long d2h0 = g_d2h.load();
     smcl_frame_result r;
@@ -1361,17 +1380,12 @@ struct smcl_engine {
     double t_like = 0.0, t_upd = 0.0, t_gn = 0.0, t_solve = 0.0, t_svgd = 0.0;
     const ScanDev& gn_scan = sl.gn_view();
     if (!empty) {
-      for (int it = 0; it < cfg.n_svgd_iters; ++it) {
+      for (int it = 0; it < cfg.n_svgd_iters; ++it) {  // filter.cpp:166-180
+        gn_iter = it;
         run_likelihood(true, gn_scan);
-        mark(E_SOLVE);
+        mark_it(it, I_SOLVE);
         svgd(true);
-        mark(E_SVGD);
-        if (it + 1 < cfg.n_svgd_iters) {  // events are reused: read them before the next iteration
-          sync();
-          t_gn += since(E_GN0, E_GN1);
-          t_solve += since(E_GN1, E_SOLVE);
-          t_svgd += since(E_SOLVE, E_SVGD);
-        }
+        mark_it(it, I_SVGD);
       }
       run_likelihood(false, sl.full);
       mark(E_BAYES);
@@ -1400,11 +1414,12 @@ struct smcl_engine {
       last_nm_sum = cnt[1];
     }
     finish_nb_stats();
-    if (!empty) {  // last (or only) Gauss-Newton iteration
-      t_gn += since(E_GN0, E_GN1);
-      t_solve += since(E_GN1, E_SOLVE);
-      t_svgd += since(E_SOLVE, E_SVGD);
-    }
+    if (!empty)
+      for (int it = 0; it < cfg.n_svgd_iters; ++it) {
+        t_gn += since_it(it, I_GN0, I_GN1);
+        t_solve += since_it(it, I_GN1, I_SOLVE);
+        t_svgd += since_it(it, I_SOLVE, I_SVGD);
+      }
     t_like = t_gn + t_solve;
     t_upd = t_svgd;
     const double t_ll = since(E_LL0, E_BAYES);
@@ -1442,7 +1457,6 @@ struct smcl_engine {
     prof.kernel_launches = launch_count() - launches0;
     prof.d2h_bytes = g_d2h.load() - d2h0;
     prof.h2d_bytes = sl.upload_bytes;
-    profiling = false;
     *out = r;
     ++frame;
   }

@@ -126,7 +126,10 @@ void launch_bayes_numer(double* lp, const double* ll, const int32_t* nm, int64_t
                         const unsigned long long* matched, double fill, cudaStream_t st);
 void launch_sum_pairs(const unsigned long long* g, int world, unsigned long long* out, cudaStream_t st);
 void launch_fill(double* v, int64_t n, double value, cudaStream_t st);
-void launch_match_counts(const double* ll, const int32_t* nm, int64_t n, unsigned long long* out, cudaStream_t st);
+// out[0] += particles with ll > -1e30 (ll may be null: not counted), out[1] += sum nm;
+// zero: clear out[0..1] first.
+void launch_match_counts(const double* ll, const int32_t* nm, int64_t n, unsigned long long* out, cudaStream_t st,
+                         bool zero = true);
 int argmax_partials(int64_t n);
 void launch_argmax(const double* v, int64_t n, int64_t gbase, double* scratch_v, long long* scratch_i, double* out_v,
                    long long* out_i, cudaStream_t st);

@@ -58,7 +58,7 @@ __global__ void k_match_counts(const double* __restrict__ ll, const int32_t* __r
   unsigned long long a = 0, b = 0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    a += ll[i] > -1e30 ? 1ull : 0ull;
+    if (ll) a += ll[i] > -1e30 ? 1ull : 0ull;
     b += static_cast<unsigned long long>(nm[i]);
   }
 #pragma unroll
@@ -378,9 +378,10 @@ void launch_fill(double* v, int64_t n, double value, cudaStream_t st) {
   count_launch();
   if (n > 0) k_fill<<<blocks_for(n, 256), 256, 0, st>>>(v, n, value);
 }
-void launch_match_counts(const double* ll, const int32_t* nm, int64_t n, unsigned long long* out, cudaStream_t st) {
+void launch_match_counts(const double* ll, const int32_t* nm, int64_t n, unsigned long long* out, cudaStream_t st,
+                         bool zero) {
   count_launch();
-  cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), st);
+  if (zero) cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), st);
   if (n > 0) {
     const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(n, 256), 1184));
     k_match_counts<<<g, 256, 0, st>>>(ll, nm, n, out);
