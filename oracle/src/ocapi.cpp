@@ -210,6 +210,20 @@ int orc_solve_step(const double* H, const double* b, double lambda, double omax,
     for (int i = 0; i < 6; ++i) out[i] = v[i];
   });
 }
+// solve_step over n systems (H row-major 36, b 6, lambda per system).
+int orc_solve_step_batch(const double* H, const double* b, const double* lambda, std::int64_t n, double omax,
+                         double vmax, double* out) {
+  return guard([&] {
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < n; ++i) {
+      GnSystem s;
+      std::memcpy(s.H.m, H + 36 * i, 36 * sizeof(double));
+      for (int q = 0; q < 6; ++q) s.b[q] = b[6 * i + q];
+      const V6 v = solve_step(s, lambda[i], omax, vmax);
+      for (int q = 0; q < 6; ++q) out[6 * i + q] = v[q];
+    }
+  });
+}
 void orc_covariance_sqrt(const double* cov, double* L) {
   M6 c;
   std::memcpy(c.m, cov, 36 * sizeof(double));
@@ -447,6 +461,7 @@ std::int64_t orc_engine_num_particles(void* h) {
 int orc_engine_get(void* h, smcl_particles_view* view) {
   return guard([&] { store_set(static_cast<FilterEngine*>(h)->particles(), view); });
 }
+void orc_engine_set_frame(void* h, std::int64_t f) { static_cast<FilterEngine*>(h)->set_frame_index(f); }
 int orc_engine_set(void* h, const smcl_particles_view* view) {
   return guard([&] { static_cast<FilterEngine*>(h)->particles() = load_set(view); });
 }

@@ -247,6 +247,9 @@ class FilterEngine {  // filter.hpp:104-130
   const NearestNeighborField& nnf() const { return nnf_; }
   const GaussianCloud& map() const { return map_; }
   std::int64_t frame_index() const { return frame_; }
+  // Test harness only (no reference counterpart): start an oracle engine at
+  // another engine's frame index, so both derive the same per-frame seeds.
+  void set_frame_index(std::int64_t f) { frame_ = f; }
   const FilterConfig& config() const { return cfg_; }
 
  private:
