@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define SMCL_ABI_VERSION 2
+#define SMCL_ABI_VERSION 3
 #define SMCL_MAX_HIST 1026
 
 enum {
@@ -214,6 +214,10 @@ typedef struct smcl_step_profile {
   int32_t fast_path, n_svgd_iters;
   int64_t kernel_launches;        /* hand-written kernels launched by the step */
   int64_t h2d_bytes, d2h_bytes;   /* host<->device bytes: last scan upload, step read-backs */
+  /* LSH near-integer guard (lsh.cu), engine lifetime totals: particles whose
+   * hash K3 flagged for a host (glibc) check, and neighbour passes replayed
+   * because a host key differed from the device's. */
+  int64_t hash_guard_flagged, hash_guard_replays;
 } smcl_step_profile;
 int smcl_last_step_profile(smcl_engine* h, smcl_step_profile* out);
 /* Device timer on the engine stream (CUDA events): start, then stop returns

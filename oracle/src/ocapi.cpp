@@ -329,6 +329,21 @@ int orc_update_neighbors(smcl_particles_view* view, const smcl_config* cfg, std:
     store_stats(st, stats);
   });
 }
+// NeighborGraph::init_self(1, k) followed by offer(0, js[q], kvs[q]) for each
+// q (neighbor_graph.hpp:24-72); the final list of particle 0.
+int orc_graph_offers(int k, const std::int32_t* js, const float* kvs, int n_offers, std::int32_t* idx_out,
+                     float* kval_out, std::int32_t* count_out) {
+  return guard([&] {
+    NeighborGraph g;
+    g.init_self(1, k);
+    for (int q = 0; q < n_offers; ++q) g.offer(0, js[q], kvs[q]);
+    for (int s = 0; s < k; ++s) {
+      idx_out[s] = g.idx[static_cast<std::size_t>(s)];
+      kval_out[s] = g.kval[static_cast<std::size_t>(s)];
+    }
+    *count_out = g.count[0];
+  });
+}
 int orc_brute_knn(const double* poses, std::int64_t n, int k, double sr, double st, std::int32_t* out) {
   return guard([&] {
     std::vector<Pose> ps(static_cast<std::size_t>(n));

@@ -142,7 +142,8 @@ class SmclStepProfile(C.Structure):
         "gn_kernel_ms", "solve_ms", "svgd_ms", "ll_kernel_ms", "bayes_ms", "smooth_ms", "rep_ms", "total_ms")] + [
         ("gn_points", C.c_int64), ("ll_points", C.c_int64), ("gn_matched", C.c_int64), ("ll_matched", C.c_int64),
         ("fast_path", C.c_int32), ("n_svgd_iters", C.c_int32), ("kernel_launches", C.c_int64),
-        ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+        ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+        ("hash_guard_flagged", C.c_int64), ("hash_guard_replays", C.c_int64)]
 
     def to_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -352,7 +352,7 @@ struct smcl_engine {
   DBuf<float4> map_fast;
 
   // particles
-  DBuf<Pose> poses, poses2;
+  DBuf<Pose> poses, poses2, poses3;  // poses3: SVGD's output never lands on the guard checkpoint
   DBuf<double> log_post, log_post2;
   DBuf<int32_t> id, id2, idx, idx2, count, count2;
   DBuf<float> kval, kval2;
@@ -616,6 +616,7 @@ struct smcl_engine {
     }
     poses.ensure(un);
     poses2.ensure(un);
+    poses3.ensure(un);
     log_post.ensure(un);
     log_post2.ensure(un);
     id.ensure(un);
@@ -1000,15 +1001,10 @@ struct smcl_engine {
     CK(cudaGetLastError());
   }
 
-  void update_neighbors(uint64_t pass_seed, const double* bounds, smcl_neighbor_stats* out) {
+  // Pass scalars on the host (neighbor_search.cpp:71-103): identical
+  // SplitMix64 + libm as the reference.
+  LshPass make_pass(uint64_t pass_seed, const double* bounds) const {
     const int64_t n = n_total;
-    join_aux();
-    nb_out = nullptr;
-    if (out) std::memset(out, 0, sizeof(*out));
-    if (n == 0) return;
-    if (k != cfg.k_neighbors) throw std::invalid_argument("update_neighbors: graph not initialized for this set");
-    // Pass randomness on the host (neighbor_search.cpp:71-73): identical
-    // SplitMix64 + libm as the reference.
     SplitMix64 rng(pass_seed);
     LshPass lp{};
     random_rotation(rng, lp.frame.R);
@@ -1027,10 +1023,148 @@ struct smcl_engine {
     lp.h_bits = std::max(1, static_cast<int>(std::bit_width(static_cast<uint32_t>(nb - 1))));
     lp.prio_bits = std::max(0, 64 - lp.h_bits - lp.idx_bits);
     lp.prio_seed = mix_seed(pass_seed, 0x70726f6974ull);
+    return lp;
+  }
+
+  // ---- LSH near-integer guard (lsh.cu): speculate, verify, replay.
+  // K3 hashes with CUDA's libm and counts the particles whose cell
+  // coordinates sit within the libm-discrepancy bound of an integer. After the
+  // pass's (or step's) sync, a nonzero count makes the host rehash this
+  // shard's particles with glibc (the reference's arithmetic, lsh_key_host);
+  // if any key differs, the pre-pass state is restored from the checkpoint
+  // and the neighbour pass (and, in a step, everything after it) is replayed
+  // on the corrected keys. The checkpoint costs nothing with reorder (the
+  // pre-pass arrays survive in the second buffers and SVGD never writes the
+  // post-predict pose buffer, see svgd()); without reorder the lists and
+  // log-posteriors are copied aside (172 B per particle).
+  DBuf<unsigned> lsh_flagged;
+  LshPass last_lp{};
+  double last_bounds[6] = {};
+  bool ckpt_reorder = false;
+  const Pose* ckpt_poses = nullptr;
+  unsigned long long guard_flagged_total = 0, guard_replays = 0;
+  DBuf<int> guard_flag_dev, guard_flag_all;
+
+  void begin_neighbors(uint64_t pass_seed, const double* bounds) {
+    last_lp = make_pass(pass_seed, bounds);
+    std::memcpy(last_bounds, bounds, sizeof(last_bounds));
+    ckpt_poses = poses.p;
+    ckpt_reorder = cfg.reorder_particles != 0;
+    if (!ckpt_reorder) {
+      const size_t nl = static_cast<size_t>(n_local), kk = static_cast<size_t>(k);
+      CK(cudaMemcpyAsync(log_post2.p, log_post.p, sizeof(double) * nl, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(idx2.p, idx.p, sizeof(int32_t) * nl * kk, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(kval2.p, kval.p, sizeof(float) * nl * kk, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(count2.p, count.p, sizeof(int32_t) * nl, cudaMemcpyDeviceToDevice, st));
+    }
+    lsh_flagged.ensure(1);
+    launch_lsh_keys(poses.p, n_local, gbase, last_lp, keys.p, lsh_flagged.p, st);
+  }
+
+  // After a sync: flagged = this pass's flag count summed over all shards.
+  // Rehashes on the host; patches keys.p and returns true when any shard
+  // must replay.
+  bool guard_mismatch(unsigned long long flagged) {
+    if (flagged == 0) return false;
+    guard_flagged_total += flagged;
+    const size_t nl = static_cast<size_t>(n_local);
+    std::vector<Pose> hp(nl);
+    std::vector<uint64_t> hk(nl);
+    CK(cudaMemcpyAsync(hp.data(), ckpt_poses, sizeof(Pose) * nl, cudaMemcpyDeviceToHost, st));
+    keys.download(hk.data(), nl, st);
+    sync();
+    int mism = 0;
+#pragma omp parallel for schedule(static) reduction(| : mism)
+    for (int64_t i = 0; i < n_local; ++i) {
+      const uint64_t kh = lsh_key_host(hp[static_cast<size_t>(i)], static_cast<uint64_t>(gbase + i), last_lp);
+      if (kh != hk[static_cast<size_t>(i)]) {
+        hk[static_cast<size_t>(i)] = kh;
+        mism = 1;
+      }
+    }
+    if (mism) keys.upload(hk.data(), nl, st);
+    if (sharded) {  // every shard replays if any shard must
+      guard_flag_dev.ensure(1);
+      guard_flag_all.ensure(static_cast<size_t>(world));
+      CK(cudaMemcpyAsync(guard_flag_dev.p, &mism, sizeof(int), cudaMemcpyHostToDevice, st));
+      allgather(guard_flag_dev.p, guard_flag_all.p, sizeof(int));
+      std::vector<int> all(static_cast<size_t>(world));
+      guard_flag_all.download(all.data(), all.size(), st);
+      sync();
+      for (int v : all) mism |= v;
+    } else {
+      sync();
+    }
+    return mism != 0;
+  }
+
+  // Pre-pass state back in place (the pass's outputs are discarded).
+  void restore_pass() {
+    log_post.swap(log_post2);
+    idx.swap(idx2);
+    kval.swap(kval2);
+    count.swap(count2);
+    if (ckpt_reorder) id.swap(id2);
+    if (poses.p != ckpt_poses) (poses2.p == ckpt_poses ? poses.swap(poses2) : poses.swap(poses3));
+    poses_changed();
+    steps_valid = phis_valid = ll_valid = false;
+    ++guard_replays;
+  }
+
+  // Global flag count of the last K3 (sharded: summed over shards; stage API only).
+  unsigned long long flagged_global() {
+    unsigned v = 0;
+    CK(cudaMemcpyAsync(&v, lsh_flagged.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    sync();
+    unsigned long long tot = v;
+    if (sharded) {
+      guard_flag_dev.ensure(1);
+      guard_flag_all.ensure(static_cast<size_t>(world));
+      const int vi = static_cast<int>(v);
+      CK(cudaMemcpyAsync(guard_flag_dev.p, &vi, sizeof(int), cudaMemcpyHostToDevice, st));
+      allgather(guard_flag_dev.p, guard_flag_all.p, sizeof(int));
+      std::vector<int> all(static_cast<size_t>(world));
+      guard_flag_all.download(all.data(), all.size(), st);
+      sync();
+      tot = 0;
+      for (int x : all) tot += static_cast<unsigned long long>(x);
+    }
+    return tot;
+  }
+
+  // Stage API update_neighbors (neighbor_search.cpp:61-192): K3, the rest of
+  // the pass, and the guard's verification / replay.
+  void update_neighbors(uint64_t pass_seed, const double* bounds, smcl_neighbor_stats* out) {
+    if (!begin_pass_checks(out)) return;
+    begin_neighbors(pass_seed, bounds);
+    neighbor_rest(out);
+    if (guard_mismatch(flagged_global())) {
+      restore_pass();
+      neighbor_rest(out);
+    }
+  }
+
+  bool begin_pass_checks(smcl_neighbor_stats* out) {
+    join_aux();
+    nb_out = nullptr;
+    if (out) std::memset(out, 0, sizeof(*out));
+    if (n_total == 0) return false;
+    if (k != cfg.k_neighbors) throw std::invalid_argument("update_neighbors: graph not initialized for this set");
+    return true;
+  }
+
+  // The neighbour pass after K3: key exchange, sort, reorder, bucket runs,
+  // fused refresh + gather, statistics.
+  void neighbor_rest(smcl_neighbor_stats* out) {
+    const int64_t n = n_total;
+    join_aux();
+    nb_out = nullptr;
+    if (out) std::memset(out, 0, sizeof(*out));
+    const LshPass& lp = last_lp;
+    const double* bounds = last_bounds;
+    const int32_t nb = static_cast<int32_t>(lp.n_buckets);
     const uint64_t idx_mask = (uint64_t(1) << lp.idx_bits) - 1;
     const int shift = lp.prio_bits + lp.idx_bits;
-
-    launch_lsh_keys(poses.p, n_local, gbase, lp, keys.p, st);
     // Exchange 1: every rank needs all N keys (global sort, bucket
     // runs) and all N poses (candidates of its own particles).
     const uint64_t* keys_all = keys.p;
@@ -1160,9 +1294,10 @@ struct smcl_engine {
     // Exchange 2: neighbours' poses and Gauss-Newton steps.
     const Pose* pa = all_poses();
     const double* sa = all_steps();
-    if (fused_apply) {
-      launch_svgd(pa, sa, n_local, gbase, idx.p, count.p, k, sp, nullptr, poses2.p, st);
-      poses.swap(poses2);
+    if (fused_apply) {  // into whichever spare buffer does not hold the post-predict checkpoint
+      DBuf<Pose>& dst = poses2.p != ckpt_poses ? poses2 : poses3;
+      launch_svgd(pa, sa, n_local, gbase, idx.p, count.p, k, sp, nullptr, dst.p, st);
+      poses.swap(dst);
       poses_changed();
     } else {
       launch_svgd(pa, sa, n_local, gbase, idx.p, count.p, k, sp, phis.p, nullptr, st);
@@ -1282,21 +1417,24 @@ struct smcl_engine {
   // Value, index, pose and id of the winner gathered on the device into one
   // staging record, read back into pinned memory (no host round trip until
   // the caller's sync).
+  // rep_stage[15] (sharded: summed over shards): the last K3's hash-guard flag count.
   void representative_enqueue() {
     if (n_local == 0) throw std::invalid_argument("representative: empty or mismatched particle set");
+    lsh_flagged.ensure(1);
     global_argmax(4, 1);
     rep_stage.ensure(16);
     if (sharded) {  // the owner rank publishes the winner's pose and id (one slot per rank)
       double* mine = g_rep.p + 14 * static_cast<size_t>(rank);
-      launch_rep_local(scal.p + 4, scal_i.p + 1, n_local, rank, true, poses.p, id.p, reinterpret_cast<Pose*>(mine),
-                       nullptr, nullptr, st);
+      launch_rep_local(scal.p + 4, scal_i.p + 1, n_local, rank, true, poses.p, id.p, lsh_flagged.p,
+                       reinterpret_cast<Pose*>(mine), nullptr, nullptr, st);
       allgather(mine, g_rep.p, 14 * sizeof(double));
       launch_rep_select(scal.p + 4, scal_i.p + 1, n_local, world, g_rep.p, rep_stage.p, st);
     } else {
-      launch_rep_local(scal.p + 4, scal_i.p + 1, n_local, 0, false, poses.p, id.p, nullptr, nullptr, rep_stage.p, st);
+      launch_rep_local(scal.p + 4, scal_i.p + 1, n_local, 0, false, poses.p, id.p, lsh_flagged.p, nullptr, nullptr,
+                       rep_stage.p, st);
     }
-    CK(cudaMemcpyAsync(step_host->rep, rep_stage.p, sizeof(double) * 15, cudaMemcpyDeviceToHost, st));
-    g_d2h += sizeof(double) * 15;
+    CK(cudaMemcpyAsync(step_host->rep, rep_stage.p, sizeof(double) * 16, cudaMemcpyDeviceToHost, st));
+    g_d2h += sizeof(double) * 16;
   }
   void representative_read(int64_t* index, double* pose, double* value) {  // after a sync
     const double* h = step_host->rep;
@@ -1375,36 +1513,49 @@ struct smcl_engine {
     mark(E_PRED);
     const double bounds[6] = {map_bounds.min[0], map_bounds.min[1], map_bounds.min[2],
                               map_bounds.max[0], map_bounds.max[1], map_bounds.max[2]};
-    update_neighbors(mix_seed(cfg.seed, k_stream_neighbors, static_cast<uint64_t>(frame)), bounds, &r.neighbor_stats);
-    mark(E_NB);
-    double t_like = 0.0, t_upd = 0.0, t_gn = 0.0, t_solve = 0.0, t_svgd = 0.0;
-    const ScanDev& gn_scan = sl.gn_view();
-    if (!empty) {
-      for (int it = 0; it < cfg.n_svgd_iters; ++it) {  // filter.cpp:166-180
-        gn_iter = it;
-        run_likelihood(true, gn_scan);
-        mark_it(it, I_SOLVE);
-        svgd(true);
-        mark_it(it, I_SVGD);
-      }
-      run_likelihood(false, sl.full);
-      mark(E_BAYES);
-      bayes_async(cfg.beta, cfg.log_post_floor);  // rejection flag read at the end of the step
-    } else {
-      mark(E_LL0);
-      mark(E_LL1);
-      mark(E_BAYES);
-    }
-    mark(E_SMOOTH);  // posterior smoothing starts
-    smooth(cfg.smooth_iters, cfg.log_post_floor);
-    mark(E_END);
     int64_t ix;
     double v;
-    representative_enqueue();
-    join_aux();
-    CK(cudaMemcpyAsync(step_host->cnt, d_counts.p, sizeof(unsigned long long) * 6, cudaMemcpyDeviceToHost, st));
-    g_d2h += sizeof(unsigned long long) * 6;
-    sync();  // the step's one end-of-frame host synchronisation
+    begin_pass_checks(&r.neighbor_stats);
+    begin_neighbors(mix_seed(cfg.seed, k_stream_neighbors, static_cast<uint64_t>(frame)), bounds);  // K3
+    double t_like = 0.0, t_upd = 0.0, t_gn = 0.0, t_solve = 0.0, t_svgd = 0.0;
+    const ScanDev& gn_scan = sl.gn_view();
+    // Everything after K3, up to the end-of-frame readback and sync; run a
+    // second time only if the hash guard finds a key to correct.
+    auto run_from_keys = [&]() {
+      neighbor_rest(&r.neighbor_stats);
+      mark(E_NB);
+      if (!empty) {
+        for (int it = 0; it < cfg.n_svgd_iters; ++it) {  // filter.cpp:166-180
+          gn_iter = it;
+          run_likelihood(true, gn_scan);
+          mark_it(it, I_SOLVE);
+          svgd(true);
+          mark_it(it, I_SVGD);
+        }
+        run_likelihood(false, sl.full);
+        mark(E_BAYES);
+        bayes_async(cfg.beta, cfg.log_post_floor);  // rejection flag read at the end of the step
+      } else {
+        mark(E_LL0);
+        mark(E_LL1);
+        mark(E_BAYES);
+      }
+      mark(E_SMOOTH);  // posterior smoothing starts
+      smooth(cfg.smooth_iters, cfg.log_post_floor);
+      mark(E_END);
+      representative_enqueue();
+      join_aux();
+      CK(cudaMemcpyAsync(step_host->cnt, d_counts.p, sizeof(unsigned long long) * 6, cudaMemcpyDeviceToHost, st));
+      g_d2h += sizeof(unsigned long long) * 6;
+      sync();  // the step's one end-of-frame host synchronisation
+    };
+    run_from_keys();
+    // step_host->rep[15]: this pass's hash-guard flags, summed over all shards
+    if (guard_mismatch(static_cast<unsigned long long>(step_host->rep[15]))) {
+      restore_pass();
+      CK(cudaMemsetAsync(d_counts.p, 0, sizeof(unsigned long long) * 6, st));
+      run_from_keys();
+    }
     representative_read(&ix, r.representative, &v);
     unsigned long long cnt[6];
     std::memcpy(cnt, step_host->cnt, sizeof(cnt));
@@ -1770,6 +1921,9 @@ int smcl_last_step_profile(smcl_engine* h, smcl_step_profile* out) {
   return guard([&] {
     if (!h) throw std::invalid_argument("null engine handle");
     *out = h->prof;
+    // engine-lifetime totals, current also after stage-API passes
+    out->hash_guard_flagged = static_cast<int64_t>(h->guard_flagged_total);
+    out->hash_guard_replays = static_cast<int64_t>(h->guard_replays);
   });
 }
 
@@ -2037,12 +2191,18 @@ int smcl_lsh_hash_batch(const double* poses, int64_t n, const double frame[12], 
     lp.sigma_t = sigma_t;
     DBuf<Pose> dp;
     DBuf<uint64_t> dout;
+    DBuf<unsigned char> damb;
     dp.upload(h.data(), h.size(), nullptr);
     dout.ensure(static_cast<size_t>(n));
-    launch_hash_batch(dp.p, n, lp, dout.p, nullptr);
+    damb.ensure(static_cast<size_t>(n));
+    launch_hash_batch(dp.p, n, lp, dout.p, damb.p, nullptr);
     CK(cudaGetLastError());
     dout.download(out, static_cast<size_t>(n), nullptr);
+    std::vector<unsigned char> amb(static_cast<size_t>(n));
+    damb.download(amb.data(), amb.size(), nullptr);
     CK(cudaDeviceSynchronize());
+    for (int64_t i = 0; i < n; ++i)  // near-integer guard: the reference's (glibc) hash
+      if (amb[static_cast<size_t>(i)]) out[i] = lsh_hash_host(h[static_cast<size_t>(i)], lp);
   });
 }
 

@@ -54,8 +54,15 @@ void launch_log_batch(const Pose* p, int64_t n, double* out, cudaStream_t st);
 void launch_kernel_batch(const Pose* a, const Pose* b, int64_t n, double sr, double st_, double* out, cudaStream_t st);
 
 // lsh.cu
-void launch_lsh_keys(const Pose* poses, int64_t n, int64_t gbase, const LshPass& lp, uint64_t* keys, cudaStream_t st);
-void launch_hash_batch(const Pose* poses, int64_t n, const LshPass& lp, uint64_t* out, cudaStream_t st);
+// K3. flagged (may be null): count of particles whose hash the host must
+// verify with glibc (lsh.cu near-integer guard).
+void launch_lsh_keys(const Pose* poses, int64_t n, int64_t gbase, const LshPass& lp, uint64_t* keys,
+                     unsigned* flagged, cudaStream_t st);
+// out: raw hashes (no modulo); amb[i] = 1 where the host must rehash (lsh_hash_host).
+void launch_hash_batch(const Pose* poses, int64_t n, const LshPass& lp, uint64_t* out, unsigned char* amb,
+                       cudaStream_t st);
+uint64_t lsh_hash_host(const Pose& pose, const LshPass& lp);  // glibc, as the reference
+uint64_t lsh_key_host(const Pose& pose, uint64_t gi, const LshPass& lp);  // K3's key, host (glibc)
 size_t sort_temp_bytes(int64_t n);
 void sort_keys(const uint64_t* in, uint64_t* out, int64_t n, int begin_bit, int end_bit, void* temp, size_t temp_bytes,
                cudaStream_t st);
@@ -117,8 +124,10 @@ cudaError_t scan_gather_stride(const double* d_mu, const double* d_sigma, int n_
                                double* sigma_out, cudaStream_t st);
 
 // posterior.cu
+// flagged: the last K3's hash-guard count (stage[15], or the record's 14th double when sharded).
 void launch_rep_local(const double* v, const long long* ix, int64_t n_local, int rank, bool sharded, const Pose* poses,
-                      const int32_t* id, Pose* dst_pose, int32_t* dst_id, double* stage, cudaStream_t st);
+                      const int32_t* id, const unsigned* flagged, Pose* dst_pose, int32_t* dst_id, double* stage,
+                      cudaStream_t st);
 void launch_rep_select(const double* v, const long long* ix, int64_t n_local, int world, const double* g_rec,
                        double* stage, cudaStream_t st);
 void launch_merge_pairs(const double* g, int world, double* out_v, long long* out_i, cudaStream_t st);

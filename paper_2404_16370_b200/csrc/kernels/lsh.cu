@@ -22,40 +22,86 @@ namespace {
 
 inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
-__constant__ uint64_t c_primes[6] = {73856093ull, 19349663ull, 83492791ull, 49979687ull, 39916801ull, 15485863ull};
+// neighbor_search.cpp:20-21 (host and device; c is a compile-time index after unrolling)
+__host__ __device__ __forceinline__ uint64_t lsh_prime(int c) {
+  return c == 0 ? 73856093ull
+                : c == 1 ? 19349663ull : c == 2 ? 83492791ull : c == 3 ? 49979687ull : c == 4 ? 39916801ull : 15485863ull;
+}
 
-// neighbor_search.cpp:25-35. Casts follow x86 (out-of-range -> INT64_MIN).
-__device__ __forceinline__ uint64_t lsh_hash_dev(const Pose& pose, const Pose& frame, const double noise[6],
-                                                 double alpha, double sr, double st) {
+// neighbor_search.cpp:25-35 on the host (glibc atan2 / sin, as the reference)
+// and on the device (CUDA libm). Casts follow x86 (out-of-range -> INT64_MIN).
+//
+// Near-integer guard (device): CUDA's atan2 / sin differ from glibc's by up
+// to ~2 ulp (glibc's are not correctly rounded either: ~0.1 % of arguments
+// are 1 ulp off), so a cell coordinate zeta within a few ulp of an integer
+// (or a rotation angle at one of se3_log's branch thresholds) may floor
+// differently from the reference. *amb is set when that cannot be excluded:
+// |zeta - round(zeta)| below a bound on the propagated libm discrepancy,
+//   G_c = 64 eps (|zeta_c| + alpha w_c (theta + |t|_1 + 1)(2 + theta / sin theta)),
+// (theta / sin theta: an angle error amplified by theta / (2 sin theta) near
+// pi). The engine counts flagged particles; after the step it rehashes them
+// on the host with glibc (the reference's own arithmetic) and replays the
+// neighbour pass onward if any key differs (engine.cu verify_lsh_guard), so
+// the keys are the reference's by construction. For random poses G ~ 1e-13:
+// about one flag per 10^11 hashes, i.e. the check is free.
+__host__ __device__ __forceinline__ uint64_t lsh_hash_hd(const Pose& pose, const Pose& frame, const double noise[6],
+                                                         double alpha, double sr, double st, bool* amb) {
+  const Pose rel = inv_compose_x(frame, pose);
   double d[6];
-  se3_log(inv_compose_x(frame, pose), d);
+  se3_log(rel, d);
   uint64_t h = 0;
+  double zeta[6];
 #pragma unroll
   for (int c = 0; c < 6; ++c) {
     const double w = c < 3 ? sr : st;
-    const double zeta = xadd(xmul(alpha, xmul(w, d[c])), noise[c]);
-    const double f = floor(zeta);
+    zeta[c] = xadd(xmul(alpha, xmul(w, d[c])), noise[c]);
+    const double f = floor(zeta[c]);
     const int64_t cell = (f >= -9223372036854775808.0 && f < 9223372036854775808.0) ? static_cast<int64_t>(f)
                                                                                     : INT64_MIN;
-    h ^= static_cast<uint64_t>(cell) * c_primes[c];
+    h ^= static_cast<uint64_t>(cell) * lsh_prime(c);
   }
+#ifdef __CUDA_ARCH__
+  if (amb) {
+    constexpr double kEps = 2.220446049250313e-16;
+    const double th = sqrt(fma(d[0], d[0], fma(d[1], d[1], d[2] * d[2])));
+    const double tn = fabs(rel.t[0]) + fabs(rel.t[1]) + fabs(rel.t[2]);
+    const double amp = 2.0 + (th > 1e-300 ? th / fmax(sin(th), 1e-300) : 1.0);
+    bool a = fabs(th - (kPi - 1e-6)) <= 1e-9 || fabs(th - 1e-8) <= 1e-17 || fabs(th * th - 1e-8) <= 1e-17;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      const double w = c < 3 ? sr : st;
+      const double g = 64.0 * kEps * (fabs(zeta[c]) + alpha * w * (th + tn + 1.0) * amp);
+      const double fr = zeta[c] - floor(zeta[c]);
+      a = a || !(fr >= g && 1.0 - fr >= g) || !(fabs(zeta[c]) < 1e15);
+    }
+    *amb = a;
+  }
+#else
+  if (amb) *amb = false;
+#endif
   return h;
 }
 
 __global__ void k_lsh_keys(const Pose* __restrict__ poses, int64_t n, int64_t gbase, LshPass lp,
-                           uint64_t* __restrict__ keys) {
+                           uint64_t* __restrict__ keys, unsigned* __restrict__ flagged) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint64_t gi = static_cast<uint64_t>(gbase + i);
-  const uint64_t h = lsh_hash_dev(poses[i], lp.frame, lp.noise, lp.alpha, lp.sigma_r, lp.sigma_t) %
+  bool amb = false;
+  const uint64_t h = lsh_hash_hd(poses[i], lp.frame, lp.noise, lp.alpha, lp.sigma_r, lp.sigma_t, &amb) %
                      static_cast<uint64_t>(lp.n_buckets);
   const uint64_t prio = lp.prio_bits > 0 ? mix_seed(lp.prio_seed, gi) >> (64 - lp.prio_bits) : 0;
   keys[i] = (h << (lp.prio_bits + lp.idx_bits)) | (prio << lp.idx_bits) | gi;
+  if (amb && flagged) atomicAdd(flagged, 1u);
 }
 
-__global__ void k_hash_batch(const Pose* __restrict__ poses, int64_t n, LshPass lp, uint64_t* __restrict__ out) {
+__global__ void k_hash_batch(const Pose* __restrict__ poses, int64_t n, LshPass lp, uint64_t* __restrict__ out,
+                             unsigned char* __restrict__ amb_out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = lsh_hash_dev(poses[i], lp.frame, lp.noise, lp.alpha, lp.sigma_r, lp.sigma_t);
+  if (i >= n) return;
+  bool amb = false;
+  out[i] = lsh_hash_hd(poses[i], lp.frame, lp.noise, lp.alpha, lp.sigma_r, lp.sigma_t, &amb);
+  amb_out[i] = amb ? 1 : 0;
 }
 
 // member_of[p] = key & mask; head flag of bucket runs.
@@ -713,13 +759,24 @@ void launch_owned_scatter(const int32_t* flag, const int32_t* incl, int64_t n, i
   if (n > 0) k_owned_scatter<<<blocks_for(n, 256), 256, 0, st>>>(flag, incl, n, pos_list);
 }
 
-void launch_lsh_keys(const Pose* poses, int64_t n, int64_t gbase, const LshPass& lp, uint64_t* keys, cudaStream_t st) {
+void launch_lsh_keys(const Pose* poses, int64_t n, int64_t gbase, const LshPass& lp, uint64_t* keys,
+                     unsigned* flagged, cudaStream_t st) {
   count_launch();
-  if (n > 0) k_lsh_keys<<<blocks_for(n, 128), 128, 0, st>>>(poses, n, gbase, lp, keys);
+  if (flagged) cudaMemsetAsync(flagged, 0, sizeof(unsigned), st);
+  if (n > 0) k_lsh_keys<<<blocks_for(n, 128), 128, 0, st>>>(poses, n, gbase, lp, keys, flagged);
 }
-void launch_hash_batch(const Pose* poses, int64_t n, const LshPass& lp, uint64_t* out, cudaStream_t st) {
+void launch_hash_batch(const Pose* poses, int64_t n, const LshPass& lp, uint64_t* out, unsigned char* amb,
+                       cudaStream_t st) {
   count_launch();
-  if (n > 0) k_hash_batch<<<blocks_for(n, 128), 128, 0, st>>>(poses, n, lp, out);
+  if (n > 0) k_hash_batch<<<blocks_for(n, 128), 128, 0, st>>>(poses, n, lp, out, amb);
+}
+uint64_t lsh_hash_host(const Pose& pose, const LshPass& lp) {
+  return lsh_hash_hd(pose, lp.frame, lp.noise, lp.alpha, lp.sigma_r, lp.sigma_t, nullptr);
+}
+uint64_t lsh_key_host(const Pose& pose, uint64_t gi, const LshPass& lp) {
+  const uint64_t h = lsh_hash_host(pose, lp) % static_cast<uint64_t>(lp.n_buckets);
+  const uint64_t prio = lp.prio_bits > 0 ? mix_seed(lp.prio_seed, gi) >> (64 - lp.prio_bits) : 0;
+  return (h << (lp.prio_bits + lp.idx_bits)) | (prio << lp.idx_bits) | gi;
 }
 
 size_t sort_temp_bytes(int64_t n) {

@@ -318,14 +318,17 @@ __global__ void k_merge_pairs(const double* __restrict__ g, int world, double* _
 // (bits), [2..13] pose, [14] id (as double).
 __global__ void k_rep_local(const double* __restrict__ v_ptr, const long long* __restrict__ ix_ptr, int64_t n_local,
                             int rank, int sharded, const Pose* __restrict__ poses, const int32_t* __restrict__ id,
-                            Pose* __restrict__ dst_pose, int32_t* __restrict__ dst_id, double* __restrict__ stage) {
+                            const unsigned* __restrict__ flagged, Pose* __restrict__ dst_pose,
+                            int32_t* __restrict__ dst_id, double* __restrict__ stage) {
   const long long ix = *ix_ptr;
   const long long owner = sharded ? ix / n_local : 0;
   const long long li = ix - owner * n_local;
   const long long mine = (owner == rank && li >= 0 && li < n_local) ? li : 0;
-  if (sharded) {  // this rank's slot of the all-gathered candidates (pose, then id, one record)
+  const double fl = flagged ? static_cast<double>(*flagged) : 0.0;
+  if (sharded) {  // this rank's slot of the all-gathered candidates (pose, id, hash-guard flags: one record)
     *dst_pose = poses[mine];
     *reinterpret_cast<int32_t*>(dst_pose + 1) = id[mine];
+    reinterpret_cast<double*>(dst_pose)[13] = fl;
     return;
   }
   stage[0] = *v_ptr;
@@ -334,8 +337,10 @@ __global__ void k_rep_local(const double* __restrict__ v_ptr, const long long* _
   for (int q = 0; q < 9; ++q) stage[2 + q] = p.R[q];
   for (int a = 0; a < 3; ++a) stage[11 + a] = p.t[a];
   stage[14] = static_cast<double>(id[mine]);
+  stage[15] = fl;
 }
-// g_rec: per rank one record of 14 doubles (pose, the id in the 13th, pad).
+// g_rec: per rank one record of 14 doubles (pose, the id in the 13th, the
+// rank's hash-guard flag count in the 14th).
 __global__ void k_rep_select(const double* __restrict__ v_ptr, const long long* __restrict__ ix_ptr, int64_t n_local,
                              int world, const double* __restrict__ g_rec, double* __restrict__ stage) {
   const long long ix = *ix_ptr;
@@ -346,14 +351,18 @@ __global__ void k_rep_select(const double* __restrict__ v_ptr, const long long* 
   const double* r = g_rec + 14 * owner;
   for (int q = 0; q < 12; ++q) stage[2 + q] = r[q];
   stage[14] = static_cast<double>(*reinterpret_cast<const int32_t*>(r + 12));
+  double fl = 0.0;
+  for (int w = 0; w < world; ++w) fl += g_rec[14 * w + 13];
+  stage[15] = fl;
 }
 
 }  // namespace
 
 void launch_rep_local(const double* v, const long long* ix, int64_t n_local, int rank, bool sharded, const Pose* poses,
-                      const int32_t* id, Pose* dst_pose, int32_t* dst_id, double* stage, cudaStream_t st) {
+                      const int32_t* id, const unsigned* flagged, Pose* dst_pose, int32_t* dst_id, double* stage,
+                      cudaStream_t st) {
   count_launch();
-  k_rep_local<<<1, 1, 0, st>>>(v, ix, n_local, rank, sharded ? 1 : 0, poses, id, dst_pose, dst_id, stage);
+  k_rep_local<<<1, 1, 0, st>>>(v, ix, n_local, rank, sharded ? 1 : 0, poses, id, flagged, dst_pose, dst_id, stage);
 }
 void launch_rep_select(const double* v, const long long* ix, int64_t n_local, int world, const double* g_rec,
                        double* stage, cudaStream_t st) {

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(L, n), n
     assert set(names) == set(_lib.SIGNATURES), set(names) ^ set(_lib.SIGNATURES)
-    assert L.smcl_abi_version() == 2
+    assert L.smcl_abi_version() == 3
 
 
 def test_default_config_matches_reference_defaults():
