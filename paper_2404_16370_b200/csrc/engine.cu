@@ -349,7 +349,11 @@ struct smcl_engine {
   std::vector<int32_t> h_cells;
   DBuf<int32_t> cells;
   DBuf<double> map_mu, map_sigma;
-  DBuf<float4> map_fast;
+  DBuf<float4> map_fast;   // 2 float4 per record + one trailing empty record (MapFast::empty)
+  DBuf<uint32_t> map_occ;   // occupancy bitmap by record index (MapFast::occ)
+  uint64_t map_records = 0;
+  DBuf<int32_t> live_list;  // K2a: particles the likelihood gate keeps
+  DBuf<unsigned> live_count;
 
   // particles
   DBuf<Pose> poses, poses2, poses3;  // poses3: SVGD's output never lands on the guard checkpoint
@@ -559,9 +563,15 @@ struct smcl_engine {
       DBuf<float4> d_plane;
       d_plane.upload(plane.data(), plane.size(), st);
       map_brick = MapFast::choose_brick(g.dims);
-      map_fast.ensure(2 * static_cast<size_t>(MapFast::n_records(g.dims, map_brick)));
+      map_records = MapFast::n_records(g.dims, map_brick);
+      map_fast.ensure(2 * static_cast<size_t>(map_records) + 2);
       CK(build_map_records_device(cells.p, n_cells, g.origin, g.dims, g.resolution, map_mu.p, d_plane.p, map_fast.p,
                                   st));
+      const float4 empty_rec[2] = {make_float4(0.f, 0.f, 0.f, -1.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+      CK(cudaMemcpyAsync(map_fast.p + 2 * map_records, empty_rec, sizeof(empty_rec), cudaMemcpyHostToDevice, st));
+      map_occ.ensure(static_cast<size_t>((map_records + 31) / 32));
+      launch_build_occupancy(map_fast.p, map_records, map_occ.p, st);
+      CK(cudaGetLastError());
       sync();
     }
     has_map = true;
@@ -957,15 +967,22 @@ struct smcl_engine {
   }
 
   // ------------------------------------------------------------ stages
-  void run_likelihood(bool gn, const ScanDev& sd) {
+  // need_cost: the GN pass's raw log-likelihood (the stage API returns it;
+  // FilterEngine::step overwrites it with the likelihood pass's, so the step
+  // does not compute it).
+  void run_likelihood(bool gn, const ScanDev& sd, bool need_cost = true) {
     if (!has_map) throw std::invalid_argument("engine has no map");
     if (sd.n == 0) throw std::invalid_argument("gicp::evaluate: empty scan");
     ScanView sv{sd.n, sd.mu.p, sd.sigma.p, sd.structured ? sd.rec.p : nullptr, sd.l1max};
     if (profiling) gn ? mark_it(gn_iter, I_GN0) : mark(E_LL0);
     fast_used = use_fast(sd);
     if (fast_used) {
-      MapFast mf{geom, map_fast.p, map_brick};
-      launch_gicp_fast(gn, poses.p, n_local, sv, mf, sysf.p, raw_ll.p, nm.p, st);
+      MapFast mf{geom, map_fast.p, map_brick, map_occ.p, map_fast.p + 2 * map_records};
+      const GicpParamsDev gp0 = gicp_params(sd.n);
+      live_list.ensure(static_cast<size_t>(std::max<int64_t>(n_local, 1)));
+      live_count.ensure(1);
+      launch_gicp_fast(gn, poses.p, n_local, sv, mf, sysf.p, raw_ll.p, nm.p, need_cost, gp0.min_matched, live_list.p,
+                       live_count.p, st);
     } else {
       MapExact me{geom, cells.p, map_mu.p, map_sigma.p};
       if (gn) sys.ensure(static_cast<size_t>(std::max<int64_t>(n_local, 1)) * kSysStride);
@@ -1527,7 +1544,7 @@ struct smcl_engine {
       if (!empty) {
         for (int it = 0; it < cfg.n_svgd_iters; ++it) {  // filter.cpp:166-180
           gn_iter = it;
-          run_likelihood(true, gn_scan);
+          run_likelihood(true, gn_scan, /*need_cost=*/false);
           mark_it(it, I_SOLVE);
           svgd(true);
           mark_it(it, I_SVGD);

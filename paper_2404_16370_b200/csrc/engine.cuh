@@ -45,6 +45,13 @@ struct MapFast {
   NnfGeom g;
   const float4* rec;
   int brick = 0;
+  // Occupancy bitmap by record index (bit r: record r is a map Gaussian),
+  // the likelihood pass's match-count prepass (K2a): 191 KB for the corridor
+  // map, mostly L1-resident.
+  const uint32_t* occ = nullptr;
+  // One always-empty record (beta = -1): the target of unmatched gathers, so
+  // they need no predication.
+  const float4* empty = nullptr;
   // Host-side / map-build slot; the likelihood kernels use rec_index<kBrick>.
   // 32-bit index math: the NNF budget (2^30 cells) keeps every table < 2^32 records.
   __host__ __device__ __forceinline__ uint32_t index(uint32_t ix, uint32_t iy, uint32_t iz) const {
@@ -92,8 +99,19 @@ struct GicpParamsDev {
 // likelihood.cu
 void launch_gicp_exact(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapExact& map,
                        double* sys, double* raw_ll, int32_t* nm, cudaStream_t st);
+// Fast (plane-model) likelihood passes.
+// gn: K1, the Gauss-Newton system into sysf (need_cost: also the raw
+//     log-likelihood; FilterEngine::step discards the GN pass's likelihood,
+//     filter.cpp:166-187, so the step skips it).
+// !gn: K2, raw log-likelihood + n_matched. With min_matched > 0 and the map's
+//     occupancy bitmap, K2a counts every particle's matches first and the
+//     cost is evaluated only for particles the gate keeps (n >= min_matched,
+//     gicp.cpp:79-85): the others' likelihood is the sentinel whatever their
+//     cost. live_list (n) / live_count (1) are scratch.
 void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
-                      double* raw_ll, int32_t* nm, cudaStream_t st);
+                      double* raw_ll, int32_t* nm, bool need_cost, int min_matched, int32_t* live_list,
+                      unsigned* live_count, cudaStream_t st);
+void launch_build_occupancy(const float4* rec, uint64_t n_records, uint32_t* occ, cudaStream_t st);
 // Exactly one of sys (exact record) / sysf (fast record) is non-null.
 void launch_solve(const double* sys, const float* sysf, const double* raw_ll, const int32_t* nm, int64_t n,
                   const GicpParamsDev& p, double* steps, double* ll, cudaStream_t st);

@@ -88,6 +88,15 @@ __device__ __forceinline__ void ldg_rec_pred(const float4* src, bool pred, float
   m0 = make_float4(a0, a1, a2, a3);
   m1 = make_float4(b0, b1, b2, b3);
 }
+// Unpredicated 256-bit record load (unmatched points read MapFast::empty).
+__device__ __forceinline__ void ldg_rec(const float4* src, float4& m0, float4& m1) {
+  float a0, a1, a2, a3, b0, b1, b2, b3;
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3)
+      : "l"(src));
+  m0 = make_float4(a0, a1, a2, a3);
+  m1 = make_float4(b0, b1, b2, b3);
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
@@ -131,7 +140,7 @@ __device__ __forceinline__ float fast_cost(const float Rf[9], const float fr[3],
   return fmaf(ex * ex + ey * ey + ez * ez, invA, inner * (invD * invA));
 }
 
-template <bool GN>
+template <bool GN, bool kCost = true>
 __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const float fr[3], float res, const float4 m0,
                                           const float4 m1, const float4 s0, const float4 s1) {
   if (!GN) {
@@ -167,7 +176,7 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
   const float x = mx * ex + my * ey + mz * ez;
   const float y = nx * ex + ny * ey + nz * ez;
   const float am = fmaf(Pa, x, Ta * y), an = fmaf(Qa, y, Ta * x);  // (Omega' - invA I) e = am m + an n
-  acc.cost += fmaf(ex * ex + ey * ey + ez * ez, invA, fmaf(am, x, an * y));
+  if (kCost) acc.cost += fmaf(ex * ex + ey * ey + ez * ez, invA, fmaf(am, x, an * y));
   if (GN) {
     const float gx = fmaf(ex, invA, fmaf(am, mx, an * nx));  // g = Omega' e
     const float gy = fmaf(ey, invA, fmaf(am, my, an * ny));
@@ -253,10 +262,11 @@ __device__ __forceinline__ void transform_x(const double* R, const double* t, co
     p[i] = xadd(xadd(xadd(xmul(R[i * 3 + 0], mu[0]), xmul(R[i * 3 + 1], mu[1])), xmul(R[i * 3 + 2], mu[2])), t[i]);
 }
 
-template <bool GN, int kFastUnroll, int kWarps, int kBrick, bool kLdg = false>
+template <bool GN, int kFastUnroll, int kWarps, int kBrick, bool kLdg = false, bool kCost = true>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     k_gicp_fast(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, float* __restrict__ sysf,
-                double* __restrict__ raw_ll, int32_t* __restrict__ nm_out) {
+                double* __restrict__ raw_ll, int32_t* __restrict__ nm_out, const int32_t* __restrict__ list,
+                const unsigned* __restrict__ list_count) {
   constexpr int kStep = 32 * kFastUnroll;
   using Stage = WarpStage<kStep>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -287,7 +297,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   Stage& ws = stages[wid];
   constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-down add leaves floor(x) in the low word
 
-  for (int64_t i = gwarp; i < n; i += nwarps) {
+  const int64_t n_eff = list ? static_cast<int64_t>(*list_count) : n;  // list: the gate's live particles
+  for (int64_t it = gwarp; it < n_eff; it += nwarps) {
+    const int64_t i = list ? static_cast<int64_t>(list[it]) : it;
     // Pose in voxel units x = Rv mu + tv (Rv = R/res, tv = (t - o)/res) in
     // fp64 registers; Rf = R (fp32) for the body-frame algebra.
     float Rf[9];
@@ -428,7 +440,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             m1 = ws.m1[slot];
           }
           valid = valid && m0.w >= 0.f;
-          if (valid) fast_item<GN>(acc, Rf, fr, res, m0, m1, s_r0[k], s_r1[k]);
+          if (valid) fast_item<GN, kCost>(acc, Rf, fr, res, m0, m1, s_r0[k], s_r1[k]);
         }
         nmatch += __popc(__ballot_sync(0xffffffffu, valid));
       }
@@ -463,12 +475,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       // One 128-byte line per particle (lanes 28-31 hold zeros), widened to
       // fp64 by the solve (SMCL_FAST_SYS_OFF).
       sysf[i * kSysF + lane] = v[0];
-      if (lane == 27) raw_ll[i] = nmatch == 0 ? -1e30 : -static_cast<double>(v[0]);
+      if (kCost && lane == 27) raw_ll[i] = nmatch == 0 ? -1e30 : -static_cast<double>(v[0]);
     } else {
       const float cost = warp_sum(acc.cost);
       if (lane == 0) raw_ll[i] = nmatch == 0 ? -1e30 : -static_cast<double>(cost);
     }
-    if (lane == 0) nm_out[i] = nmatch;
+    if (lane == 0 && !list) nm_out[i] = nmatch;  // list: K2a already wrote it
     __syncwarp();
   }
 }
@@ -485,8 +497,12 @@ template <int U, int kWarps, int kBrick, bool kLdg, int kMinB = 1>
 __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose* __restrict__ poses, int64_t n,
                                                              ScanView scan, MapFast map,
                                                              double* __restrict__ raw_ll,
-                                                             int32_t* __restrict__ nm_out) {
+                                                             int32_t* __restrict__ nm_out,
+                                                             const int32_t* __restrict__ list,
+                                                             const unsigned* __restrict__ list_count) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t n_eff = list ? static_cast<int64_t>(*list_count) : n;  // list: the gate's live particles
+  if (static_cast<int64_t>(blockIdx.x) * (kWarps * 32) >= n_eff) return;  // block-uniform
   float4* stage = reinterpret_cast<float4*>(smem_raw);  // [kWarps][U][2][32] (cp.async variant)
   const int S = scan.n;
   float4* s_r0 = stage + (kLdg ? 0 : kWarps * U * 2 * 32);  // S: mu.xyz, gamma
@@ -499,8 +515,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
   for (int q = threadIdx.x; q < 3 * S; q += blockDim.x) s_mu[q] = scan.mu[q];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * (kWarps * 32) + threadIdx.x;
-  const bool active = i < n;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * (kWarps * 32) + threadIdx.x;
+  const bool active = r < n_eff;
+  const int64_t i = active ? (list ? static_cast<int64_t>(list[r]) : r) : 0;
   float4* ws = stage + wid * U * 2 * 32;
   const NnfGeom g = map.g;
   const float res = static_cast<float>(g.res);
@@ -602,8 +619,132 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
   }
   if (active) {
     raw_ll[i] = nmatch == 0 ? -1e30 : -cost;
-    nm_out[i] = nmatch;
+    if (!list) nm_out[i] = nmatch;  // list: K2a already wrote it
   }
+}
+
+__device__ __forceinline__ bool occupied(const MapFast& m, uint32_t r) {
+  return (__ldg(m.occ + (r >> 5)) >> (r & 31u)) & 1u;
+}
+
+// K2a: n_matched of every particle (lane per particle, occupancy bitmap
+// instead of the 32-byte records) and the list of particles the gate keeps.
+// The cell decision runs in fp32 with a proven margin and falls back to the
+// reference-order fp64 transform (nnf.hpp:24-35) near a face, so n_matched is
+// exactly the reference's:
+//   x32 = fma(Rv2, mu2, fma(Rv1, mu1, fma(Rv0, mu0, tv))) in fp32, Rv = R / res,
+//   tv = (t - o) / res and mu rounded once to fp32 (u = 2^-24 each), differs
+//   from the exact x by <= u (5 sum_j |Rv_j| |mu_j| + 4 |tv|) (two input
+//   roundings per product, three FMA roundings of partial sums), and the
+//   reference's fp64 x differs from the exact one by < 2.2e-8 voxel (k_gicp_fast);
+//   a point whose fp32 fraction is farther than that from both faces has the
+//   reference's cell. Per particle the margin uses max|Rv| |mu|_1 <= |mu|_1max / res.
+// ~1 point in 1000 takes the fp64 path (corridor map, 0.1 m voxels).
+template <int kBrick>
+__global__ void __launch_bounds__(256, 3) k_ll_count(const Pose* __restrict__ poses, int64_t n, ScanView scan,
+                                                     MapFast map, int min_matched, int32_t* __restrict__ nm_out,
+                                                     int32_t* __restrict__ live, unsigned* __restrict__ live_count) {
+  constexpr int U = 4;  // points in flight per lane
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4* s_m = reinterpret_cast<float4*>(smem_raw);  // fp32 mu (scan record .xyz), padded with NaN
+  const int S = scan.n;
+  const int Sp = (S + U - 1) / U * U;
+  for (int q = threadIdx.x; q < Sp; q += blockDim.x) {
+    const float nan = __int_as_float(0x7fc00000);
+    s_m[q] = q < S ? scan.rec[2 * q] : make_float4(nan, nan, nan, nan);
+  }
+  __syncthreads();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool active = i < n;
+  const NnfGeom g = map.g;
+  const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
+                 dz = static_cast<unsigned>(g.dims[2]);
+  const Pose P = poses[active ? i : 0];
+  float Rv[9], tv[3];
+  float margin;
+  {
+    double tmax = 0.0;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) Rv[q] = static_cast<float>(P.R[q] * g.inv_res);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double t = (P.t[a] - g.origin[a]) * g.inv_res;
+      tv[a] = static_cast<float>(t);
+      tmax = fmax(tmax, fabs(t));
+    }
+    // u (5 |mu|_1max / res + 4 |tv|) + 2.2e-8, x1.25 for the fp64 set-up roundings; |x| < 2^21 for the
+    // round-down floor below, else every point takes the fp64 path.
+    const double e = 0x1p-24 * (5.0 * scan.mu_l1_max * g.inv_res + 4.0 * tmax) * 1.25 + 2.5e-8;
+    margin = (e < 0.01 && tmax + scan.mu_l1_max * g.inv_res < 2097152.0) ? static_cast<float>(e) : 2.0f;
+  }
+  constexpr float kMagic32 = 12582912.0f;  // 1.5 * 2^23: round-down add leaves floor(x) in the low mantissa bits
+  const float hi = 1.0f - margin;
+  int nmatch = 0;
+  for (int k0 = 0; k0 < Sp; k0 += U) {
+    uint32_t rec[U];
+    bool ok[U];
+    unsigned amb = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float4 m = s_m[k0 + u];
+      unsigned ic[3];
+      float fmn = 1.0f, fmx = 0.0f;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        const float x = fmaf(Rv[ax * 3 + 2], m.z, fmaf(Rv[ax * 3 + 1], m.y, fmaf(Rv[ax * 3 + 0], m.x, tv[ax])));
+        const float y = __fadd_rd(x, kMagic32);
+        const float f = x - (y - kMagic32);
+        ic[ax] = static_cast<unsigned>(__float_as_int(y) - 0x4B400000);
+        fmn = fminf(fmn, f);
+        fmx = fmaxf(fmx, f);
+      }
+      const bool safe = fmn >= margin && fmx <= hi;  // NaN fails
+      const bool inb = ic[0] < dx && ic[1] < dy && ic[2] < dz;
+      ok[u] = safe && inb;
+      rec[u] = ok[u] ? rec_index<kBrick>(map, ic[0], ic[1], ic[2]) : 0u;
+      if (!safe && k0 + u < S) amb |= 1u << u;  // padded points (NaN) are never counted
+    }
+    uint32_t w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) w[u] = ok[u] ? __ldg(map.occ + (rec[u] >> 5)) : 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) nmatch += static_cast<int>((w[u] >> (rec[u] & 31u)) & 1u);
+    if (amb) {  // reference-order transform, floor and bounds (nnf.hpp:24-35)
+#pragma unroll 1
+      for (int u = 0; u < U; ++u) {
+        if (!((amb >> u) & 1u)) continue;
+        const int k = k0 + u;
+        const double mu[3] = {scan.mu[3 * k], scan.mu[3 * k + 1], scan.mu[3 * k + 2]};
+        double p[3];
+        transform_x(P.R, P.t, mu, p);
+        bool valid = true;
+        unsigned ic[3];
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          const double x = xmul(xsub(p[ax], g.origin[ax]), g.inv_res);
+          const double fl = floor(x);
+          valid = valid && (fl >= 0.0 && fl < static_cast<double>(g.dims[ax]));
+          ic[ax] = valid ? static_cast<unsigned>(fl) : 0u;
+        }
+        nmatch += (valid && occupied(map, rec_index<kBrick>(map, ic[0], ic[1], ic[2]))) ? 1 : 0;
+      }
+    }
+  }
+  if (active) nm_out[i] = nmatch;
+  const bool keep = active && nmatch >= min_matched;
+  const unsigned mask = __ballot_sync(0xffffffffu, keep);
+  const int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == 0 && mask) base = atomicAdd(live_count, static_cast<unsigned>(__popc(mask)));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (keep) live[base + __popc(mask & ((1u << lane) - 1u))] = static_cast<int32_t>(i);
+}
+
+__global__ void k_build_occ(const float4* __restrict__ rec, uint64_t n_records, uint32_t* __restrict__ occ) {
+  const uint64_t r = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool on = r < n_records && rec[2 * r].w >= 0.f;
+  const unsigned m = __ballot_sync(0xffffffffu, on);
+  if ((threadIdx.x & 31) == 0 && (r >> 5) < (n_records + 31) / 32) occ[r >> 5] = m;
 }
 
 template <int U, int W, bool kLdg = false>
@@ -612,19 +753,29 @@ size_t ll_lanes_smem(int S) {
          sizeof(double) * 3 * static_cast<size_t>(S);
 }
 
+// Launch arguments beyond the kernels' common ones: the live-particle list
+// of K2a (null: every particle) and whether K1 accumulates the cost.
+struct Extra {
+  const int32_t* list = nullptr;
+  const unsigned* list_count = nullptr;
+  bool cost = true;
+};
+
 template <int U, int W, bool kLdg, int kMinB = 1>
 void launch_ll_lanes_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, double* raw_ll,
-                       int32_t* nm, cudaStream_t st) {
+                       int32_t* nm, const Extra& x, cudaStream_t st) {
   const size_t smem = ll_lanes_smem<U, W, kLdg>(scan.n);
   const unsigned grid = static_cast<unsigned>((n + W * 32 - 1) / (W * 32));
   if (map.brick) {
     cudaFuncSetAttribute(k_gicp_ll_lanes<U, W, 1, kLdg, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    k_gicp_ll_lanes<U, W, 1, kLdg, kMinB><<<grid, W * 32, smem, st>>>(poses, n, scan, map, raw_ll, nm);
+    k_gicp_ll_lanes<U, W, 1, kLdg, kMinB><<<grid, W * 32, smem, st>>>(poses, n, scan, map, raw_ll, nm, x.list,
+                                                                      x.list_count);
   } else {
     cudaFuncSetAttribute(k_gicp_ll_lanes<U, W, 0, kLdg, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
-    k_gicp_ll_lanes<U, W, 0, kLdg, kMinB><<<grid, W * 32, smem, st>>>(poses, n, scan, map, raw_ll, nm);
+    k_gicp_ll_lanes<U, W, 0, kLdg, kMinB><<<grid, W * 32, smem, st>>>(poses, n, scan, map, raw_ll, nm, x.list,
+                                                                      x.list_count);
   }
 }
 
@@ -634,39 +785,48 @@ size_t fast_smem(int S) {
   return sizeof(WarpStage<32 * U>) * W + sizeof(float4) * 2 * Sp + sizeof(double) * 3 * Sp;
 }
 
-template <bool GN, int U, int W, int B, bool L>
-void launch_fast_tbl(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
-                    double* raw_ll, int32_t* nm, cudaStream_t st) {
+template <bool GN, int U, int W, int B, bool L, bool C>
+void launch_fast_tblc(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
+                      double* raw_ll, int32_t* nm, const Extra& x, cudaStream_t st) {
   const size_t smem = fast_smem<U, W>(scan.n);
   int dev, n_sm, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(k_gicp_fast<GN, U, W, B, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gicp_fast<GN, U, W, B, L>, W * 32, smem);
+  cudaFuncSetAttribute(k_gicp_fast<GN, U, W, B, L, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gicp_fast<GN, U, W, B, L, C>, W * 32, smem);
   const int64_t want = (n + W - 1) / W;
   const unsigned grid =
       static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(n_sm) * std::max(per_sm, 1)));
-  k_gicp_fast<GN, U, W, B, L><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sysf, raw_ll, nm);
+  k_gicp_fast<GN, U, W, B, L, C><<<grid, W * 32, smem, st>>>(poses, n, scan, map, sysf, raw_ll, nm, x.list,
+                                                              x.list_count);
+}
+
+template <bool GN, int U, int W, int B, bool L>
+void launch_fast_tbl(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
+                     double* raw_ll, int32_t* nm, const Extra& x, cudaStream_t st) {
+  (GN && !x.cost) ? launch_fast_tblc<GN, U, W, B, L, false>(poses, n, scan, map, sysf, raw_ll, nm, x, st)
+                  : launch_fast_tblc<GN, U, W, B, L, true>(poses, n, scan, map, sysf, raw_ll, nm, x, st);
 }
 
 template <bool GN, int U, int W, int B>
 void launch_fast_tb(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
-                    double* raw_ll, int32_t* nm, cudaStream_t st) {
+                    double* raw_ll, int32_t* nm, const Extra& x, cudaStream_t st) {
   // Record gathers: the GN pass keeps cp.async (issue bound: 4.57 ms against
   // 5.25 with 256-bit loads + shared stores); the likelihood-only warp variant
   // (bricked HBM-sized tables) gathers with 256-bit loads (outdoor kidnap LL
   // 2.49-2.72 ms against 2.82-2.88; HBM cp.async gathers measure 0.73 TB/s
   // against 1.34 for loads).
   static const bool ldg = GN ? std::getenv("SMCL_K1_LDG") != nullptr : std::getenv("SMCL_K2W_CPASYNC") == nullptr;
-  ldg ? launch_fast_tbl<GN, U, W, B, true>(poses, n, scan, map, sysf, raw_ll, nm, st)
-      : launch_fast_tbl<GN, U, W, B, false>(poses, n, scan, map, sysf, raw_ll, nm, st);
+  ldg ? launch_fast_tbl<GN, U, W, B, true>(poses, n, scan, map, sysf, raw_ll, nm, x, st)
+      : launch_fast_tbl<GN, U, W, B, false>(poses, n, scan, map, sysf, raw_ll, nm, x, st);
 }
 
 template <bool GN, int U, int W>
 void launch_fast_t(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf, double* raw_ll,
-                   int32_t* nm, cudaStream_t st) {
-  map.brick ? launch_fast_tb<GN, U, W, 1>(poses, n, scan, map, sysf, raw_ll, nm, st)
-            : launch_fast_tb<GN, U, W, 0>(poses, n, scan, map, sysf, raw_ll, nm, st);
+                   int32_t* nm, const Extra& x, cudaStream_t st) {
+  map.brick ? launch_fast_tb<GN, U, W, 1>(poses, n, scan, map, sysf, raw_ll, nm, x, st)
+            : launch_fast_tb<GN, U, W, 0>(poses, n, scan, map, sysf, raw_ll, nm, x, st);
 }
 
 }  // namespace
@@ -674,9 +834,30 @@ void launch_fast_t(const Pose* poses, int64_t n, const ScanView& scan, const Map
 // U points per lane in flight x W warps per SM (one CTA per SM).
 // SMCL_FAST_CFG=UxW overrides the default (tuning sweeps only).
 void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
-                      double* raw_ll, int32_t* nm, cudaStream_t st) {
+                      double* raw_ll, int32_t* nm, bool need_cost, int min_matched, int32_t* live_list,
+                      unsigned* live_count, cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
+  Extra x;
+  x.cost = need_cost;
+  static const bool no_gate = std::getenv("SMCL_NO_LL_GATE") != nullptr;  // experiments: K2 on every particle
+  if (!gn && min_matched > 0 && map.occ && scan.rec && live_list && live_count && !no_gate) {
+    // K2a: n_matched of every particle + the list the gate keeps; K2 then
+    // evaluates the cost of those particles only.
+    count_launch();
+    cudaMemsetAsync(live_count, 0, sizeof(unsigned), st);
+    const size_t smem = sizeof(float4) * static_cast<size_t>((scan.n + 3) / 4 * 4);
+    const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+    if (map.brick) {
+      cudaFuncSetAttribute(k_ll_count<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_ll_count<1><<<grid, 256, smem, st>>>(poses, n, scan, map, min_matched, nm, live_list, live_count);
+    } else {
+      cudaFuncSetAttribute(k_ll_count<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_ll_count<0><<<grid, 256, smem, st>>>(poses, n, scan, map, min_matched, nm, live_list, live_count);
+    }
+    x.list = live_list;
+    x.list_count = live_count;
+  }
   auto parse = [](const char* e) {
     if (!e) return 0;
     int u = 0, w = 0;
@@ -708,17 +889,19 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
     // per SM: 2.79 ms at 1M x 512 (cp.async 8 x 8: 3.43; LDG 2 x 8: 2.91;
     // 4 x 8: 3.23; 1 x 8 at 5 / 6 CTAs spills: 3.33 / 3.42).
     if (c == 9000) {  // 3 CTAs per SM when 4 do not fit next to the scan (S > ~1000)
-      if (4 * ll_lanes_smem<1, 8, true>(scan.n) <= 227 * 1024)
-        launch_ll_lanes_t<1, 8, true, 4>(poses, n, scan, map, raw_ll, nm, st);
+      // the gated pass (x.list) needs the list indirection's registers: 3 CTAs (80 registers)
+      static const bool minb3 = std::getenv("SMCL_LL_MINB3") != nullptr;
+      if (!minb3 && !x.list && 4 * ll_lanes_smem<1, 8, true>(scan.n) <= 227 * 1024)
+        launch_ll_lanes_t<1, 8, true, 4>(poses, n, scan, map, raw_ll, nm, x, st);
       else
-        launch_ll_lanes_t<1, 8, true, 3>(poses, n, scan, map, raw_ll, nm, st);
+        launch_ll_lanes_t<1, 8, true, 3>(poses, n, scan, map, raw_ll, nm, x, st);
       return;
     }
     const int u = (c / 100) % 10, w = c % 100;
 #define LL_CASE(UU, WW)                                                                         \
     if (!gn && u == UU && w == WW && ll_lanes_smem<UU, WW>(scan.n) <= 227 * 1024) {            \
-      ldg ? launch_ll_lanes_t<UU, WW, true>(poses, n, scan, map, raw_ll, nm, st)               \
-          : launch_ll_lanes_t<UU, WW, false>(poses, n, scan, map, raw_ll, nm, st);             \
+      ldg ? launch_ll_lanes_t<UU, WW, true>(poses, n, scan, map, raw_ll, nm, x, st)               \
+          : launch_ll_lanes_t<UU, WW, false>(poses, n, scan, map, raw_ll, nm, x, st);             \
       return;                                                                                  \
     }
     LL_CASE(8, 8)
@@ -729,25 +912,25 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
 #undef LL_CASE
     if (!gn && (u == 2 || u == 1) && w >= 80) {  // SMCL_FAST_CFG_LL=L2x84 / L1x84: 8 warps, >= 4 CTAs per SM
       const int mb = w - 80;
-      if (u == 2 && mb == 4) return launch_ll_lanes_t<2, 8, true, 4>(poses, n, scan, map, raw_ll, nm, st);
-      if (u == 2 && mb == 5) return launch_ll_lanes_t<2, 8, true, 5>(poses, n, scan, map, raw_ll, nm, st);
-      if (u == 1 && mb == 4) return launch_ll_lanes_t<1, 8, true, 4>(poses, n, scan, map, raw_ll, nm, st);
-      if (u == 1 && mb == 5) return launch_ll_lanes_t<1, 8, true, 5>(poses, n, scan, map, raw_ll, nm, st);
-      if (u == 1 && mb == 6) return launch_ll_lanes_t<1, 8, true, 6>(poses, n, scan, map, raw_ll, nm, st);
+      if (u == 2 && mb == 4) return launch_ll_lanes_t<2, 8, true, 4>(poses, n, scan, map, raw_ll, nm, x, st);
+      if (u == 2 && mb == 5) return launch_ll_lanes_t<2, 8, true, 5>(poses, n, scan, map, raw_ll, nm, x, st);
+      if (u == 1 && mb == 4) return launch_ll_lanes_t<1, 8, true, 4>(poses, n, scan, map, raw_ll, nm, x, st);
+      if (u == 1 && mb == 5) return launch_ll_lanes_t<1, 8, true, 5>(poses, n, scan, map, raw_ll, nm, x, st);
+      if (u == 1 && mb == 6) return launch_ll_lanes_t<1, 8, true, 6>(poses, n, scan, map, raw_ll, nm, x, st);
     }
     if (!gn && u == 1 && w >= 40 && w < 80) {  // L1x4M: 4 warps per CTA, >= M CTAs per SM
       const int mb = w - 40;
-      if (mb == 8) return launch_ll_lanes_t<1, 4, true, 8>(poses, n, scan, map, raw_ll, nm, st);
-      if (mb == 10) return launch_ll_lanes_t<1, 4, true, 10>(poses, n, scan, map, raw_ll, nm, st);
-      if (mb == 12) return launch_ll_lanes_t<1, 4, true, 12>(poses, n, scan, map, raw_ll, nm, st);
+      if (mb == 8) return launch_ll_lanes_t<1, 4, true, 8>(poses, n, scan, map, raw_ll, nm, x, st);
+      if (mb == 10) return launch_ll_lanes_t<1, 4, true, 10>(poses, n, scan, map, raw_ll, nm, x, st);
+      if (mb == 12) return launch_ll_lanes_t<1, 4, true, 12>(poses, n, scan, map, raw_ll, nm, x, st);
     }
     c = gn ? 416 : 424;
   }
 #define FAST_CASE(U, W)                                                                    \
   case U * 100 + W:                                                                        \
     if (fast_smem<U, W>(scan.n) <= 227 * 1024) {                                           \
-      gn ? launch_fast_t<true, U, W>(poses, n, scan, map, sysf, raw_ll, nm, st)            \
-         : launch_fast_t<false, U, W>(poses, n, scan, map, sysf, raw_ll, nm, st);          \
+      gn ? launch_fast_t<true, U, W>(poses, n, scan, map, sysf, raw_ll, nm, x, st)            \
+         : launch_fast_t<false, U, W>(poses, n, scan, map, sysf, raw_ll, nm, x, st);          \
       return;                                                                              \
     }                                                                                      \
     break;
@@ -762,8 +945,14 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
       break;
   }
 #undef FAST_CASE
-  gn ? launch_fast_t<true, 4, 16>(poses, n, scan, map, sysf, raw_ll, nm, st)
-     : launch_fast_t<false, 4, 16>(poses, n, scan, map, sysf, raw_ll, nm, st);
+  gn ? launch_fast_t<true, 4, 16>(poses, n, scan, map, sysf, raw_ll, nm, x, st)
+     : launch_fast_t<false, 4, 16>(poses, n, scan, map, sysf, raw_ll, nm, x, st);
+}
+
+void launch_build_occupancy(const float4* rec, uint64_t n_records, uint32_t* occ, cudaStream_t st) {
+  count_launch();
+  if (n_records == 0) return;
+  k_build_occ<<<static_cast<unsigned>((n_records + 255) / 256), 256, 0, st>>>(rec, n_records, occ);
 }
 
 }  // namespace smcl
