@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "../engine.cuh"
@@ -559,7 +560,11 @@ __global__ void k_pose_mirror(const Pose* __restrict__ poses, int64_t n, double3
 // lane replays its offers in window order.
 constexpr int kRgChunk = 16;
 
-template <int BLOCK, int KMAX>
+// SMCL_RG_STATS=1 (diagnostics only): window members considered, survivors
+// of the filter (exact evaluations), insertions, refresh evaluations.
+__device__ unsigned long long g_rg_stats[4];
+
+template <int BLOCK, int KMAX, bool kStats = false>
 __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restrict__ all_poses, int64_t n,
                                                             int64_t gbase, const int32_t* __restrict__ pos_list,
                                                             const int32_t* __restrict__ member_of,
@@ -615,6 +620,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
       const int32_t j = s_idx[s * BLOCK + t];
       if (j != gi) s_kv[t * KMAX + s] = kval_of(pi, ldg_pose(all_poses + j), sr, st);
     }
+    if (kStats) atomicAdd(&g_rg_stats[3], static_cast<unsigned long long>(cnt > 0 ? cnt - 1 : 0));
   }
   s_gi[t] = gi;
   // Rounding margins of the fp32 filter. Mirror rotations carry 2^-24 relative
@@ -674,6 +680,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
         if ((listed >> (q - rb)) & 1ull) continue;  // listed: a duplicate offer (also self)
         const int32_t j = member_of[q];
         if (j == gi) continue;
+        if (kStats) atomicAdd(&g_rg_stats[0], 1ull);
         if (full) {
           if (weakest < 0) continue;  // self-only full list (k == 1): nothing evictable
           const float4 b0 = __ldg(mir + 3 * j), b1 = __ldg(mir + 3 * j + 1), b2 = __ldg(mir + 3 * j + 2);
@@ -688,6 +695,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
         s_cand[ns * BLOCK + t] = j;
         ++ns;
       }
+      if (kStats) atomicAdd(&g_rg_stats[1], static_cast<unsigned long long>(ns));
     }
     // ---- warp-wide evaluation of all lanes' survivors
     int incl = ns;
@@ -710,6 +718,7 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
       const float kij = s_ckv[s * BLOCK + t];
       if (cnt == k && !(weakest >= 0 && kij > wk)) continue;  // dropped
       const int32_t j = s_cand[s * BLOCK + t];
+      if (kStats) atomicAdd(&g_rg_stats[2], 1ull);
       if (cnt < k) {
         s_idx[cnt * BLOCK + t] = j;
         s_kv[t * KMAX + cnt] = kij;
@@ -897,6 +906,25 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                                                                seg_start, n_sorted, pos_of, idx, kval,            \
                                                                count, k,                                          \
                                                                cap, sr, st_, mir, tmax_bits)
+    static const bool stats = std::getenv("SMCL_RG_STATS") != nullptr;
+    if (stats && k == 20) {
+      const unsigned long long z[4] = {0, 0, 0, 0};
+      cudaMemcpyToSymbolAsync(g_rg_stats, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+#define B_ B
+      k_refresh_gather_f<B, 20, true><<<blocks_for(n, B), B,
+                                        static_cast<size_t>(k) * B * 4 + static_cast<size_t>(20) * B * 4 +
+                                            static_cast<size_t>(kRgChunk) * B * 8 + B * 4 +
+                                            static_cast<size_t>(B) * kRgChunk * 2,
+                                        st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, seg_start, n_sorted,
+                                              pos_of, idx, kval, count, k, cap, sr, st_, mir, tmax_bits);
+#undef B_
+      unsigned long long h[4];
+      cudaMemcpyFromSymbolAsync(h, g_rg_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      std::fprintf(stderr, "[rg] n %lld considered %.2f evaluated %.2f inserted %.2f refresh %.2f per particle\n",
+                   static_cast<long long>(n), h[0] / double(n), h[1] / double(n), h[2] / double(n), h[3] / double(n));
+      return;
+    }
     if (k <= 8)
       RGF(8);
     else if (k <= 20)
