@@ -20,7 +20,7 @@ HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/host/*.hpp) include/smcl_gp
 CU_OBJ := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRC))
 CPP_OBJ := $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(CPP_SRC))
 
-all: $(LIB) oracle examples/facade_demo build/tools/micro_peaks
+all: $(LIB) oracle examples/scenario_callsite build/tools/micro_peaks
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(dir $@)
@@ -45,9 +45,9 @@ clean:
 
 .PHONY: all oracle clean
 
-# C++ facade example (reference-shaped API over the C ABI).
-examples/facade_demo: examples/facade_demo.cpp include/steinmcl_b200.hpp include/smcl_gpu.h $(LIB)
-	$(HOSTCXX) -std=c++20 -O2 -Iinclude -o $@ examples/facade_demo.cpp -L$(PKG)/lib -lsmcl_gpu -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
+# Reference-shaped call site compiled against the source-compatible steinmcl:: facade.
+examples/scenario_callsite: examples/scenario_callsite.cpp $(wildcard include/steinmcl/*.hpp) include/smcl_gpu.h $(LIB)
+	$(HOSTCXX) -std=c++20 -O2 -Wall -Wextra -Iinclude -o $@ examples/scenario_callsite.cpp -L$(PKG)/lib -lsmcl_gpu -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
 
 # Roofline microbenchmarks (FP32/FP64 FMA, random record gathers from L2 / HBM).
 build/tools/micro_peaks: $(CSRC)/tools/micro_peaks.cu

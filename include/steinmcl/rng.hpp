@@ -1,0 +1,3 @@
+// Reference header name (proj/include/steinmcl/rng.hpp): forwards to the B200 facade.
+#pragma once
+#include "steinmcl/b200.hpp"
