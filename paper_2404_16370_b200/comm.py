@@ -19,7 +19,11 @@ Backends:
   128-byte unique id travels over any host channel (``NcclComm.from_torch``
   uses the torch.distributed group bench.py already has).
 * ``TorchComm`` — ``torch.distributed`` over NCCL (device buffers, one process
-  per GPU) or gloo (host buffers; used by the CPU tests of this layer).
+  per GPU), gloo on host buffers (the CPU tests of this layer), or gloo
+  host-staged (``staged=True``: the engine's device buffers are copied to the
+  host around a gloo collective after its stream drains, so several
+  processes can drive sharded engines on one GPU with no kernel ever waiting
+  on another process — the two-process GPU test).
 
 torch is plumbing here: it is imported lazily and only by ``TorchComm``.
 """
@@ -115,12 +119,16 @@ class TorchComm:
     and the all-gather is enqueued on the engine's stream (ExternalStream), so
     it is ordered after the engine's producers and before its consumers.
     ``device=False`` (gloo): send/recv are host pointers.
+    ``staged=True`` (gloo): send/recv are device pointers; the engine stream is
+    drained, the bytes go through host memory and are back on the device
+    before the call returns.
     """
 
-    def __init__(self, group=None, device=True):
+    def __init__(self, group=None, device=True, staged=False):
         import torch.distributed as dist
         self.group = group
-        self.device = device
+        self.device = device and not staged
+        self.staged = staged
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.error = None
@@ -135,7 +143,16 @@ class TorchComm:
             nbytes = int(nbytes)
             if nbytes == 0:
                 return 0
-            if self.device:
+            if self.staged:
+                dev = torch.device("cuda", torch.cuda.current_device())
+                torch.cuda.ExternalStream(int(stream or 0), device=dev).synchronize()
+                s = torch.as_tensor(_DeviceBytes(send, nbytes), device=dev).cpu()
+                parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(self.world)]
+                dist.all_gather(parts, s, group=self.group)
+                r = torch.as_tensor(_DeviceBytes(recv, nbytes * self.world), device=dev)
+                r.copy_(torch.cat(parts))
+                torch.cuda.synchronize(dev)
+            elif self.device:
                 dev = torch.device("cuda", torch.cuda.current_device())
                 s = torch.as_tensor(_DeviceBytes(send, nbytes), device=dev)
                 r = torch.as_tensor(_DeviceBytes(recv, nbytes * self.world), device=dev)
@@ -157,7 +174,17 @@ class TorchComm:
             sb = [int(send_bytes[i]) for i in range(self.world)]
             rb = [int(recv_bytes[i]) for i in range(self.world)]
             ns, nr = sum(sb), sum(rb)
-            if self.device:
+            if self.staged:
+                dev = torch.device("cuda", torch.cuda.current_device())
+                torch.cuda.ExternalStream(int(stream or 0), device=dev).synchronize()
+                s = (torch.as_tensor(_DeviceBytes(send, ns), device=dev).cpu() if ns
+                     else torch.empty(0, dtype=torch.uint8))
+                r = torch.empty(nr, dtype=torch.uint8)
+                dist.all_to_all_single(r, s, output_split_sizes=rb, input_split_sizes=sb, group=self.group)
+                if nr:
+                    torch.as_tensor(_DeviceBytes(recv, nr), device=dev).copy_(r)
+                    torch.cuda.synchronize(dev)
+            elif self.device:
                 dev = torch.device("cuda", torch.cuda.current_device())
                 s = torch.as_tensor(_DeviceBytes(send, ns), device=dev) if ns else torch.empty(0, dtype=torch.uint8,
                                                                                                 device=dev)

@@ -410,9 +410,9 @@ struct smcl_engine {
   // Step profile: one event per boundary, read after the step's final sync.
   enum Ev { E_START, E_PRED, E_KEYS, E_SORT, E_REORDER, E_SEG, E_RG, E_NB, E_LL0, E_LL1, E_BAYES, E_SMOOTH, E_END, E_COUNT };
   cudaEvent_t ev[E_COUNT] = {};
-  // One (GN start, GN end, solve end, SVGD end) quadruple per SVGD iteration,
-  // all read after the step's single end-of-frame sync.
-  enum ItEv { I_GN0, I_GN1, I_SOLVE, I_SVGD, I_COUNT };
+  // One (GN start, GN end, solve end, SVGD start, SVGD end) set per SVGD
+  // iteration, all read after the step's single end-of-frame sync.
+  enum ItEv { I_GN0, I_GN1, I_SOLVE, I_SV0, I_SVGD, I_COUNT };
   std::vector<cudaEvent_t> it_ev;
   int gn_iter = 0;  // SVGD iteration of the running step (event slot)
   void mark_it(int it, ItEv e) {
@@ -420,6 +420,11 @@ struct smcl_engine {
     if (it_ev.size() <= q) it_ev.resize(q + 1, nullptr);
     if (!it_ev[q]) CK(cudaEventCreate(&it_ev[q]));
     CK(cudaEventRecord(it_ev[q], st));
+  }
+  float since_it_ev(cudaEvent_t a, int it, ItEv b) const {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, it_ev[static_cast<size_t>(it) * I_COUNT + b]);
+    return ms;
   }
   float since_it(int it, ItEv a, ItEv b) const {
     float ms = 0.f;
@@ -1546,6 +1551,7 @@ struct smcl_engine {
           gn_iter = it;
           run_likelihood(true, gn_scan, /*need_cost=*/false);
           mark_it(it, I_SOLVE);
+          mark_it(it, I_SV0);
           svgd(true);
           mark_it(it, I_SVGD);
         }
@@ -1586,8 +1592,19 @@ struct smcl_engine {
       for (int it = 0; it < cfg.n_svgd_iters; ++it) {
         t_gn += since_it(it, I_GN0, I_GN1);
         t_solve += since_it(it, I_GN1, I_SOLVE);
-        t_svgd += since_it(it, I_SOLVE, I_SVGD);
+        t_svgd += since_it(it, I_SV0, I_SVGD);
       }
+    static const bool timeline = std::getenv("SMCL_STEP_TIMELINE") != nullptr;  // diagnostics: event offsets
+    if (timeline) {
+      static const char* names[E_COUNT] = {"start", "pred", "keys", "sort", "reorder", "seg", "rg", "nb",
+                                           "ll0", "ll1", "bayes", "smooth", "end"};
+      std::fprintf(stderr, "[timeline]");
+      for (int e = 1; e < E_COUNT; ++e) std::fprintf(stderr, " %s=%.3f", names[e], since(E_START, static_cast<Ev>(e)));
+      static const char* inames[I_COUNT] = {"gn0", "gn1", "solve", "sv0", "svgd"};
+      for (int it = 0; it < (empty ? 0 : cfg.n_svgd_iters); ++it)
+        for (int e = 0; e < I_COUNT; ++e) std::fprintf(stderr, " %s%d=%.3f", inames[e], it, since_it_ev(ev[E_START], it, static_cast<ItEv>(e)));
+      std::fprintf(stderr, "\n");
+    }
     t_like = t_gn + t_solve;
     t_upd = t_svgd;
     const double t_ll = since(E_LL0, E_BAYES);

@@ -575,7 +575,8 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
                                                             float* __restrict__ kval, int32_t* __restrict__ count,
                                                             int k, int cap, double sr, double st,
                                                             const float4* __restrict__ mir,
-                                                            const unsigned int* __restrict__ tmax_bits) {
+                                                            const unsigned int* __restrict__ tmax_bits,
+                                                            bool members_identity) {
   extern __shared__ __align__(16) unsigned char rg_smem[];
   int32_t* s_idx = reinterpret_cast<int32_t*>(rg_smem);                  // [k][BLOCK]
   // List values per thread row [BLOCK][KMAX] (16-byte aligned rows: the
@@ -676,24 +677,65 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
       // st |dt|^2 - margin_t > 110 proves the translation underflow).
       const float thr32 = static_cast<float>(thr);
       const float4 a0 = __ldg(mir + 3 * gi), a1 = __ldg(mir + 3 * gi + 1), a2 = __ldg(mir + 3 * gi + 2);
-      for (; q < q_end && ns < kRgChunk; ++q) {
-        if ((listed >> (q - rb)) & 1ull) continue;  // listed: a duplicate offer (also self)
-        const int32_t j = member_of[q];
-        if (j == gi) continue;
-        if (kStats) atomicAdd(&g_rg_stats[0], 1ull);
-        if (full) {
-          if (weakest < 0) continue;  // self-only full list (k == 1): nothing evictable
-          const float4 b0 = __ldg(mir + 3 * j), b1 = __ldg(mir + 3 * j + 1), b2 = __ldg(mir + 3 * j + 2);
-          const float d0 = b2.y - a2.y, d1 = b2.z - a2.z, d2 = b2.w - a2.w;
-          const float uu = fmaf(d0, d0, fmaf(d1, d1, d2 * d2));
-          if (fmaf(st32, uu, -mt) > 110.0f) continue;  // kernel_underflows: k = 0 <= wk
-          const float tr = fmaf(a0.x, b0.x, fmaf(a0.y, b0.y, fmaf(a0.z, b0.z, a0.w * b0.w))) +
-                           fmaf(a1.x, b1.x, fmaf(a1.y, b1.y, fmaf(a1.z, b1.z, a1.w * b1.w))) + a2.x * b2.x;
-          const float L = fmaf(sr32, 3.0f - tr, st32 * uu);
-          if (L * (1.0f - 1e-5f) - mL > thr32) continue;  // float(exp(-q)) <= wk: dropped
+      // Members are examined kFB at a time: their member_of and mirror loads
+      // are all issued before any test (the loop is load-latency bound), then
+      // the survivors are appended in window order until the chunk is full;
+      // the thresholds only change in the offer phase, so batching leaves the
+      // survivor sequence unchanged. A member not consumed because the chunk
+      // filled up is examined again in the next chunk, as in the serial loop.
+      constexpr int kFB = 4;
+      while (q < q_end && ns < kRgChunk) {
+        int32_t jj[kFB];
+        bool cand[kFB];
+#pragma unroll
+        for (int u = 0; u < kFB; ++u) {
+          const int64_t qq = q + u;
+          const bool in = qq < q_end && !((listed >> (qq - rb)) & 1ull);  // listed: a duplicate offer (also self)
+          jj[u] = in ? (members_identity ? static_cast<int32_t>(qq) : member_of[qq]) : gi;
+          cand[u] = in;
         }
-        s_cand[ns * BLOCK + t] = j;
-        ++ns;
+#pragma unroll
+        for (int u = 0; u < kFB; ++u) cand[u] = cand[u] && jj[u] != gi;
+        bool pass[kFB];
+        if (full) {
+          float4 b0[kFB], b1[kFB], b2[kFB];
+#pragma unroll
+          for (int u = 0; u < kFB; ++u) {
+            const int32_t j = cand[u] ? jj[u] : gi;
+            b0[u] = __ldg(mir + 3 * j);
+            b1[u] = __ldg(mir + 3 * j + 1);
+            b2[u] = __ldg(mir + 3 * j + 2);
+          }
+#pragma unroll
+          for (int u = 0; u < kFB; ++u) {
+            const float d0 = b2[u].y - a2.y, d1 = b2[u].z - a2.z, d2 = b2[u].w - a2.w;
+            const float uu = fmaf(d0, d0, fmaf(d1, d1, d2 * d2));
+            const float tr = fmaf(a0.x, b0[u].x, fmaf(a0.y, b0[u].y, fmaf(a0.z, b0[u].z, a0.w * b0[u].w))) +
+                             fmaf(a1.x, b1[u].x, fmaf(a1.y, b1[u].y, fmaf(a1.z, b1[u].z, a1.w * b1[u].w))) +
+                             a2.x * b2[u].x;
+            const float L = fmaf(sr32, 3.0f - tr, st32 * uu);
+            // kernel_underflows (k = 0 <= wk), or float(exp(-q)) <= wk: dropped;
+            // a self-only full list (k == 1) has nothing evictable
+            pass[u] = cand[u] && weakest >= 0 && !(fmaf(st32, uu, -mt) > 110.0f) &&
+                      !(L * (1.0f - 1e-5f) - mL > thr32);
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < kFB; ++u) pass[u] = cand[u];
+        }
+        int used = kFB;
+#pragma unroll
+        for (int u = 0; u < kFB; ++u) {
+          if (u < used && q + u < q_end) {
+            if (kStats && cand[u]) atomicAdd(&g_rg_stats[0], 1ull);
+            if (pass[u]) {
+              s_cand[ns * BLOCK + t] = jj[u];
+              ++ns;
+              if (ns == kRgChunk) used = u + 1;  // chunk full: the rest of the batch waits
+            }
+          }
+        }
+        q += used;
       }
       if (kStats) atomicAdd(&g_rg_stats[1], static_cast<unsigned long long>(ns));
     }
@@ -905,7 +947,7 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                               st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, \
                                                                seg_start, n_sorted, pos_of, idx, kval,            \
                                                                count, k,                                          \
-                                                               cap, sr, st_, mir, tmax_bits)
+                                                               cap, sr, st_, mir, tmax_bits, pos_of == nullptr)
     static const bool stats = std::getenv("SMCL_RG_STATS") != nullptr;
     if (stats && k == 20) {
       const unsigned long long z[4] = {0, 0, 0, 0};
@@ -916,7 +958,8 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                                             static_cast<size_t>(kRgChunk) * B * 8 + B * 4 +
                                             static_cast<size_t>(B) * kRgChunk * 2,
                                         st>>>(all_poses, n, gbase, pos_list, member_of, seg_id, seg_start, n_sorted,
-                                              pos_of, idx, kval, count, k, cap, sr, st_, mir, tmax_bits);
+                                              pos_of, idx, kval, count, k, cap, sr, st_, mir, tmax_bits,
+                                              pos_of == nullptr);
 #undef B_
       unsigned long long h[4];
       cudaMemcpyFromSymbolAsync(h, g_rg_stats, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
