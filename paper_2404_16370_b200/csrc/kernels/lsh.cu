@@ -617,9 +617,15 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
     const Pose pi = ldg_pose(all_poses + gi);
 #pragma unroll
     for (int s = 0; s < KMAX; ++s) s_kv[t * KMAX + s] = __int_as_float(0x7f800000);
-    for (int s = 0; s < cnt; ++s) {  // refresh (neighbor_graph.hpp:76-90); self stays +inf (see above)
+    // refresh (neighbor_graph.hpp:76-90); self stays +inf (see above). The
+    // next entry's pose is loaded while the current one is evaluated.
+    Pose nxt;
+    if (cnt > 0) nxt = ldg_pose(all_poses + s_idx[t]);
+    for (int s = 0; s < cnt; ++s) {
       const int32_t j = s_idx[s * BLOCK + t];
-      if (j != gi) s_kv[t * KMAX + s] = kval_of(pi, ldg_pose(all_poses + j), sr, st);
+      const Pose pj = nxt;
+      if (s + 1 < cnt) nxt = ldg_pose(all_poses + s_idx[(s + 1) * BLOCK + t]);
+      if (j != gi) s_kv[t * KMAX + s] = kval_of(pi, pj, sr, st);
     }
     if (kStats) atomicAdd(&g_rg_stats[3], static_cast<unsigned long long>(cnt > 0 ? cnt - 1 : 0));
   }
@@ -752,7 +758,8 @@ __global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restri
     for (int f = lane; f < total; f += 32) {
       const int e = w_flat[f];
       const int ot = (wid << 5) | (e >> 5), sl = e & 31;
-      s_ckv[sl * BLOCK + ot] = kval_of(ldg_pose(all_poses + s_gi[ot]), ldg_pose(all_poses + s_cand[sl * BLOCK + ot]), sr, st);
+      s_ckv[sl * BLOCK + ot] =
+          kval_of(ldg_pose(all_poses + s_gi[ot]), ldg_pose(all_poses + s_cand[sl * BLOCK + ot]), sr, st);
     }
     __syncwarp();
     // ---- offers in window order (neighbor_graph.hpp:47-74)
@@ -940,7 +947,7 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
     k_pose_mirror<<<blocks_for(n_sorted, 256), 256, 0, st>>>(all_poses, n_sorted,
                                                             make_double3(anchor[0], anchor[1], anchor[2]), mir,
                                                             tmax_bits);
-#define RGF(KM)                                                                                                   \
+#define RGF(KM)                                                                                               \
   k_refresh_gather_f<B, KM><<<blocks_for(n, B), B,                                                                 \
                               static_cast<size_t>(k) * B * 4 + static_cast<size_t>(KM) * B * 4 +                   \
                                   static_cast<size_t>(kRgChunk) * B * 8 + B * 4 + static_cast<size_t>(B) * kRgChunk * 2, \
