@@ -65,14 +65,18 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // 16-byte async copy; when !pred nothing is read and the destination is zero-filled.
 // kL1: also allocate in L1 (.ca) — pays for bricked HBM-sized tables, where
 // neighbouring particles re-read the same records; L2-resident tables use .cg.
+// The zero fill uses the ignore-src predicate form (no src-size register).
 template <bool kL1>
 __device__ __forceinline__ void cp_async16_pred(void* smem, const void* gmem, bool pred) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int src_bytes = pred ? 16 : 0;
   if (kL1)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+    asm volatile("{\n .reg .pred q;\n setp.eq.u32 q, %2, 0;\n cp.async.ca.shared.global [%0], [%1], 16, q;\n}\n" ::"r"(s),
+                 "l"(gmem), "r"(static_cast<unsigned>(pred))
+                 : "memory");
   else
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+    asm volatile("{\n .reg .pred q;\n setp.eq.u32 q, %2, 0;\n cp.async.cg.shared.global [%0], [%1], 16, q;\n}\n" ::"r"(s),
+                 "l"(gmem), "r"(static_cast<unsigned>(pred))
+                 : "memory");
 }
 // One 32-byte record as a single 256-bit load (sm_100 LDG.256), predicated:
 // when !pred nothing is read and the record reads as empty (beta = -1).
@@ -878,11 +882,13 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
   // The lane kernel needs two resident CTAs per SM (16 warps): scans too large
   // for that (S > ~900 points) take the warp-per-particle kernel as well.
   if (!gn && c == 0) c = (map.brick || 3 * ll_lanes_smem<1, 8, true>(scan.n) > 227 * 1024) ? 416 : 9000;
-  // GN pass: 24 warps per SM (80 registers) where the scan fits in shared
-  // memory next to 24 warp stages (S <= ~1300), else 16. Bricked (HBM-sized)
-  // tables keep 16 warps: their L1-allocating gathers need the L1 that 8 more
-  // warp stages would take (outdoor kidnap GN 2.43 -> 2.31 ms, LL 2.55 -> 2.32).
-  if (c == 0) c = (gn && !map.brick && fast_smem<4, 24>(scan.n) <= 227 * 1024) ? 424 : 416;
+  // GN pass: 20 warps per SM (96 registers, no spills; 24 warps at 80
+  // registers spill: 4.58 ms against 4.42 at 1M x 512) where the scan fits in
+  // shared memory next to 20 warp stages (S <= ~1700), else 16. Bricked
+  // (HBM-sized) tables keep 16 warps: their L1-allocating gathers need the L1
+  // that more warp stages would take (outdoor kidnap GN 2.43 -> 2.31 ms, LL
+  // 2.55 -> 2.32).
+  if (c == 0) c = (gn && !map.brick && fast_smem<4, 20>(scan.n) <= 227 * 1024) ? 420 : 416;
   if (c >= 9000) {  // SMCL_FAST_CFG=LUxW: lane-per-particle variants (9000 = default)
     static const bool ldg = std::getenv("SMCL_LL_CPASYNC") == nullptr;
     // Default: one record in flight per lane, 8-warp CTAs, 4 CTAs (32 warps)
