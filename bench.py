@@ -274,6 +274,9 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # communicator set-up in the log (ranks, NVLS/NVLink transport) for the scaling runs
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
         pg = dist

@@ -280,7 +280,9 @@ struct smcl_engine {
   // (count matrix + per-destination cursors, packed send and received records).
   DBuf<unsigned int> mig_mat;
   DBuf<unsigned char> mig_send, mig_recv;
-  std::vector<unsigned int> mig_host;
+  unsigned int* mig_host = nullptr;  // pinned copy of the count matrix (world x world)
+  size_t mig_host_n = 0;
+  cudaEvent_t ev_mig = nullptr;
   DBuf<unsigned long long> g_counts;
   DBuf<double> g_argv, arg_pair;
   DBuf<double> g_rep;  // per rank: representative pose (12 doubles) + id, 14-double (16-B aligned) records
@@ -302,13 +304,27 @@ struct smcl_engine {
   // Sharded reorder, non-pose state: count matrix from the replicated
   // member_of (one small device->host read), pack this rank's outgoing
   // records, alltoallv, scatter the received ones to their new positions.
-  void migrate_reorder() {
-    const size_t w = static_cast<size_t>(world), rec = migrate_record_bytes(k);
+  // The host needs the shard-to-shard counts to size the alltoallv. Their
+  // read-back is asynchronous (pinned buffer + event): migrate_begin enqueues
+  // the count kernel and the copy, the caller enqueues independent work (the
+  // bucket segments), and migrate_finish waits for the event only, so the GPU
+  // is busy with that work while the host reads the counts.
+  void migrate_begin() {
+    const size_t w = static_cast<size_t>(world);
+    if (mig_host_n < w * w) {
+      if (mig_host) CK(cudaFreeHost(mig_host));
+      CK(cudaMallocHost(reinterpret_cast<void**>(&mig_host), sizeof(unsigned int) * w * w));
+      mig_host_n = w * w;
+    }
+    if (!ev_mig) CK(cudaEventCreateWithFlags(&ev_mig, cudaEventDisableTiming));
     CK(cudaMemsetAsync(mig_mat.p, 0, sizeof(unsigned int) * (w * w + w), st));
     launch_migrate_counts(member_of.p, n_total, n_local, world, mig_mat.p, st);
-    mig_host.resize(w * w);
-    CK(cudaMemcpyAsync(mig_host.data(), mig_mat.p, sizeof(unsigned int) * w * w, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpyAsync(mig_host, mig_mat.p, sizeof(unsigned int) * w * w, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(ev_mig, st));
+  }
+  void migrate_finish() {
+    const size_t w = static_cast<size_t>(world), rec = migrate_record_bytes(k);
+    CK(cudaEventSynchronize(ev_mig));
     std::vector<uint64_t> sb(w), rb(w);
     for (size_t d = 0; d < w; ++d) {
       sb[d] = rec * mig_host[d * w + static_cast<size_t>(rank)];
@@ -508,6 +524,8 @@ struct smcl_engine {
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    if (ev_mig) cudaEventDestroy(ev_mig);
+    if (mig_host) cudaFreeHost(mig_host);
     if (nb_host) cudaFreeHost(nb_host);
     if (step_host) cudaFreeHost(step_host);
     for (auto& e : ev)
@@ -1201,6 +1219,7 @@ struct smcl_engine {
     if (profiling) mark(E_SORT);
     launch_members(skeys.p, n, idx_mask, shift, member_of.p, head.p, st);
     const int32_t* members = member_of.p;
+    bool segments_done = false;
     if (cfg.reorder_particles) {
       launch_inverse_perm(member_of.p, n, new_of_old.p, st);
       if (sharded) {
@@ -1214,7 +1233,12 @@ struct smcl_engine {
         const size_t nl = static_cast<size_t>(n_local), kk = static_cast<size_t>(k);
         all_poses();  // old poses of every particle (cached gather)
         if (comm.alltoallv) {
-          migrate_reorder();
+          migrate_begin();
+          // bucket runs depend only on the sorted keys: computed while the host reads the counts
+          inclusive_sum_i32(head.p, seg_id.p, n, temp.p, temp_bytes, st);
+          launch_segments(head.p, seg_id.p, n, seg_start.p, st);
+          segments_done = true;
+          migrate_finish();
         } else {
           allgather(log_post.p, g_lp.p, sizeof(double) * nl);
           allgather(id.p, g_id.p, sizeof(int32_t) * nl);
@@ -1244,8 +1268,10 @@ struct smcl_engine {
     }
     const Pose* poses_all = all_poses();  // after the reorder: candidates read the current storage
     if (profiling) mark(E_REORDER);
-    inclusive_sum_i32(head.p, seg_id.p, n, temp.p, temp_bytes, st);
-    launch_segments(head.p, seg_id.p, n, seg_start.p, st);
+    if (!segments_done) {
+      inclusive_sum_i32(head.p, seg_id.p, n, temp.p, temp_bytes, st);
+      launch_segments(head.p, seg_id.p, n, seg_start.p, st);
+    }
     const int32_t* n_seg = seg_id.p + (n - 1);  // number of buckets (device)
     // Sorted positions of this shard's particles, in sorted order.
     const int32_t* owned = nullptr;

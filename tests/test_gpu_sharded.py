@@ -121,3 +121,47 @@ def test_sharded_rejects_unaligned_shards(world):
         e.init_uniform(world[1].bounds)
     e.close()
     comms.close()
+
+
+def test_sharded_profile_counts_all_shards_once(world):
+    """bench.py's pp/step comes from the step profile: every rank reports the
+    particle-point evaluations of ALL shards (gn_points + ll_points = N * (S_gn
+    + S) for one SVGD iteration), so the whole-job value needs no world factor,
+    and it equals one engine's count (bench.pp_per_step)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    n, G = 8192, 2
+    cfg = make_config(n_particles=n, seed=7, nnf_resolution=0.2, reorder_particles=1)
+    scans_, delta, cov = scans(world, cfg, 1)
+    single = FilterEngine(world[1], cfg)
+    single.init_uniform(world[1].bounds)
+    single.step(scans_[0], delta, cov, True)
+    p1 = single.last_step_profile()
+    single.close()
+    comms = LoopbackComms(G)
+    engines = [FilterEngine(world[1], cfg, comm=comms[r]) for r in range(G)]
+    profs = [None] * G
+
+    def body(r):
+        engines[r].init_uniform(world[1].bounds)
+        engines[r].step(scans_[0], delta, cov, True)
+        profs[r] = engines[r].last_step_profile()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    S = len(scans_[0])
+    for p in profs:
+        assert p["gn_points"] == n * S and p["ll_points"] == n * S
+        assert p["gn_points"] + p["ll_points"] == bench.pp_per_step(n, S, cfg)
+    assert p1["gn_points"] + p1["ll_points"] == bench.pp_per_step(n, S, cfg)
+    # matched counts are per shard: they add up to the single engine's
+    assert sum(p["ll_matched"] for p in profs) == p1["ll_matched"]
+    for e in engines:
+        e.close()
+    comms.close()
