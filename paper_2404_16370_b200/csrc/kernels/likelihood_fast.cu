@@ -627,6 +627,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
   }
 }
 
+// max that propagates NaN (fmaxf returns the other operand).
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 __device__ __forceinline__ bool occupied(const MapFast& m, uint32_t r) {
   return (__ldg(m.occ + (r >> 5)) >> (r & 31u)) & 1u;
 }
@@ -673,16 +680,20 @@ __global__ void __launch_bounds__(256, 3) k_ll_count(const Pose* __restrict__ po
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const double t = (P.t[a] - g.origin[a]) * g.inv_res;
-      tv[a] = static_cast<float>(t);
-      tmax = fmax(tmax, fabs(t));
+      tv[a] = static_cast<float>(t - 0.5);  // x - 1/2: its nearest integer is floor(x) away from faces
+      tmax = fmax(tmax, fabs(t) + 0.5);
     }
     // u (5 |mu|_1max / res + 4 |tv|) + 2.2e-8, x1.25 for the fp64 set-up roundings; |x| < 2^21 for the
     // round-down floor below, else every point takes the fp64 path.
     const double e = 0x1p-24 * (5.0 * scan.mu_l1_max * g.inv_res + 4.0 * tmax) * 1.25 + 2.5e-8;
     margin = (e < 0.01 && tmax + scan.mu_l1_max * g.inv_res < 2097152.0) ? static_cast<float>(e) : 2.0f;
   }
-  constexpr float kMagic32 = 12582912.0f;  // 1.5 * 2^23: round-down add leaves floor(x) in the low mantissa bits
-  const float hi = 1.0f - margin;
+  // 1.5 * 2^23: a round-to-nearest add of x - 1/2 leaves round(x - 1/2) =
+  // floor(x) in the low mantissa bits (|x| < 2^21); g = (x - 1/2) - floor(x)
+  // = frac(x) - 1/2, so the fraction clears both faces by margin iff
+  // max |g| <= 1/2 - margin (NaN fails).
+  constexpr float kMagic32 = 12582912.0f;
+  const float gmax = 0.5f - margin;
   int nmatch = 0;
   for (int k0 = 0; k0 < Sp; k0 += U) {
     uint32_t rec[U];
@@ -692,17 +703,16 @@ __global__ void __launch_bounds__(256, 3) k_ll_count(const Pose* __restrict__ po
     for (int u = 0; u < U; ++u) {
       const float4 m = s_m[k0 + u];
       unsigned ic[3];
-      float fmn = 1.0f, fmx = 0.0f;
+      float gabs = 0.0f;
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         const float x = fmaf(Rv[ax * 3 + 2], m.z, fmaf(Rv[ax * 3 + 1], m.y, fmaf(Rv[ax * 3 + 0], m.x, tv[ax])));
-        const float y = __fadd_rd(x, kMagic32);
-        const float f = x - (y - kMagic32);
+        const float y = __fadd_rn(x, kMagic32);
+        const float gc = x - (y - kMagic32);
         ic[ax] = static_cast<unsigned>(__float_as_int(y) - 0x4B400000);
-        fmn = fminf(fmn, f);
-        fmx = fmaxf(fmx, f);
+        gabs = fmax_nan(gabs, fabsf(gc));
       }
-      const bool safe = fmn >= margin && fmx <= hi;  // NaN fails
+      const bool safe = gabs <= gmax;  // NaN (padded points, non-finite poses) fails
       const bool inb = ic[0] < dx && ic[1] < dy && ic[2] < dz;
       ok[u] = safe && inb;
       rec[u] = ok[u] ? rec_index<kBrick>(map, ic[0], ic[1], ic[2]) : 0u;
@@ -920,6 +930,7 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
       const int mb = w - 80;
       if (u == 2 && mb == 4) return launch_ll_lanes_t<2, 8, true, 4>(poses, n, scan, map, raw_ll, nm, x, st);
       if (u == 2 && mb == 5) return launch_ll_lanes_t<2, 8, true, 5>(poses, n, scan, map, raw_ll, nm, x, st);
+      if (u == 1 && mb == 2) return launch_ll_lanes_t<1, 8, true, 2>(poses, n, scan, map, raw_ll, nm, x, st);
       if (u == 1 && mb == 4) return launch_ll_lanes_t<1, 8, true, 4>(poses, n, scan, map, raw_ll, nm, x, st);
       if (u == 1 && mb == 5) return launch_ll_lanes_t<1, 8, true, 5>(poses, n, scan, map, raw_ll, nm, x, st);
       if (u == 1 && mb == 6) return launch_ll_lanes_t<1, 8, true, 6>(poses, n, scan, map, raw_ll, nm, x, st);
