@@ -244,6 +244,14 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
 __device__ __forceinline__ bool frac_clear_of_faces(double f) {
   return static_cast<unsigned>(__double2hiint(f)) - 0x3E700000u < 0x3FEFFFFFu - 0x3E700000u;
 }
+// The same test on the fraction rounded to fp32 (the value phase A stores):
+// 2^-24 <= fr <= 1 - 2^-21 (one unsigned range test on the float bits; NaN
+// fails). Rounding moves f by < 2^-25 near 0 and < 2^-25 near 1, so a
+// passing fraction still clears both faces by > 4e-7 voxel near 1 and
+// > 2^-24 (1 - 2^-24) near 0, above the 2.2e-8 transform bound.
+__device__ __forceinline__ bool fracf_clear_of_faces(float fr) {
+  return static_cast<unsigned>(__float_as_uint(fr)) - 0x33800000u <= 0x3F7FFFF8u - 0x33800000u;
+}
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -370,14 +378,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           ic[ax] = __double2loint(y);
           inb = inb & (static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz)));
           fr[ax] = __double2float_rn(f);
-          safe = safe & frac_clear_of_faces(f);
+          safe = safe & fracf_clear_of_faces(fr[ax]);  // on the stored fp32 value: one use of f
         }
         const bool amb = !safe;
         const bool real = k < S;
         const bool resolve = amb && real;
         const bool stage = !amb && inb;  // padded points are NaN: never staged
-        const uint64_t cell = stage ? rec_index<kBrick>(map, ic[0], ic[1], ic[2]) : 0u;
-        const float4* src = map.rec + 2 * cell;
+        // Unstaged points form an address that is never read (predicated
+        // load / ignore-src copy), so the cell needs no select.
+        const float4* src = map.rec + 2 * static_cast<uint64_t>(rec_index<kBrick>(map, ic[0], ic[1], ic[2]));
         if (kLdg) {
           ldg_rec_pred(src, stage, rm0[kLdg ? u : 0], rm1[kLdg ? u : 0]);
         } else {
