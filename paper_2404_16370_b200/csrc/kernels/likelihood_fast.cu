@@ -41,11 +41,14 @@ namespace {
 constexpr uint32_t kMetaStage = 1u << 16;    // fq.w: record staged (in bounds, cell proven)
 constexpr uint32_t kMetaResolve = 1u << 17;  // fq.w: fraction within ~5e-8 of a cell face: reference-order path
 
+// Slots [0, kStep) hold the current step's points; slots [kStep, kStep + 32)
+// the carry: candidates left over from earlier steps of the same particle
+// (fewer than 32), so phase B runs full warps except on a particle's last step.
 template <int kStep>
 struct WarpStage {
-  float4 m0[kStep];  // staged cell records by point slot (SoA halves: conflict-free LDS.128)
-  float4 m1[kStep];
-  float4 fq[kStep];  // (fraction.xyz fp32, meta bits: k | kMetaStage | kMetaResolve) by point slot
+  float4 m0[kStep + 32];  // staged cell records by point slot (SoA halves: conflict-free LDS.128)
+  float4 m1[kStep + 32];
+  float4 fq[kStep + 32];  // (fraction.xyz fp32, meta bits: k | kMetaStage | kMetaResolve) by point slot
   uint16_t q[kStep];  // compacted candidate slots
   double pose_v[12];  // Rv (row-major), tv: reloaded by phase A each step (no registers held in phase B)
 };
@@ -236,21 +239,35 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
   }
 }
 
-// f = x - floor(x) at least ~5e-8 from both cell faces: 2^-24 <= f < 1 - 2^-21,
-// decided on the high word of f with one unsigned range test (integer pipe;
-// NaN and negative values fail). The transform differs from the reference's
-// by < 2.2e-8 voxel (the per-particle resolve bound), so such a point's cell
-// is the reference's.
-__device__ __forceinline__ bool frac_clear_of_faces(double f) {
-  return static_cast<unsigned>(__double2hiint(f)) - 0x3E700000u < 0x3FEFFFFFu - 0x3E700000u;
-}
-// The same test on the fraction rounded to fp32 (the value phase A stores):
-// 2^-24 <= fr <= 1 - 2^-21 (one unsigned range test on the float bits; NaN
-// fails). Rounding moves f by < 2^-25 near 0 and < 2^-25 near 1, so a
-// passing fraction still clears both faces by > 4e-7 voxel near 1 and
-// > 2^-24 (1 - 2^-24) near 0, above the 2.2e-8 transform bound.
-__device__ __forceinline__ bool fracf_clear_of_faces(float fr) {
-  return static_cast<unsigned>(__float_as_uint(fr)) - 0x33800000u <= 0x3F7FFFF8u - 0x33800000u;
+// Cell and fraction of a voxel coordinate x (|x| < 2^27) from ONE fp64 add:
+// y = RD(x + 1.5 * 2^28) has ulp 2^-24, so its 52-bit mantissa holds the
+// fixed-point value (2^27 + x) * 2^24 rounded down: the integer part
+// (2^27 + floor(x), 28 bits) straddles the two words and the low 24 bits are
+// f24 = floor(frac(x) * 2^24). With exponent 1051 (0x41B) in the high word,
+//   ic  = funnelshift_l(lo, hi, 8) - 0xB8000000 = floor(x)  (negative: huge unsigned)
+//   fr  = (f24 >> 1) * 2^-23 + 2^-24  (midpoint of the 2^-23 interval holding
+//         frac(x): |fr - frac(x)| <= 2^-24 ~ 6e-8 voxel, the fp32 fraction's own
+//         rounding), built from the bits with one FADD
+//   clear of both faces by more than the 2.2e-8-voxel transform bound iff
+//         1 <= f24 <= 2^24 - 2 (frac(x) in [2^-24, 1 - 2^-24)).
+// 4 fp64 operations per axis instead of 6 plus a conversion (no F2F: the
+// short-scoreboard stall of phase A). NaN x gives garbage bits: callers stage
+// only real scan points of finite-pose particles (huge covers non-finite poses).
+struct CellFrac {
+  unsigned ic;
+  float fr;
+  bool clear;
+};
+__device__ __forceinline__ CellFrac cell_frac(double x) {
+  constexpr double kMagic28 = 402653184.0;  // 1.5 * 2^28
+  const double y = __dadd_rd(x, kMagic28);
+  const unsigned lo = static_cast<unsigned>(__double2loint(y)), hi = static_cast<unsigned>(__double2hiint(y));
+  CellFrac c;
+  c.ic = __funnelshift_l(lo, hi, 8) - 0xB8000000u;
+  const unsigned f24 = lo & 0xFFFFFFu;
+  c.fr = __uint_as_float(0x3F800000u | (f24 >> 1)) - (1.0f - 0x1p-24f);
+  c.clear = f24 - 1u < 0xFFFFFEu;
+  return c;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -307,7 +324,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
                  dz = static_cast<unsigned>(g.dims[2]);
   Stage& ws = stages[wid];
-  constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: round-down add leaves floor(x) in the low word
 
   const int64_t n_eff = list ? static_cast<int64_t>(*list_count) : n;  // list: the gate's live particles
   for (int64_t it = gwarp; it < n_eff; it += nwarps) {
@@ -354,6 +370,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     for (int q = 0; q < 9; ++q) acc.htr[q] = 0.f;
     acc.cost = 0.f;
     int nmatch = 0;
+    int n_carry = 0;  // candidates waiting in the carry slots (< 32)
 
     for (int base = 0; base < S; base += kStep) {
       // ---- phase A: fp64 cell + exact fraction, predicated async gather
@@ -373,17 +390,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
           const double x = fma(Rv[ax * 3 + 2], m2, fma(Rv[ax * 3 + 1], m1, fma(Rv[ax * 3 + 0], m0, tv[ax])));
-          const double y = __dadd_rd(x, kMagic);
-          const double f = x - (y - kMagic);
-          ic[ax] = __double2loint(y);
-          inb = inb & (static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz)));
-          fr[ax] = __double2float_rn(f);
-          safe = safe & fracf_clear_of_faces(fr[ax]);  // on the stored fp32 value: one use of f
+          const CellFrac cf = cell_frac(x);
+          ic[ax] = static_cast<int>(cf.ic);
+          inb = inb & (cf.ic < (ax == 0 ? dx : (ax == 1 ? dy : dz)));
+          fr[ax] = cf.fr;
+          safe = safe & cf.clear;
         }
+        const bool real = k < S;  // padded points (NaN) are neither staged nor resolved
         const bool amb = !safe;
-        const bool real = k < S;
         const bool resolve = amb && real;
-        const bool stage = !amb && inb;  // padded points are NaN: never staged
+        const bool stage = !amb && inb && real;
         // Unstaged points form an address that is never read (predicated
         // load / ignore-src copy), so the cell needs no select.
         const float4* src = map.rec + 2 * static_cast<uint64_t>(rec_index<kBrick>(map, ic[0], ic[1], ic[2]));
@@ -419,12 +435,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         n_cand += __popc(mask);
       }
       __syncwarp();
-      // ---- phase B: structured algebra on full warps
-      for (int b0 = 0; b0 < n_cand; b0 += 32) {
+      // ---- phase B: structured algebra on full warps; carried candidates
+      // first, then this step's. Only the particle's last step runs a partial
+      // warp; otherwise the remainder (< 32) moves to the carry slots.
+      const int total = n_carry + n_cand;
+      const bool last_step = base + kStep >= S;
+      const int n_run = last_step ? total : (total & ~31);
+      for (int b0 = 0; b0 < n_run; b0 += 32) {
         const int e = b0 + lane;
         bool valid = false;
-        if (e < n_cand) {
-          const int slot = ws.q[e];
+        if (e < n_run) {
+          const int slot = e < n_carry ? kStep + e : ws.q[e - n_carry];
           const float4 fq = ws.fq[slot];
           const uint32_t meta = __float_as_uint(fq.w);
           const int k = static_cast<int>(meta & 0xFFFFu);
@@ -458,6 +479,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         nmatch += __popc(__ballot_sync(0xffffffffu, valid));
       }
       __syncwarp();
+      if (!last_step) {  // remainder elements [n_run, total) -> carry slots [0, total - n_run)
+        const int e = n_run + lane;
+        if (e < total && e >= n_carry) {  // e < n_carry (n_run == 0): already in carry slot e
+          const int src = ws.q[e - n_carry], dst = kStep + e - n_run;
+          ws.m0[dst] = ws.m0[src];
+          ws.m1[dst] = ws.m1[src];
+          ws.fq[dst] = ws.fq[src];
+        }
+        n_carry = total - n_run;
+        __syncwarp();
+      }
     }
 
     // ---- epilogue: lane q ends up with the warp total of accumulator q
@@ -537,7 +569,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
   const int nx = g.dims[0], ny = g.dims[1];
   const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
                  dz = static_cast<unsigned>(g.dims[2]);
-  constexpr double kMagic = 6755399441055744.0;
   double Rv[9], tv[3];
   float Rf[9];
   bool huge;
@@ -555,7 +586,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
     for (int q = 0; q < 9; ++q) mr = fmax(mr, fabs(P.R[q]));
 #pragma unroll
     for (int a = 0; a < 3; ++a) mt = fmax(mt, fabs(P.t[a]) + fabs(g.origin[a]));
-    huge = !((mr * scan.mu_l1_max + mt) * g.inv_res < 6.7e7);
+    double sum = 0.0;  // NaN-propagating (fmax drops NaN): non-finite poses resolve every point
+#pragma unroll
+    for (int q = 0; q < 12; ++q) sum += q < 9 ? P.R[q] : P.t[q - 9];
+    huge = !((mr * scan.mu_l1_max + mt) * g.inv_res < 6.7e7) || !(sum == sum);
   }
   double cost = 0.0;
   int nmatch = 0;
@@ -574,12 +608,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
 #pragma unroll
       for (int ax = 0; ax < 3; ++ax) {
         const double x = fma(Rv[ax * 3 + 2], m2, fma(Rv[ax * 3 + 1], m1, fma(Rv[ax * 3 + 0], m0, tv[ax])));
-        const double y = __dadd_rd(x, kMagic);
-        const double f = x - (y - kMagic);
-        ic[ax] = __double2loint(y);
-        inb = inb & (static_cast<unsigned>(ic[ax]) < (ax == 0 ? dx : (ax == 1 ? dy : dz)));
-        fr[u][ax] = __double2float_rn(f);
-        safe = safe & frac_clear_of_faces(f);
+        const CellFrac cf = cell_frac(x);
+        ic[ax] = static_cast<int>(cf.ic);
+        inb = inb & (cf.ic < (ax == 0 ? dx : (ax == 1 ? dy : dz)));
+        fr[u][ax] = cf.fr;
+        safe = safe & cf.clear;
       }
       const bool amb = !safe;
       const bool stg = real && !amb && inb;
