@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -453,9 +454,22 @@ struct smcl_engine {
   bool profiling = false;
   int32_t rep_id = -1;                // id of the last representative
   unsigned long long last_nm_sum = 0;  // sum of n_matched over all shards (last Bayes update)
+  // NVTX: one host range per step stage (opened at the stage's start event,
+  // closed at the next), nested in the step's range; header-only NVTX v3, a
+  // no-op unless a profiler (ncu --nvtx) is attached.
+  bool nvtx_open = false;
+  void nvtx_stage(Ev e) {
+    static const char* names[E_COUNT] = {"predict",  "lsh_keys",  "sort",     "reorder", "segments",
+                                         "refresh_gather", "nb_stats", "gn_svgd", "likelihood", "ll_gate",
+                                         "bayes_update", "smooth", nullptr};
+    if (nvtx_open) nvtxRangePop();
+    nvtx_open = names[e] != nullptr;
+    if (nvtx_open) nvtxRangePushA(names[e]);
+  }
   void mark(Ev e) {
     if (!ev[e]) CK(cudaEventCreate(&ev[e]));
     CK(cudaEventRecord(ev[e], st));
+    if (profiling) nvtx_stage(e);
   }
   float since(Ev a, Ev b) const {
     float ms = 0.f;
@@ -1530,8 +1544,15 @@ struct smcl_engine {
     profiling = true;
     struct ProfilingOff {  // cleared on every exit path (a throwing stage must not leave the step's events armed)
       bool& f;
-      ~ProfilingOff() { f = false; }
-    } profiling_off{profiling};
+      bool& nvtx;
+      ~ProfilingOff() {
+        f = false;
+        if (nvtx) nvtxRangePop();  // the open stage range
+        nvtx = false;
+        nvtxRangePop();  // the step range
+      }
+    } profiling_off{profiling, nvtx_open};
+    nvtxRangePushA("smcl::step");
     const long long launches0 = launch_count();
     const long long d2h0 = g_d2h.load();
     smcl_frame_result r;

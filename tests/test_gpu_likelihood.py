@@ -198,3 +198,47 @@ def test_fast_paths_far_from_origin(scene, offset):
     assert np.array_equal(nmg, nmg2)
     m = ll2 > -1e29
     assert np.all(np.abs(ll[m] - ll2[m]) <= TOL_LL * np.abs(ll2[m]))
+
+
+def test_fast_paths_points_on_cell_faces(scene):
+    """Points placed on (or within 1e-15 .. 1e-4 voxel of) NNF cell faces: the
+    scan is snapped to a lattice of res/4, rotations are exact multiples of
+    90 degrees and translations are whole cells plus a small offset, so a
+    quarter of the coordinates per axis land on a face. The fast kernels' cell
+    decisions (K1's and K2's fixed-point split, K2a's fp32 count with its
+    proven margin) must fall back to the reference-order transform there:
+    n_matched exact for both passes, ll within tolerance (nnf.hpp:24-35)."""
+    mapc, scan, parts, om = scene
+    from paper_2404_16370_b200.abi import Particles
+    e0 = FilterEngine(mapc, config(nnf_resolution=0.2, likelihood_mode=2))
+    d, o, res, _ = e0.nnf()
+    q = res / 4.0
+    mu = np.round(scan.mu / q) * q
+    sc = GaussianCloud(mu, scan.sigma)
+    rots = [np.eye(3),
+            np.array([[0., -1, 0], [1, 0, 0], [0, 0, 1]]),
+            np.array([[-1., 0, 0], [0, -1, 0], [0, 0, 1]]),
+            np.array([[1., 0, 0], [0, 0, -1], [0, 1, 0]]),
+            np.array([[0., 0, 1], [0, 1, 0], [-1, 0, 0]])]
+    deltas = [0.0, 1e-15, -1e-15, 1e-12, -1e-12, 1e-9, -1e-9, 2e-8, -2e-8, 6e-8, -6e-8, 1e-7, -1e-7,
+              1e-6, -1e-6, 1e-5, -1e-5, 1e-4, -1e-4, 0.5]
+    rng = np.random.default_rng(11)
+    poses = []
+    for R in rots:
+        for dl in deltas:
+            for _ in range(8):
+                cell = np.array([rng.integers(int(0.2 * d[a]), int(0.8 * d[a])) for a in range(3)], float)
+                t = np.asarray(o) + res * cell + dl * res
+                poses.append(np.concatenate([R.reshape(-1), t]))
+    poses = np.array(poses)
+    e = FilterEngine(mapc, config(nnf_resolution=0.2, likelihood_mode=2))
+    e.set_particles(Particles.from_poses(poses, 20))
+    ll, nm = e.evaluate_likelihoods(sc)
+    ll2, nm2 = O.evaluate_likelihoods(om, sc.mu, sc.sigma, poses, config())
+    assert (nm2 > 0).sum() > 200
+    assert np.array_equal(nm, nm2)
+    m = ll2 > -1e29
+    assert np.all(np.abs(ll[m] - ll2[m]) <= TOL_LL * np.abs(ll2[m]))
+    _, llg, nmg = e.evaluate_all(sc)
+    _, llg2, nmg2 = O.evaluate_all(om, sc.mu, sc.sigma, poses, config())
+    assert np.array_equal(nmg, nmg2)
