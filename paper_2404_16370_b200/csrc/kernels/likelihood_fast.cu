@@ -285,6 +285,19 @@ __device__ __forceinline__ uint32_t rec_index(const MapFast& m, uint32_t ix, uin
   return (b << 6) | ((iz & 3u) << 4) | ((iy & 3u) << 2) | (ix & 3u);
 }
 
+// Pose reload the compiler cannot merge with an earlier load of the same
+// address: the rare resolve paths re-read the pose instead of keeping its
+// 24 fp64 registers live across the whole scan loop.
+__device__ __forceinline__ Pose reload_pose(const Pose* p) {
+  Pose P;
+  double* w = reinterpret_cast<double*>(&P);
+  const double* s = reinterpret_cast<const double*>(p);
+#pragma unroll
+  for (int q = 0; q < 12; q += 2)
+    asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(w[q]), "=d"(w[q + 1]) : "l"(s + q));
+  return P;
+}
+
 __device__ __forceinline__ void transform_x(const double* R, const double* t, const double mu[3], double p[3]) {
 #pragma unroll
   for (int i = 0; i < 3; ++i)
@@ -565,14 +578,15 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
   const int64_t i = active ? (list ? static_cast<int64_t>(list[r]) : r) : 0;
   float4* ws = stage + wid * U * 2 * 32;
   const NnfGeom g = map.g;
-  const float res = static_cast<float>(g.res);
+  float res;  // kept in a register (otherwise re-converted from the parameter at every matched point)
+  asm volatile("cvt.rn.f32.f64 %0, %1;" : "=f"(res) : "d"(g.res));
   const int nx = g.dims[0], ny = g.dims[1];
   const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
                  dz = static_cast<unsigned>(g.dims[2]);
   double Rv[9], tv[3];
   float Rf[9];
   bool huge;
-  {
+  {  // the pose itself is not kept: the resolve path reloads it
     const Pose P = poses[active ? i : 0];
 #pragma unroll
     for (int q = 0; q < 9; ++q) {
@@ -592,6 +606,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
     huge = !((mr * scan.mu_l1_max + mt) * g.inv_res < 6.7e7) || !(sum == sum);
   }
   double cost = 0.0;
+  float cpart = 0.f;  // fp32 partial over <= 16 points, folded into the fp64 total (one conversion per 16 points)
   int nmatch = 0;
   for (int base = 0; base < S; base += U) {
     float fr[U][3];
@@ -634,7 +649,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
       float4 m1 = kLdg ? rm1[kLdg ? u : 0] : ws[(u * 2 + 1) * 32 + lane];
       bool valid = (st[u] & 1u) != 0;
       if (st[u] & 2u) {  // reference-order transform, floor and bounds (nnf.hpp:24-35)
-        const Pose P = poses[i];
+        const Pose P = reload_pose(poses + i);
         const double mu[3] = {s_mu[3 * k], s_mu[3 * k + 1], s_mu[3 * k + 2]};
         double p[3];
         transform_x(P.R, P.t, mu, p);
@@ -657,9 +672,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
         Acc a;
         a.cost = 0.f;
         fast_item<false>(a, Rf, fr[u], res, m0, m1, s_r0[k], s_r1[k]);
-        cost += static_cast<double>(a.cost);
+        cpart += a.cost;
         ++nmatch;
       }
+    }
+    if (((base / U) & (16 / U - 1)) == 16 / U - 1 || base + U >= S) {  // warp-uniform
+      cost += static_cast<double>(cpart);
+      cpart = 0.f;
     }
     __syncwarp();
   }
@@ -712,10 +731,10 @@ __global__ void __launch_bounds__(256, 3) k_ll_count(const Pose* __restrict__ po
   const NnfGeom g = map.g;
   const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
                  dz = static_cast<unsigned>(g.dims[2]);
-  const Pose P = poses[active ? i : 0];
   float Rv[9], tv[3];
   float margin;
-  {
+  {  // the pose itself is not kept: the resolve path reloads it
+    const Pose P = poses[active ? i : 0];
     double tmax = 0.0;
 #pragma unroll
     for (int q = 0; q < 9; ++q) Rv[q] = static_cast<float>(P.R[q] * g.inv_res);
@@ -771,8 +790,9 @@ __global__ void __launch_bounds__(256, 3) k_ll_count(const Pose* __restrict__ po
         if (!((amb >> u) & 1u)) continue;
         const int k = k0 + u;
         const double mu[3] = {scan.mu[3 * k], scan.mu[3 * k + 1], scan.mu[3 * k + 2]};
+        const Pose Pr = reload_pose(poses + (active ? i : 0));
         double p[3];
-        transform_x(P.R, P.t, mu, p);
+        transform_x(Pr.R, Pr.t, mu, p);
         bool valid = true;
         unsigned ic[3];
 #pragma unroll
