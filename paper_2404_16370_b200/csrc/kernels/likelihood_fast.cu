@@ -51,7 +51,18 @@ struct WarpStage {
   float4 fq[kStep + 32];  // (fraction.xyz fp32, meta bits: k | kMetaStage | kMetaResolve) by point slot
   uint16_t q[kStep];  // compacted candidate slots
   double pose_v[12];  // Rv (row-major), tv: reloaded by phase A each step (no registers held in phase B)
+  float rf[12];       // R in fp32 (row-major, 9 used): reloaded by each phase-B batch (no registers held in phase A)
 };
+
+// Shared-memory loads the compiler may not hoist out of the batch loop (the
+// values are re-read where they are used instead of pinning registers).
+__device__ __forceinline__ float4 lds_f4_volatile(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
 
 struct Acc {
   float hbr[6];  // Omega' lower: 00,10,11,20,21,22
@@ -332,7 +343,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
   const NnfGeom g = map.g;
-  const float res = static_cast<float>(g.res);
+  float res;  // kept in a register (not re-converted from the parameter in every batch)
+  asm volatile("cvt.rn.f32.f64 %0, %1;" : "=f"(res) : "d"(g.res));
   const int nx = g.dims[0], ny = g.dims[1];
   const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
                  dz = static_cast<unsigned>(g.dims[2]);
@@ -343,20 +355,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
     const int64_t i = list ? static_cast<int64_t>(list[it]) : it;
     // Pose in voxel units x = Rv mu + tv (Rv = R/res, tv = (t - o)/res) in
     // fp64 registers; Rf = R (fp32) for the body-frame algebra.
-    float Rf[9];
     bool huge;
     {
       // Lane q < 12 loads pose word q (R row-major, then t) and writes its
-      // voxel-unit value; the fp32 rotation and the |x| bound are shared by
-      // shuffles.
+      // voxel-unit value and (q < 9) its fp32 rotation entry; the |x| bound is
+      // shared by shuffles.
       const double pv = __ldg(reinterpret_cast<const double*>(poses + i) + (lane < 12 ? lane : 0));
       const bool isR = lane < 9, isT = lane >= 9 && lane < 12;
       const double o = lane == 9 ? g.origin[0] : (lane == 10 ? g.origin[1] : (lane == 11 ? g.origin[2] : 0.0));
       const double centered = pv - o;
       if (lane < 12) ws.pose_v[lane] = centered * g.inv_res;
       const float rf = static_cast<float>(pv);
-#pragma unroll
-      for (int q = 0; q < 9; ++q) Rf[q] = __shfl_sync(0xffffffffu, rf, q);
+      if (lane < 12) ws.rf[lane] = rf;
       // Resolve every point (NaN too) unless (max|R| |mu|_1 + max(|t| + |o|))
       // / res < 2^26: the reference forms p = R mu + t in world coordinates,
       // whose rounding (~3 ulp of |t| + |R mu|, plus p - o) stays below 2.2e-8
@@ -457,6 +467,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       for (int b0 = 0; b0 < n_run; b0 += 32) {
         const int e = b0 + lane;
         bool valid = false;
+        float Rf[9];
+        {
+          const float4 r0 = lds_f4_volatile(ws.rf), r1 = lds_f4_volatile(ws.rf + 4), r2 = lds_f4_volatile(ws.rf + 8);
+          Rf[0] = r0.x, Rf[1] = r0.y, Rf[2] = r0.z, Rf[3] = r0.w, Rf[4] = r1.x, Rf[5] = r1.y, Rf[6] = r1.z,
+          Rf[7] = r1.w, Rf[8] = r2.x;
+        }
         if (e < n_run) {
           const int slot = e < n_carry ? kStep + e : ws.q[e - n_carry];
           const float4 fq = ws.fq[slot];
@@ -960,7 +976,9 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
   // (HBM-sized) tables keep 16 warps: their L1-allocating gathers need the L1
   // that more warp stages would take (outdoor kidnap GN 2.43 -> 2.31 ms, LL
   // 2.55 -> 2.32).
-  if (c == 0) c = (gn && !map.brick && fast_smem<4, 20>(scan.n) <= 227 * 1024) ? 420 : 416;
+  if (c == 0 && gn && !map.brick) c = fast_smem<4, 24>(scan.n) <= 227 * 1024 ? 424
+                                     : (fast_smem<4, 20>(scan.n) <= 227 * 1024 ? 420 : 416);
+  if (c == 0) c = 416;
   if (c >= 9000) {  // SMCL_FAST_CFG=LUxW: lane-per-particle variants (9000 = default)
     static const bool ldg = std::getenv("SMCL_LL_CPASYNC") == nullptr;
     // Default: one record in flight per lane, 8-warp CTAs, 4 CTAs (32 warps)
