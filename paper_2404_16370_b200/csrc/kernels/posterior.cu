@@ -134,18 +134,22 @@ __global__ void k_list_sums(const float* __restrict__ kval, const int32_t* __res
   csum[i] = static_cast<double>(cnt);
 }
 
-// reduce.hpp:22-27: one warp per 4096-element chunk. The warp stages the
-// whole chunk in shared memory with coalesced 128-bit loads (one round trip),
-// then lane 0 adds it serially in index order, so every chunk partial is
-// bit-identical to the reference's. Two independent vectors per launch
-// (blocks [0, chunks) sum v0, [chunks, 2*chunks) sum v1). The serial chain
-// is DADD-latency bound: lane 0 reads the staged values 16 at a time (LDS.128)
-// ahead of the adds.
+// reduce.hpp:22-27: one block per 4096-element chunk. The block's 256
+// threads stage the whole chunk in shared memory (16 independent loads each:
+// a single warp streaming 32 KB with a few loads in flight was load-latency
+// bound, ~25 us), then thread 0 adds it serially in index order, so every
+// chunk partial is bit-identical to the reference's. Two independent vectors
+// per launch (blocks [0, chunks) sum v0, [chunks, 2*chunks) sum v1). The
+// serial chain is DADD-latency bound: thread 0 reads the staged values 16 at
+// a time (LDS.128) ahead of the adds.
 // m_ptr != nullptr: the staged values are exp(v - *m_ptr) (the value_at of
-// posterior.cpp:17), computed by the 32 lanes while staging.
-__global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ v0, const double* __restrict__ v1,
-                                                     int64_t n, int64_t chunks, double* __restrict__ p0,
-                                                     double* __restrict__ p1, const double* __restrict__ m_ptr) {
+// posterior.cpp:17), computed by the block while staging.
+constexpr int kChunkThreads = 256;
+__global__ void __launch_bounds__(kChunkThreads) k_chunk_serial(const double* __restrict__ v0,
+                                                                const double* __restrict__ v1, int64_t n,
+                                                                int64_t chunks, double* __restrict__ p0,
+                                                                double* __restrict__ p1,
+                                                                const double* __restrict__ m_ptr) {
   __shared__ __align__(16) double s[kReduceChunk];
   const bool second = blockIdx.x >= chunks;
   const double* __restrict__ v = second ? v1 : v0;
@@ -153,34 +157,41 @@ __global__ void __launch_bounds__(32) k_chunk_serial(const double* __restrict__ 
   const int64_t c = second ? blockIdx.x - chunks : blockIdx.x;
   const int64_t begin = c * kReduceChunk;
   const int m = static_cast<int>(begin + kReduceChunk < n ? kReduceChunk : n - begin);
-  const bool vec = (reinterpret_cast<uintptr_t>(v + begin) & 15u) == 0;
   if (m_ptr) {
     const double mv = *m_ptr;
 #pragma unroll 4
-    for (int q = threadIdx.x; q < m; q += 32) s[q] = exp(xsub(__ldg(v + begin + q), mv));
-  } else if (vec) {
-    const double2* src = reinterpret_cast<const double2*>(v + begin);
-    double2* dst = reinterpret_cast<double2*>(s);
-#pragma unroll 8
-    for (int q = threadIdx.x; q < m / 2; q += 32) dst[q] = __ldg(src + q);
-    if ((m & 1) && threadIdx.x == 0) s[m - 1] = v[begin + m - 1];
+    for (int q = threadIdx.x; q < m; q += kChunkThreads) s[q] = exp(xsub(__ldg(v + begin + q), mv));
   } else {
-    for (int q = threadIdx.x; q < m; q += 32) s[q] = v[begin + q];
+#pragma unroll 8
+    for (int q = threadIdx.x; q < m; q += kChunkThreads) s[q] = __ldg(v + begin + q);
   }
-  __syncwarp();
+  __syncthreads();
   if (threadIdx.x != 0) return;
   double acc = 0.0;
   int q = 0;
   const double2* s2 = reinterpret_cast<const double2*>(s);
-  for (; q + 16 <= m; q += 16) {
+  if (m >= 16) {  // the next 16 values are read while the current 16 are added
     double2 x[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = s2[q / 2 + u];
+    for (int u = 0; u < 8; ++u) x[u] = s2[u];
+    for (; q + 32 <= m; q += 16) {
+      double2 y[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) y[u] = s2[(q + 16) / 2 + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc = xadd(acc, x[u].x);
+        acc = xadd(acc, x[u].y);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = y[u];
+    }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       acc = xadd(acc, x[u].x);
       acc = xadd(acc, x[u].y);
     }
+    q += 16;
   }
   for (; q < m; ++q) acc = xadd(acc, s[q]);
   partial[c] = acc;
@@ -412,13 +423,13 @@ void launch_max_of_partials(const double* pv, const long long* pi, int64_t n, do
 static void chunk_serial2(const double* a, const double* b, int64_t n, double* pa, double* pb, cudaStream_t st) {
   count_launch();
   const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
-  if (chunks > 0) k_chunk_serial<<<static_cast<unsigned>(2 * chunks), 32, 0, st>>>(a, b, n, chunks, pa, pb, nullptr);
+  if (chunks > 0) k_chunk_serial<<<static_cast<unsigned>(2 * chunks), kChunkThreads, 0, st>>>(a, b, n, chunks, pa, pb, nullptr);
 }
 void launch_chunk_sum_exp(const double* v, int64_t n, const double* m, double* partial, cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
   const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
-  k_chunk_serial<<<static_cast<unsigned>(chunks), 32, 0, st>>>(v, v, n, chunks, partial, partial, m);
+  k_chunk_serial<<<static_cast<unsigned>(chunks), kChunkThreads, 0, st>>>(v, v, n, chunks, partial, partial, m);
 }
 void launch_chunk_sum_kernel(const float* kval, const int32_t* count, int64_t n, int k, double* s1, double* s2,
                              double* pk, double* pc, cudaStream_t st) {
