@@ -219,7 +219,12 @@ typedef struct smcl_step_profile {
    * because a host key differed from the device's. */
   int64_t hash_guard_flagged, hash_guard_replays;
 } smcl_step_profile;
+/* Per-kernel stage times are read from the step's events on the first call
+ * after a step (valid until the next step). */
 int smcl_last_step_profile(smcl_engine* h, smcl_step_profile* out);
+/* The same without reading the stage times (no driver calls): point counts,
+ * matched counts, launches, copy bytes, total/predict/GN/solve/SVGD times. */
+int smcl_last_step_counts(smcl_engine* h, smcl_step_profile* out);
 /* Device timer on the engine stream (CUDA events): start, then stop returns
  * the elapsed milliseconds of everything the engine ran in between. */
 int smcl_timer_start(smcl_engine* h);

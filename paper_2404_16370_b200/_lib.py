@@ -39,6 +39,7 @@ SIGNATURES = {
     "smcl_scan_get": (_int, [C.c_void_p, _int, _P(_d), _P(_d), _P(_i64)]),
     "smcl_step_points": (_int, [C.c_void_p, _P(_d), _i64, _P(SmclOdom), _P(SmclFrameResult)]),
     "smcl_last_step_profile": (_int, [C.c_void_p, _P(SmclStepProfile)]),
+    "smcl_last_step_counts": (_int, [C.c_void_p, _P(SmclStepProfile)]),
     "smcl_timer_start": (_int, [C.c_void_p]),
     "smcl_timer_stop": (_int, [C.c_void_p, _P(_d)]),
     "smcl_frame_index": (_i64, [C.c_void_p]),

@@ -270,12 +270,11 @@ class Particles:
 def odom_struct(delta=None, cov=None, valid=True):
     """OdometryInput (filter.hpp:56-60); delta None = identity, cov None = zero."""
     o = SmclOdom()
-    pose = identity_pose() if delta is None else np.asarray(delta, np.float64).reshape(12)
-    for i in range(12):
-        o.delta[i] = float(pose[i])
-    c = np.zeros(36) if cov is None else np.asarray(cov, np.float64).reshape(36)
-    for i in range(36):
-        o.cov[i] = float(c[i])
+    pose = identity_pose() if delta is None else np.ascontiguousarray(delta, np.float64).reshape(12)
+    C.memmove(o.delta, pose.ctypes.data, 12 * 8)
+    if cov is not None:  # a fresh structure is zero-filled
+        c = np.ascontiguousarray(cov, np.float64).reshape(36)
+        C.memmove(o.cov, c.ctypes.data, 36 * 8)
     o.valid = 1 if valid else 0
     return o
 

@@ -145,9 +145,12 @@ class FilterEngine:
         check(_lib.lib().smcl_step_points(self.h, f64ptr(pts), pts.shape[0], C.byref(o), C.byref(r)))
         return r.to_dict()
 
-    def last_step_profile(self):
+    def last_step_profile(self, times=True):
+        """Profile of the last step; times=False skips the per-kernel stage
+        times (read from CUDA events on demand) and returns the counters."""
         p = SmclStepProfile()
-        check(_lib.lib().smcl_last_step_profile(self.h, C.byref(p)))
+        fn = _lib.lib().smcl_last_step_profile if times else _lib.lib().smcl_last_step_counts
+        check(fn(self.h, C.byref(p)))
         return p.to_dict()
 
     def timer_start(self):

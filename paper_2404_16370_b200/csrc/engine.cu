@@ -466,6 +466,23 @@ struct smcl_engine {
     nvtx_open = names[e] != nullptr;
     if (nvtx_open) nvtxRangePushA(names[e]);
   }
+  // The step's per-kernel stage times stay in the events until the next step
+  // records them again; read on demand (each cudaEventElapsedTime is a driver
+  // call, ~20 us per step for all of them, on the host path between frames).
+  bool prof_times_pending = false, prof_empty = false;
+  void fill_prof_times() {
+    if (!prof_times_pending) return;
+    prof_times_pending = false;
+    prof.lsh_keys_ms = since(E_PRED, E_KEYS);
+    prof.sort_ms = since(E_KEYS, E_SORT);
+    prof.reorder_ms = since(E_SORT, E_REORDER);
+    prof.segments_ms = since(E_REORDER, E_SEG);
+    prof.refresh_gather_ms = since(E_SEG, E_RG);
+    prof.nb_stats_ms = since(E_RG, E_NB);
+    prof.ll_kernel_ms = prof_empty ? 0.0 : since(E_LL0, E_LL1);
+    prof.bayes_ms = since(E_LL1, E_SMOOTH);
+    prof.smooth_ms = since(E_SMOOTH, E_END);
+  }
   void mark(Ev e) {
     if (!ev[e]) CK(cudaEventCreate(&ev[e]));
     CK(cudaEventRecord(ev[e], st));
@@ -1541,6 +1558,8 @@ struct smcl_engine {
     wait_slot(slot_i);
     ScanSlot& sl = slot_at(slot_i);
     if (!sl.valid) throw std::invalid_argument("scan slot not uploaded");
+    static const bool host_timing = std::getenv("SMCL_HOST_TIMING") != nullptr;  // diagnostics: host time around the GPU work
+    const auto h0 = std::chrono::steady_clock::now();
     profiling = true;
     struct ProfilingOff {  // cleared on every exit path (a throwing stage must not leave the step's events armed)
       bool& f;
@@ -1558,6 +1577,7 @@ struct smcl_engine {
     smcl_frame_result r;
     std::memset(&r, 0, sizeof(r));
     std::memset(&prof, 0, sizeof(prof));
+    prof_times_pending = false;
     r.n_particles = n_total;
     const bool empty = sl.full.n == 0;
     r.scan_empty = empty ? 1 : 0;
@@ -1579,6 +1599,7 @@ struct smcl_engine {
       }
       predict(delta, cov, mix_seed(cfg.seed, k_stream_predict, static_cast<uint64_t>(frame)));
     }
+    const auto h1 = std::chrono::steady_clock::now();
     mark(E_PRED);
     const double bounds[6] = {map_bounds.min[0], map_bounds.min[1], map_bounds.min[2],
                               map_bounds.max[0], map_bounds.max[1], map_bounds.max[2]};
@@ -1590,6 +1611,7 @@ struct smcl_engine {
     const ScanDev& gn_scan = sl.gn_view();
     // Everything after K3, up to the end-of-frame readback and sync; run a
     // second time only if the hash guard finds a key to correct.
+    std::chrono::steady_clock::time_point h_sync;
     auto run_from_keys = [&]() {
       neighbor_rest(&r.neighbor_stats);
       mark(E_NB);
@@ -1618,6 +1640,7 @@ struct smcl_engine {
       CK(cudaMemcpyAsync(step_host->cnt, d_counts.p, sizeof(unsigned long long) * 6, cudaMemcpyDeviceToHost, st));
       g_d2h += sizeof(unsigned long long) * 6;
       sync();  // the step's one end-of-frame host synchronisation
+      h_sync = std::chrono::steady_clock::now();
     };
     run_from_keys();
     // step_host->rep[15]: this pass's hash-guard flags, summed over all shards
@@ -1666,20 +1689,15 @@ struct smcl_engine {
     r.posterior_ms = since(E_BAYES, E_END);
     r.total_ms = since(E_START, E_END);
     // per-kernel profile
+    // per-kernel stage times: read from the events on the first
+    // smcl_last_step_profile call (fill_prof_times), not on every step
     prof.predict_ms = r.predict_ms;
-    prof.lsh_keys_ms = since(E_PRED, E_KEYS);
-    prof.sort_ms = since(E_KEYS, E_SORT);
-    prof.reorder_ms = since(E_SORT, E_REORDER);
-    prof.segments_ms = since(E_REORDER, E_SEG);
-    prof.refresh_gather_ms = since(E_SEG, E_RG);
-    prof.nb_stats_ms = since(E_RG, E_NB);
     prof.gn_kernel_ms = t_gn;
     prof.solve_ms = t_solve;
     prof.svgd_ms = t_svgd;
-    prof.ll_kernel_ms = empty ? 0.0 : since(E_LL0, E_LL1);
-    prof.bayes_ms = since(E_LL1, E_SMOOTH);
-    prof.smooth_ms = since(E_SMOOTH, E_END);
     prof.total_ms = r.total_ms;
+    prof_times_pending = true;
+    prof_empty = empty;
     prof.gn_points = empty ? 0 : static_cast<int64_t>(gn_scan.n) * n_total * cfg.n_svgd_iters;
     prof.ll_points = empty ? 0 : static_cast<int64_t>(sl.full.n) * n_total;
     prof.gn_matched = static_cast<int64_t>(cnt[3]);
@@ -1691,6 +1709,12 @@ struct smcl_engine {
     prof.h2d_bytes = sl.upload_bytes;
     *out = r;
     ++frame;
+    if (host_timing) {
+      const auto h2 = std::chrono::steady_clock::now();
+      auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+      std::fprintf(stderr, "[host] enter->predict launched %.1f us, sync return->exit %.1f us\n", us(h0, h1),
+                   us(h_sync, h2));
+    }
   }
 
   void step(const smcl_cloud* scan, const smcl_odom* odo, smcl_frame_result* out) {
@@ -1998,9 +2022,19 @@ int smcl_timer_stop(smcl_engine* h, double* ms) {
   });
 }
 
+int smcl_last_step_counts(smcl_engine* h, smcl_step_profile* out) {
+  return guard([&] {
+    if (!h) throw std::invalid_argument("null engine handle");
+    *out = h->prof;  // stage times not read: only the fields the step itself filled
+    out->hash_guard_flagged = static_cast<int64_t>(h->guard_flagged_total);
+    out->hash_guard_replays = static_cast<int64_t>(h->guard_replays);
+  });
+}
+
 int smcl_last_step_profile(smcl_engine* h, smcl_step_profile* out) {
   return guard([&] {
     if (!h) throw std::invalid_argument("null engine handle");
+    h->fill_prof_times();
     *out = h->prof;
     // engine-lifetime totals, current also after stage-API passes
     out->hash_guard_flagged = static_cast<int64_t>(h->guard_flagged_total);

@@ -4,6 +4,8 @@
 // particle index (so results do not depend on the shard count).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "../engine.cuh"
 #include "../kernels.cuh"
 
@@ -130,7 +132,7 @@ __device__ __forceinline__ void se3_log_rel_fast(const Pose& a, const Pose& b, d
 
 // svgd.cpp:7-34 compute_phi, optionally fused with apply_updates (svgd.cpp:51-62)
 // writing a second pose buffer so every read sees the frozen snapshot.
-template <bool APPLY, int MINB>
+template <bool APPLY, int MINB, bool PF = true>
 __global__ void __launch_bounds__(128, MINB) k_svgd(const Pose* __restrict__ all_poses, const double* __restrict__ all_steps,
                                               int64_t n, int64_t gbase, const int32_t* __restrict__ idx,
                                               const int32_t* __restrict__ count, int k, SvgdParams sp,
@@ -142,16 +144,46 @@ __global__ void __launch_bounds__(128, MINB) k_svgd(const Pose* __restrict__ all
   double numer[6] = {0, 0, 0, 0, 0, 0};
   double denom = 0.0;
   const int cnt = count[i];
+  const int32_t* __restrict__ row = idx + i * k;
+  // PF: neighbour s + 1's pose and step are loaded while neighbour s is
+  // evaluated (the loop is bound by these dependent L2/HBM gathers).
+  int32_t jn = 0;
+  Pose pn;
+  double sn[6];
+  auto fetch = [&](int s) {
+    jn = row[s];
+    pn = ldg_pose(all_poses + jn);
+    const double2* sp2 = reinterpret_cast<const double2*>(all_steps + 6 * static_cast<int64_t>(jn));
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double2 v = __ldg(sp2 + c);
+      sn[2 * c] = v.x;
+      sn[2 * c + 1] = v.y;
+    }
+  };
+  if (PF && cnt > 0) fetch(0);
   for (int s = 0; s < cnt; ++s) {
-    const int32_t j = idx[i * k + s];
-    const double* sj = all_steps + 6 * static_cast<int64_t>(j);
+    int32_t j;
+    Pose pj;
+    double sj[6];
+    if (PF) {
+      j = jn;
+      pj = pn;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) sj[c] = sn[c];
+      if (s + 1 < cnt) fetch(s + 1);
+    } else {
+      j = row[s];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) sj[c] = all_steps[6 * static_cast<int64_t>(j) + c];
+    }
     if (j == gi) {
 #pragma unroll
       for (int c = 0; c < 6; ++c) numer[c] = numer[c] + sj[c];
       denom = denom + 1.0;
       continue;
     }
-    const Pose pj = ldg_pose(all_poses + j);
+    if (!PF) pj = ldg_pose(all_poses + j);
     if (kernel_underflows(pi, pj, sp.sigma_t)) continue;
     double d[6];
     se3_log_rel_fast(pi, pj, d);
@@ -222,14 +254,29 @@ void launch_svgd(const Pose* all_poses, const double* all_steps, int64_t n, int6
                  cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
-  // 7 CTAs x 4 warps per SM (72 registers): measured best on B200 at 1M
-  // (MINB 4 / 5 / 6 / 7 / 8: 0.86 / 0.80 / 0.79 / 0.77 / 0.85 ms).
-  if (poses_out)
-    k_svgd<true, 7><<<blocks_for(n, 128), 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out,
-                                                         poses_out);
-  else
-    k_svgd<false, 7><<<blocks_for(n, 128), 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out,
-                                                          nullptr);
+  // The loop is bound by the dependent neighbour gathers (long-scoreboard
+  // stalls): with the next neighbour's pose and step prefetched, 3 CTAs x 4
+  // warps per SM (160 registers, no spills) measured best on B200 at 1M:
+  // 0.58 ms (prefetch at 4 / 5 / 6 CTAs: 0.66 / 1.19 / 1.47 ms, spilling;
+  // no prefetch at 7 CTAs, 72 registers: 0.78 ms).
+  static const int cfg = [] {  // A/B: SMCL_SVGD_CFG=0 (no prefetch, 7 CTAs) or the CTAs per SM with prefetch
+    const char* e = std::getenv("SMCL_SVGD_CFG");
+    return e ? std::atoi(e) : 3;
+  }();
+  const unsigned g = static_cast<unsigned>(blocks_for(n, 128));
+#define SVGD_LAUNCH(PF, MB)                                                                                      \
+  if (poses_out)                                                                                                 \
+    k_svgd<true, MB, PF><<<g, 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out, poses_out); \
+  else                                                                                                           \
+    k_svgd<false, MB, PF><<<g, 128, 0, st>>>(all_poses, all_steps, n, gbase, idx, count, k, sp, phi_out, nullptr);
+  if (cfg == 0) {
+    SVGD_LAUNCH(false, 7)
+  } else if (cfg == 4) {
+    SVGD_LAUNCH(true, 4)
+  } else {
+    SVGD_LAUNCH(true, 3)
+  }
+#undef SVGD_LAUNCH
 }
 void launch_apply(Pose* poses, const double* phis, int64_t n, cudaStream_t st) {
   count_launch();

@@ -15,6 +15,7 @@ for f in range(24):
     eng.scan_upload(f, wl.scans[f])
 for f in range(3):
     eng.step_slot(f, *wl.odometry[f])
+import os as _os
 for label, with_prof in (("step_slot+profile", True), ("step_slot only", False)):
     eng.timer_start()
     t0 = time.perf_counter()
@@ -31,3 +32,12 @@ t0 = time.perf_counter()
 for _ in range(100):
     eng.last_step_profile()
 print(f"last_step_profile: {(time.perf_counter() - t0) * 1e4:.1f} us")
+# per-call wall time between step_slot entries (host gap = wall - device span)
+t_prev = time.perf_counter()
+gaps = []
+for f in range(3, 13):
+    r = eng.step_slot(f, *wl.odometry[f])
+    t = time.perf_counter()
+    gaps.append((t - t_prev) * 1e3 - r["total_ms"])
+    t_prev = t
+print("wall - span per call (ms):", np.round(gaps[1:], 3))
