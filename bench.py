@@ -241,27 +241,27 @@ def roofline(prof_avg, hbm_peak, peak_kind, ms_kernels, workload="global_init", 
         ms, nbytes = kernels[name]
     achieved = nbytes / (ms * 1e-3) / 1e9
     # DRAM bytes per launch of the same kernel from the committed ncu --set full
-    # capture (profiles/r01_dram_traffic.json); the map records are L2-resident,
+    # capture (profiles/r02_dram_traffic.json); the map records are L2-resident,
     # so DRAM traffic is a small fraction of the algorithmic gather bytes.
     traffic = None
     issue = None
     try:
         if workload != "global_init":  # the committed capture is of the global_init workload
             raise LookupError
-        with open(os.path.join(ROOT, "profiles", "r01_dram_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_dram_traffic.json")) as f:
             t = json.load(f)["kernels"].get(name)
         if t:
             traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
             if "ipc_issued" in t:  # the kernel's actual limiter: instruction issue (4 per SM per cycle)
                 issue = {"kernel": name, "achieved_ipc": t["ipc_issued"], "peak_ipc": 4.0,
                          "frac": t["issue_pct_of_peak"] / 100.0,
-                         "source": "profiles/r01_dram_traffic.json (ncu --set full, sm__inst_issued)"}
+                         "source": "profiles/r02_dram_traffic.json (ncu --set full, sm__inst_issued)"}
     except Exception:
         traffic = None
     return {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_kind,
             "algorithmic_bytes_per_launch": nbytes, "kernel_ms": ms,
-            "traffic_source": "profiles/r01_dram_traffic.json (ncu --set full, bytes per launch)", "issue": issue}
+            "traffic_source": "profiles/r02_dram_traffic.json (ncu --set full, bytes per launch)", "issue": issue}
 
 
 def main():
@@ -326,10 +326,12 @@ def main():
     profs = []
     clocks.mark()
     eng.timer_start()
+    frames = []  # (scan_empty, device span E_START..E_END) per timed frame
     for f in range(args.warmup, args.warmup + args.steps):
         d, c, v = wl.odometry[f]
-        eng.step_slot(f, d, c, v)
+        r = eng.step_slot(f, d, c, v)
         profs.append(eng.last_step_profile(times=False))  # counters only: no event reads between frames
+        frames.append((r["scan_empty"], r["total_ms"]))
     ms_total = eng.timer_stop()
     clk = clocks.stop()
     barrier()
@@ -459,6 +461,10 @@ def main():
         "roofline": roof,
         "roofline_gather": roof_gather,
         "clocks": clk,
+        "frame_ms": {  # device span per frame kind (blackout frames of the kidnap workload skip the likelihood)
+            "full_scan": float(np.mean([t for e, t in frames if not e])) if any(not e for e, _ in frames) else None,
+            "blackout": float(np.mean([t for e, t in frames if e])) if any(e for e, _ in frames) else None,
+            "n_full_scan": sum(1 for e, _ in frames if not e), "n_blackout": sum(1 for e, _ in frames if e)},
         "stage_ms": {k: avg[k] for k in keys},
         "stage_ms_source": "CUDA events per stage: an untimed re-run of the timed frames from the same particle state",
         "mean_n_matched_last": res["mean_n_matched"],

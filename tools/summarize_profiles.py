@@ -46,7 +46,9 @@ def traffic(rep, out, src):
                                     "sm__inst_issued.avg.pct_of_peak_sustained_active")}
     units = rows[1]
     res = {}
-    names = {"k_refresh_gather": "refresh_gather", "k_gicp_fast": "gicp_gn (K1)", "k_gicp_ll": "gicp_ll (K2)"}
+    names = {"k_refresh_gather": "refresh_gather", "k_gicp_fast": "gicp_gn (K1)", "k_gicp_ll": "gicp_ll (K2)",
+             "k_ll_count": "ll_count (K2a)", "k_svgd": "svgd (K8)", "k_smooth_round": "smooth round (K12)",
+             "k_reorder": "reorder (K4)", "k_chunk_serial": "chunk serial sums (K11)"}
     def val(r, m):
         v = float(r[cols[m]].replace(",", ""))
         u = units[cols[m]]
@@ -67,6 +69,12 @@ def traffic(rep, out, src):
     print(json.dumps(res, indent=1))
 
 if __name__ == "__main__":
-    launches("gpurun_out/launches.csv", "profiles/r01_launch_summary.txt")
-    traffic("gpurun_out/prof_final.ncu-rep", "profiles/r01_dram_traffic.json",
-            "ncu --set full --clock-control none, python bench.py --steps 1 --warmup 3 (r01, final)")
+    # summarize_profiles.py <launches.csv> <full.ncu-rep>[,<more.ncu-rep>] <round tag> <command>
+    csv_path, reps, tag, cmd = sys.argv[1], sys.argv[2].split(","), sys.argv[3], sys.argv[4]
+    launches(csv_path, f"profiles/{tag}_launch_summary.txt")
+    merged = {}
+    for rep in reps:
+        traffic(rep, "/tmp/_traffic.json", cmd)
+        merged.update(json.load(open("/tmp/_traffic.json"))["kernels"])
+    json.dump({"source": f"ncu --set full --clock-control none, {cmd} ({tag})", "kernels": merged},
+              open(f"profiles/{tag}_dram_traffic.json", "w"), indent=1)
