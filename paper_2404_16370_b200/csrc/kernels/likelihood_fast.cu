@@ -985,10 +985,15 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
     // per SM: 2.79 ms at 1M x 512 (cp.async 8 x 8: 3.43; LDG 2 x 8: 2.91;
     // 4 x 8: 3.23; 1 x 8 at 5 / 6 CTAs spills: 3.33 / 3.42).
     if (c == 9000) {  // 3 CTAs per SM when 4 do not fit next to the scan (S > ~1000)
-      // the gated pass (x.list) needs the list indirection's registers: 3 CTAs (80 registers)
+      // The gated pass (x.list) needs the list indirection's registers: 3 CTAs
+      // (80 registers) with two records in flight per lane (LL 2.20 -> 2.02 ms
+      // at 1M x 512; one record: 2.20, three / four spill: 2.30 / 2.48, two at
+      // 2 CTAs / 104 registers: 2.17).
       static const bool minb3 = std::getenv("SMCL_LL_MINB3") != nullptr;
       if (!minb3 && !x.list && 4 * ll_lanes_smem<1, 8, true>(scan.n) <= 227 * 1024)
         launch_ll_lanes_t<1, 8, true, 4>(poses, n, scan, map, raw_ll, nm, x, st);
+      else if (x.list)
+        launch_ll_lanes_t<2, 8, true, 3>(poses, n, scan, map, raw_ll, nm, x, st);
       else
         launch_ll_lanes_t<1, 8, true, 3>(poses, n, scan, map, raw_ll, nm, x, st);
       return;
@@ -1006,8 +1011,12 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
     LL_CASE(2, 16)
     LL_CASE(3, 8)
 #undef LL_CASE
-    if (!gn && (u == 2 || u == 1) && w >= 80) {  // SMCL_FAST_CFG_LL=L2x84 / L1x84: 8 warps, >= 4 CTAs per SM
+    if (!gn && u >= 1 && u <= 4 && w >= 80) {  // SMCL_FAST_CFG_LL=L2x84 / L1x84: 8 warps, >= 4 CTAs per SM
       const int mb = w - 80;
+      if (u == 2 && mb == 3) return launch_ll_lanes_t<2, 8, true, 3>(poses, n, scan, map, raw_ll, nm, x, st);
+      if (u == 3 && mb == 3) return launch_ll_lanes_t<3, 8, true, 3>(poses, n, scan, map, raw_ll, nm, x, st);
+      if (u == 4 && mb == 3) return launch_ll_lanes_t<4, 8, true, 3>(poses, n, scan, map, raw_ll, nm, x, st);
+      if (u == 2 && mb == 2) return launch_ll_lanes_t<2, 8, true, 2>(poses, n, scan, map, raw_ll, nm, x, st);
       if (u == 2 && mb == 4) return launch_ll_lanes_t<2, 8, true, 4>(poses, n, scan, map, raw_ll, nm, x, st);
       if (u == 2 && mb == 5) return launch_ll_lanes_t<2, 8, true, 5>(poses, n, scan, map, raw_ll, nm, x, st);
       if (u == 1 && mb == 2) return launch_ll_lanes_t<1, 8, true, 2>(poses, n, scan, map, raw_ll, nm, x, st);
