@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       // ---- phase A: fp64 cell + exact fraction, predicated async gather
       double Rv[9], tv[3];
       float4 rm0[kLdg ? kFastUnroll : 1], rm1[kLdg ? kFastUnroll : 1];  // kLdg: records in flight
+      unsigned sflags = 0;  // per point slot u: bit 2u staged, bit 2u+1 resolve (compaction reads no meta back)
 #pragma unroll
       for (int q = 0; q < 9; ++q) Rv[q] = ws.pose_v[q];
 #pragma unroll
@@ -434,6 +435,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
         const uint32_t meta = static_cast<uint32_t>(k) | (stage ? kMetaStage : 0u) | (resolve ? kMetaResolve : 0u);
         ws.fq[slot] = make_float4(fr[0], fr[1], fr[2], __uint_as_float(meta));
+        sflags |= (stage ? 1u : 0u) << (2 * u);
+        sflags |= (resolve ? 2u : 0u) << (2 * u);
       }
       if (kLdg) {
 #pragma unroll
@@ -450,9 +453,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 #pragma unroll
       for (int u = 0; u < kFastUnroll; ++u) {
         const int slot = u * 32 + lane;
-        const uint32_t meta = __float_as_uint(ws.fq[slot].w);
-        const float mw = ws.m0[slot].w;  // unstaged slots were zero-filled: the meta bit decides
-        const bool keep = ((meta & kMetaResolve) != 0u) | (((meta & kMetaStage) != 0u) & (mw >= 0.f));
+        const bool staged = (sflags >> (2 * u)) & 1u, resolving = (sflags >> (2 * u + 1)) & 1u;
+        // the record's occupancy is read only where one was staged (strided 4-byte reads conflict 4 ways)
+        const bool keep = resolving || (staged && ws.m0[slot].w >= 0.f);
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
         if (keep) ws.q[n_cand + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(slot);
         n_cand += __popc(mask);
@@ -475,7 +478,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         }
         if (e < n_run) {
           const int slot = e < n_carry ? kStep + e : ws.q[e - n_carry];
-          const float4 fq = ws.fq[slot];
+          const float4 fq = lds_f4_volatile(reinterpret_cast<const float*>(&ws.fq[slot]));  // one 128-bit read (meta included)
           const uint32_t meta = __float_as_uint(fq.w);
           const int k = static_cast<int>(meta & 0xFFFFu);
           float fr[3] = {fq.x, fq.y, fq.z};
