@@ -376,6 +376,7 @@ def main():
     # 2-stage pipeline: frame f+1's make_scan_cloud runs on the preparation
     # stream while frame f steps on the engine stream (slots alternate).
     raw_frames = list(range(args.warmup + args.steps, args.warmup + 2 * args.steps))
+    raw_scan_pts = []  # points per frame after make_scan_cloud (the headline scans have S)
     t0 = time.perf_counter()
     eng.scan_prepare_async(62, wl.raw[raw_frames[0]])
     for i, f in enumerate(raw_frames):
@@ -385,6 +386,7 @@ def main():
         res_raw = eng.step_slot(62 + i % 2, d, c, v)
         p = eng.last_step_profile(times=False)
         pp_raw += p["gn_points"] + p["ll_points"]
+        raw_scan_pts.append(p["ll_points"] / args.particles)
         h2d_raw += wl.raw[f].nbytes + 12 * 8 + 36 * 8 + 4
         assert math.isfinite(res_raw["rep_log_post"])
     raw_ms = 1e3 * (time.perf_counter() - t0) / args.steps
@@ -453,6 +455,7 @@ def main():
                 "d2h_bytes_per_step": int(d2h / args.steps), "ms_per_step": e2e_ms},
         "e2e_raw_points": {"value": pp_raw_step / (raw_ms * 1e-3), "unit": UNIT, "ms_per_step": raw_ms,
                            "pp_per_step": pp_raw_step, "h2d_bytes_per_step": int(h2d_raw / args.steps),
+                           "scan_points_mean": float(np.mean(raw_scan_pts)),
                            "what": f"{len(wl.raw[f0])} raw sensor points/frame -> device make_scan_cloud "
                                    f"(n_scan_max={S}) on the preparation stream, pipelined one frame ahead "
                                    f"of the step (smcl_scan_prepare_async + smcl_step_slot)"},

@@ -732,7 +732,7 @@ __device__ __forceinline__ bool occupied(const MapFast& m, uint32_t r) {
 //   reference's cell. Per particle the margin uses max|Rv| |mu|_1 <= |mu|_1max / res.
 // ~1 point in 1000 takes the fp64 path (corridor map, 0.1 m voxels).
 template <int kBrick>
-__global__ void __launch_bounds__(256, 3) k_ll_count(const Pose* __restrict__ poses, int64_t n, ScanView scan,
+__global__ void __launch_bounds__(256, 4) k_ll_count(const Pose* __restrict__ poses, int64_t n, ScanView scan,
                                                      MapFast map, int min_matched, int32_t* __restrict__ nm_out,
                                                      int32_t* __restrict__ live, unsigned* __restrict__ live_count) {
   constexpr int U = 4;  // points in flight per lane
@@ -751,22 +751,31 @@ __global__ void __launch_bounds__(256, 3) k_ll_count(const Pose* __restrict__ po
   const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
                  dz = static_cast<unsigned>(g.dims[2]);
   float Rv[9], tv[3];
+  int coff[3];  // per-axis cell offset: the particle's own cell coordinate, minus the magic's bits
   float margin;
   {  // the pose itself is not kept: the resolve path reloads it
     const Pose P = poses[active ? i : 0];
     double tmax = 0.0;
+    bool fin = true;
 #pragma unroll
     for (int q = 0; q < 9; ++q) Rv[q] = static_cast<float>(P.R[q] * g.inv_res);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const double t = (P.t[a] - g.origin[a]) * g.inv_res;
-      tv[a] = static_cast<float>(t - 0.5);  // x - 1/2: its nearest integer is floor(x) away from faces
-      tmax = fmax(tmax, fabs(t) + 0.5);
+      // x - 1/2 (its nearest integer is floor(x) away from faces), centred on
+      // the integer c = rint((t - o)/res - 1/2): |tv| <= 1/2, so the fp32
+      // rounding of the translation term is ~800x smaller than uncentred
+      // (corridor map) and fewer points fall inside the margin.
+      const double t = (P.t[a] - g.origin[a]) * g.inv_res - 0.5;
+      const double c = rint(t);
+      fin = fin && fabs(c) < 1.0e9;
+      tv[a] = static_cast<float>(t - c);
+      coff[a] = (fin ? static_cast<int>(c) : 0) - 0x4B400000;
+      tmax = fmax(tmax, fabs(t - c));
     }
-    // u (5 |mu|_1max / res + 4 |tv|) + 2.2e-8, x1.25 for the fp64 set-up roundings; |x| < 2^21 for the
-    // round-down floor below, else every point takes the fp64 path.
+    // u (5 |mu|_1max / res + 4 |tv|) + 2.2e-8, x1.25 for the fp64 set-up roundings; |x - c| < 2^21 for the
+    // round-to-nearest split below, else (and for non-finite poses) every point takes the fp64 path.
     const double e = 0x1p-24 * (5.0 * scan.mu_l1_max * g.inv_res + 4.0 * tmax) * 1.25 + 2.5e-8;
-    margin = (e < 0.01 && tmax + scan.mu_l1_max * g.inv_res < 2097152.0) ? static_cast<float>(e) : 2.0f;
+    margin = (fin && e < 0.01 && tmax + scan.mu_l1_max * g.inv_res < 2097152.0) ? static_cast<float>(e) : 2.0f;
   }
   // 1.5 * 2^23: a round-to-nearest add of x - 1/2 leaves round(x - 1/2) =
   // floor(x) in the low mantissa bits (|x| < 2^21); g = (x - 1/2) - floor(x)
@@ -789,7 +798,7 @@ __global__ void __launch_bounds__(256, 3) k_ll_count(const Pose* __restrict__ po
         const float x = fmaf(Rv[ax * 3 + 2], m.z, fmaf(Rv[ax * 3 + 1], m.y, fmaf(Rv[ax * 3 + 0], m.x, tv[ax])));
         const float y = __fadd_rn(x, kMagic32);
         const float gc = x - (y - kMagic32);
-        ic[ax] = static_cast<unsigned>(__float_as_int(y) - 0x4B400000);
+        ic[ax] = __float_as_uint(y) + static_cast<unsigned>(coff[ax]);
         gabs = fmax_nan(gabs, fabsf(gc));
       }
       const bool safe = gabs <= gmax;  // NaN (padded points, non-finite poses) fails
