@@ -208,3 +208,24 @@ def test_step_exact_mode_other_list_sizes(world, k):
     assert np.array_equal(pg.kval, pr.kval)
     assert np.abs(pg.poses - pr.poses).max() < 1e-9
     assert np.abs(pg.log_post - pr.log_post).max() < 1e-9
+
+
+def test_step_profile_counters_and_lazy_stage_times(world):
+    """smcl_last_step_counts returns the step's counters without reading the
+    per-kernel stage times; smcl_last_step_profile reads them from the step's
+    events on demand (the same counters, stage times filled in)."""
+    cfg = make_config(n_particles=2000, seed=3, nnf_resolution=0.2, likelihood_mode=2)
+    eng, frames = run_frames(world, cfg, 3)
+    c = eng.last_step_profile(times=False)
+    p = eng.last_step_profile()
+    S = c["ll_points"] // cfg.n_particles
+    assert S > 0 and c["gn_points"] == S * cfg.n_particles * cfg.n_svgd_iters
+    for k in ("gn_points", "ll_points", "gn_matched", "ll_matched", "kernel_launches", "fast_path"):
+        assert c[k] == p[k]
+    assert c["lsh_keys_ms"] == 0.0 and c["smooth_ms"] == 0.0  # not read
+    assert p["lsh_keys_ms"] > 0.0 and p["smooth_ms"] > 0.0 and p["refresh_gather_ms"] > 0.0
+    stages = sum(p[k] for k in ("predict_ms", "lsh_keys_ms", "sort_ms", "reorder_ms", "segments_ms",
+                                "refresh_gather_ms", "nb_stats_ms", "gn_kernel_ms", "solve_ms", "svgd_ms",
+                                "ll_kernel_ms", "bayes_ms", "smooth_ms"))
+    assert abs(stages - p["total_ms"]) <= 0.05 * p["total_ms"] + 0.05
+    assert abs(frames[-1]["total_ms"] - p["total_ms"]) < 1e-6
