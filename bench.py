@@ -469,6 +469,9 @@ def main():
             "blackout": float(np.mean([t for e, t in frames if e])) if any(e for e, _ in frames) else None,
             "n_full_scan": sum(1 for e, _ in frames if not e), "n_blackout": sum(1 for e, _ in frames if e)},
         "stage_ms": {k: avg[k] for k in keys},
+        "hash_guard": {"flagged": int(stage_profs[-1]["hash_guard_flagged"]),
+                       "replays": int(stage_profs[-1]["hash_guard_replays"]),
+                       "what": "engine-lifetime LSH near-integer flags checked on the host / neighbour passes replayed"},
         "stage_ms_source": "CUDA events per stage: an untimed re-run of the timed frames from the same particle state",
         "mean_n_matched_last": res["mean_n_matched"],
     }

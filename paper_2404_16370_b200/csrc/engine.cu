@@ -1128,32 +1128,66 @@ struct smcl_engine {
       CK(cudaMemcpyAsync(kval2.p, kval.p, sizeof(float) * nl * kk, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(count2.p, count.p, sizeof(int32_t) * nl, cudaMemcpyDeviceToDevice, st));
     }
-    lsh_flagged.ensure(1);
+    lsh_flagged.ensure(1 + kGuardListCap);
     launch_lsh_keys(poses.p, n_local, gbase, last_lp, keys.p, lsh_flagged.p, st);
   }
 
   // After a sync: flagged = this pass's flag count summed over all shards.
   // Rehashes on the host; patches keys.p and returns true when any shard
   // must replay.
+  DBuf<Pose> guard_pose;
+  DBuf<uint64_t> guard_key;
   bool guard_mismatch(unsigned long long flagged) {
     if (flagged == 0) return false;
     guard_flagged_total += flagged;
-    const size_t nl = static_cast<size_t>(n_local);
-    std::vector<Pose> hp(nl);
-    std::vector<uint64_t> hk(nl);
-    CK(cudaMemcpyAsync(hp.data(), ckpt_poses, sizeof(Pose) * nl, cudaMemcpyDeviceToHost, st));
-    keys.download(hk.data(), nl, st);
+    // This shard's flags: only those particles can hash differently on the
+    // host, so only they are gathered and rehashed (a whole-shard download
+    // and rehash cost ~50 ms at 1M particles).
+    unsigned nloc = 0;
+    CK(cudaMemcpyAsync(&nloc, lsh_flagged.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
     sync();
     int mism = 0;
-#pragma omp parallel for schedule(static) reduction(| : mism)
-    for (int64_t i = 0; i < n_local; ++i) {
-      const uint64_t kh = lsh_key_host(hp[static_cast<size_t>(i)], static_cast<uint64_t>(gbase + i), last_lp);
-      if (kh != hk[static_cast<size_t>(i)]) {
-        hk[static_cast<size_t>(i)] = kh;
-        mism = 1;
+    if (nloc > 0 && nloc <= static_cast<unsigned>(kGuardListCap)) {
+      const int m = static_cast<int>(nloc);
+      guard_pose.ensure(static_cast<size_t>(m));
+      guard_key.ensure(static_cast<size_t>(m));
+      launch_gather_flagged(ckpt_poses, keys.p, lsh_flagged.p + 1, m, guard_pose.p, guard_key.p, st);
+      std::vector<unsigned> li(static_cast<size_t>(m));
+      std::vector<Pose> hp(static_cast<size_t>(m));
+      std::vector<uint64_t> hk(static_cast<size_t>(m));
+      CK(cudaMemcpyAsync(li.data(), lsh_flagged.p + 1, sizeof(unsigned) * m, cudaMemcpyDeviceToHost, st));
+      guard_pose.download(hp.data(), static_cast<size_t>(m), st);
+      guard_key.download(hk.data(), static_cast<size_t>(m), st);
+      sync();
+      for (int q = 0; q < m; ++q) {
+        const uint64_t kh = lsh_key_host(hp[static_cast<size_t>(q)], static_cast<uint64_t>(gbase + li[static_cast<size_t>(q)]),
+                                         last_lp);
+        if (kh != hk[static_cast<size_t>(q)]) {
+          hk[static_cast<size_t>(q)] = kh;
+          mism = 1;
+        }
       }
+      if (mism) {
+        guard_key.upload(hk.data(), static_cast<size_t>(m), st);
+        launch_scatter_keys(keys.p, lsh_flagged.p + 1, m, guard_key.p, st);
+      }
+    } else if (nloc > 0) {  // more flags than the list holds: rehash the whole shard
+      const size_t nl = static_cast<size_t>(n_local);
+      std::vector<Pose> hp(nl);
+      std::vector<uint64_t> hk(nl);
+      CK(cudaMemcpyAsync(hp.data(), ckpt_poses, sizeof(Pose) * nl, cudaMemcpyDeviceToHost, st));
+      keys.download(hk.data(), nl, st);
+      sync();
+#pragma omp parallel for schedule(static) reduction(| : mism)
+      for (int64_t i = 0; i < n_local; ++i) {
+        const uint64_t kh = lsh_key_host(hp[static_cast<size_t>(i)], static_cast<uint64_t>(gbase + i), last_lp);
+        if (kh != hk[static_cast<size_t>(i)]) {
+          hk[static_cast<size_t>(i)] = kh;
+          mism = 1;
+        }
+      }
+      if (mism) keys.upload(hk.data(), nl, st);
     }
-    if (mism) keys.upload(hk.data(), nl, st);
     if (sharded) {  // every shard replays if any shard must
       guard_flag_dev.ensure(1);
       guard_flag_all.ensure(static_cast<size_t>(world));

@@ -56,6 +56,12 @@ void launch_kernel_batch(const Pose* a, const Pose* b, int64_t n, double sr, dou
 // lsh.cu
 // K3. flagged (may be null): count of particles whose hash the host must
 // verify with glibc (lsh.cu near-integer guard).
+// LSH near-integer guard: K3 appends up to kGuardListCap flagged local
+// indices after the count (flagged[0]); the host checks only those.
+constexpr int kGuardListCap = 4096;
+void launch_gather_flagged(const Pose* poses, const uint64_t* keys, const unsigned* list, int m, Pose* out_pose,
+                           uint64_t* out_key, cudaStream_t st);
+void launch_scatter_keys(uint64_t* keys, const unsigned* list, int m, const uint64_t* vals, cudaStream_t st);
 void launch_lsh_keys(const Pose* poses, int64_t n, int64_t gbase, const LshPass& lp, uint64_t* keys,
                      unsigned* flagged, cudaStream_t st);
 // out: raw hashes (no modulo); amb[i] = 1 where the host must rehash (lsh_hash_host).

@@ -183,31 +183,43 @@ __global__ void __launch_bounds__(128) k_gicp_exact(const Pose* __restrict__ pos
 
 // ---------------------------------------------------------------- solve
 // Eigen LLT (lower, unblocked) + two triangular solves, oracle order.
-__device__ bool llt6_solve(const double* A, const double* b, double* x) {
-  double L[36];
+// Packed lower triangle of a symmetric 6x6: element (i, j), j <= i.
+__host__ __device__ constexpr int lp6(int i, int j) { return i * (i + 1) / 2 + j; }
+
+// LLT solve on the packed lower triangle, the oracle's operation order
+// (every entry it reads is on or below the diagonal). Register-resident:
+// fully unrolled, constant indices. kRcp (the fast path's fp32-accumulated
+// systems only): one IEEE reciprocal per pivot, reused by the column and both
+// substitutions, instead of 27 IEEE divisions (the solve's cost; results
+// differ from the divisions by ~1 ulp, far below the fast path's tolerance).
+template <bool kRcp = false>
+__device__ __forceinline__ bool llt6_solve_lower(const double (&A)[21], const double (&b)[6], double (&x)[6]) {
+  double rinv[6];
+  double L[21];
 #pragma unroll
-  for (int q = 0; q < 36; ++q) L[q] = A[q];
+  for (int q = 0; q < 21; ++q) L[q] = A[q];
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
-    double xk = L[k * 6 + k];
+    double xk = L[lp6(k, k)];
     if (k > 0) {
       double sq = 0.0;
 #pragma unroll
-      for (int j = 0; j < k; ++j) sq = xadd(sq, xmul(L[k * 6 + j], L[k * 6 + j]));
+      for (int j = 0; j < k; ++j) sq = xadd(sq, xmul(L[lp6(k, j)], L[lp6(k, j)]));
       xk = xsub(xk, sq);
     }
     if (xk <= 0.0) return false;
     xk = sqrt(xk);
-    L[k * 6 + k] = xk;
+    L[lp6(k, k)] = xk;
+    if (kRcp) rinv[k] = 1.0 / xk;
 #pragma unroll
     for (int i = k + 1; i < 6; ++i) {
       if (k > 0) {
         double s = 0.0;
 #pragma unroll
-        for (int j = 0; j < k; ++j) s = xadd(s, xmul(L[i * 6 + j], L[k * 6 + j]));
-        L[i * 6 + k] = xsub(L[i * 6 + k], s);
+        for (int j = 0; j < k; ++j) s = xadd(s, xmul(L[lp6(i, j)], L[lp6(k, j)]));
+        L[lp6(i, k)] = xsub(L[lp6(i, k)], s);
       }
-      L[i * 6 + k] = L[i * 6 + k] / xk;
+      L[lp6(i, k)] = kRcp ? L[lp6(i, k)] * rinv[k] : L[lp6(i, k)] / xk;
     }
   }
   double y[6];
@@ -215,22 +227,23 @@ __device__ bool llt6_solve(const double* A, const double* b, double* x) {
   for (int i = 0; i < 6; ++i) {
     double s = 0.0;
 #pragma unroll
-    for (int j = 0; j < i; ++j) s = xadd(s, xmul(L[i * 6 + j], y[j]));
-    y[i] = xsub(b[i], s) / L[i * 6 + i];
+    for (int j = 0; j < i; ++j) s = xadd(s, xmul(L[lp6(i, j)], y[j]));
+    y[i] = kRcp ? xsub(b[i], s) * rinv[i] : xsub(b[i], s) / L[lp6(i, i)];
   }
 #pragma unroll
   for (int i = 5; i >= 0; --i) {
     double s = 0.0;
 #pragma unroll
-    for (int j = i + 1; j < 6; ++j) s = xadd(s, xmul(L[j * 6 + i], x[j]));
-    x[i] = xsub(y[i], s) / L[i * 6 + i];
+    for (int j = i + 1; j < 6; ++j) s = xadd(s, xmul(L[lp6(j, i)], x[j]));
+    x[i] = kRcp ? xsub(y[i], s) * rinv[i] : xsub(y[i], s) / L[lp6(i, i)];
   }
   return true;
 }
 
-// gicp.cpp:47-75
-__device__ void solve_step_dev(const double* H, const double* b, double lambda, double omax, double vmax,
-                               double* step) {
+// gicp.cpp:47-75 on the packed lower triangle of H.
+template <bool kRcp = false>
+__device__ __forceinline__ void solve_step_lower(const double (&H)[21], const double (&b)[6], double lambda,
+                                                 double omax, double vmax, double (&step)[6]) {
 #pragma unroll
   for (int c = 0; c < 6; ++c) step[c] = 0.0;
   bool zero = true;
@@ -239,13 +252,14 @@ __device__ void solve_step_dev(const double* H, const double* b, double lambda, 
   if (zero) return;
   double lm = lambda;
   bool solved = false;
+#pragma unroll 1
   for (int attempt = 0; attempt < 4; ++attempt) {
-    double D[36], x[6];
+    double D[21], x[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i)
 #pragma unroll
-      for (int j = 0; j < 6; ++j) D[i * 6 + j] = (i == j) ? xadd(H[i * 6 + j], lm) : xadd(H[i * 6 + j], 0.0);
-    if (llt6_solve(D, b, x)) {
+      for (int j = 0; j <= i; ++j) D[lp6(i, j)] = (i == j) ? xadd(H[lp6(i, j)], lm) : xadd(H[lp6(i, j)], 0.0);
+    if (llt6_solve_lower<kRcp>(D, b, x)) {
       bool finite = true;
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
@@ -273,6 +287,21 @@ __device__ void solve_step_dev(const double* H, const double* b, double lambda, 
   }
 }
 
+// Full row-major H (the batch primitive of the parity tests): its lower triangle.
+__device__ __forceinline__ void solve_step_dev(const double* H, const double* b, double lambda, double omax,
+                                               double vmax, double* step) {
+  double Hl[21], bb[6], st[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) Hl[lp6(i, j)] = H[i * 6 + j];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) bb[c] = b[c];
+  solve_step_lower(Hl, bb, lambda, omax, vmax, st);
+#pragma unroll
+  for (int c = 0; c < 6; ++c) step[c] = st[c];
+}
+
 __device__ __forceinline__ double gated(const GicpParamsDev& p, double raw, int nm) {
   if (nm < p.min_matched) return -1e30;
   return xsub(raw, xmul(p.miss_cost, xsub(static_cast<double>(p.scan_size), static_cast<double>(nm))));
@@ -291,11 +320,9 @@ __global__ void k_solve(const double* __restrict__ sys, const float* __restrict_
   ll[i] = gated(p, raw_ll[i], m);
   double step[6] = {0, 0, 0, 0, 0, 0};
   if (m != 0) {
-    double Hb[42];  // H row-major, b
+    double Hl[21], bb[6];  // packed lower triangle of H, b
     if (F32) {
-      constexpr int off[27] = SMCL_FAST_SYS_OFF;
-#pragma unroll
-      for (int q = 0; q < 42; ++q) Hb[q] = 0.0;
+      constexpr int off[27] = SMCL_FAST_SYS_OFF;  // row-major H (lower) then b, in record order
       const float4* r = reinterpret_cast<const float4*>(sysf + i * kSysF);
       float v[28];
 #pragma unroll
@@ -304,17 +331,26 @@ __global__ void k_solve(const double* __restrict__ sys, const float* __restrict_
         v[4 * q] = a.x, v[4 * q + 1] = a.y, v[4 * q + 2] = a.z, v[4 * q + 3] = a.w;
       }
 #pragma unroll
-      for (int q = 0; q < 27; ++q) Hb[off[q]] = static_cast<double>(v[q]);
+      for (int q = 0; q < 27; ++q) {
+        if (off[q] < 36)
+          Hl[lp6(off[q] / 6, off[q] % 6)] = static_cast<double>(v[q]);
+        else
+          bb[off[q] - 36] = static_cast<double>(v[q]);
+      }
     } else {
       const double* s = sys + i * kSysStride;
 #pragma unroll
-      for (int q = 0; q < 42; ++q) Hb[q] = s[q];
+      for (int r = 0; r < 6; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) Hl[lp6(r, c)] = s[r * 6 + c];
+#pragma unroll
+      for (int c = 0; c < 6; ++c) bb[c] = s[36 + c];
     }
     double tr = 0.0;
 #pragma unroll
-    for (int q = 0; q < 6; ++q) tr = xadd(tr, Hb[q * 7]);
+    for (int q = 0; q < 6; ++q) tr = xadd(tr, Hl[lp6(q, q)]);
     const double lambda = xmul(p.damping_scale, tr) / 6.0;
-    solve_step_dev(Hb, Hb + 36, lambda, p.omega_max, p.v_max, step);
+    solve_step_lower(Hl, bb, lambda, p.omega_max, p.v_max, step);
   }
 #pragma unroll
   for (int q = 0; q < 6; ++q) steps[6 * i + q] = step[q];

@@ -93,7 +93,25 @@ __global__ void k_lsh_keys(const Pose* __restrict__ poses, int64_t n, int64_t gb
                      static_cast<uint64_t>(lp.n_buckets);
   const uint64_t prio = lp.prio_bits > 0 ? mix_seed(lp.prio_seed, gi) >> (64 - lp.prio_bits) : 0;
   keys[i] = (h << (lp.prio_bits + lp.idx_bits)) | (prio << lp.idx_bits) | gi;
-  if (amb && flagged) atomicAdd(flagged, 1u);
+  if (amb && flagged) {  // flagged[0] = count, flagged[1 ..] = the first kGuardListCap local indices
+    const unsigned s = atomicAdd(flagged, 1u);
+    if (s < static_cast<unsigned>(kGuardListCap)) flagged[1 + s] = static_cast<unsigned>(i);
+  }
+}
+
+// The flagged particles' poses and keys, gathered for the host check.
+__global__ void k_gather_flagged(const Pose* __restrict__ poses, const uint64_t* __restrict__ keys,
+                                 const unsigned* __restrict__ list, int m, Pose* __restrict__ out_pose,
+                                 uint64_t* __restrict__ out_key) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= m) return;
+  out_pose[q] = poses[list[q]];
+  out_key[q] = keys[list[q]];
+}
+__global__ void k_scatter_keys(uint64_t* __restrict__ keys, const unsigned* __restrict__ list, int m,
+                               const uint64_t* __restrict__ vals) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < m) keys[list[q]] = vals[q];
 }
 
 __global__ void k_hash_batch(const Pose* __restrict__ poses, int64_t n, LshPass lp, uint64_t* __restrict__ out,
@@ -822,6 +840,15 @@ void launch_lsh_keys(const Pose* poses, int64_t n, int64_t gbase, const LshPass&
   count_launch();
   if (flagged) cudaMemsetAsync(flagged, 0, sizeof(unsigned), st);
   if (n > 0) k_lsh_keys<<<blocks_for(n, 128), 128, 0, st>>>(poses, n, gbase, lp, keys, flagged);
+}
+void launch_gather_flagged(const Pose* poses, const uint64_t* keys, const unsigned* list, int m, Pose* out_pose,
+                           uint64_t* out_key, cudaStream_t st) {
+  count_launch();
+  if (m > 0) k_gather_flagged<<<(m + 127) / 128, 128, 0, st>>>(poses, keys, list, m, out_pose, out_key);
+}
+void launch_scatter_keys(uint64_t* keys, const unsigned* list, int m, const uint64_t* vals, cudaStream_t st) {
+  count_launch();
+  if (m > 0) k_scatter_keys<<<(m + 127) / 128, 128, 0, st>>>(keys, list, m, vals);
 }
 void launch_hash_batch(const Pose* poses, int64_t n, const LshPass& lp, uint64_t* out, unsigned char* amb,
                        cudaStream_t st) {

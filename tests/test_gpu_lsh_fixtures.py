@@ -141,15 +141,18 @@ def test_near_integer_zeta_hashes_bitwise():
     assert np.array_equal(got, want)
 
 
-def test_near_integer_zeta_neighbour_pass_bitwise():
-    """The product path: K3 keys (guarded, host rehash) -> sort -> lists."""
+@pytest.mark.parametrize("n", [512, 4096, 6000])
+def test_near_integer_zeta_neighbour_pass_bitwise(n):
+    """The product path: K3 keys (guarded, host rehash) -> sort -> lists.
+    Up to kGuardListCap (4096) flags the host rehashes only the flagged
+    particles; beyond, the whole shard."""
     cfg = make_config()
     bounds = [-10.0] * 3 + [10.0] * 3
     seed = O.mix_seed(91, 0)
     rng = O.SplitMix64(seed)  # the pass frame and noise, drawn as update_neighbors draws them
     frame = rng.random_lsh_frame(bounds)
     noise = cfg.lsh_noise_sigma * rng.normal6()
-    s = Particles.from_poses(near_integer_poses(4096, frame, noise, 2, spread=3), 20)
+    s = Particles.from_poses(near_integer_poses(n, frame, noise, 2, spread=3), 20)
     e = FilterEngine(dummy_map(), cfg)
     e.set_particles(s)
     e.update_neighbors(seed, bounds)
