@@ -188,13 +188,10 @@ __host__ __device__ constexpr int lp6(int i, int j) { return i * (i + 1) / 2 + j
 
 // LLT solve on the packed lower triangle, the oracle's operation order
 // (every entry it reads is on or below the diagonal). Register-resident:
-// fully unrolled, constant indices. kRcp (the fast path's fp32-accumulated
-// systems only): one IEEE reciprocal per pivot, reused by the column and both
-// substitutions, instead of 27 IEEE divisions (the solve's cost; results
-// differ from the divisions by ~1 ulp, far below the fast path's tolerance).
-template <bool kRcp = false>
+// fully unrolled, constant indices. (Pivot reciprocals instead of the 27
+// IEEE divisions would save ~25 us per step but break the bitwise equality
+// with the oracle's solve that the parity tests pin.)
 __device__ __forceinline__ bool llt6_solve_lower(const double (&A)[21], const double (&b)[6], double (&x)[6]) {
-  double rinv[6];
   double L[21];
 #pragma unroll
   for (int q = 0; q < 21; ++q) L[q] = A[q];
@@ -210,7 +207,6 @@ __device__ __forceinline__ bool llt6_solve_lower(const double (&A)[21], const do
     if (xk <= 0.0) return false;
     xk = sqrt(xk);
     L[lp6(k, k)] = xk;
-    if (kRcp) rinv[k] = 1.0 / xk;
 #pragma unroll
     for (int i = k + 1; i < 6; ++i) {
       if (k > 0) {
@@ -219,7 +215,7 @@ __device__ __forceinline__ bool llt6_solve_lower(const double (&A)[21], const do
         for (int j = 0; j < k; ++j) s = xadd(s, xmul(L[lp6(i, j)], L[lp6(k, j)]));
         L[lp6(i, k)] = xsub(L[lp6(i, k)], s);
       }
-      L[lp6(i, k)] = kRcp ? L[lp6(i, k)] * rinv[k] : L[lp6(i, k)] / xk;
+      L[lp6(i, k)] = L[lp6(i, k)] / xk;
     }
   }
   double y[6];
@@ -228,20 +224,19 @@ __device__ __forceinline__ bool llt6_solve_lower(const double (&A)[21], const do
     double s = 0.0;
 #pragma unroll
     for (int j = 0; j < i; ++j) s = xadd(s, xmul(L[lp6(i, j)], y[j]));
-    y[i] = kRcp ? xsub(b[i], s) * rinv[i] : xsub(b[i], s) / L[lp6(i, i)];
+    y[i] = xsub(b[i], s) / L[lp6(i, i)];
   }
 #pragma unroll
   for (int i = 5; i >= 0; --i) {
     double s = 0.0;
 #pragma unroll
     for (int j = i + 1; j < 6; ++j) s = xadd(s, xmul(L[lp6(j, i)], x[j]));
-    x[i] = kRcp ? xsub(y[i], s) * rinv[i] : xsub(y[i], s) / L[lp6(i, i)];
+    x[i] = xsub(y[i], s) / L[lp6(i, i)];
   }
   return true;
 }
 
 // gicp.cpp:47-75 on the packed lower triangle of H.
-template <bool kRcp = false>
 __device__ __forceinline__ void solve_step_lower(const double (&H)[21], const double (&b)[6], double lambda,
                                                  double omax, double vmax, double (&step)[6]) {
 #pragma unroll
@@ -259,7 +254,7 @@ __device__ __forceinline__ void solve_step_lower(const double (&H)[21], const do
     for (int i = 0; i < 6; ++i)
 #pragma unroll
       for (int j = 0; j <= i; ++j) D[lp6(i, j)] = (i == j) ? xadd(H[lp6(i, j)], lm) : xadd(H[lp6(i, j)], 0.0);
-    if (llt6_solve_lower<kRcp>(D, b, x)) {
+    if (llt6_solve_lower(D, b, x)) {
       bool finite = true;
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
