@@ -578,12 +578,16 @@ __global__ void k_pose_mirror(const Pose* __restrict__ poses, int64_t n, double3
 // lane replays its offers in window order.
 constexpr int kRgChunk = 16;
 
+
 // SMCL_RG_STATS=1 (diagnostics only): window members considered, survivors
 // of the filter (exact evaluations), insertions, refresh evaluations.
 __device__ unsigned long long g_rg_stats[4];
 
+// 8 CTAs x 2 warps per SM: 128 registers without spills (a window-evaluation
+// pose prefetch measured slower: 184 registers 2.03 ms, capped at 128 with
+// spills 1.69, against 1.48).
 template <int BLOCK, int KMAX, bool kStats = false>
-__global__ void __launch_bounds__(BLOCK) k_refresh_gather_f(const Pose* __restrict__ all_poses, int64_t n,
+__global__ void __launch_bounds__(BLOCK, 8) k_refresh_gather_f(const Pose* __restrict__ all_poses, int64_t n,
                                                             int64_t gbase, const int32_t* __restrict__ pos_list,
                                                             const int32_t* __restrict__ member_of,
                                                             const int32_t* __restrict__ seg_id,
@@ -1009,6 +1013,7 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
     else
       RGF(32);
 #undef RGF
+
     return;
   }
   k_refresh_gather<B><<<blocks_for(n, B), B, static_cast<size_t>(k) * B * 8, st>>>(all_poses, n, gbase, pos_list,
