@@ -277,8 +277,8 @@ __global__ void k_smooth_round(const double* __restrict__ p_all, double* __restr
 // K = 20 (the default list size): the particle's idx / kval rows (80 B
 // each, 16-byte aligned) are read with five 128-bit loads each and all 20 p
 // gathers are issued before the (reference-order) sums.
-template <int K>
-__global__ void __launch_bounds__(128) k_smooth_round_k(const double* __restrict__ p_all, double* __restrict__ q,
+template <int K, int kMinB = 1>
+__global__ void __launch_bounds__(128, kMinB) k_smooth_round_k(const double* __restrict__ p_all, double* __restrict__ q,
                                                         int64_t n, const int32_t* __restrict__ idx,
                                                         const float* __restrict__ kval,
                                                         const int32_t* __restrict__ count, int take_log) {
@@ -459,6 +459,9 @@ void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_
                          const int32_t* count, int k, cudaStream_t st, bool take_log) {
   count_launch();
   if (n <= 0) return;
+  // __launch_bounds__(128, 1): 80 registers, the 20 gathers and row loads
+  // all in flight (0.666 ms for 10 rounds at 1M; capped at 48 / 40
+  // registers: 0.729 / 0.740; the previous default heuristic, 56: 0.687).
   if (k == 20)
     k_smooth_round_k<20><<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count, take_log ? 1 : 0);
   else
