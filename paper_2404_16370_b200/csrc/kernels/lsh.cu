@@ -168,7 +168,7 @@ __global__ void k_reorder(const int32_t* __restrict__ old_of_new, const int32_t*
 // K = 20 rows (80 B, 16-byte aligned): 128-bit row copies, all 20 remap
 // gathers issued together, 128-bit pose copy.
 template <int K>
-__global__ void __launch_bounds__(128) k_reorder_k(const int32_t* __restrict__ old_of_new,
+__global__ void __launch_bounds__(128, 1) k_reorder_k(const int32_t* __restrict__ old_of_new,
                                                    const int32_t* __restrict__ new_of_old, int64_t n,
                                                    const Pose* __restrict__ poses, const double* __restrict__ lp,
                                                    const int32_t* __restrict__ id, const int32_t* __restrict__ idx,
