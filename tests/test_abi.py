@@ -72,6 +72,34 @@ def test_host_prep_matches_oracle_bitwise():
     assert len(api.make_scan_cloud(np.zeros((3, 3)), cfg)) == 0
 
 
+def test_covariances_against_independent_numpy_restatement():
+    """The host product's estimate_covariances (gaussian_cloud.cpp:36-88)
+    against an implementation sharing no code with it or with the oracle:
+    brute-force kNN, numpy (LAPACK) eigen-decomposition, plane model
+    lambda_max (I - (1 - eps) u u^T). The product and the oracle agree bit for
+    bit (test above) through the same Jacobi solver; this pins both to the
+    reference's mathematics independently, within 1e-12 of lambda_max."""
+    rng = np.random.default_rng(5)
+    pts = np.concatenate([
+        np.c_[rng.uniform(0, 4, 300), rng.uniform(0, 3, 300), 1e-3 * rng.standard_normal(300)],  # a noisy plane
+        rng.uniform(0, 2, (200, 3)),                                                               # a volume
+    ])
+    k, eps = 10, 1e-3
+    got = api.estimate_covariances(pts, k, eps).reshape(-1, 3, 3)
+    d2 = ((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1)
+    for i in range(len(pts)):
+        nb = np.argsort(d2[i], kind="stable")[: k + 1]
+        nb = nb[nb != i][:k]
+        q = pts[nb]
+        c = q - q.mean(0)
+        cov = c.T @ c / k
+        w, v = np.linalg.eigh(cov)
+        lmax = max(w[2], 1e-12)
+        u = v[:, 0]
+        want = lmax * (np.eye(3) - (1.0 - eps) * np.outer(u, u))
+        assert np.abs(got[i] - want).max() <= 1e-12 * lmax, i
+
+
 def test_nnf_exhaustive_brute_force():
     """test_map_model.cpp: every cell holds the exact nearest map point within
     max_query_dist (ties to the lower index), else -1."""
