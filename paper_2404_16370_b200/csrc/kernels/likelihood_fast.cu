@@ -562,6 +562,231 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   }
 }
 
+// K1 variant with a per-warp candidate queue (L2-resident, plain-layout
+// tables). Phase A gathers each point's 32-byte record straight into
+// registers (one predicated 256-bit load), so the cell's occupancy is known
+// before anything touches shared memory: only the candidates (occupied cells
+// and resolving points, ~45 %) are written, at consecutive queue positions
+// (ballot prefix), as (record, fraction + meta) = 48 B. Phase B consumes the
+// queue 32 entries at a time from consecutive positions: conflict-free reads,
+// no slot indirection, and the < 32 leftovers simply stay queued for the
+// next step (ring of kQ = 32 U + 32 entries). Against k_gicp_fast this
+// removes the all-point cp.async and fraction stores, the compaction
+// read-back and the bank conflicts of the compacted-slot reads.
+template <int kStepPts>
+struct WarpQueue {
+  static constexpr int kQ = kStepPts + 32;
+  float4 m0[kQ];
+  float4 m1[kQ];
+  float4 fq[kQ];      // (fraction.xyz, meta: k | kMetaResolve)
+  double pose_v[12];  // Rv (row-major), tv
+  float rf[12];       // R in fp32 (row-major, 9 used)
+};
+
+template <bool GN, int U, int kWarps, bool kCost>
+__global__ void __launch_bounds__(kWarps * 32, 1)
+    k_gicp_fast_q(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, float* __restrict__ sysf,
+                  double* __restrict__ raw_ll, int32_t* __restrict__ nm_out, const int32_t* __restrict__ list,
+                  const unsigned* __restrict__ list_count) {
+  constexpr int kStep = 32 * U;
+  using Q = WarpQueue<kStep>;
+  constexpr int kQ = Q::kQ;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Q* queues = reinterpret_cast<Q*>(smem_raw);
+  const int S = scan.n;
+  const int Sp = (S + kStep - 1) / kStep * kStep;
+  float4* s_r0 = reinterpret_cast<float4*>(smem_raw + sizeof(Q) * kWarps);  // Sp: mu.xyz, gamma
+  float4* s_r1 = s_r0 + Sp;                                                 // Sp: u.xyz, s
+  double* s_mu = reinterpret_cast<double*>(s_r1 + Sp);                      // Sp*3
+  for (int q = threadIdx.x; q < Sp; q += blockDim.x) {
+    s_r0[q] = q < S ? scan.rec[2 * q] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s_r1[q] = q < S ? scan.rec[2 * q + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int q = threadIdx.x; q < 3 * Sp; q += blockDim.x)
+    s_mu[q] = q < 3 * S ? scan.mu[q] : __longlong_as_double(0x7ff8000000000000ll);
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t gwarp = static_cast<int64_t>(blockIdx.x) * kWarps + wid;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kWarps;
+  const NnfGeom g = map.g;
+  float res;
+  asm volatile("cvt.rn.f32.f64 %0, %1;" : "=f"(res) : "d"(g.res));
+  const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
+                 dz = static_cast<unsigned>(g.dims[2]);
+  Q& ws = queues[wid];
+  const unsigned lt_mask = (1u << lane) - 1u;
+
+  const int64_t n_eff = list ? static_cast<int64_t>(*list_count) : n;
+  for (int64_t it = gwarp; it < n_eff; it += nwarps) {
+    const int64_t i = list ? static_cast<int64_t>(list[it]) : it;
+    bool huge;
+    {  // as k_gicp_fast: lane q < 12 sets up pose word q
+      const double pv = __ldg(reinterpret_cast<const double*>(poses + i) + (lane < 12 ? lane : 0));
+      const bool isR = lane < 9, isT = lane >= 9 && lane < 12;
+      const double o = lane == 9 ? g.origin[0] : (lane == 10 ? g.origin[1] : (lane == 11 ? g.origin[2] : 0.0));
+      if (lane < 12) ws.pose_v[lane] = (pv - o) * g.inv_res;
+      const float rf = static_cast<float>(pv);
+      if (lane < 12) ws.rf[lane] = rf;
+      float mr = isR ? fabsf(rf) : 0.f,
+            mt = isT ? fabsf(static_cast<float>(pv)) + fabsf(static_cast<float>(o)) : 0.f;
+#pragma unroll
+      for (int m = 8; m > 0; m >>= 1) {
+        mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, m));
+        mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, m));
+      }
+      mr = __shfl_sync(0xffffffffu, mr, 0);
+      mt = __shfl_sync(0xffffffffu, mt, 0);
+      huge = !((static_cast<double>(mr) * scan.mu_l1_max + static_cast<double>(mt)) * g.inv_res < 6.7e7) ||
+             !(pv == pv);
+      huge = __any_sync(0xffffffffu, huge);
+    }
+    __syncwarp();
+    Acc acc;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) acc.hbr[q] = acc.htl[q] = acc.b[q] = 0.f;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc.htr[q] = 0.f;
+    acc.cost = 0.f;
+    int nmatch = 0;
+    int head = 0, pending = 0;  // queue: entries [head, head + pending) mod kQ
+
+    for (int base = 0; base < S; base += kStep) {
+      // ---- phase A: fp64 cell + fraction, predicated 256-bit record loads into registers
+      float4 rm0[U], rm1[U];
+      float fr[U][3];
+      uint32_t meta[U];
+      {
+        double Rv[9], tv[3];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) Rv[q] = ws.pose_v[q];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) tv[a] = ws.pose_v[9 + a];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = base + u * 32 + lane;
+          const double m0 = s_mu[3 * k], m1 = s_mu[3 * k + 1], m2 = s_mu[3 * k + 2];
+          unsigned ic[3];
+          bool safe = !huge, inb = true;
+#pragma unroll
+          for (int ax = 0; ax < 3; ++ax) {
+            const double x = fma(Rv[ax * 3 + 2], m2, fma(Rv[ax * 3 + 1], m1, fma(Rv[ax * 3 + 0], m0, tv[ax])));
+            const CellFrac cf = cell_frac(x);
+            ic[ax] = cf.ic;
+            inb = inb & (cf.ic < (ax == 0 ? dx : (ax == 1 ? dy : dz)));
+            fr[u][ax] = cf.fr;
+            safe = safe & cf.clear;
+          }
+          const bool real = k < S;
+          const bool resolve = !safe && real;
+          const bool stage = safe && inb && real;
+          const float4* src = map.rec + 2 * static_cast<uint64_t>(rec_index<0>(map, ic[0], ic[1], ic[2]));
+          ldg_rec_pred(src, stage, rm0[u], rm1[u]);  // unstaged: reads as empty (m0.w = -1)
+          meta[u] = static_cast<uint32_t>(k) | (resolve ? kMetaResolve : 0u);
+        }
+      }
+      // ---- enqueue the candidates at consecutive positions
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool keep = (meta[u] & kMetaResolve) != 0u || rm0[u].w >= 0.f;
+        const unsigned mask = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          int pos = head + pending + __popc(mask & lt_mask);
+          pos = pos >= kQ ? pos - kQ : pos;
+          ws.m0[pos] = rm0[u];
+          ws.m1[pos] = rm1[u];
+          ws.fq[pos] = make_float4(fr[u][0], fr[u][1], fr[u][2], __uint_as_float(meta[u]));
+        }
+        pending += __popc(mask);
+      }
+      __syncwarp();
+      // ---- phase B: full warps; a partial one only at the particle's last step
+      const bool last_step = base + kStep >= S;
+      const int n_run = last_step ? pending : (pending & ~31);
+      for (int b0 = 0; b0 < n_run; b0 += 32) {
+        const int e = b0 + lane;
+        bool valid = false;
+        float Rf[9];
+        {
+          const float4 r0 = lds_f4_volatile(ws.rf), r1 = lds_f4_volatile(ws.rf + 4), r2 = lds_f4_volatile(ws.rf + 8);
+          Rf[0] = r0.x, Rf[1] = r0.y, Rf[2] = r0.z, Rf[3] = r0.w, Rf[4] = r1.x, Rf[5] = r1.y, Rf[6] = r1.z,
+          Rf[7] = r1.w, Rf[8] = r2.x;
+        }
+        if (e < n_run) {
+          int slot = head + e;
+          slot = slot >= kQ ? slot - kQ : slot;
+          const float4 fq = lds_f4_volatile(reinterpret_cast<const float*>(&ws.fq[slot]));
+          const uint32_t mt = __float_as_uint(fq.w);
+          const int k = static_cast<int>(mt & 0xFFFFu);
+          float f3[3] = {fq.x, fq.y, fq.z};
+          float4 m0, m1;
+          valid = true;
+          if (mt & kMetaResolve) {  // exact transform, floor and bounds (nnf.hpp:24-35), direct gather
+            const Pose P = poses[i];
+            const double mu[3] = {scan.mu[3 * k], scan.mu[3 * k + 1], scan.mu[3 * k + 2]};
+            double p[3];
+            transform_x(P.R, P.t, mu, p);
+            int c3[3];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+              const double x = xmul(xsub(p[ax], g.origin[ax]), g.inv_res);
+              const double fl = floor(x);
+              valid = valid && (fl >= 0.0 && fl < static_cast<double>(g.dims[ax]));
+              c3[ax] = valid ? static_cast<int>(fl) : 0;
+              f3[ax] = __double2float_rn(xsub(x, fl));
+            }
+            const uint64_t c = rec_index<0>(map, c3[0], c3[1], c3[2]);
+            m0 = valid ? __ldg(map.rec + 2 * c) : make_float4(0.f, 0.f, 0.f, -1.f);
+            m1 = valid ? __ldg(map.rec + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            m0 = ws.m0[slot];
+            m1 = ws.m1[slot];
+          }
+          valid = valid && m0.w >= 0.f;
+          if (valid) fast_item<GN, kCost>(acc, Rf, f3, res, m0, m1, s_r0[k], s_r1[k]);
+        }
+        nmatch += __popc(__ballot_sync(0xffffffffu, valid));
+      }
+      head += n_run;
+      head = head >= kQ ? head - kQ : head;
+      pending -= n_run;
+      __syncwarp();
+    }
+
+    // ---- epilogue (as k_gicp_fast)
+    if (GN) {
+      float v[32];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        v[q] = acc.htl[q];
+        v[15 + q] = acc.hbr[q];
+        v[21 + q] = acc.b[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 9; ++q) v[6 + q] = acc.htr[q];
+      v[27] = acc.cost;
+      v[28] = v[29] = v[30] = v[31] = 0.f;
+#pragma unroll
+      for (int s = 16; s >= 1; s >>= 1) {
+        const bool up = (lane & s) != 0;
+#pragma unroll
+        for (int j = 0; j < s; ++j) {
+          const float send = up ? v[j] : v[j + s];
+          const float keep = up ? v[j + s] : v[j];
+          v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+      }
+      sysf[i * kSysF + lane] = v[0];
+      if (kCost && lane == 27) raw_ll[i] = nmatch == 0 ? -1e30 : -static_cast<double>(v[0]);
+    } else {
+      const float cost = warp_sum(acc.cost);
+      if (lane == 0) raw_ll[i] = nmatch == 0 ? -1e30 : -static_cast<double>(cost);
+    }
+    if (lane == 0 && !list) nm_out[i] = nmatch;  // list: K2a already wrote it
+    __syncwarp();
+  }
+}
+
 // K2 with one lane per particle (likelihood only). The likelihood algebra is
 // short (~45 instructions), so running it on every lane for every point that
 // matches on ANY lane costs less than compaction and queue traffic; the scan
@@ -935,6 +1160,41 @@ void launch_fast_t(const Pose* poses, int64_t n, const ScanView& scan, const Map
 
 }  // namespace
 
+template <int U, int W>
+size_t fast_q_smem(int S) {
+  const size_t Sp = static_cast<size_t>((S + 32 * U - 1) / (32 * U) * (32 * U));
+  return sizeof(WarpQueue<32 * U>) * W + sizeof(float4) * 2 * Sp + sizeof(double) * 3 * Sp;
+}
+template <bool GN, int U, int W>
+bool launch_fast_q(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
+                   double* raw_ll, int32_t* nm, const Extra& x, cudaStream_t st) {
+  const size_t smem = fast_q_smem<U, W>(scan.n);
+  if (smem > 227 * 1024 || map.brick) return false;
+  int dev, n_sm, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  auto run = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W * 32, smem);
+    const int64_t want = (n + W - 1) / W;
+    const unsigned grid =
+        static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(n_sm) * std::max(per_sm, 1)));
+    kern<<<grid, W * 32, smem, st>>>(poses, n, scan, map, sysf, raw_ll, nm, x.list, x.list_count);
+  };
+  if (GN && !x.cost)
+    run(k_gicp_fast_q<GN, U, W, false>);
+  else
+    run(k_gicp_fast_q<GN, U, W, true>);
+  return true;
+}
+
+// A staged-slot configuration requested for the GN pass (SMCL_FAST_CFG_GN /
+// SMCL_FAST_CFG): the queue variant stands aside.
+static int cfg_gn_override() {
+  static const int v = (std::getenv("SMCL_FAST_CFG_GN") || std::getenv("SMCL_FAST_CFG")) ? 1 : 0;
+  return v;
+}
+
 // U points per lane in flight x W warps per SM (one CTA per SM).
 // SMCL_FAST_CFG=UxW overrides the default (tuning sweeps only).
 void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
@@ -968,6 +1228,29 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
     if (std::sscanf(e, "L%dx%d", &u, &w) == 2) return 9000 + u * 100 + w;  // lane-per-particle likelihood
     return std::sscanf(e, "%dx%d", &u, &w) == 2 ? u * 100 + w : 0;
   };
+  // GN pass on plain-layout (L2-resident) tables: the queue variant, 4 points
+  // per lane x 20 warps per SM (GN 3.98 -> 3.86 ms at 1M x 512 against the
+  // staged-slot kernel at 4 x 24; queue 2 x 24 / 2 x 28 / 4 x 16: 3.89 / 3.96
+  // / 4.00, 4 x 24 spills: 4.78). SMCL_K1_QUEUE=UxW overrides, =0 takes the
+  // staged-slot kernel.
+  static const int q_cfg = [] {
+    const char* e = std::getenv("SMCL_K1_QUEUE");
+    int u = 0, w = 0;
+    if (!e) return 420;
+    return std::sscanf(e, "%dx%d", &u, &w) == 2 ? u * 100 + w : 0;
+  }();
+  if (gn && q_cfg && cfg_gn_override() == 0) {
+    bool done = false;
+    switch (q_cfg) {
+      case 420: done = launch_fast_q<true, 4, 20>(poses, n, scan, map, sysf, raw_ll, nm, x, st); break;
+      case 416: done = launch_fast_q<true, 4, 16>(poses, n, scan, map, sysf, raw_ll, nm, x, st); break;
+      case 224: done = launch_fast_q<true, 2, 24>(poses, n, scan, map, sysf, raw_ll, nm, x, st); break;
+      case 228: done = launch_fast_q<true, 2, 28>(poses, n, scan, map, sysf, raw_ll, nm, x, st); break;
+      case 422: done = launch_fast_q<true, 4, 22>(poses, n, scan, map, sysf, raw_ll, nm, x, st); break;
+      default: break;
+    }
+    if (done) return;
+  }
   static const int cfg_gn = parse(std::getenv("SMCL_FAST_CFG_GN") ? std::getenv("SMCL_FAST_CFG_GN")
                                                                    : std::getenv("SMCL_FAST_CFG"));
   static const int cfg_ll = parse(std::getenv("SMCL_FAST_CFG_LL") ? std::getenv("SMCL_FAST_CFG_LL")
