@@ -583,7 +583,7 @@ struct WarpQueue {
   float rf[12];       // R in fp32 (row-major, 9 used)
 };
 
-template <bool GN, int U, int kWarps, bool kCost>
+template <bool GN, int U, int kWarps, bool kCost, int kBrick>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     k_gicp_fast_q(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, float* __restrict__ sysf,
                   double* __restrict__ raw_ll, int32_t* __restrict__ nm_out, const int32_t* __restrict__ list,
@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           const bool real = k < S;
           const bool resolve = !safe && real;
           const bool stage = safe && inb && real;
-          const float4* src = map.rec + 2 * static_cast<uint64_t>(rec_index<0>(map, ic[0], ic[1], ic[2]));
+          const float4* src = map.rec + 2 * static_cast<uint64_t>(rec_index<kBrick>(map, ic[0], ic[1], ic[2]));
           ldg_rec_pred(src, stage, rm0[u], rm1[u]);  // unstaged: reads as empty (m0.w = -1)
           meta[u] = static_cast<uint32_t>(k) | (resolve ? kMetaResolve : 0u);
         }
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
               c3[ax] = valid ? static_cast<int>(fl) : 0;
               f3[ax] = __double2float_rn(xsub(x, fl));
             }
-            const uint64_t c = rec_index<0>(map, c3[0], c3[1], c3[2]);
+            const uint64_t c = rec_index<kBrick>(map, c3[0], c3[1], c3[2]);
             m0 = valid ? __ldg(map.rec + 2 * c) : make_float4(0.f, 0.f, 0.f, -1.f);
             m1 = valid ? __ldg(map.rec + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
           } else {
@@ -1169,7 +1169,7 @@ template <bool GN, int U, int W>
 bool launch_fast_q(const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
                    double* raw_ll, int32_t* nm, const Extra& x, cudaStream_t st) {
   const size_t smem = fast_q_smem<U, W>(scan.n);
-  if (smem > 227 * 1024 || map.brick) return false;
+  if (smem > 227 * 1024) return false;
   int dev, n_sm, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
@@ -1181,10 +1181,8 @@ bool launch_fast_q(const Pose* poses, int64_t n, const ScanView& scan, const Map
         static_cast<unsigned>(std::min<int64_t>(want, static_cast<int64_t>(n_sm) * std::max(per_sm, 1)));
     kern<<<grid, W * 32, smem, st>>>(poses, n, scan, map, sysf, raw_ll, nm, x.list, x.list_count);
   };
-  if (GN && !x.cost)
-    run(k_gicp_fast_q<GN, U, W, false>);
-  else
-    run(k_gicp_fast_q<GN, U, W, true>);
+  if (map.brick) return false;  // plain-layout tables only (see launch_gicp_fast)
+  (GN && !x.cost) ? run(k_gicp_fast_q<GN, U, W, false, 0>) : run(k_gicp_fast_q<GN, U, W, true, 0>);
   return true;
 }
 
@@ -1239,7 +1237,10 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
     if (!e) return 420;
     return std::sscanf(e, "%dx%d", &u, &w) == 2 ? u * 100 + w : 0;
   }();
-  if (gn && q_cfg && cfg_gn_override() == 0) {
+  // Bricked (HBM-sized) tables keep the staged-slot kernel: there the pass is
+  // bound by HBM gathers and the queue variant measured the same (kidnap GN
+  // 6.76 vs 6.77 ms at 16 warps/SM, 7.02 at 20).
+  if (gn && q_cfg && cfg_gn_override() == 0 && !map.brick) {
     bool done = false;
     switch (q_cfg) {
       case 420: done = launch_fast_q<true, 4, 20>(poses, n, scan, map, sysf, raw_ll, nm, x, st); break;
