@@ -54,6 +54,17 @@ struct WarpStage {
   float rf[12];       // R in fp32 (row-major, 9 used): reloaded by each phase-B batch (no registers held in phase A)
 };
 
+// 128-bit shared-memory store / load at a shared-window address.
+__device__ __forceinline__ void sts_f4(unsigned a, const float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 lds_f4(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
 // Shared-memory loads the compiler may not hoist out of the batch loop (the
 // values are re-read where they are used instead of pinning registers).
 __device__ __forceinline__ float4 lds_f4_volatile(const float* p) {
@@ -615,7 +626,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
   const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
                  dz = static_cast<unsigned>(g.dims[2]);
   Q& ws = queues[wid];
-  const unsigned lt_mask = (1u << lane) - 1u;
+  unsigned lt_mask;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt_mask));
+  // The ring's shared-memory address, opaque to the compiler (otherwise it is
+  // rematerialised from the CTA id, thread id and struct size at every use).
+  unsigned qaddr;
+  asm volatile("mov.u32 %0, %1;" : "=r"(qaddr) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(ws.m0))));
 
   const int64_t n_eff = list ? static_cast<int64_t>(*list_count) : n;
   for (int64_t it = gwarp; it < n_eff; it += nwarps) {
@@ -655,7 +671,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       // ---- phase A: fp64 cell + fraction, predicated 256-bit record loads into registers
       float4 rm0[U], rm1[U];
       float fr[U][3];
-      uint32_t meta[U];
+      bool rsv[U];  // resolving point (reference-order path in phase B)
       {
         double Rv[9], tv[3];
 #pragma unroll
@@ -682,23 +698,27 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           const bool stage = safe && inb && real;
           const float4* src = map.rec + 2 * static_cast<uint64_t>(rec_index<kBrick>(map, ic[0], ic[1], ic[2]));
           ldg_rec_pred(src, stage, rm0[u], rm1[u]);  // unstaged: reads as empty (m0.w = -1)
-          meta[u] = static_cast<uint32_t>(k) | (resolve ? kMetaResolve : 0u);
+          rsv[u] = resolve;
         }
       }
       // ---- enqueue the candidates at consecutive positions
+      int wpos = head + pending;  // warp-uniform write cursor (mod kQ)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const bool keep = (meta[u] & kMetaResolve) != 0u || rm0[u].w >= 0.f;
+        const bool keep = rsv[u] || rm0[u].w >= 0.f;
         const unsigned mask = __ballot_sync(0xffffffffu, keep);
-        if (keep) {
-          int pos = head + pending + __popc(mask & lt_mask);
-          pos = pos >= kQ ? pos - kQ : pos;
-          ws.m0[pos] = rm0[u];
-          ws.m1[pos] = rm1[u];
-          ws.fq[pos] = make_float4(fr[u][0], fr[u][1], fr[u][2], __uint_as_float(meta[u]));
+        int pos = wpos + __popc(mask & lt_mask);
+        pos = pos >= kQ ? pos - kQ : pos;
+        if (keep) {  // m1, fq at fixed offsets kQ, 2 kQ from m0
+          const unsigned a = qaddr + 16u * static_cast<unsigned>(pos);
+          const uint32_t meta = static_cast<uint32_t>(base + u * 32 + lane) | (rsv[u] ? kMetaResolve : 0u);
+          sts_f4(a, rm0[u]);
+          sts_f4(a + 16u * kQ, rm1[u]);
+          sts_f4(a + 32u * kQ, make_float4(fr[u][0], fr[u][1], fr[u][2], __uint_as_float(meta)));
         }
-        pending += __popc(mask);
+        wpos += __popc(mask);
       }
+      pending = wpos - head;
       __syncwarp();
       // ---- phase B: full warps; a partial one only at the particle's last step
       const bool last_step = base + kStep >= S;
@@ -715,7 +735,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
         if (e < n_run) {
           int slot = head + e;
           slot = slot >= kQ ? slot - kQ : slot;
-          const float4 fq = lds_f4_volatile(reinterpret_cast<const float*>(&ws.fq[slot]));
+          const unsigned a = qaddr + 16u * static_cast<unsigned>(slot);
+          const float4 fq = lds_f4(a + 32u * kQ);
           const uint32_t mt = __float_as_uint(fq.w);
           const int k = static_cast<int>(mt & 0xFFFFu);
           float f3[3] = {fq.x, fq.y, fq.z};
@@ -739,8 +760,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             m0 = valid ? __ldg(map.rec + 2 * c) : make_float4(0.f, 0.f, 0.f, -1.f);
             m1 = valid ? __ldg(map.rec + 2 * c + 1) : make_float4(0.f, 0.f, 0.f, 0.f);
           } else {
-            m0 = ws.m0[slot];
-            m1 = ws.m1[slot];
+            m0 = lds_f4(a);
+            m1 = lds_f4(a + 16u * kQ);
           }
           valid = valid && m0.w >= 0.f;
           if (valid) fast_item<GN, kCost>(acc, Rf, f3, res, m0, m1, s_r0[k], s_r1[k]);
