@@ -1248,10 +1248,10 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
     return std::sscanf(e, "%dx%d", &u, &w) == 2 ? u * 100 + w : 0;
   };
   // GN pass on plain-layout (L2-resident) tables: the queue variant, 4 points
-  // per lane x 20 warps per SM (GN 3.98 -> 3.86 ms at 1M x 512 against the
-  // staged-slot kernel at 4 x 24; queue 2 x 24 / 2 x 28 / 4 x 16: 3.89 / 3.96
-  // / 4.00, 4 x 24 spills: 4.78). SMCL_K1_QUEUE=UxW overrides, =0 takes the
-  // staged-slot kernel.
+  // per lane x 20 warps per SM (GN 3.74 ms at 1M x 512 against 3.98 for the
+  // staged-slot kernel at 4 x 24; queue 2 x 28: 3.74, 2 x 24: 3.90, 4 x 16:
+  // 3.96, 4 x 18: 4.06, 4 x 24 spills: 4.78). SMCL_K1_QUEUE=UxW overrides,
+  // =0 takes the staged-slot kernel.
   static const int q_cfg = [] {
     const char* e = std::getenv("SMCL_K1_QUEUE");
     int u = 0, w = 0;
@@ -1268,7 +1268,6 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
       case 416: done = launch_fast_q<true, 4, 16>(poses, n, scan, map, sysf, raw_ll, nm, x, st); break;
       case 224: done = launch_fast_q<true, 2, 24>(poses, n, scan, map, sysf, raw_ll, nm, x, st); break;
       case 228: done = launch_fast_q<true, 2, 28>(poses, n, scan, map, sysf, raw_ll, nm, x, st); break;
-      case 422: done = launch_fast_q<true, 4, 22>(poses, n, scan, map, sysf, raw_ll, nm, x, st); break;
       default: break;
     }
     if (done) return;
