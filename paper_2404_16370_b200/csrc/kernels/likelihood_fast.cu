@@ -723,15 +723,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       // ---- phase B: full warps; a partial one only at the particle's last step
       const bool last_step = base + kStep >= S;
       const int n_run = last_step ? pending : (pending & ~31);
+      float Rf[9];  // per step (registers held through phase B only)
+      {
+        const float4 r0 = lds_f4_volatile(ws.rf), r1 = lds_f4_volatile(ws.rf + 4), r2 = lds_f4_volatile(ws.rf + 8);
+        Rf[0] = r0.x, Rf[1] = r0.y, Rf[2] = r0.z, Rf[3] = r0.w, Rf[4] = r1.x, Rf[5] = r1.y, Rf[6] = r1.z,
+        Rf[7] = r1.w, Rf[8] = r2.x;
+      }
       for (int b0 = 0; b0 < n_run; b0 += 32) {
         const int e = b0 + lane;
         bool valid = false;
-        float Rf[9];
-        {
-          const float4 r0 = lds_f4_volatile(ws.rf), r1 = lds_f4_volatile(ws.rf + 4), r2 = lds_f4_volatile(ws.rf + 8);
-          Rf[0] = r0.x, Rf[1] = r0.y, Rf[2] = r0.z, Rf[3] = r0.w, Rf[4] = r1.x, Rf[5] = r1.y, Rf[6] = r1.z,
-          Rf[7] = r1.w, Rf[8] = r2.x;
-        }
         if (e < n_run) {
           int slot = head + e;
           slot = slot >= kQ ? slot - kQ : slot;
