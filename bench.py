@@ -271,14 +271,20 @@ def main():
         return
     rank, world, local = dist_env()
     pg = None
+    # SMCL_BENCH_GLOO=1 (functional checks of the multi-rank bench path on a
+    # one-GPU box only, never a measurement): gloo, host-staged exchanges, all
+    # ranks on device 0.
+    gloo = os.environ.get("SMCL_BENCH_GLOO") == "1"
     if world > 1:
         import torch
         import torch.distributed as dist
         # communicator set-up in the log (ranks, NVLS/NVLink transport) for the scaling runs
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        if gloo:
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if gloo else "nccl")
         pg = dist
     from paper_2404_16370_b200 import workload
     from paper_2404_16370_b200.api import FilterEngine
@@ -297,10 +303,12 @@ def main():
             cfg.reorder_particles = 0
         # native NCCL on the engine stream (fallback: torch.distributed trampoline)
         try:
+            if gloo:
+                raise RuntimeError("gloo functional mode")
             comm = NcclComm.from_torch()
         except Exception as e:  # noqa: BLE001
             print(f"[bench] native NCCL comm unavailable ({e}); using TorchComm", file=sys.stderr)
-            comm = TorchComm()
+            comm = TorchComm(staged=True) if gloo else TorchComm()
     eng = FilterEngine(wl.map, cfg, device=local, comm=comm)
     eng.init_uniform(wl.bounds)
     setup_s = time.perf_counter() - t_setup
@@ -338,7 +346,7 @@ def main():
     ms_step = ms_total / args.steps
     if pg:
         import torch
-        t = torch.tensor([ms_step], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([ms_step], device="cpu" if gloo else f"cuda:{local}", dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         ms_step = float(t.item())
     # Particle-point evaluations actually performed (empty scans of the kidnap
@@ -363,7 +371,7 @@ def main():
     e2e_ms = 1e3 * (time.perf_counter() - t0) / args.steps
     if pg:
         import torch
-        t = torch.tensor([e2e_ms], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([e2e_ms], device="cpu" if gloo else f"cuda:{local}", dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e = pp_e2e / args.steps / (e2e_ms * 1e-3)
@@ -392,7 +400,7 @@ def main():
     raw_ms = 1e3 * (time.perf_counter() - t0) / args.steps
     if pg:
         import torch
-        t = torch.tensor([raw_ms], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([raw_ms], device="cpu" if gloo else f"cuda:{local}", dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         raw_ms = float(t.item())
     pp_raw_step = pp_raw / args.steps  # all shards
