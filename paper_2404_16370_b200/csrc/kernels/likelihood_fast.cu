@@ -151,10 +151,10 @@ __device__ __forceinline__ float fast_cost(const float Rf[9], const float fr[3],
   const float ny = Rf[3] * s1.x + Rf[4] * s1.y + Rf[5] * s1.z;
   const float nz = Rf[6] * s1.x + Rf[7] * s1.y + Rf[8] * s1.z;
   const float beta = m0.w, sM = m1.w, gam = s0.w, sS = s1.w;
-  const float A = (beta + sM) + (gam + sS);
   const float Ssum = sM + sS;
-  const float AmB = sM + gam + sS;   // A - beta
-  const float AmG = beta + sM + sS;  // A - gamma
+  const float AmB = Ssum + gam;   // A - beta
+  const float AmG = Ssum + beta;  // A - gamma
+  const float A = AmG + gam;      // beta + gamma + s_M + s_S (4 adds instead of 8)
   const float c = mx * nx + my * ny + mz * nz;
   const float cx = my * nz - mz * ny, cy = mz * nx - mx * nz, cz = mx * ny - my * nx;
   const float w = cx * cx + cy * cy + cz * cz;
@@ -187,10 +187,10 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
   const float mz = Rf[2] * m1.x + Rf[5] * m1.y + Rf[8] * m1.z;
   const float nx = s1.x, ny = s1.y, nz = s1.z;
   const float beta = m0.w, sM = m1.w, gam = s0.w, sS = s1.w;
-  const float A = (beta + sM) + (gam + sS);
   const float Ssum = sM + sS;
-  const float AmB = sM + gam + sS;   // A - beta
-  const float AmG = beta + sM + sS;  // A - gamma
+  const float AmB = Ssum + gam;   // A - beta
+  const float AmG = Ssum + beta;  // A - gamma
+  const float A = AmG + gam;      // beta + gamma + s_M + s_S (4 adds instead of 8)
   const float c = mx * nx + my * ny + mz * nz;
   const float cx = my * nz - mz * ny, cy = mz * nx - mx * nz, cz = mx * ny - my * nx;
   const float w = cx * cx + cy * cy + cz * cz;
@@ -201,7 +201,8 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
   const float invA = rcp_approx(A);
   // P, Q, T pre-scaled by 1/A: Omega' = invA I + Pa m m^T + Qa n n^T + Ta (m n^T + n m^T)
   const float invDA = invD * invA;
-  const float Pa = beta * AmG * invDA, Qa = gam * AmB * invDA, Ta = c * bg * invDA;
+  const float bI = beta * invDA;
+  const float Pa = bI * AmG, Qa = gam * AmB * invDA, Ta = c * (bI * gam);
   const float x = mx * ex + my * ey + mz * ez;
   const float y = nx * ex + ny * ey + nz * ez;
   const float am = fmaf(Pa, x, Ta * y), an = fmaf(Qa, y, Ta * x);  // (Omega' - invA I) e = am m + an n
