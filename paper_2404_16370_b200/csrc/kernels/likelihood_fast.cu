@@ -83,10 +83,6 @@ struct Acc {
   float cost;    // sum e^T Omega e
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
 // 16-byte async copy; when !pred nothing is read and the destination is zero-filled.
 // kL1: also allocate in L1 (.ca) — pays for bricked HBM-sized tables, where
 // neighbouring particles re-read the same records; L2-resident tables use .cg.
@@ -114,15 +110,6 @@ __device__ __forceinline__ void ldg_rec_pred(const float4* src, bool pred, float
       " @p ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n}"
       : "+f"(a0), "+f"(a1), "+f"(a2), "+f"(a3), "+f"(b0), "+f"(b1), "+f"(b2), "+f"(b3)
       : "l"(src), "r"(static_cast<unsigned>(pred)));
-  m0 = make_float4(a0, a1, a2, a3);
-  m1 = make_float4(b0, b1, b2, b3);
-}
-// Unpredicated 256-bit record load (unmatched points read MapFast::empty).
-__device__ __forceinline__ void ldg_rec(const float4* src, float4& m0, float4& m1) {
-  float a0, a1, a2, a3, b0, b1, b2, b3;
-  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-      : "=f"(a0), "=f"(a1), "=f"(a2), "=f"(a3), "=f"(b0), "=f"(b1), "=f"(b2), "=f"(b3)
-      : "l"(src));
   m0 = make_float4(a0, a1, a2, a3);
   m1 = make_float4(b0, b1, b2, b3);
 }
