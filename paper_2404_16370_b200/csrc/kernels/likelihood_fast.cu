@@ -1,25 +1,28 @@
 // K1 / K2 fast path: per-particle GICP likelihood (+ Gauss-Newton system) for
 // plane-model maps and scans (reference gicp.cpp:11-45, 109-137).
 //
-// One warp per particle; lanes stride over the scan points, 32*U points per
-// step (U per lane).
+// Kernels:
+//  * k_gicp_fast_q   K1 on L2-resident (plain-layout) record tables: warp per
+//    particle, lanes stride the scan points (4 per lane per step); records
+//    gathered into registers, candidates enqueued in a per-warp shared ring,
+//    phase B on full warps from consecutive ring positions.
+//  * k_gicp_fast     the staged-slot form (cp.async of every in-bounds record
+//    into the warp's stage, compaction by slot index): K1 and the
+//    likelihood-only warp pass on bricked, HBM-sized tables.
+//  * k_ll_count      K2a: exact n_matched of every particle from an occupancy
+//    bitmap with a proven fp32 margin, and the list of particles the gate keeps.
+//  * k_gicp_ll_lanes K2: lane per particle, the likelihood of the gate's list.
 //
 // Phase A (every point): the point is transformed in fp64 with the pose
-// pre-scaled to voxel units (x = Rv mu + tv, 9 DFMA); floor by a round-down
-// add of 1.5*2^52, the exact fractional coordinate f = x - floor(x) goes to
-// shared memory as fp32 (its 1e-8 m resolution is below the fp32 map record
-// precision). x differs from the reference's ((R mu + t) - o) * inv_res
-// (nnf.hpp:24-35) by < 2.2e-8 voxel (coordinates below 2^26 voxels; beyond,
-// every point resolves), so the cell is the reference's unless f is
-// within ~5e-8 of a face (frac_clear_of_faces): such points "resolve" in phase B through the
-// reference-order fp64 transform. In-bounds points start a cp.async of their
-// 32-byte cell record into the warp's stage, so U x 2 16-byte gathers per lane
-// are in flight (the global-init gathers are random L2 hits).
-// Compaction: after the wait, empty cells are dropped and the slots of the
-// survivors (plus resolving points) are ballot-compacted; records and
-// fractions stay where phase A put them.
-// Phase B (compacted candidates, full warps): the body-frame
-// structured-covariance algebra in fp32:
+// pre-scaled to voxel units (x = Rv mu + tv, 9 DFMA); one round-down add of
+// 1.5 * 2^28 splits x into the cell and a 24-bit fraction (cell_frac). x
+// differs from the reference's ((R mu + t) - o) * inv_res (nnf.hpp:24-35) by
+// < 2.2e-8 voxel (coordinates below 2^26 voxels; beyond, every point
+// resolves), so the cell is the reference's unless the fraction is within
+// 2^-24 of a face: such points "resolve" in phase B through the
+// reference-order fp64 transform.
+// Phase B (candidates, full warps): the body-frame structured-covariance
+// algebra in fp32:
 //   Sigma_M' + Sigma_s = A I - beta m m^T - gamma n n^T,
 //   Omega' = (1/A)(I + P m m^T + Q n n^T + T (m n^T + n m^T)),
 //   Delta  = A (s_M + s_S) + beta gamma |m x n|^2   (no cancellation),
