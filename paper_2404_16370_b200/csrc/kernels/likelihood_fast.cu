@@ -42,7 +42,7 @@ namespace smcl {
 namespace {
 
 constexpr uint32_t kMetaStage = 1u << 16;    // fq.w: record staged (in bounds, cell proven)
-constexpr uint32_t kMetaResolve = 1u << 17;  // fq.w: fraction within ~5e-8 of a cell face: reference-order path
+constexpr uint32_t kMetaResolve = 1u << 17;  // fq.w: fraction within 2^-24 of a cell face: reference-order path
 
 // Slots [0, kStep) hold the current step's points; slots [kStep, kStep + 32)
 // the carry: candidates left over from earlier steps of the same particle
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       // Resolve every point (NaN too) unless (max|R| |mu|_1 + max(|t| + |o|))
       // / res < 2^26: the reference forms p = R mu + t in world coordinates,
       // whose rounding (~3 ulp of |t| + |R mu|, plus p - o) stays below 2.2e-8
-      // voxel there, inside the 5e-8 face margin; the round-down floor needs
+      // voxel there, inside the 2^-24 face margin; the round-down split needs
       // |x| < 2^40 (implied).
       float mr = isR ? fabsf(rf) : 0.f,
             mt = isT ? fabsf(static_cast<float>(pv)) + fabsf(static_cast<float>(o)) : 0.f;
