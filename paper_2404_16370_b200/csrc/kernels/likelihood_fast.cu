@@ -372,8 +372,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       // Resolve every point (NaN too) unless (max|R| |mu|_1 + max(|t| + |o|))
       // / res < 2^26: the reference forms p = R mu + t in world coordinates,
       // whose rounding (~3 ulp of |t| + |R mu|, plus p - o) stays below 2.2e-8
-      // voxel there, inside the 2^-24 face margin; the round-down split needs
-      // |x| < 2^40 (implied).
+      // voxel there, inside the 2^-24 face margin; the fixed-point split
+      // (cell_frac) needs |x| < 2^27 (implied).
       float mr = isR ? fabsf(rf) : 0.f,
             mt = isT ? fabsf(static_cast<float>(pv)) + fabsf(static_cast<float>(o)) : 0.f;
 #pragma unroll
