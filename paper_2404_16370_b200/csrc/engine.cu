@@ -1432,9 +1432,20 @@ struct smcl_engine {
     }
   }
 
-  void normalize(double floor_v, const unsigned long long* skip_if_zero = nullptr) {
+  // p_out (optional): exp of the normalised log-posterior, the smoothing
+  // pass's input, written by the same sweep.
+  void normalize(double floor_v, const unsigned long long* skip_if_zero = nullptr, double* p_out = nullptr) {
     const int64_t n = n_local;
     if (n == 0) return;
+    const int64_t chunks_local = (n + kReduceChunk - 1) / kReduceChunk;
+    if (!sharded) {  // three launches: argmax partials, chunk sums (max from the partials), finish + apply
+      launch_argmax_partials(log_post.p, n, gbase, argv.p, argi.p, st);
+      launch_chunk_sum_exp_parts(log_post.p, n, argv.p, argmax_partials(n), scal.p + 2, partial.p, st);
+      launch_apply_lse_fin(log_post.p, n, partial.p, chunks_local, scal.p + 2, floor_v, skip_if_zero, scal.p + 3,
+                           p_out, st);
+      CK(cudaGetLastError());
+      return;
+    }
     global_argmax(2, 0);
     launch_chunk_sum_exp(log_post.p, n, scal.p + 2, partial.p, st);
     const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
@@ -1445,6 +1456,7 @@ struct smcl_engine {
       launch_finish_lse(partial.p, chunks, scal.p + 2, scal.p + 3, st);
     }
     launch_apply_lse(log_post.p, n, scal.p + 3, floor_v, st, skip_if_zero);
+    if (p_out) launch_exp(log_post.p, p_out, n, st);
     CK(cudaGetLastError());
   }
 
@@ -1488,7 +1500,7 @@ struct smcl_engine {
   // stay in d_counts[0..1], the uniform reset and the skipped normalization of
   // a rejected observation are decided on the device; the caller reads the
   // counts with its end-of-step sync.
-  void bayes_async(double beta, double floor_v) {
+  void bayes_async(double beta, double floor_v, double* p_out = nullptr) {
     if (!(beta >= 0.0)) throw std::invalid_argument("bayes_update: beta must be >= 0");
     const int64_t n = n_local;
     if (n == 0) return;
@@ -1498,14 +1510,16 @@ struct smcl_engine {
       launch_sum_pairs(g_counts.p, world, d_counts.p, st);
     }
     launch_bayes_numer(log_post.p, ll.p, nm.p, n, beta, d_counts.p, -std::log(static_cast<double>(n_total)), st);
-    normalize(floor_v, d_counts.p);
+    // the step's smoothing follows: its exp(log_post) comes out of the same sweep
+    normalize(floor_v, d_counts.p, p_out);
   }
 
-  void smooth(int iters, double floor_v) {
+  // p_ready: pbuf already holds exp(log_post) (bayes_async's normalisation).
+  void smooth(int iters, double floor_v, bool p_ready = false) {
     if (iters < 0) throw std::invalid_argument("smooth: iters must be >= 0");
     const int64_t n = n_local;
     if (n == 0 || iters == 0) return;
-    launch_exp(log_post.p, pbuf.p, n, st);
+    if (!p_ready) launch_exp(log_post.p, pbuf.p, n, st);
     for (int r = 0; r < iters; ++r) {
       // Exchange 3: neighbours' probabilities every round.
       const double* p_all = pbuf.p;
@@ -1647,6 +1661,7 @@ struct smcl_engine {
     // second time only if the hash guard finds a key to correct.
     std::chrono::steady_clock::time_point h_sync;
     auto run_from_keys = [&]() {
+      bool p_ready = false;  // pbuf = exp(log_post) from the Bayes normalisation
       neighbor_rest(&r.neighbor_stats);
       mark(E_NB);
       if (!empty) {
@@ -1660,14 +1675,16 @@ struct smcl_engine {
         }
         run_likelihood(false, sl.full);
         mark(E_BAYES);
-        bayes_async(cfg.beta, cfg.log_post_floor);  // rejection flag read at the end of the step
+        // rejection flag read at the end of the step; exp(log_post) for the smoothing rides along
+        bayes_async(cfg.beta, cfg.log_post_floor, cfg.smooth_iters > 0 ? pbuf.p : nullptr);
+        p_ready = cfg.smooth_iters > 0;
       } else {
         mark(E_LL0);
         mark(E_LL1);
         mark(E_BAYES);
       }
       mark(E_SMOOTH);  // posterior smoothing starts
-      smooth(cfg.smooth_iters, cfg.log_post_floor);
+      smooth(cfg.smooth_iters, cfg.log_post_floor, p_ready);
       mark(E_END);
       representative_enqueue();
       join_aux();

@@ -159,6 +159,17 @@ void launch_finish_sum2(const double* a, const double* b, int64_t n_chunks, doub
 void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, cudaStream_t st,
                       const unsigned long long* skip_if_zero = nullptr);
 void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st);
+// Unsharded normalisation in three launches: per-block argmax partials, chunk
+// sums with the max taken from those partials (block 0 stores it in m_out),
+// then finish + apply (+ p_out = exp of the result) in one kernel.
+int argmax_partials(int64_t n);
+void launch_argmax_partials(const double* v, int64_t n, int64_t gbase, double* scratch_v, long long* scratch_i,
+                            cudaStream_t st);
+void launch_chunk_sum_exp_parts(const double* v, int64_t n, const double* m_parts, int n_parts, double* m_out,
+                                double* partial, cudaStream_t st);
+void launch_apply_lse_fin(double* v, int64_t n, const double* partial, int64_t n_chunks, const double* m,
+                          double floor_v, const unsigned long long* skip_if_zero, double* lse_out, double* p_out,
+                          cudaStream_t st);
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
                          const int32_t* count, int k, cudaStream_t st, bool take_log = false);
 

@@ -149,7 +149,9 @@ __global__ void __launch_bounds__(kChunkThreads) k_chunk_serial(const double* __
                                                                 const double* __restrict__ v1, int64_t n,
                                                                 int64_t chunks, double* __restrict__ p0,
                                                                 double* __restrict__ p1,
-                                                                const double* __restrict__ m_ptr) {
+                                                                const double* __restrict__ m_ptr,
+                                                                const double* __restrict__ m_parts = nullptr,
+                                                                int n_parts = 0, double* __restrict__ m_out = nullptr) {
   __shared__ __align__(16) double s[kReduceChunk];
   const bool second = blockIdx.x >= chunks;
   const double* __restrict__ v = second ? v1 : v0;
@@ -157,8 +159,23 @@ __global__ void __launch_bounds__(kChunkThreads) k_chunk_serial(const double* __
   const int64_t c = second ? blockIdx.x - chunks : blockIdx.x;
   const int64_t begin = c * kReduceChunk;
   const int m = static_cast<int>(begin + kReduceChunk < n ? kReduceChunk : n - begin);
-  if (m_ptr) {
-    const double mv = *m_ptr;
+  if (m_ptr || m_parts) {
+    double mv;
+    if (m_parts) {  // the max of the argmax kernel's per-block partial values (exact, order-free)
+      __shared__ double s_max[kChunkThreads / 32];
+      double b = -__longlong_as_double(0x7ff0000000000000ll);
+      for (int q = threadIdx.x; q < n_parts; q += kChunkThreads) b = fmax(b, __ldg(m_parts + q));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+      if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = b;
+      __syncthreads();
+      mv = s_max[0];
+#pragma unroll
+      for (int w = 1; w < kChunkThreads / 32; ++w) mv = fmax(mv, s_max[w]);
+      if (blockIdx.x == 0 && threadIdx.x == 0 && m_out) *m_out = mv;
+    } else {
+      mv = *m_ptr;
+    }
 #pragma unroll 4
     for (int q = threadIdx.x; q < m; q += kChunkThreads) s[q] = exp(xsub(__ldg(v + begin + q), mv));
   } else {
@@ -250,6 +267,40 @@ __global__ void k_apply_lse(double* __restrict__ v, int64_t n, const double* __r
   if (skip_if_zero && *skip_if_zero == 0ull) return;
   const double r = xsub(v[i], *lse_ptr);
   v[i] = r < floor_v ? floor_v : r;  // std::max(v - lse, floor)
+}
+
+// finish_lse + apply_lse in one kernel (unsharded normalisation): every
+// block's first warp forms lse = m + log(serial sum of the chunk partials)
+// exactly as k_finish_lse does (same order, same operations), then the block
+// applies it grid-stride; p_out (optional): exp of the result, the smoothing
+// pass's input, written in the same sweep.
+__global__ void __launch_bounds__(256) k_apply_lse_fin(double* __restrict__ v, int64_t n,
+                                                       const double* __restrict__ partial, int64_t n_chunks,
+                                                       const double* __restrict__ m_ptr, double floor_v,
+                                                       const unsigned long long* __restrict__ skip_if_zero,
+                                                       double* __restrict__ lse_out, double* __restrict__ p_out) {
+  __shared__ double s[kFinStage];
+  __shared__ double s_lse;
+  if (threadIdx.x < 32) {
+    const double t = serial_sum_staged(partial, n_chunks, s);
+    if (threadIdx.x == 0) {
+      s_lse = xadd(*m_ptr, log(t));
+      if (blockIdx.x == 0 && lse_out) *lse_out = s_lse;
+    }
+  }
+  __syncthreads();
+  const double lse = s_lse;
+  const bool skip = skip_if_zero && *skip_if_zero == 0ull;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double r = v[i];
+    if (!skip) {
+      r = xsub(r, lse);
+      r = r < floor_v ? floor_v : r;  // std::max(v - lse, floor)
+      v[i] = r;
+    }
+    if (p_out) p_out[i] = exp(r);
+  }
 }
 
 __global__ void k_exp(const double* __restrict__ lp, double* __restrict__ p, int64_t n) {
@@ -450,6 +501,31 @@ void launch_apply_lse(double* v, int64_t n, const double* lse, double floor_v, c
                       const unsigned long long* skip_if_zero) {
   count_launch();
   if (n > 0) k_apply_lse<<<blocks_for(n, 256), 256, 0, st>>>(v, n, lse, floor_v, skip_if_zero);
+}
+void launch_chunk_sum_exp_parts(const double* v, int64_t n, const double* m_parts, int n_parts, double* m_out,
+                                double* partial, cudaStream_t st) {
+  count_launch();
+  if (n <= 0) return;
+  const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
+  k_chunk_serial<<<static_cast<unsigned>(chunks), kChunkThreads, 0, st>>>(v, v, n, chunks, partial, partial, nullptr,
+                                                                          m_parts, n_parts, m_out);
+}
+void launch_apply_lse_fin(double* v, int64_t n, const double* partial, int64_t n_chunks, const double* m,
+                          double floor_v, const unsigned long long* skip_if_zero, double* lse_out, double* p_out,
+                          cudaStream_t st) {
+  count_launch();
+  if (n <= 0) return;
+  int dev, n_sm;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(n, 256), 4LL * n_sm));
+  k_apply_lse_fin<<<g, 256, 0, st>>>(v, n, partial, n_chunks, m, floor_v, skip_if_zero, lse_out, p_out);
+}
+void launch_argmax_partials(const double* v, int64_t n, int64_t gbase, double* scratch_v, long long* scratch_i,
+                            cudaStream_t st) {
+  count_launch();
+  const int g = argmax_partials(n);
+  k_argmax<<<g, 256, 0, st>>>(v, nullptr, n, gbase, scratch_v, scratch_i);
 }
 void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st) {
   count_launch();
