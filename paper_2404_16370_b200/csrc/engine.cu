@@ -1045,7 +1045,8 @@ struct smcl_engine {
     CK(cudaGetLastError());
     if (profiling) {  // matched particle-points of this pass, summed over the step's passes (counts only)
       gn ? mark_it(gn_iter, I_GN1) : mark(E_LL1);
-      launch_match_counts(nullptr, nm.p, n_local, d_counts.p + (gn ? 2 : 4), st, /*zero=*/false);
+      // unsharded, the likelihood pass's sum is the Bayes update's own count (d_counts[1])
+      if (gn || sharded) launch_match_counts(nullptr, nm.p, n_local, d_counts.p + (gn ? 2 : 4), st, /*zero=*/false);
     }
     const GicpParamsDev gp = gicp_params(sd.n);
     if (gn)
@@ -1752,7 +1753,7 @@ struct smcl_engine {
     prof.gn_points = empty ? 0 : static_cast<int64_t>(gn_scan.n) * n_total * cfg.n_svgd_iters;
     prof.ll_points = empty ? 0 : static_cast<int64_t>(sl.full.n) * n_total;
     prof.gn_matched = static_cast<int64_t>(cnt[3]);
-    prof.ll_matched = static_cast<int64_t>(cnt[5]);
+    prof.ll_matched = static_cast<int64_t>(sharded ? cnt[5] : (empty ? 0 : cnt[1]));
     prof.fast_path = fast_used ? 1 : 0;
     prof.n_svgd_iters = cfg.n_svgd_iters;
     prof.kernel_launches = launch_count() - launches0;
