@@ -1435,17 +1435,20 @@ struct smcl_engine {
 
   // p_out (optional): exp of the normalised log-posterior, the smoothing
   // pass's input, written by the same sweep.
-  void normalize(double floor_v, const unsigned long long* skip_if_zero = nullptr, double* p_out = nullptr) {
+  // rep_parts (unsharded): also leave the argmax partials of the result in
+  // argv/argi for representative_enqueue; returns whether it did.
+  bool normalize(double floor_v, const unsigned long long* skip_if_zero = nullptr, double* p_out = nullptr,
+                 bool rep_parts = false) {
     const int64_t n = n_local;
-    if (n == 0) return;
+    if (n == 0) return false;
     const int64_t chunks_local = (n + kReduceChunk - 1) / kReduceChunk;
     if (!sharded) {  // three launches: argmax partials, chunk sums (max from the partials), finish + apply
       launch_argmax_partials(log_post.p, n, gbase, argv.p, argi.p, st);
       launch_chunk_sum_exp_parts(log_post.p, n, argv.p, argmax_partials(n), scal.p + 2, partial.p, st);
       launch_apply_lse_fin(log_post.p, n, partial.p, chunks_local, scal.p + 2, floor_v, skip_if_zero, scal.p + 3,
-                           p_out, st);
+                           p_out, gbase, rep_parts ? argv.p : nullptr, rep_parts ? argi.p : nullptr, st);
       CK(cudaGetLastError());
-      return;
+      return rep_parts;
     }
     global_argmax(2, 0);
     launch_chunk_sum_exp(log_post.p, n, scal.p + 2, partial.p, st);
@@ -1459,6 +1462,7 @@ struct smcl_engine {
     launch_apply_lse(log_post.p, n, scal.p + 3, floor_v, st, skip_if_zero);
     if (p_out) launch_exp(log_post.p, p_out, n, st);
     CK(cudaGetLastError());
+    return false;
   }
 
   // (matched particles, sum of n_matched) over all shards: exact integers.
@@ -1516,10 +1520,12 @@ struct smcl_engine {
   }
 
   // p_ready: pbuf already holds exp(log_post) (bayes_async's normalisation).
-  void smooth(int iters, double floor_v, bool p_ready = false) {
+  // rep_parts: leave the representative's argmax partials (see normalize);
+  // returns whether they were left.
+  bool smooth(int iters, double floor_v, bool p_ready = false, bool rep_parts = false) {
     if (iters < 0) throw std::invalid_argument("smooth: iters must be >= 0");
     const int64_t n = n_local;
-    if (n == 0 || iters == 0) return;
+    if (n == 0 || iters == 0) return false;
     if (!p_ready) launch_exp(log_post.p, pbuf.p, n, st);
     for (int r = 0; r < iters; ++r) {
       // Exchange 3: neighbours' probabilities every round.
@@ -1534,7 +1540,7 @@ struct smcl_engine {
       pbuf.swap(qbuf);
     }
     CK(cudaGetLastError());
-    normalize(floor_v);
+    return normalize(floor_v, nullptr, nullptr, rep_parts);
   }
 
   void representative(int64_t* index, double* pose, double* value) {
@@ -1546,10 +1552,15 @@ struct smcl_engine {
   // staging record, read back into pinned memory (no host round trip until
   // the caller's sync).
   // rep_stage[15] (sharded: summed over shards): the last K3's hash-guard flag count.
-  void representative_enqueue() {
+  // parts_ready: argv/argi hold the argmax partials of the current
+  // log-posterior (left by the step's final normalisation, unsharded).
+  void representative_enqueue(bool parts_ready = false) {
     if (n_local == 0) throw std::invalid_argument("representative: empty or mismatched particle set");
     lsh_flagged.ensure(1);
-    global_argmax(4, 1);
+    if (parts_ready && !sharded)
+      launch_max_of_partials(argv.p, argi.p, apply_fin_blocks(n_local), scal.p + 4, scal_i.p + 1, st);
+    else
+      global_argmax(4, 1);
     rep_stage.ensure(16);
     if (sharded) {  // the owner rank publishes the winner's pose and id (one slot per rank)
       double* mine = g_rep.p + 14 * static_cast<size_t>(rank);
@@ -1685,9 +1696,9 @@ struct smcl_engine {
         mark(E_BAYES);
       }
       mark(E_SMOOTH);  // posterior smoothing starts
-      smooth(cfg.smooth_iters, cfg.log_post_floor, p_ready);
+      const bool rep_parts = smooth(cfg.smooth_iters, cfg.log_post_floor, p_ready, /*rep_parts=*/true);
       mark(E_END);
-      representative_enqueue();
+      representative_enqueue(rep_parts);
       join_aux();
       CK(cudaMemcpyAsync(step_host->cnt, d_counts.p, sizeof(unsigned long long) * 6, cudaMemcpyDeviceToHost, st));
       g_d2h += sizeof(unsigned long long) * 6;

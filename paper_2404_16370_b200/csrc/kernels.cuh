@@ -167,9 +167,11 @@ void launch_argmax_partials(const double* v, int64_t n, int64_t gbase, double* s
                             cudaStream_t st);
 void launch_chunk_sum_exp_parts(const double* v, int64_t n, const double* m_parts, int n_parts, double* m_out,
                                 double* partial, cudaStream_t st);
+// am_v / am_i (optional): per-block argmax partials of the result (apply_fin_blocks(n) of them).
+int apply_fin_blocks(int64_t n);
 void launch_apply_lse_fin(double* v, int64_t n, const double* partial, int64_t n_chunks, const double* m,
                           double floor_v, const unsigned long long* skip_if_zero, double* lse_out, double* p_out,
-                          cudaStream_t st);
+                          int64_t gbase, double* am_v, long long* am_i, cudaStream_t st);
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
                          const int32_t* count, int k, cudaStream_t st, bool take_log = false);
 

@@ -278,7 +278,9 @@ __global__ void __launch_bounds__(256) k_apply_lse_fin(double* __restrict__ v, i
                                                        const double* __restrict__ partial, int64_t n_chunks,
                                                        const double* __restrict__ m_ptr, double floor_v,
                                                        const unsigned long long* __restrict__ skip_if_zero,
-                                                       double* __restrict__ lse_out, double* __restrict__ p_out) {
+                                                       double* __restrict__ lse_out, double* __restrict__ p_out,
+                                                       int64_t gbase, double* __restrict__ am_v,
+                                                       long long* __restrict__ am_i) {
   __shared__ double s[kFinStage];
   __shared__ double s_lse;
   if (threadIdx.x < 32) {
@@ -291,6 +293,8 @@ __global__ void __launch_bounds__(256) k_apply_lse_fin(double* __restrict__ v, i
   __syncthreads();
   const double lse = s_lse;
   const bool skip = skip_if_zero && *skip_if_zero == 0ull;
+  double best = -__longlong_as_double(0x7ff0000000000000ll);  // am_v: per-block argmax of the result
+  long long bi = -1;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double r = v[i];
@@ -300,6 +304,27 @@ __global__ void __launch_bounds__(256) k_apply_lse_fin(double* __restrict__ v, i
       v[i] = r;
     }
     if (p_out) p_out[i] = exp(r);
+    if (am_v) argmax_merge(best, bi, r, gbase + i);
+  }
+  if (am_v) {  // the representative's argmax partials (posterior.cpp:99-108), merged as k_argmax does
+    __shared__ double sv[8];
+    __shared__ long long si[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
+      const long long i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+      argmax_merge(best, bi, v2, i2);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sv[threadIdx.x >> 5] = best;
+      si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 1; q < 8; ++q) argmax_merge(best, bi, sv[q], si[q]);
+      am_v[blockIdx.x] = best;
+      am_i[blockIdx.x] = bi;
+    }
   }
 }
 
@@ -510,16 +535,23 @@ void launch_chunk_sum_exp_parts(const double* v, int64_t n, const double* m_part
   k_chunk_serial<<<static_cast<unsigned>(chunks), kChunkThreads, 0, st>>>(v, v, n, chunks, partial, partial, nullptr,
                                                                           m_parts, n_parts, m_out);
 }
+int apply_fin_blocks(int64_t n) {
+  static const int n_sm = [] {
+    int dev, v;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return static_cast<int>(std::min<int64_t>(blocks_for(n, 256), 4LL * n_sm));
+}
 void launch_apply_lse_fin(double* v, int64_t n, const double* partial, int64_t n_chunks, const double* m,
                           double floor_v, const unsigned long long* skip_if_zero, double* lse_out, double* p_out,
-                          cudaStream_t st) {
+                          int64_t gbase, double* am_v, long long* am_i, cudaStream_t st) {
   count_launch();
   if (n <= 0) return;
-  int dev, n_sm;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned g = static_cast<unsigned>(std::min<int64_t>(blocks_for(n, 256), 4LL * n_sm));
-  k_apply_lse_fin<<<g, 256, 0, st>>>(v, n, partial, n_chunks, m, floor_v, skip_if_zero, lse_out, p_out);
+  const unsigned g = static_cast<unsigned>(apply_fin_blocks(n));
+  k_apply_lse_fin<<<g, 256, 0, st>>>(v, n, partial, n_chunks, m, floor_v, skip_if_zero, lse_out, p_out, gbase, am_v,
+                                     am_i);
 }
 void launch_argmax_partials(const double* v, int64_t n, int64_t gbase, double* scratch_v, long long* scratch_i,
                             cudaStream_t st) {
