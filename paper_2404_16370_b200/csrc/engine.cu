@@ -1053,7 +1053,9 @@ struct smcl_engine {
       launch_solve(fast_used ? nullptr : sys.p, fast_used ? sysf.p : nullptr, raw_ll.p, nm.p, n_local, gp, steps.p,
                    ll.p, st);
     else
-      launch_gate_ll(raw_ll.p, nm.p, n_local, gp, ll.p, st);
+      // in a step the gate also forms the Bayes update's match counts (d_counts[0..1])
+      launch_gate_ll(raw_ll.p, nm.p, n_local, gp, ll.p, st, profiling ? d_counts.p : nullptr);
+      gate_counted = profiling;
     CK(cudaGetLastError());
     ll_valid = true;
     if (gn) steps_valid = true;
@@ -1437,19 +1439,31 @@ struct smcl_engine {
   // pass's input, written by the same sweep.
   // rep_parts (unsharded): also leave the argmax partials of the result in
   // argv/argi for representative_enqueue; returns whether it did.
+  // numer (unsharded): apply the Bayes numerator (k_bayes_numer) in the
+  // argmax sweep first.
+  struct Numer {
+    double beta, fill;
+    const unsigned long long* matched;
+  };
+  bool gate_counted = false;  // this step's gate already formed d_counts[0..1]
   bool normalize(double floor_v, const unsigned long long* skip_if_zero = nullptr, double* p_out = nullptr,
-                 bool rep_parts = false) {
+                 bool rep_parts = false, const Numer* numer = nullptr) {
     const int64_t n = n_local;
     if (n == 0) return false;
     const int64_t chunks_local = (n + kReduceChunk - 1) / kReduceChunk;
     if (!sharded) {  // three launches: argmax partials, chunk sums (max from the partials), finish + apply
-      launch_argmax_partials(log_post.p, n, gbase, argv.p, argi.p, st);
+      if (numer)
+        launch_numer_argmax_partials(log_post.p, ll.p, nm.p, n, gbase, numer->beta, numer->matched, numer->fill,
+                                     argv.p, argi.p, st);
+      else
+        launch_argmax_partials(log_post.p, n, gbase, argv.p, argi.p, st);
       launch_chunk_sum_exp_parts(log_post.p, n, argv.p, argmax_partials(n), scal.p + 2, partial.p, st);
       launch_apply_lse_fin(log_post.p, n, partial.p, chunks_local, scal.p + 2, floor_v, skip_if_zero, scal.p + 3,
                            p_out, gbase, rep_parts ? argv.p : nullptr, rep_parts ? argi.p : nullptr, st);
       CK(cudaGetLastError());
       return rep_parts;
     }
+    if (numer) launch_bayes_numer(log_post.p, ll.p, nm.p, n, numer->beta, numer->matched, numer->fill, st);
     global_argmax(2, 0);
     launch_chunk_sum_exp(log_post.p, n, scal.p + 2, partial.p, st);
     const int64_t chunks = (n + kReduceChunk - 1) / kReduceChunk;
@@ -1509,14 +1523,16 @@ struct smcl_engine {
     if (!(beta >= 0.0)) throw std::invalid_argument("bayes_update: beta must be >= 0");
     const int64_t n = n_local;
     if (n == 0) return;
-    launch_match_counts(ll.p, nm.p, n_local, d_counts.p, st);
+    if (!gate_counted) launch_match_counts(ll.p, nm.p, n_local, d_counts.p, st);
+    gate_counted = false;
     if (sharded) {
       allgather(d_counts.p, g_counts.p, 2 * sizeof(unsigned long long));
       launch_sum_pairs(g_counts.p, world, d_counts.p, st);
     }
-    launch_bayes_numer(log_post.p, ll.p, nm.p, n, beta, d_counts.p, -std::log(static_cast<double>(n_total)), st);
-    // the step's smoothing follows: its exp(log_post) comes out of the same sweep
-    normalize(floor_v, d_counts.p, p_out);
+    // numerator, normalisation and (the step's smoothing follows) its
+    // exp(log_post), fused where unsharded
+    const Numer numer{beta, -std::log(static_cast<double>(n_total)), d_counts.p};
+    normalize(floor_v, d_counts.p, p_out, false, &numer);
   }
 
   // p_ready: pbuf already holds exp(log_post) (bayes_async's normalisation).

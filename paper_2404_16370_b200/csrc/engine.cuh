@@ -116,7 +116,7 @@ void launch_build_occupancy(const float4* rec, uint64_t n_records, uint32_t* occ
 void launch_solve(const double* sys, const float* sysf, const double* raw_ll, const int32_t* nm, int64_t n,
                   const GicpParamsDev& p, double* steps, double* ll, cudaStream_t st);
 void launch_gate_ll(const double* raw_ll, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* ll,
-                    cudaStream_t st);
+                    cudaStream_t st, unsigned long long* counts = nullptr);
 void launch_solve_batch(const double* H, const double* b, const double* lam, int64_t n, double omax, double vmax,
                         double* out, cudaStream_t st);
 

@@ -165,6 +165,9 @@ void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st);
 int argmax_partials(int64_t n);
 void launch_argmax_partials(const double* v, int64_t n, int64_t gbase, double* scratch_v, long long* scratch_i,
                             cudaStream_t st);
+void launch_numer_argmax_partials(double* lp, const double* ll, const int32_t* nm, int64_t n, int64_t gbase,
+                                  double beta, const unsigned long long* matched, double fill, double* scratch_v,
+                                  long long* scratch_i, cudaStream_t st);
 void launch_chunk_sum_exp_parts(const double* v, int64_t n, const double* m_parts, int n_parts, double* m_out,
                                 double* partial, cudaStream_t st);
 // am_v / am_i (optional): per-block argmax partials of the result (apply_fin_blocks(n) of them).

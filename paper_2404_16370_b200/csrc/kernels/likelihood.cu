@@ -351,11 +351,42 @@ __global__ void k_solve(const double* __restrict__ sys, const float* __restrict_
   for (int q = 0; q < 6; ++q) steps[6 * i + q] = step[q];
 }
 
-__global__ void k_gate(const double* __restrict__ raw_ll, const int32_t* __restrict__ nm, int64_t n, GicpParamsDev p,
-                       double* __restrict__ ll) {
+// counts (optional): += (particles with a matched observation, sum of
+// n_matched), the Bayes update's match counts (posterior.cpp:26-58), folded
+// into the gate's sweep (one block reduction + two atomics per block).
+__global__ void __launch_bounds__(256) k_gate(const double* __restrict__ raw_ll, const int32_t* __restrict__ nm,
+                                              int64_t n, GicpParamsDev p, double* __restrict__ ll,
+                                              unsigned long long* __restrict__ counts) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  ll[i] = gated(p, raw_ll[i], nm[i]);
+  unsigned a = 0, b = 0;
+  if (i < n) {
+    const int m = nm[i];
+    const double g = gated(p, raw_ll[i], m);
+    ll[i] = g;
+    a = g > -1e30 ? 1u : 0u;
+    b = static_cast<unsigned>(m);
+  }
+  if (!counts) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  __shared__ unsigned sa[8], sb[8];
+  if ((threadIdx.x & 31) == 0) {
+    sa[threadIdx.x >> 5] = a;
+    sb[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ta = 0, tb = 0;
+    for (int w = 0; w < 8; ++w) {
+      ta += sa[w];
+      tb += sb[w];
+    }
+    if (ta) atomicAdd(counts, ta);
+    if (tb) atomicAdd(counts + 1, tb);
+  }
 }
 
 __global__ void k_solve_batch(const double* __restrict__ H, const double* __restrict__ b,
@@ -395,10 +426,10 @@ void launch_solve(const double* sys, const float* sysf, const double* raw_ll, co
 }
 
 void launch_gate_ll(const double* raw_ll, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* ll,
-                    cudaStream_t st) {
+                    cudaStream_t st, unsigned long long* counts) {
   count_launch();
   if (n <= 0) return;
-  k_gate<<<blocks_for(n, 256), 256, 0, st>>>(raw_ll, nm, n, p, ll);
+  k_gate<<<blocks_for(n, 256), 256, 0, st>>>(raw_ll, nm, n, p, ll, counts);
 }
 
 void launch_solve_batch(const double* H, const double* b, const double* lam, int64_t n, double omax, double vmax,

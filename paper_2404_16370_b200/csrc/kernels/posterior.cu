@@ -553,6 +553,54 @@ void launch_apply_lse_fin(double* v, int64_t n, const double* partial, int64_t n
   k_apply_lse_fin<<<g, 256, 0, st>>>(v, n, partial, n_chunks, m, floor_v, skip_if_zero, lse_out, p_out, gbase, am_v,
                                      am_i);
 }
+// Bayes numerator (k_bayes_numer) and the normalisation's argmax partials in
+// one grid-stride sweep (unsharded step).
+__global__ void __launch_bounds__(256) k_numer_argmax(double* __restrict__ lp, const double* __restrict__ ll,
+                                                      const int32_t* __restrict__ nm, int64_t n, int64_t gbase,
+                                                      double beta, const unsigned long long* __restrict__ matched,
+                                                      double fill, double* __restrict__ out_v,
+                                                      long long* __restrict__ out_i) {
+  __shared__ double sv[8];
+  __shared__ long long si[8];
+  const bool reset = matched && *matched == 0ull;
+  double best = -__longlong_as_double(0x7ff0000000000000ll);
+  long long bi = -1;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double r;
+    if (reset) {
+      r = fill;
+    } else {
+      const double denom = static_cast<double>(nm[i] > 1 ? nm[i] : 1);
+      r = xadd(lp[i], xmul(beta, ll[i]) / denom);
+    }
+    lp[i] = r;
+    argmax_merge(best, bi, r, gbase + i);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, best, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    argmax_merge(best, bi, v2, i2);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < 8; ++q) argmax_merge(best, bi, sv[q], si[q]);
+    out_v[blockIdx.x] = best;
+    out_i[blockIdx.x] = bi;
+  }
+}
+void launch_numer_argmax_partials(double* lp, const double* ll, const int32_t* nm, int64_t n, int64_t gbase,
+                                  double beta, const unsigned long long* matched, double fill, double* scratch_v,
+                                  long long* scratch_i, cudaStream_t st) {
+  count_launch();
+  if (n <= 0) return;
+  k_numer_argmax<<<argmax_partials(n), 256, 0, st>>>(lp, ll, nm, n, gbase, beta, matched, fill, scratch_v, scratch_i);
+}
 void launch_argmax_partials(const double* v, int64_t n, int64_t gbase, double* scratch_v, long long* scratch_i,
                             cudaStream_t st) {
   count_launch();
