@@ -1285,11 +1285,15 @@ struct smcl_engine {
     // (neighbor_search.cpp:86-103): a stable sort of the upper bits suffices.
     sort_keys(keys_all, skeys.p, n, lp.idx_bits, 64, temp.p, temp_bytes, st);
     if (profiling) mark(E_SORT);
-    launch_members(skeys.p, n, idx_mask, shift, member_of.p, head.p, st);
+    const double anchor[3] = {0.5 * (bounds[0] + bounds[3]), 0.5 * (bounds[1] + bounds[4]),
+                              0.5 * (bounds[2] + bounds[5])};  // the pose mirror's translation origin
+    bool mirror_ready = false;
+    // with reorder, the inverse permutation comes out of the same sweep
+    launch_members(skeys.p, n, idx_mask, shift, member_of.p, head.p, st,
+                   cfg.reorder_particles ? new_of_old.p : nullptr);
     const int32_t* members = member_of.p;
     bool segments_done = false;
     if (cfg.reorder_particles) {
-      launch_inverse_perm(member_of.p, n, new_of_old.p, st);
       if (sharded) {
         // Cross-shard permutation (particle_set.cpp:7-47 over the global
         // order): every rank owns the new positions [gbase, gbase + n_local)
@@ -1320,9 +1324,12 @@ struct smcl_engine {
         g_poses.swap(g_poses2);
         if (comm.alltoallv)
           CK(cudaMemcpyAsync(poses2.p, g_poses.p + gbase, sizeof(Pose) * nl, cudaMemcpyDeviceToDevice, st));
-      } else {
-        launch_reorder(member_of.p, new_of_old.p, n, k, poses.p, log_post.p, id.p, idx.p, kval.p, count.p, poses2.p,
-                       log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st);
+      } else {  // the neighbour pass's fp32 pose mirror is written by the same sweep
+        pose_mirror.ensure(3 * static_cast<size_t>(n));
+        mirror_tmax.ensure(1);
+        mirror_ready = launch_reorder(member_of.p, new_of_old.p, n, k, poses.p, log_post.p, id.p, idx.p, kval.p,
+                                      count.p, poses2.p, log_post2.p, id2.p, idx2.p, kval2.p, count2.p, st,
+                                      pose_mirror.p, mirror_tmax.p, anchor);
       }
       poses.swap(poses2);
       log_post.swap(log_post2);
@@ -1360,11 +1367,9 @@ struct smcl_engine {
     }
     pose_mirror.ensure(3 * static_cast<size_t>(n));
     mirror_tmax.ensure(1);
-    const double anchor[3] = {0.5 * (bounds[0] + bounds[3]), 0.5 * (bounds[1] + bounds[4]),
-                              0.5 * (bounds[2] + bounds[5])};
     launch_refresh_gather(poses_all, n_local, gbase, owned, members, seg_id.p, seg_start.p, n, pos_of, idx.p,
                           kval.p, count.p, k, cfg.lsh_bucket_capacity, cfg.sigma_r, cfg.sigma_t, anchor,
-                          pose_mirror.p, mirror_tmax.p, st);
+                          pose_mirror.p, mirror_tmax.p, st, mirror_ready);
     CK(cudaGetLastError());
     if (profiling) mark(E_RG);
     // statistics (neighbor_search.cpp:172-190)

@@ -73,7 +73,7 @@ size_t sort_temp_bytes(int64_t n);
 void sort_keys(const uint64_t* in, uint64_t* out, int64_t n, int begin_bit, int end_bit, void* temp, size_t temp_bytes,
                cudaStream_t st);
 void launch_members(const uint64_t* skeys, int64_t n, uint64_t idx_mask, int shift, int32_t* member_of, int32_t* head,
-                    cudaStream_t st);
+                    cudaStream_t st, int32_t* new_of_old = nullptr);
 void inclusive_sum_i32(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t st);
 void launch_permute_poses(const int32_t* perm, int64_t n, const Pose* src, Pose* dst, cudaStream_t st);
 size_t migrate_record_bytes(int k);
@@ -85,10 +85,13 @@ void launch_migrate_pack(const int32_t* member_of, int64_t n, int64_t nl, int wo
 void launch_migrate_unpack(const void* recv, int64_t nl, int64_t gbase, int k, const int32_t* new_of_old, double* lp2,
                            int32_t* id2, int32_t* count2, int32_t* idx2, float* kval2, cudaStream_t st);
 void launch_inverse_perm(const int32_t* member_of, int64_t n, int32_t* new_of_old, cudaStream_t st);
-void launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_t n, int k, const Pose* poses,
+// mir / tmax_bits / anchor (optional, K = 20): also write the neighbour
+// pass's fp32 pose mirror of the reordered poses; returns whether it did.
+bool launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_t n, int k, const Pose* poses,
                     const double* lp, const int32_t* id, const int32_t* idx, const float* kval, const int32_t* count,
                     Pose* poses2, double* lp2, int32_t* id2, int32_t* idx2, float* kval2, int32_t* count2,
-                    cudaStream_t st);
+                    cudaStream_t st, float4* mir = nullptr, unsigned int* tmax_bits = nullptr,
+                    const double* anchor = nullptr);
 void launch_segments(const int32_t* head, const int32_t* seg_id, int64_t n, int32_t* seg_start, cudaStream_t st);
 void launch_seg_stats(const int32_t* seg_start, const int32_t* n_seg, int64_t n, int cap, unsigned long long* hist,
                       unsigned long long* overflow, cudaStream_t st);
@@ -99,7 +102,7 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                            const int32_t* member_of, const int32_t* seg_id, const int32_t* seg_start,
                            int64_t n_sorted, const int32_t* pos_of, int32_t* idx, float* kval, int32_t* count, int k,
                            int cap, double sr, double st_, const double anchor[3], float4* mir,
-                           unsigned int* tmax_bits, cudaStream_t st);
+                           unsigned int* tmax_bits, cudaStream_t st, bool mirror_ready = false);
 
 // map_build.cu (device map load: NNF + fast-map records)
 cudaError_t build_nnf_device(const double* d_mu, int64_t n, const double pg_org[3], const int pg_dims[3],

@@ -124,13 +124,17 @@ __global__ void k_hash_batch(const Pose* __restrict__ poses, int64_t n, LshPass 
 }
 
 // member_of[p] = key & mask; head flag of bucket runs.
+// new_of_old (optional): the inverse permutation of the reorder, in the same sweep.
 __global__ void k_members(const uint64_t* __restrict__ skeys, int64_t n, uint64_t idx_mask, int shift,
-                          int32_t* __restrict__ member_of, int32_t* __restrict__ head) {
+                          int32_t* __restrict__ member_of, int32_t* __restrict__ head,
+                          int32_t* __restrict__ new_of_old) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint64_t k = skeys[p];
-  member_of[p] = static_cast<int32_t>(k & idx_mask);
+  const int32_t m = static_cast<int32_t>(k & idx_mask);
+  member_of[p] = m;
   head[p] = (p == 0 || (skeys[p - 1] >> shift) != (k >> shift)) ? 1 : 0;
+  if (new_of_old) new_of_old[m] = static_cast<int32_t>(p);
 }
 
 __global__ void k_inverse_perm(const int32_t* __restrict__ member_of, int64_t n, int32_t* __restrict__ new_of_old) {
@@ -167,7 +171,9 @@ __global__ void k_reorder(const int32_t* __restrict__ old_of_new, const int32_t*
 
 // K = 20 rows (80 B, 16-byte aligned): 128-bit row copies, all 20 remap
 // gathers issued together, 128-bit pose copy.
-template <int K>
+// kMirror: also write the neighbour pass's fp32 pose mirror of the reordered
+// poses and its max |t - c| (what k_pose_mirror computes), in the same sweep.
+template <int K, bool kMirror = false>
 __global__ void __launch_bounds__(128, 1) k_reorder_k(const int32_t* __restrict__ old_of_new,
                                                    const int32_t* __restrict__ new_of_old, int64_t n,
                                                    const Pose* __restrict__ poses, const double* __restrict__ lp,
@@ -175,9 +181,34 @@ __global__ void __launch_bounds__(128, 1) k_reorder_k(const int32_t* __restrict_
                                                    const float* __restrict__ kval, const int32_t* __restrict__ count,
                                                    Pose* __restrict__ poses2, double* __restrict__ lp2,
                                                    int32_t* __restrict__ id2, int32_t* __restrict__ idx2,
-                                                   float* __restrict__ kval2, int32_t* __restrict__ count2) {
+                                                   float* __restrict__ kval2, int32_t* __restrict__ count2,
+                                                   float4* __restrict__ mir = nullptr,
+                                                   unsigned int* __restrict__ tmax_bits = nullptr,
+                                                   double3 anc = double3{0.0, 0.0, 0.0}) {
   static_assert(K % 4 == 0, "rows must be whole 16-byte vectors");
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (kMirror) {  // the block's max |t - c| needs every thread: no early return
+    float tm = 0.f;
+    if (p < n) {
+      const Pose q = ldg_pose(poses + old_of_new[p]);
+      const float t0 = static_cast<float>(q.t[0] - anc.x), t1 = static_cast<float>(q.t[1] - anc.y),
+                  t2 = static_cast<float>(q.t[2] - anc.z);
+      mir[3 * p] = make_float4(q.R[0], q.R[1], q.R[2], q.R[3]);
+      mir[3 * p + 1] = make_float4(q.R[4], q.R[5], q.R[6], q.R[7]);
+      mir[3 * p + 2] = make_float4(q.R[8], t0, t1, t2);
+      tm = fmaxf(fabsf(t0), fmaxf(fabsf(t1), fabsf(t2)));
+      if (!(tm <= 3.0e38f)) tm = 3.0e38f;  // NaN / inf poses: the margin becomes useless (filter passes all)
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, o));
+    __shared__ float wmax[4];  // 128 threads
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = tm;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const float b = fmaxf(fmaxf(wmax[0], wmax[1]), fmaxf(wmax[2], wmax[3]));
+      if (b > 0.f) atomicMax(tmax_bits, __float_as_uint(b));
+    }
+  }
   if (p >= n) return;
   const int64_t src = old_of_new[p];
   poses2[p] = ldg_pose(poses + src);
@@ -886,9 +917,9 @@ void sort_keys(const uint64_t* in, uint64_t* out, int64_t n, int begin_bit, int 
 }
 
 void launch_members(const uint64_t* skeys, int64_t n, uint64_t idx_mask, int shift, int32_t* member_of, int32_t* head,
-                    cudaStream_t st) {
+                    cudaStream_t st, int32_t* new_of_old) {
   count_launch();
-  if (n > 0) k_members<<<blocks_for(n, 256), 256, 0, st>>>(skeys, n, idx_mask, shift, member_of, head);
+  if (n > 0) k_members<<<blocks_for(n, 256), 256, 0, st>>>(skeys, n, idx_mask, shift, member_of, head, new_of_old);
 }
 
 void inclusive_sum_i32(const int32_t* in, int32_t* out, int64_t n, void* temp, size_t temp_bytes, cudaStream_t st) {
@@ -900,19 +931,27 @@ void launch_inverse_perm(const int32_t* member_of, int64_t n, int32_t* new_of_ol
   if (n > 0) k_inverse_perm<<<blocks_for(n, 256), 256, 0, st>>>(member_of, n, new_of_old);
 }
 
-void launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_t n, int k, const Pose* poses,
+bool launch_reorder(const int32_t* old_of_new, const int32_t* new_of_old, int64_t n, int k, const Pose* poses,
                     const double* lp, const int32_t* id, const int32_t* idx, const float* kval, const int32_t* count,
                     Pose* poses2, double* lp2, int32_t* id2, int32_t* idx2, float* kval2, int32_t* count2,
-                    cudaStream_t st) {
+                    cudaStream_t st, float4* mir, unsigned int* tmax_bits, const double* anchor) {
   count_launch();
   if (n > 0 && k == 20) {
+    if (mir) {
+      cudaMemsetAsync(tmax_bits, 0, sizeof(unsigned int), st);
+      k_reorder_k<20, true><<<blocks_for(n, 128), 128, 0, st>>>(
+          old_of_new, new_of_old, n, poses, lp, id, idx, kval, count, poses2, lp2, id2, idx2, kval2, count2, mir,
+          tmax_bits, make_double3(anchor[0], anchor[1], anchor[2]));
+      return true;
+    }
     k_reorder_k<20><<<blocks_for(n, 128), 128, 0, st>>>(old_of_new, new_of_old, n, poses, lp, id, idx, kval, count,
                                                         poses2, lp2, id2, idx2, kval2, count2);
-    return;
+    return false;
   }
   if (n > 0)
     k_reorder<<<blocks_for(n, 128), 128, 0, st>>>(old_of_new, new_of_old, n, k, poses, lp, id, idx, kval, count, poses2,
                                                   lp2, id2, idx2, kval2, count2);
+  return false;
 }
 
 void launch_permute_poses(const int32_t* perm, int64_t n, const Pose* src, Pose* dst, cudaStream_t st) {
@@ -966,18 +1005,20 @@ void launch_refresh_gather(const Pose* all_poses, int64_t n, int64_t gbase, cons
                            const int32_t* seg_id, const int32_t* seg_start, int64_t n_sorted,
                            const int32_t* pos_of, int32_t* idx, float* kval, int32_t* count, int k, int cap,
                            double sr, double st_, const double anchor[3], float4* mir, unsigned int* tmax_bits,
-                           cudaStream_t st) {
+                           cudaStream_t st, bool mirror_ready) {
   count_launch();
   constexpr int B = 64;
   if (n <= 0) return;
   static const bool filtered = std::getenv("SMCL_RG_PLAIN") == nullptr;
   if (filtered && k <= 32 && cap <= 64) {
     // fp32 pose mirror of every particle (the window members may be any shard's)
-    count_launch();
-    cudaMemsetAsync(tmax_bits, 0, sizeof(unsigned int), st);
-    k_pose_mirror<<<blocks_for(n_sorted, 256), 256, 0, st>>>(all_poses, n_sorted,
-                                                            make_double3(anchor[0], anchor[1], anchor[2]), mir,
-                                                            tmax_bits);
+    if (!mirror_ready) {  // (the unsharded reorder writes it with the reordered poses)
+      count_launch();
+      cudaMemsetAsync(tmax_bits, 0, sizeof(unsigned int), st);
+      k_pose_mirror<<<blocks_for(n_sorted, 256), 256, 0, st>>>(all_poses, n_sorted,
+                                                              make_double3(anchor[0], anchor[1], anchor[2]), mir,
+                                                              tmax_bits);
+    }
 #define RGF(KM)                                                                                               \
   k_refresh_gather_f<B, KM><<<blocks_for(n, B), B,                                                                 \
                               static_cast<size_t>(k) * B * 4 + static_cast<size_t>(KM) * B * 4 +                   \
