@@ -1045,13 +1045,14 @@ struct smcl_engine {
     CK(cudaGetLastError());
     if (profiling) {  // matched particle-points of this pass, summed over the step's passes (counts only)
       gn ? mark_it(gn_iter, I_GN1) : mark(E_LL1);
-      // unsharded, the likelihood pass's sum is the Bayes update's own count (d_counts[1])
-      if (gn || sharded) launch_match_counts(nullptr, nm.p, n_local, d_counts.p + (gn ? 2 : 4), st, /*zero=*/false);
+      // the GN pass's sum comes out of the solve (d_counts[3]); unsharded, the
+      // likelihood pass's is the Bayes update's own count (d_counts[1])
+      if (!gn && sharded) launch_match_counts(nullptr, nm.p, n_local, d_counts.p + 4, st, /*zero=*/false);
     }
     const GicpParamsDev gp = gicp_params(sd.n);
     if (gn)
       launch_solve(fast_used ? nullptr : sys.p, fast_used ? sysf.p : nullptr, raw_ll.p, nm.p, n_local, gp, steps.p,
-                   ll.p, st);
+                   ll.p, st, profiling ? d_counts.p + 3 : nullptr);
     else
       // in a step the gate also forms the Bayes update's match counts (d_counts[0..1])
       launch_gate_ll(raw_ll.p, nm.p, n_local, gp, ll.p, st, profiling ? d_counts.p : nullptr);

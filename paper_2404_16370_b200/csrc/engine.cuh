@@ -114,7 +114,8 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
 void launch_build_occupancy(const float4* rec, uint64_t n_records, uint32_t* occ, cudaStream_t st);
 // Exactly one of sys (exact record) / sysf (fast record) is non-null.
 void launch_solve(const double* sys, const float* sysf, const double* raw_ll, const int32_t* nm, int64_t n,
-                  const GicpParamsDev& p, double* steps, double* ll, cudaStream_t st);
+                  const GicpParamsDev& p, double* steps, double* ll, cudaStream_t st,
+                  unsigned long long* nm_sum = nullptr);
 void launch_gate_ll(const double* raw_ll, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* ll,
                     cudaStream_t st, unsigned long long* counts = nullptr);
 void launch_solve_batch(const double* H, const double* b, const double* lam, int64_t n, double omax, double vmax,

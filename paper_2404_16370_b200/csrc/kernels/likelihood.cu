@@ -305,13 +305,20 @@ __device__ __forceinline__ double gated(const GicpParamsDev& p, double raw, int 
 // F32: the fast kernel's fp32 record (kSysF lanes), widened to fp64 as the
 // kernel's own conversion would; else the exact kernel's fp64 record. Only
 // the lower triangle of H is read (LLT, trace).
+// nm_sum (optional): += sum of n_matched (the step profile's matched
+// particle-points of the pass), one warp-reduced atomic per warp.
 template <bool F32>
 __global__ void k_solve(const double* __restrict__ sys, const float* __restrict__ sysf,
                         const double* __restrict__ raw_ll, const int32_t* __restrict__ nm, int64_t n,
-                        GicpParamsDev p, double* __restrict__ steps, double* __restrict__ ll) {
+                        GicpParamsDev p, double* __restrict__ steps, double* __restrict__ ll,
+                        unsigned long long* __restrict__ nm_sum) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int m = i < n ? nm[i] : 0;
+  if (nm_sum) {
+    const unsigned w = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(m));
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(nm_sum, static_cast<unsigned long long>(w));
+  }
   if (i >= n) return;
-  const int m = nm[i];
   ll[i] = gated(p, raw_ll[i], m);
   double step[6] = {0, 0, 0, 0, 0, 0};
   if (m != 0) {
@@ -416,13 +423,13 @@ void launch_gicp_exact(bool gn, const Pose* poses, int64_t n, const ScanView& sc
 }
 
 void launch_solve(const double* sys, const float* sysf, const double* raw_ll, const int32_t* nm, int64_t n,
-                  const GicpParamsDev& p, double* steps, double* ll, cudaStream_t st) {
+                  const GicpParamsDev& p, double* steps, double* ll, cudaStream_t st, unsigned long long* nm_sum) {
   count_launch();
   if (n <= 0) return;
   if (sysf)
-    k_solve<true><<<blocks_for(n, 128), 128, 0, st>>>(nullptr, sysf, raw_ll, nm, n, p, steps, ll);
+    k_solve<true><<<blocks_for(n, 128), 128, 0, st>>>(nullptr, sysf, raw_ll, nm, n, p, steps, ll, nm_sum);
   else
-    k_solve<false><<<blocks_for(n, 128), 128, 0, st>>>(sys, nullptr, raw_ll, nm, n, p, steps, ll);
+    k_solve<false><<<blocks_for(n, 128), 128, 0, st>>>(sys, nullptr, raw_ll, nm, n, p, steps, ll, nm_sum);
 }
 
 void launch_gate_ll(const double* raw_ll, const int32_t* nm, int64_t n, const GicpParamsDev& p, double* ll,
