@@ -371,6 +371,12 @@ struct smcl_engine {
   uint64_t map_records = 0;
   DBuf<int32_t> live_list;  // K2a: particles the likelihood gate keeps
   DBuf<unsigned> live_count;
+  DBuf<int32_t> sub_list;   // the gate split's predicted-dead particles (K2a's input)
+  DBuf<unsigned> sub_count;
+  // nm holds this step's GN-pass counts (a prediction for the likelihood
+  // pass's gate) with the GN pass's own threshold
+  bool nm_from_gn = false;
+  int gn_gate_thr = 0;
 
   // particles
   DBuf<Pose> poses, poses2, poses3;  // poses3: SVGD's output never lands on the guard checkpoint
@@ -1035,12 +1041,23 @@ struct smcl_engine {
       const GicpParamsDev gp0 = gicp_params(sd.n);
       live_list.ensure(static_cast<size_t>(std::max<int64_t>(n_local, 1)));
       live_count.ensure(1);
+      // Likelihood pass of a step right after its GN pass: the GN counts
+      // predict the gate (k_ll_split); results do not depend on the prediction.
+      const bool predict_gate = !gn && profiling && nm_from_gn && gn_gate_thr > 0;
+      if (predict_gate) {
+        sub_list.ensure(static_cast<size_t>(std::max<int64_t>(n_local, 1)));
+        sub_count.ensure(1);
+      }
       launch_gicp_fast(gn, poses.p, n_local, sv, mf, sysf.p, raw_ll.p, nm.p, need_cost, gp0.min_matched, live_list.p,
-                       live_count.p, st);
+                       live_count.p, st, predict_gate ? gn_gate_thr : 0, predict_gate ? sub_list.p : nullptr,
+                       predict_gate ? sub_count.p : nullptr);
+      nm_from_gn = gn && profiling;
+      gn_gate_thr = gn ? gp0.min_matched : 0;
     } else {
       MapExact me{geom, cells.p, map_mu.p, map_sigma.p};
       if (gn) sys.ensure(static_cast<size_t>(std::max<int64_t>(n_local, 1)) * kSysStride);
       launch_gicp_exact(gn, poses.p, n_local, sv, me, sys.p, raw_ll.p, nm.p, st);
+      nm_from_gn = false;
     }
     CK(cudaGetLastError());
     if (profiling) {  // matched particle-points of this pass, summed over the step's passes (counts only)

@@ -108,9 +108,13 @@ void launch_gicp_exact(bool gn, const Pose* poses, int64_t n, const ScanView& sc
 //     cost is evaluated only for particles the gate keeps (n >= min_matched,
 //     gicp.cpp:79-85): the others' likelihood is the sentinel whatever their
 //     cost. live_list (n) / live_count (1) are scratch.
+// pred_thr > 0 (with sub_list / sub_count): nm holds a prediction of this
+// pass's n_matched (the GN pass's counts); particles at or above pred_thr go
+// straight to the likelihood kernel, the others through the K2a count.
 void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
                       double* raw_ll, int32_t* nm, bool need_cost, int min_matched, int32_t* live_list,
-                      unsigned* live_count, cudaStream_t st);
+                      unsigned* live_count, cudaStream_t st, int pred_thr = 0, int32_t* sub_list = nullptr,
+                      unsigned* sub_count = nullptr);
 void launch_build_occupancy(const float4* rec, uint64_t n_records, uint32_t* occ, cudaStream_t st);
 // Exactly one of sys (exact record) / sysf (fast record) is non-null.
 void launch_solve(const double* sys, const float* sysf, const double* raw_ll, const int32_t* nm, int64_t n,

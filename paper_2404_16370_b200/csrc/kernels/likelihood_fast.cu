@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       const float cost = warp_sum(acc.cost);
       if (lane == 0) raw_ll[i] = nmatch == 0 ? -1e30 : -static_cast<double>(cost);
     }
-    if (lane == 0 && !list) nm_out[i] = nmatch;  // list: K2a already wrote it
+    if (lane == 0) nm_out[i] = nmatch;  // also under the gate (predicted-live particles skip K2a)
     __syncwarp();
   }
 }
@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       const float cost = warp_sum(acc.cost);
       if (lane == 0) raw_ll[i] = nmatch == 0 ? -1e30 : -static_cast<double>(cost);
     }
-    if (lane == 0 && !list) nm_out[i] = nmatch;  // list: K2a already wrote it
+    if (lane == 0) nm_out[i] = nmatch;  // also under the gate (predicted-live particles skip K2a)
     __syncwarp();
   }
 }
@@ -940,7 +940,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinB) k_gicp_ll_lanes(const Pose
   }
   if (active) {
     raw_ll[i] = nmatch == 0 ? -1e30 : -cost;
-    if (!list) nm_out[i] = nmatch;  // list: K2a already wrote it
+    nm_out[i] = nmatch;  // also under the gate (predicted-live particles skip K2a)
   }
 }
 
@@ -971,8 +971,13 @@ __device__ __forceinline__ bool occupied(const MapFast& m, uint32_t r) {
 template <int kBrick>
 __global__ void __launch_bounds__(256, 4) k_ll_count(const Pose* __restrict__ poses, int64_t n, ScanView scan,
                                                      MapFast map, int min_matched, int32_t* __restrict__ nm_out,
-                                                     int32_t* __restrict__ live, unsigned* __restrict__ live_count) {
+                                                     int32_t* __restrict__ live, unsigned* __restrict__ live_count,
+                                                     const int32_t* __restrict__ sub,
+                                                     const unsigned* __restrict__ sub_count) {
   constexpr int U = 4;  // points in flight per lane
+  // sub: count only these particles (the split's predicted-dead ones)
+  const int64_t n_eff = sub ? static_cast<int64_t>(*sub_count) : n;
+  if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= n_eff) return;  // block-uniform
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float4* s_m = reinterpret_cast<float4*>(smem_raw);  // fp32 mu (scan record .xyz), padded with NaN
   const int S = scan.n;
@@ -982,8 +987,9 @@ __global__ void __launch_bounds__(256, 4) k_ll_count(const Pose* __restrict__ po
     s_m[q] = q < S ? scan.rec[2 * q] : make_float4(nan, nan, nan, nan);
   }
   __syncthreads();
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool active = i < n;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool active = r < n_eff;
+  const int64_t i = active ? (sub ? static_cast<int64_t>(sub[r]) : r) : 0;
   const NnfGeom g = map.g;
   const unsigned dx = static_cast<unsigned>(g.dims[0]), dy = static_cast<unsigned>(g.dims[1]),
                  dz = static_cast<unsigned>(g.dims[2]);
@@ -1079,6 +1085,32 @@ __global__ void __launch_bounds__(256, 4) k_ll_count(const Pose* __restrict__ po
   if (lane == 0 && mask) base = atomicAdd(live_count, static_cast<unsigned>(__popc(mask)));
   base = __shfl_sync(0xffffffffu, base, 0);
   if (keep) live[base + __popc(mask & ((1u << lane) - 1u))] = static_cast<int32_t>(i);
+}
+
+// Speculative gate split (step only): the GN pass just counted n_matched of
+// every particle at its pre-update pose; particles whose count already passes
+// the GN pass's gate go straight to the live list (K2 counts them exactly and
+// its n_matched and gating decide), the others to K2a. A misprediction only
+// costs time: K2 gates exactly on its own count.
+__global__ void k_ll_split(const int32_t* __restrict__ nm_pred, int64_t n, int thr, int32_t* __restrict__ live,
+                           unsigned* __restrict__ live_count, int32_t* __restrict__ sub,
+                           unsigned* __restrict__ sub_count) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool active = i < n;
+  const bool to_live = active && nm_pred[i] >= thr;
+  const bool to_sub = active && !to_live;
+  const int lane = threadIdx.x & 31;
+  const unsigned ml = __ballot_sync(0xffffffffu, to_live), ms = __ballot_sync(0xffffffffu, to_sub);
+  unsigned bl = 0, bs = 0;
+  if (lane == 0) {
+    if (ml) bl = atomicAdd(live_count, static_cast<unsigned>(__popc(ml)));
+    if (ms) bs = atomicAdd(sub_count, static_cast<unsigned>(__popc(ms)));
+  }
+  bl = __shfl_sync(0xffffffffu, bl, 0);
+  bs = __shfl_sync(0xffffffffu, bs, 0);
+  const unsigned lt = (1u << lane) - 1u;
+  if (to_live) live[bl + __popc(ml & lt)] = static_cast<int32_t>(i);
+  if (to_sub) sub[bs + __popc(ms & lt)] = static_cast<int32_t>(i);
 }
 
 __global__ void k_build_occ(const float4* __restrict__ rec, uint64_t n_records, uint32_t* __restrict__ occ) {
@@ -1209,25 +1241,37 @@ static int cfg_gn_override() {
 // SMCL_FAST_CFG=UxW overrides the default (tuning sweeps only).
 void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& scan, const MapFast& map, float* sysf,
                       double* raw_ll, int32_t* nm, bool need_cost, int min_matched, int32_t* live_list,
-                      unsigned* live_count, cudaStream_t st) {
+                      unsigned* live_count, cudaStream_t st, int pred_thr, int32_t* sub_list, unsigned* sub_count) {
   count_launch();
   if (n <= 0) return;
   Extra x;
   x.cost = need_cost;
   static const bool no_gate = std::getenv("SMCL_NO_LL_GATE") != nullptr;  // experiments: K2 on every particle
+  static const bool no_split = std::getenv("SMCL_NO_LL_SPLIT") != nullptr;  // experiments: K2a on every particle
   if (!gn && min_matched > 0 && map.occ && scan.rec && live_list && live_count && !no_gate) {
     // K2a: n_matched of every particle + the list the gate keeps; K2 then
-    // evaluates the cost of those particles only.
+    // evaluates the cost of those particles only. With a prediction (nm holds
+    // the GN pass's counts, pred_thr its gate), predicted-live particles skip
+    // K2a (k_ll_split) and K2 counts them exactly.
     count_launch();
+    const bool split = pred_thr > 0 && sub_list && sub_count && !no_split;
     cudaMemsetAsync(live_count, 0, sizeof(unsigned), st);
+    if (split) {
+      count_launch();
+      cudaMemsetAsync(sub_count, 0, sizeof(unsigned), st);
+      k_ll_split<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(nm, n, pred_thr, live_list, live_count,
+                                                                        sub_list, sub_count);
+    }
+    const int32_t* sub = split ? sub_list : nullptr;
+    const unsigned* sc = split ? sub_count : nullptr;
     const size_t smem = sizeof(float4) * static_cast<size_t>((scan.n + 3) / 4 * 4);
     const unsigned grid = static_cast<unsigned>((n + 255) / 256);
     if (map.brick) {
       cudaFuncSetAttribute(k_ll_count<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_ll_count<1><<<grid, 256, smem, st>>>(poses, n, scan, map, min_matched, nm, live_list, live_count);
+      k_ll_count<1><<<grid, 256, smem, st>>>(poses, n, scan, map, min_matched, nm, live_list, live_count, sub, sc);
     } else {
       cudaFuncSetAttribute(k_ll_count<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_ll_count<0><<<grid, 256, smem, st>>>(poses, n, scan, map, min_matched, nm, live_list, live_count);
+      k_ll_count<0><<<grid, 256, smem, st>>>(poses, n, scan, map, min_matched, nm, live_list, live_count, sub, sc);
     }
     x.list = live_list;
     x.list_count = live_count;
