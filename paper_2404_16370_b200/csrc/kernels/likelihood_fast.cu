@@ -1255,6 +1255,7 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
     // K2a (k_ll_split) and K2 counts them exactly.
     count_launch();
     const bool split = pred_thr > 0 && sub_list && sub_count && !no_split;
+
     cudaMemsetAsync(live_count, 0, sizeof(unsigned), st);
     if (split) {
       count_launch();
@@ -1275,6 +1276,15 @@ void launch_gicp_fast(bool gn, const Pose* poses, int64_t n, const ScanView& sca
     }
     x.list = live_list;
     x.list_count = live_count;
+    static const bool stats = std::getenv("SMCL_LL_SPLIT_STATS") != nullptr;  // diagnostics: list sizes (syncs)
+    if (stats) {
+      unsigned h[2] = {0, 0};
+      cudaMemcpyAsync(&h[0], live_count, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+      if (split) cudaMemcpyAsync(&h[1], sub_count, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      std::fprintf(stderr, "[ll-gate] n %lld live %u counted by K2a %u\n", static_cast<long long>(n), h[0],
+                   split ? h[1] : static_cast<unsigned>(n));
+    }
   }
   auto parse = [](const char* e) {
     if (!e) return 0;
