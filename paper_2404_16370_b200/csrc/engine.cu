@@ -1677,6 +1677,8 @@ struct smcl_engine {
     std::memset(&r, 0, sizeof(r));
     std::memset(&prof, 0, sizeof(prof));
     prof_times_pending = false;
+    nm_from_gn = false;  // set again by this step's GN pass (the likelihood gate's prediction)
+    gate_counted = false;
     r.n_particles = n_total;
     const bool empty = sl.full.n == 0;
     r.scan_empty = empty ? 1 : 0;
