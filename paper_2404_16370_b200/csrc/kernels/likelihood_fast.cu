@@ -585,7 +585,7 @@ struct WarpQueue {
   float rf[12];       // R in fp32 (row-major, 9 used)
 };
 
-template <bool GN, int U, int kWarps, bool kCost, int kBrick>
+template <bool GN, int U, int kWarps, bool kCost, int kBrick, bool kSmemRed = true>
 __global__ void __launch_bounds__(kWarps * 32, 1)
     k_gicp_fast_q(const Pose* __restrict__ poses, int64_t n, ScanView scan, MapFast map, float* __restrict__ sysf,
                   double* __restrict__ raw_ll, int32_t* __restrict__ nm_out, const int32_t* __restrict__ list,
@@ -765,8 +765,42 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
       __syncwarp();
     }
 
-    // ---- epilogue (as k_gicp_fast)
-    if (GN) {
+    // ---- epilogue: lane q ends up with the warp total of accumulator q
+    if (GN && kSmemRed) {
+      // Reduce-scatter through the drained queue (phase B left it empty and
+      // ended with __syncwarp): lane l writes its 28 partial sums down column
+      // l of a [28][36] table, lane q < 28 sums row q with eight 128-bit
+      // loads. 28 stores + 8 loads + 31 adds instead of the butterfly's 31
+      // shuffles, 62 selects and 31 adds; both access patterns are
+      // bank-conflict free (row stride 36 words).
+      constexpr unsigned kRow = 36u * 4u;
+      static_assert(28 * 36 * 4 <= 3 * kQ * 16, "reduction table must fit the queue");
+      const float v28[28] = {acc.htl[0], acc.htl[1], acc.htl[2], acc.htl[3], acc.htl[4], acc.htl[5],
+                             acc.htr[0], acc.htr[1], acc.htr[2], acc.htr[3], acc.htr[4], acc.htr[5],
+                             acc.htr[6], acc.htr[7], acc.htr[8], acc.hbr[0], acc.hbr[1], acc.hbr[2],
+                             acc.hbr[3], acc.hbr[4], acc.hbr[5], acc.b[0],   acc.b[1],   acc.b[2],
+                             acc.b[3],   acc.b[4],   acc.b[5],   acc.cost};
+#pragma unroll
+      for (int q = 0; q < 28; ++q)
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(qaddr + kRow * q + 4u * lane), "f"(v28[q]) : "memory");
+      __syncwarp();
+      float tot = 0.f;
+      if (lane < 28) {
+        float4 r[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(r[c].x), "=f"(r[c].y), "=f"(r[c].z), "=f"(r[c].w)
+                       : "r"(qaddr + kRow * lane + 16u * c)
+                       : "memory");
+        float h[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) h[c] = (r[c].x + r[c].y) + (r[c].z + r[c].w);
+        tot = ((h[0] + h[1]) + (h[2] + h[3])) + ((h[4] + h[5]) + (h[6] + h[7]));
+      }
+      sysf[i * kSysF + lane] = tot;
+      if (kCost && lane == 27) raw_ll[i] = nmatch == 0 ? -1e30 : -static_cast<double>(tot);
+    } else if (GN) {
       float v[32];
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
@@ -1226,7 +1260,11 @@ bool launch_fast_q(const Pose* poses, int64_t n, const ScanView& scan, const Map
     kern<<<grid, W * 32, smem, st>>>(poses, n, scan, map, sysf, raw_ll, nm, x.list, x.list_count);
   };
   if (map.brick) return false;  // plain-layout tables only (see launch_gicp_fast)
-  (GN && !x.cost) ? run(k_gicp_fast_q<GN, U, W, false, 0>) : run(k_gicp_fast_q<GN, U, W, true, 0>);
+  static const bool shfl_red = std::getenv("SMCL_K1_SHFL_RED") != nullptr;  // A/B: butterfly epilogue
+  if (GN && !x.cost)
+    shfl_red ? run(k_gicp_fast_q<GN, U, W, false, 0, false>) : run(k_gicp_fast_q<GN, U, W, false, 0, true>);
+  else
+    run(k_gicp_fast_q<GN, U, W, true, 0>);
   return true;
 }
 
