@@ -1575,7 +1575,10 @@ struct smcl_engine {
       }
       // the last round writes log(q) straight into log_post (posterior.cpp:94)
       const bool last = r + 1 == iters;
-      launch_smooth_round(p_all, last ? log_post.p : qbuf.p, n, idx.p, kval.p, count.p, k, st, last);
+      // alternate sweep directions: each round starts on the L2-resident rows
+      static const bool no_rev = std::getenv("SMCL_SMOOTH_NOREV") != nullptr;  // A/B
+      launch_smooth_round(p_all, last ? log_post.p : qbuf.p, n, idx.p, kval.p, count.p, k, st, last,
+                          !no_rev && (r & 1) != 0);
       pbuf.swap(qbuf);
     }
     CK(cudaGetLastError());

@@ -179,6 +179,7 @@ void launch_apply_lse_fin(double* v, int64_t n, const double* partial, int64_t n
                           double floor_v, const unsigned long long* skip_if_zero, double* lse_out, double* p_out,
                           int64_t gbase, double* am_v, long long* am_i, cudaStream_t st);
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
-                         const int32_t* count, int k, cudaStream_t st, bool take_log = false);
+                         const int32_t* count, int k, cudaStream_t st, bool take_log = false,
+                         bool reverse = false);
 
 }  // namespace smcl

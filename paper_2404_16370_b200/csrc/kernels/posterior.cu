@@ -352,14 +352,25 @@ __global__ void k_smooth_round(const double* __restrict__ p_all, double* __restr
 
 // K = 20 (the default list size): the particle's idx / kval rows (80 B
 // each, 16-byte aligned) are read with five 128-bit loads each and all 20 p
-// gathers are issued before the (reference-order) sums.
+// gathers are issued before the (reference-order) sums. reverse: blocks walk
+// the particles from the top, so a round starts on the rows the previous
+// round read last (the 160 MB of rows at 1M exceed L2; an always-ascending
+// sweep evicts each row before the next round needs it). Rounds are Jacobi
+// sweeps: the order does not change any value.
 template <int K, int kMinB = 1>
 __global__ void __launch_bounds__(128, kMinB) k_smooth_round_k(const double* __restrict__ p_all, double* __restrict__ q,
                                                         int64_t n, const int32_t* __restrict__ idx,
                                                         const float* __restrict__ kval,
-                                                        const int32_t* __restrict__ count, int take_log) {
+                                                        const int32_t* __restrict__ count, int take_log,
+                                                        int reverse, int pdl) {
   static_assert(K % 4 == 0, "rows must be whole 16-byte vectors");
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // Programmatic dependent launch (pdl): the next round's CTAs may start as
+  // soon as every CTA of this one is running; they load their rows (constant
+  // through the smoothing) and then wait for this round's grid to complete
+  // before reading p or writing q.
+  if (pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t blk = reverse ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+  const int64_t i = blk * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int cnt = count[i];
   int32_t j[K];
@@ -373,9 +384,15 @@ __global__ void __launch_bounds__(128, kMinB) k_smooth_round_k(const double* __r
     j[4 * v] = a.x, j[4 * v + 1] = a.y, j[4 * v + 2] = a.z, j[4 * v + 3] = a.w;
     w[4 * v] = b.x, w[4 * v + 1] = b.y, w[4 * v + 2] = b.z, w[4 * v + 3] = b.w;
   }
+  if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // p is the previous round's output: plain (coherent) loads, ordered after
+  // the wait (volatile asm is never hoisted above it)
   double pv[K];
 #pragma unroll
-  for (int s = 0; s < K; ++s) pv[s] = s < cnt ? p_all[j[s]] : 0.0;
+  for (int s = 0; s < K; ++s) {
+    pv[s] = 0.0;
+    if (s < cnt) asm volatile("ld.global.f64 %0, [%1];" : "=d"(pv[s]) : "l"(p_all + j[s]));
+  }
   double num = 0.0, den = 0.0;
 #pragma unroll
   for (int s = 0; s < K; ++s) {
@@ -612,14 +629,30 @@ void launch_exp(const double* lp, double* p, int64_t n, cudaStream_t st) {
   if (n > 0) k_exp<<<blocks_for(n, 256), 256, 0, st>>>(lp, p, n);
 }
 void launch_smooth_round(const double* p_all, double* q, int64_t n, const int32_t* idx, const float* kval,
-                         const int32_t* count, int k, cudaStream_t st, bool take_log) {
+                         const int32_t* count, int k, cudaStream_t st, bool take_log, bool reverse) {
   count_launch();
   if (n <= 0) return;
   // __launch_bounds__(128, 1): 80 registers, the 20 gathers and row loads
   // all in flight (0.666 ms for 10 rounds at 1M; capped at 48 / 40
   // registers: 0.729 / 0.740; the previous default heuristic, 56: 0.687).
   if (k == 20)
-    k_smooth_round_k<20><<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count, take_log ? 1 : 0);
+  {
+    // Consecutive rounds overlap through programmatic dependent launch (the
+    // first round's predecessor simply completes before its wait returns).
+    static const bool no_pdl = std::getenv("SMCL_SMOOTH_NOPDL") != nullptr;  // A/B
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(static_cast<unsigned>(blocks_for(n, 128)));
+    lc.blockDim = dim3(128);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = no_pdl ? 0 : 1;
+    cudaLaunchKernelEx(&lc, k_smooth_round_k<20>, p_all, q, n, idx, kval, count, take_log ? 1 : 0,
+                       reverse ? 1 : 0, no_pdl ? 0 : 1);
+  }
   else
     k_smooth_round<<<blocks_for(n, 128), 128, 0, st>>>(p_all, q, n, idx, kval, count, k, take_log ? 1 : 0);
 }
