@@ -306,7 +306,8 @@ __device__ __forceinline__ double gated(const GicpParamsDev& p, double raw, int 
 // kernel's own conversion would; else the exact kernel's fp64 record. Only
 // the lower triangle of H is read (LLT, trace).
 // nm_sum (optional): += sum of n_matched (the step profile's matched
-// particle-points of the pass), one warp-reduced atomic per warp.
+// particle-points of the pass), one block-reduced atomic per block (a
+// same-address atomic per warp had serialised ~32 k atomics at 1M).
 template <bool F32>
 __global__ void k_solve(const double* __restrict__ sys, const float* __restrict__ sysf,
                         const double* __restrict__ raw_ll, const int32_t* __restrict__ nm, int64_t n,
@@ -314,9 +315,15 @@ __global__ void k_solve(const double* __restrict__ sys, const float* __restrict_
                         unsigned long long* __restrict__ nm_sum) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int m = i < n ? nm[i] : 0;
-  if (nm_sum) {
+  if (nm_sum) {  // block-uniform branch; launched with 128 threads
+    __shared__ unsigned s_w[4];
     const unsigned w = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(m));
-    if ((threadIdx.x & 31) == 0 && w) atomicAdd(nm_sum, static_cast<unsigned long long>(w));
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned long long t = static_cast<unsigned long long>(s_w[0]) + s_w[1] + s_w[2] + s_w[3];
+      if (t) atomicAdd(nm_sum, t);
+    }
   }
   if (i >= n) return;
   ll[i] = gated(p, raw_ll[i], m);
