@@ -269,8 +269,12 @@ __device__ __forceinline__ void fast_item(Acc& acc, const float Rf[9], const flo
 struct CellFrac {
   unsigned ic;
   float fr;
+  unsigned f24;  // the fraction's raw bits (frac_of_f24 builds fr from them)
   bool clear;
 };
+__device__ __forceinline__ float frac_of_f24(unsigned f24) {
+  return __uint_as_float(0x3F800000u | (f24 >> 1)) - (1.0f - 0x1p-24f);
+}
 __device__ __forceinline__ CellFrac cell_frac(double x) {
   constexpr double kMagic28 = 402653184.0;  // 1.5 * 2^28
   const double y = __dadd_rd(x, kMagic28);
@@ -278,7 +282,8 @@ __device__ __forceinline__ CellFrac cell_frac(double x) {
   CellFrac c;
   c.ic = __funnelshift_l(lo, hi, 8) - 0xB8000000u;
   const unsigned f24 = lo & 0xFFFFFFu;
-  c.fr = __uint_as_float(0x3F800000u | (f24 >> 1)) - (1.0f - 0x1p-24f);
+  c.f24 = f24;
+  c.fr = frac_of_f24(f24);
   c.clear = f24 - 1u < 0xFFFFFEu;
   return c;
 }
@@ -580,7 +585,7 @@ struct WarpQueue {
   static constexpr int kQ = kStepPts + 32;
   float4 m0[kQ];
   float4 m1[kQ];
-  float4 fq[kQ];      // (fraction.xyz, meta: k | kMetaResolve)
+  float4 fq[kQ];      // (raw fraction bits f24.xyz, meta: k | kMetaResolve)
   double pose_v[12];  // Rv (row-major), tv
   float rf[12];       // R in fp32 (row-major, 9 used)
 };
@@ -681,7 +686,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
             const CellFrac cf = cell_frac(x);
             ic[ax] = cf.ic;
             inb = inb & (cf.ic < (ax == 0 ? dx : (ax == 1 ? dy : dz)));
-            fr[u][ax] = cf.fr;
+            // raw fraction bits: the float is built in phase B, for candidates only
+            fr[u][ax] = __uint_as_float(cf.f24);
             safe = safe & cf.clear;
           }
           const bool real = k < S;
@@ -730,7 +736,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           const float4 fq = lds_f4(a + 32u * kQ);
           const uint32_t mt = __float_as_uint(fq.w);
           const int k = static_cast<int>(mt & 0xFFFFu);
-          float f3[3] = {fq.x, fq.y, fq.z};
+          float f3[3] = {frac_of_f24(__float_as_uint(fq.x)), frac_of_f24(__float_as_uint(fq.y)),
+                         frac_of_f24(__float_as_uint(fq.z))};
           float4 m0, m1;
           valid = true;
           if (mt & kMetaResolve) {  // exact transform, floor and bounds (nnf.hpp:24-35), direct gather
